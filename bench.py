@@ -1,0 +1,468 @@
+#!/usr/bin/env python3
+"""SBBF batched insert + lookup throughput on B200 (BASELINE.json metric).
+
+A step = one pass of the hot path over one batch: insert every key of the
+config's insert stream into a fresh (zeroed, untimed) filter, then look up
+every key of its lookup stream (packed lookup bitmap out). Inputs are
+resident in HBM before timing; L2 is flushed (256 MiB memset, untimed)
+between timed steps. `value` = (inserts + lookups) / device time per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--extra 3,4]
+    python bench.py --impl reference ...   # the reference's CPU path (oracle/_ref)
+
+N > 1 (torchrun, one rank per GPU): config 5's sharded mode — the filter is
+partitioned by contiguous block range and keys are routed to their owner
+rank with an NCCL all-to-all (paper_2101_01719_b200.sharded); per-rank keys
+are fixed, so scaling is weak. Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+import zlib
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SBBF insert/lookup Gkeys/s (device-timed) vs random-32B-sector roofline"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def golden():
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "configs.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def image_crc(blocks_bytes: bytes, num_buckets: int, hasher_id: int = 0) -> int:
+    """FilterImage v1 trailer CRC (persist.cpp:72-88) via zlib's IEEE CRC-32."""
+    hdr = b"SBBF" + bytes([1]) + hasher_id.to_bytes(4, "little") + num_buckets.to_bytes(8, "little")
+    return zlib.crc32(blocks_bytes, zlib.crc32(hdr)) & 0xFFFFFFFF
+
+
+# --------------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md "clocks" line)
+# --------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._pump, daemon=True)
+        self.thread.start()
+
+    def _pump(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        busy = [s for s in sm if s > 0.5 * (max(sm) if sm else 0)]
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------
+# device-timed config runs
+# --------------------------------------------------------------------------------
+def run_config_device(cid: int, steps: int, warmup: int, device, collect_parity=True) -> dict:
+    import numpy as np
+    import torch
+
+    from paper_2101_01719_b200 import SplitBlockFilter, launch_count
+    from paper_2101_01719_b200 import workload as W
+
+    cfg = W.CONFIGS[cid]
+    N, L = cfg.inserts.n, cfg.lookups.n
+    st = W.StreamHandle(cfg.inserts, device.index or 0)
+    ins = W.gen_inserts(st, 0, N, device=device.index or 0)
+    look = W.gen_lookups(st, cfg.lookups, N, 0, L, device=device.index or 0)
+    bits = torch.empty((L + 31) // 32, dtype=torch.int32, device=device)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
+    f = SplitBlockFilter(cfg.num_buckets, device=device.index or 0)
+    chunk = cfg.insert_chunk or N
+    stream = torch.cuda.current_stream(device)
+    torch.cuda.synchronize(device)
+
+    def one_step(ev):
+        ev[0].record(stream)
+        for s in range(0, N, chunk):
+            f.add_hashes(ins[s:s + chunk])
+        ev[1].record(stream)
+        f.find_hashes_bits(look, bits)
+        ev[2].record(stream)
+
+    for _ in range(warmup):
+        f.clear()
+        flush.zero_()
+        one_step([torch.cuda.Event(enable_timing=True) for _ in range(3)])
+    torch.cuda.synchronize(device)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    l0 = launch_count()
+    for k in range(steps):
+        f.clear()
+        flush.zero_()  # > L2: every timed step starts cold
+        one_step(evs[k])
+    torch.cuda.synchronize(device)
+    launches = launch_count() - l0
+    t_ins = [e[0].elapsed_time(e[1]) for e in evs]
+    t_find = [e[1].elapsed_time(e[2]) for e in evs]
+    t_step = [a + b for a, b in zip(t_ins, t_find)]
+    out = {
+        "config": cid, "name": cfg.name, "num_buckets": cfg.num_buckets,
+        "filter_bytes": cfg.filter_bytes, "inserts": N, "lookups": L,
+        "ms_per_step": statistics.mean(t_step), "ms_insert": statistics.mean(t_ins),
+        "ms_lookup": statistics.mean(t_find), "ms_step_min": min(t_step),
+        "launches_per_step": launches / steps,
+        "insert_variant": f.resolved_variants(chunk)[0], "find_variant": f.resolved_variants(L)[1],
+    }
+    out["value"] = (N + L) / (out["ms_per_step"] * 1e-3) / 1e9
+    out["insert_gkeys_s"] = N / (out["ms_insert"] * 1e-3) / 1e9
+    out["lookup_gkeys_s"] = L / (out["ms_lookup"] * 1e-3) / 1e9
+    if collect_parity:
+        g = golden().get(str(cid))
+        blocks = f.blocks()
+        crc = image_crc(blocks.tobytes(), cfg.num_buckets)
+        hb = bits.cpu().numpy().view(np.uint32)
+        res = np.unpackbits(hb.view(np.uint8), bitorder="little")[:L]
+        j = np.arange(L, dtype=np.uint64)
+        if cfg.lookups.members_first:
+            mem = j < N
+        else:
+            mem = ((j + 1) * cfg.lookups.p // cfg.lookups.q) > (j * cfg.lookups.p // cfg.lookups.q)
+        fp = int(res[~mem].sum())
+        mh = int(res[mem].sum())
+        par = {"image_crc": f"{crc:#010x}", "false_positives": fp, "nonmembers": int((~mem).sum()),
+               "member_hits": mh, "members": int(mem.sum())}
+        if g:
+            par["matches_reference"] = (crc == g["image_crc"] and fp == g["false_positives"]
+                                        and mh == g["members"])
+        out["parity"] = par
+    del f, ins, look, bits, flush, st
+    torch.cuda.empty_cache()
+    return out
+
+
+def sector_ceiling(device, filter_bytes: int, red: bool = False, n: int = 1 << 28) -> float:
+    """Random 32-B sector rate (G sectors/s) on a buffer of filter_bytes."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2101_01719_b200 import _lib
+    L = _lib.lib()
+    buf = torch.zeros(filter_bytes // 4, dtype=torch.int32, device=device)
+    sink = torch.zeros(1024, dtype=torch.int32, device=device)
+    s = C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    nb = filter_bytes // 32
+
+    def launch(seed):
+        if red:
+            rc = L.sbbf_bench_sector_red(C.c_void_p(buf.data_ptr()), nb, n, seed, s)
+        else:
+            rc = L.sbbf_bench_sector_read(C.c_void_p(buf.data_ptr()), nb, n, seed,
+                                          C.c_void_p(sink.data_ptr()), s)
+        assert rc == 0
+    for i in range(2):
+        launch(i)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for i in range(3):
+        e0.record()
+        launch(100 + i)
+        e1.record()
+        torch.cuda.synchronize(device)
+        times.append(e0.elapsed_time(e1))
+    del buf, sink
+    return n / (min(times) * 1e-3) / 1e9
+
+
+def run_e2e(cid: int, steps: int, device) -> dict:
+    """Same metric through the public API with pinned HOST buffers: every step
+    uploads the step's hashes and downloads the 0/1 result bytes."""
+    import numpy as np
+    import torch
+
+    from paper_2101_01719_b200 import SplitBlockFilter
+    from paper_2101_01719_b200 import workload as W
+
+    cfg = W.CONFIGS[cid]
+    N, L = cfg.inserts.n, cfg.lookups.n
+    st = W.StreamHandle(cfg.inserts, device.index or 0)
+    ins_h = torch.empty(N, dtype=torch.int64, pin_memory=True)
+    look_h = torch.empty(L, dtype=torch.int64, pin_memory=True)
+    res_h = torch.empty(L, dtype=torch.uint8, pin_memory=True)
+    ins_h.copy_(W.gen_inserts(st, 0, N, device=device.index or 0))
+    look_h.copy_(W.gen_lookups(st, cfg.lookups, N, 0, L, device=device.index or 0))
+    ins_np = ins_h.numpy().view(np.uint64)
+    look_np = look_h.numpy().view(np.uint64)
+    res_np = res_h.numpy()
+    f = SplitBlockFilter(cfg.num_buckets, device=device.index or 0)
+    times = []
+    for k in range(steps + 2):
+        f.clear()
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        f.add_hashes(ins_np)                 # H2D + insert kernels
+        f.find_hashes(look_np, res_np)       # H2D + lookup kernels + D2H of results
+        t1 = time.perf_counter()
+        if k >= 2:
+            times.append(t1 - t0)
+    ok = int(res_np.sum())
+    del f
+    return {"value": (N + L) / statistics.median(times) / 1e9, "unit": "Gkeys/s",
+            "h2d_bytes_per_step": 8 * (N + L), "d2h_bytes_per_step": L,
+            "ms_per_step": statistics.median(times) * 1e3, "hits": ok,
+            "api": "SplitBlockFilter.add_hashes/find_hashes on pinned host arrays "
+                   "(sbbf_gpu_add_hashes_host / sbbf_gpu_find_hashes_host)"}
+
+
+# --------------------------------------------------------------------------------
+# CPU baseline: the reference itself (oracle/_ref), run_bench's method
+# --------------------------------------------------------------------------------
+def cpu_reference_run(cid: int, reps: int, threads: int, device=None) -> dict:
+    import numpy as np
+
+    import oracle as O
+    from paper_2101_01719_b200 import workload as W
+
+    cfg = W.CONFIGS[cid]
+    N, L = cfg.inserts.n, cfg.lookups.n
+    orc = O.Oracle()
+    table = W.zipf_cdf_table(cfg.inserts.zipf_s, cfg.inserts.zipf_n) if cfg.inserts.dup_num else None
+    ost = orc.stream(cfg.inserts, table)
+    ins = orc.gen_inserts(ost, 0, N)
+    look = orc.gen_lookups(ost, cfg.lookups, N, 0, L)
+    try:
+        ref = O.Reference()
+        kind = "reference"
+        ti, tl, res, blocks = ref.time_build_probe(cfg.num_buckets, ins, look, threads, reps)
+    except (FileNotFoundError, OSError):
+        kind = "port"
+        ti, tl = [], []
+        for _ in range(reps):
+            b = orc.new_blocks(cfg.num_buckets)
+            t0 = time.perf_counter()
+            orc.add_hashes(b, ins)
+            ti.append(time.perf_counter() - t0)
+            t0 = time.perf_counter()
+            res = orc.find_hashes(b, look, threads)
+            tl.append(time.perf_counter() - t0)
+        blocks = b
+    mi, ml = statistics.median(ti), statistics.median(tl)
+    crc = image_crc(np.ascontiguousarray(blocks).tobytes(), cfg.num_buckets)
+    return {"value": (N + L) / (mi + ml) / 1e9, "unit": "Gkeys/s", "cores": threads, "kind": kind,
+            "sample": f"config {cid} in full ({N} inserts + {L} lookups), median of {reps} reps; "
+                      f"insert 1 thread (the reference's only writer mode), lookup {threads} "
+                      f"jthreads (harness.cpp:173-200); -O3 -DNDEBUG, AVX2 backend",
+            "insert_gkeys_s": N / mi / 1e9, "lookup_gkeys_s": L / ml / 1e9,
+            "image_crc": f"{crc:#010x}", "hits": int(res.sum())}
+
+
+def run_reference_arm(args) -> None:
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    reps = max(args.steps, 3)
+    r = cpu_reference_run(args.config, reps, threads)
+    from paper_2101_01719_b200 import workload as W
+    cfg = W.CONFIGS[args.config]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "Gkeys/s",
+        "n_gpus": args.gpus, "steps": reps, "warmup": 0,
+        "ms_per_step": (cfg.inserts.n + cfg.lookups.n) / r["value"] / 1e6,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded splitmix64 hash streams, BASELINE.json)",
+        "config": workload_config(args.config),
+        "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": r["value"], "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "insert_gkeys_s": r["insert_gkeys_s"], "lookup_gkeys_s": r["lookup_gkeys_s"],
+        "image_crc": r["image_crc"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cid: int) -> dict:
+    from paper_2101_01719_b200 import workload as W
+    cfg = W.CONFIGS[cid]
+    return {"workload": f"BASELINE config {cid}: {cfg.inserts.n:,} inserts into "
+                        f"{cfg.filter_bytes:,} B ({cfg.num_buckets} blocks), then "
+                        f"{cfg.lookups.n:,} lookups", "config_id": cid,
+            "inserts": cfg.inserts.n, "lookups": cfg.lookups.n, "num_buckets": cfg.num_buckets,
+            "l2": "flushed between timed steps (256 MiB memset, untimed)",
+            "lookup_output": "packed bitmap (1 bit/key)", "parallelism": "single GPU"}
+
+
+def roofline(res: dict, l2_sector_gs: float | None, hbm_peak: float, peak_note: str,
+             l2_bytes: int) -> dict:
+    """Dominant kernel = lookup. Algorithmic HBM bytes/key: 8 (hash in) + 1/8
+    (bitmap out) + 32 (random sector) when the filter exceeds L2."""
+    L = res["lookups"]
+    resident = res["filter_bytes"] <= l2_bytes // 2
+    per_key = 8.0 + 0.125 + (0.0 if resident else 32.0)
+    t = res["ms_lookup"] * 1e-3
+    achieved = L * per_key / t / 1e9
+    rf = {"bound": "hbm", "kernel": "find_global_kernel/find_smem_kernel (bitmap)",
+          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+          "traffic": None, "bytes_per_key": per_key,
+          "bytes_note": ("filter L2-resident: hash stream 8 B + bitmap 1/8 B per key from HBM"
+                         if resident else "32 B random sector + 8 B hash + 1/8 B bitmap per key"),
+          "peak_note": peak_note}
+    if l2_sector_gs:
+        rate = L / t / 1e9
+        rf["random_sector"] = {"lookup_gkeys_s": rate, "ceiling_gsectors_s": l2_sector_gs,
+                               "frac": rate / l2_sector_gs,
+                               "note": "one 32-B sector per key vs the measured random-sector "
+                                       "read rate on a buffer of the filter's size "
+                                       "(sbbf_bench_sector_read)"}
+    return rf
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--extra", default="3,4", help="extra configs reported under 'configs'")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    world = env_int("WORLD_SIZE", 1)
+    if world > 1:
+        from paper_2101_01719_b200 import sharded
+        sharded.bench_main(args)
+        return
+
+    import torch
+    device = torch.device("cuda", env_int("LOCAL_RANK", 0))
+    torch.cuda.set_device(device)
+    hbm_peak, peak_note = measured_peaks()
+    props = torch.cuda.get_device_properties(device)
+    l2_bytes = getattr(props, "L2_cache_size", 126 << 20)
+
+    clocks = ClockSampler(device.index or 0)
+    clocks.start()
+    main_res = run_config_device(args.config, args.steps, args.warmup, device)
+    extras = {}
+    for c in [int(x) for x in args.extra.split(",") if x.strip()]:
+        if c == args.config or c not in (1, 2, 3, 4):
+            continue
+        extras[str(c)] = run_config_device(c, max(3, min(args.steps, 5)), 3, device)
+    clk = clocks.stop()
+
+    # random-sector ceilings (roofline denominators)
+    l2_read = sector_ceiling(device, max(main_res["filter_bytes"], 1 << 20))
+    hbm_read = sector_ceiling(device, 4 << 30)
+    hbm_red = sector_ceiling(device, 4 << 30, red=True)
+    for r in [main_res] + list(extras.values()):
+        fits = r["filter_bytes"] <= l2_bytes // 2
+        ceil = l2_read if fits else hbm_read
+        if r is not main_res and fits:
+            ceil = sector_ceiling(device, r["filter_bytes"])
+        r["random_sector_frac_lookup"] = r["lookup_gkeys_s"] / ceil
+        r["random_sector_ceiling_gs"] = ceil
+        r["roofline"] = roofline(r, ceil, hbm_peak, peak_note, l2_bytes)
+
+    line = {
+        "metric": METRIC, "value": main_res["value"], "unit": "Gkeys/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": main_res["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded splitmix64 hash streams of BASELINE.json, generated in HBM)",
+        "config": workload_config(args.config),
+        "insert_gkeys_s": main_res["insert_gkeys_s"], "lookup_gkeys_s": main_res["lookup_gkeys_s"],
+        "ms_insert": main_res["ms_insert"], "ms_lookup": main_res["ms_lookup"],
+        "roofline": main_res["roofline"],
+        "random_sector_ceilings_gs": {"l2_read_1MiB": l2_read, "hbm_read_4GiB": hbm_read,
+                                      "hbm_red_4GiB": hbm_red},
+        "gpu_launches": int(main_res["launches_per_step"] * args.steps),
+        "clocks": clk, "parity": main_res.get("parity"),
+        "variants": {"insert": main_res["insert_variant"], "find": main_res["find_variant"]},
+        "configs": {k: {kk: v for kk, v in r.items() if kk not in ("name",)}
+                    for k, r in extras.items()},
+    }
+    if not args.no_e2e:
+        line["e2e"] = run_e2e(args.config, max(3, min(args.steps, 10)), device)
+    if not args.no_cpu_baseline:
+        try:
+            cb = cpu_reference_run(args.config, 5, os.cpu_count() or 1)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"]["image_crc"] = cb["image_crc"]
+        except Exception as exc:  # the baseline never blocks the GPU line
+            line["cpu_baseline"] = {"value": None, "error": repr(exc)}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

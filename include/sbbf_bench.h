@@ -1,0 +1,33 @@
+/*
+ * sbbf_bench.h — roofline microbenchmarks (not part of the reference API).
+ * They measure the random 32-byte-sector ceiling that bounds SBBF insert and
+ * lookup: the denominators of bench.py's "fraction of the random-sector
+ * roofline" (BASELINE.json metric).
+ */
+#ifndef SBBF_BENCH_H
+#define SBBF_BENCH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* n random 256-bit reads of d_buf (num_blocks * 32 bytes), block indices from
+ * splitmix64(seed) in registers; d_sink receives up to 1024 words. */
+int sbbf_bench_sector_read(const uint32_t* d_buf, uint64_t num_blocks, uint64_t n, uint64_t seed,
+                           uint32_t* d_sink, void* stream);
+/* n random 32-byte atomic-OR sector updates (8 lane reds per key). */
+int sbbf_bench_sector_red(uint32_t* d_buf, uint64_t num_blocks, uint64_t n, uint64_t seed,
+                          void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif

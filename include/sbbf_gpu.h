@@ -1,0 +1,159 @@
+/*
+ * sbbf_gpu.h — C ABI of the B200-native split block Bloom filter.
+ *
+ * Drop-in for the batched build/probe path of the reference core
+ * (/root/reference/proj/core/include/sbbf/filter.hpp, class
+ * sbbf::SplitBlockFilter). Each entry point below names the reference
+ * interface it replaces (file:line, relative to /root/reference/proj/).
+ *
+ * Bit layout is the reference's exactly (filter.hpp:11-31): an array of
+ * num_buckets 32-byte blocks, eight little-endian 32-bit lanes each, lane 0
+ * lowest-addressed. block_index = floor(hash * num_buckets / 2^64)
+ * (filter.cpp:125-127); lane i's bit = (seed_i * low32(hash)) >> 27
+ * (filter.cpp:129-138). A filter built here is byte-identical to the
+ * reference's for the same hashes in any order.
+ *
+ * Conventions
+ *  - Every function returns SBBF_OK (0) or a negative SBBF_E* code; no C++
+ *    exception crosses the ABI. sbbf_gpu_last_error() returns a
+ *    thread-local message for the most recent failure on this thread.
+ *  - "d_" pointers are device pointers on the filter's device, owned by the
+ *    caller. "h_" pointers are host pointers (pinned or pageable).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream). Device-pointer operations are asynchronous and stream-ordered.
+ *    Host-pointer operations (*_host) and to_host/from_host are synchronous.
+ *  - Inserts use atomic OR (red.global.or), so concurrent insert_batch calls
+ *    on one handle are safe — the "atomic OR writes" option SPEC.md:131
+ *    permits. A find concurrent with an insert may see either answer for
+ *    in-flight keys (bits are monotone).
+ *  - There is no CPU fallback: without a usable CUDA device, create() fails
+ *    with SBBF_ENODEV.
+ */
+#ifndef SBBF_GPU_H
+#define SBBF_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the ABI is the only exported surface */
+#endif
+
+#define SBBF_GPU_ABI_VERSION 1
+
+enum {
+  SBBF_OK = 0,
+  SBBF_EINVAL = -1,  /* bad argument; num_buckets == 0 mirrors std::invalid_argument (filter.cpp:160-162) */
+  SBBF_ENOMEM = -2,  /* device or host allocation failed ("resource error") */
+  SBBF_ECUDA = -3,   /* any other CUDA runtime error */
+  SBBF_ENODEV = -4,  /* no CUDA device / bad device ordinal */
+  SBBF_EFORMAT = -5  /* FilterImage parse failure */
+};
+
+/* Insert strategies (sbbf_gpu_set_insert_variant). AUTO picks per call. */
+enum {
+  SBBF_INSERT_AUTO = 0,
+  SBBF_INSERT_LANE8 = 1,      /* 8 threads per key, one red.or per lane: 1 sector op / key */
+  SBBF_INSERT_LANE8_TEST = 2, /* as LANE8, but skip lanes whose bit is already set (hot keys) */
+  SBBF_INSERT_THREAD = 3      /* 1 thread per key, 8 red.or per key (baseline variant) */
+};
+
+/* Lookup strategies (sbbf_gpu_set_find_variant). AUTO picks per call. */
+enum {
+  SBBF_FIND_AUTO = 0,
+  SBBF_FIND_GLOBAL = 1, /* one 256-bit LDG per key from L2/HBM */
+  SBBF_FIND_SMEM = 2    /* filter staged into shared memory per CTA (small filters only) */
+};
+
+typedef struct sbbf_gpu sbbf_gpu_t;
+
+/* --- lifetime: SplitBlockFilter(num_buckets, hasher_id, backend)
+ *     filter.hpp:67-71, filter.cpp:148-163 ----------------------------- */
+/* Allocates a zeroed, 256-byte-aligned block array of num_buckets*32 bytes on
+ * `device`. SBBF_EINVAL if num_buckets == 0. */
+int sbbf_gpu_create(uint64_t num_buckets, int device, sbbf_gpu_t** out);
+int sbbf_gpu_destroy(sbbf_gpu_t* f);
+/* Zero every block (stream-ordered). Equivalent to a fresh filter. */
+int sbbf_gpu_clear(sbbf_gpu_t* f, void* stream);
+
+/* --- accessors: filter.hpp:85-94 -------------------------------------- */
+uint64_t sbbf_gpu_num_buckets(const sbbf_gpu_t* f);
+uint64_t sbbf_gpu_size_bytes(const sbbf_gpu_t* f);
+uint32_t sbbf_gpu_hasher_id(const sbbf_gpu_t* f);
+int sbbf_gpu_set_hasher_id(sbbf_gpu_t* f, uint32_t hasher_id);
+int sbbf_gpu_device(const sbbf_gpu_t* f);
+/* Raw device pointer to the block array (num_buckets*32 bytes). */
+void* sbbf_gpu_device_blocks(sbbf_gpu_t* f);
+
+/* --- batched hot path: add_hashes / find_hashes, filter.hpp:81-83,
+ *     filter.cpp:184-207 ---------------------------------------------- */
+int sbbf_gpu_insert_batch(sbbf_gpu_t* f, const uint64_t* d_hashes, uint64_t n, void* stream);
+/* results[k] = 1 if hashes[k] may be present else 0, one byte per key,
+ * identical to the reference's `results` (filter.cpp:91). */
+int sbbf_gpu_find_batch(const sbbf_gpu_t* f, const uint64_t* d_hashes, uint64_t n,
+                        uint8_t* d_results, void* stream);
+/* Packed lookup bitmap: bit (k % 32) of word k / 32 is key k (LSB-first);
+ * bits past n in the last word are 0. d_bits holds ceil(n/32) words. */
+int sbbf_gpu_find_batch_bits(const sbbf_gpu_t* f, const uint64_t* d_hashes, uint64_t n,
+                             uint32_t* d_bits, void* stream);
+
+/* --- host-buffer drop-ins: add_hashes(span) / find_hashes(span, uint8_t*)
+ *     with the caller's host memory, filter.hpp:81-83. Chunked, with the
+ *     host<->device copies overlapped with the kernels on two streams.
+ *     Synchronous on return. ------------------------------------------ */
+int sbbf_gpu_add_hashes_host(sbbf_gpu_t* f, const uint64_t* h_hashes, uint64_t n);
+int sbbf_gpu_find_hashes_host(const sbbf_gpu_t* f, const uint64_t* h_hashes, uint64_t n,
+                              uint8_t* h_results);
+int sbbf_gpu_find_bits_host(const sbbf_gpu_t* f, const uint64_t* h_hashes, uint64_t n,
+                            uint32_t* h_bits);
+
+/* --- single-key ops: add_hash / find_hash, filter.hpp:77-78 (convenience;
+ *     each is one launch + sync — use the batch calls for throughput). - */
+int sbbf_gpu_add_hash(sbbf_gpu_t* f, uint64_t hash);
+/* *found = 0/1 */
+int sbbf_gpu_find_hash(const sbbf_gpu_t* f, uint64_t hash, int* found);
+
+/* --- blocks() / from_blocks(): filter.hpp:74-75,87. Synchronous. ------ */
+/* Copies exactly num_buckets*32 bytes (bytes must equal that). Waits for
+ * all work on the device first. */
+int sbbf_gpu_to_host(const sbbf_gpu_t* f, void* h_dst, uint64_t bytes);
+/* Copies blocks [first_block, first_block + count) (count*32 bytes); for
+ * spot checks of very large filters and for gathering shards. */
+int sbbf_gpu_blocks_to_host(const sbbf_gpu_t* f, uint64_t first_block, uint64_t count,
+                            void* h_dst);
+/* Overwrites the block array from num_buckets*32 host bytes (adopts
+ * existing contents, like from_blocks). */
+int sbbf_gpu_from_host(sbbf_gpu_t* f, const void* h_src, uint64_t bytes);
+
+/* --- free functions on device, for known-answer tests:
+ *     block_index filter.hpp:42, make_mask filter.hpp:47 ---------------- */
+int sbbf_gpu_block_index_batch(const uint64_t* d_hashes, uint64_t n, uint64_t num_buckets,
+                               uint64_t* d_out, void* stream);
+/* d_lanes holds n*8 uint32 (LaneMask per key, lane 0 first). */
+int sbbf_gpu_make_mask_batch(const uint64_t* d_hashes, uint64_t n, uint32_t* d_lanes,
+                             void* stream);
+
+/* --- tuning ----------------------------------------------------------- */
+int sbbf_gpu_set_insert_variant(sbbf_gpu_t* f, int variant);
+int sbbf_gpu_set_find_variant(sbbf_gpu_t* f, int variant);
+/* Variant the AUTO policy would use for a batch of n keys (for reporting). */
+int sbbf_gpu_resolved_insert_variant(const sbbf_gpu_t* f, uint64_t n);
+int sbbf_gpu_resolved_find_variant(const sbbf_gpu_t* f, uint64_t n);
+
+/* --- diagnostics ------------------------------------------------------ */
+const char* sbbf_gpu_last_error(void);
+int sbbf_gpu_abi_version(void);
+/* Number of kernels this library has launched in this process (all
+ * devices); bench.py reports the delta over the timed region. */
+uint64_t sbbf_gpu_launch_count(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBBF_GPU_H */

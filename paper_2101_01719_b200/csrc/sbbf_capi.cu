@@ -1,0 +1,380 @@
+// sbbf_capi.cu — the C ABI declared in include/sbbf_gpu.h.
+//
+// Replaces sbbf::SplitBlockFilter (/root/reference/proj/core/include/sbbf/
+// filter.hpp:65-109) for batched build and probe. The handle owns one
+// cudaMalloc'd block array (256-byte aligned, so every 32-byte block is
+// 32-byte aligned as the reference's alignas(32) Block requires,
+// filter.hpp:25). No exceptions cross this boundary; every failure becomes a
+// negative SBBF_E* code plus a thread-local message.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "sbbf_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  const int code = (e == cudaErrorMemoryAllocation) ? SBBF_ENOMEM
+                   : (e == cudaErrorNoDevice || e == cudaErrorInvalidDevice ||
+                      e == cudaErrorInsufficientDriver)
+                       ? SBBF_ENODEV
+                       : SBBF_ECUDA;
+  return fail(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Makes `dev` current for the scope of an ABI call and restores the caller's.
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+constexpr uint64_t kHostChunk = uint64_t{1} << 22;  // keys per pipelined host chunk (32 MiB)
+
+}  // namespace
+
+struct sbbf_gpu {
+  sbbf::DeviceInfo di;
+  uint64_t nb = 0;
+  uint32_t* d_blocks = nullptr;
+  uint32_t hasher_id = 0;
+  int insert_variant = SBBF_INSERT_AUTO;
+  int find_variant = SBBF_FIND_AUTO;
+  // Host-buffer path resources, created on first use.
+  std::mutex host_mu;
+  bool host_ready = false;
+  cudaStream_t hs[2] = {nullptr, nullptr};
+  uint64_t* d_stage[2] = {nullptr, nullptr};
+  void* d_res[2] = {nullptr, nullptr};
+  uint64_t* d_one = nullptr;  // single-key scratch: [hash, result]
+};
+
+namespace {
+
+int resolve_insert(const sbbf_gpu* f, uint64_t n) {
+  (void)n;
+  if (f->insert_variant != SBBF_INSERT_AUTO) return f->insert_variant;
+  return SBBF_INSERT_LANE8;
+}
+
+bool smem_fits(const sbbf_gpu* f) {
+  const uint64_t bytes = f->nb * 32;
+  return bytes + 1024 <= f->di.smem_optin && bytes <= (200u << 10);
+}
+
+int resolve_find(const sbbf_gpu* f, uint64_t n) {
+  if (f->find_variant == SBBF_FIND_SMEM && smem_fits(f)) return SBBF_FIND_SMEM;
+  if (f->find_variant != SBBF_FIND_AUTO) return SBBF_FIND_GLOBAL;
+  // Staging the filter costs one filter-size copy per CTA; it pays once each
+  // SM probes enough keys to amortise it.
+  if (smem_fits(f) && n >= 64 * f->nb) return SBBF_FIND_SMEM;
+  return SBBF_FIND_GLOBAL;
+}
+
+int ensure_host_path(sbbf_gpu* f) {
+  if (f->host_ready) return SBBF_OK;
+  for (int i = 0; i < 2; ++i) {
+    cudaError_t e = cudaStreamCreateWithFlags(&f->hs[i], cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+    e = cudaMalloc(&f->d_stage[i], kHostChunk * sizeof(uint64_t));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(staging)");
+    e = cudaMalloc(&f->d_res[i], kHostChunk);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(results)");
+  }
+  f->host_ready = true;
+  return SBBF_OK;
+}
+
+// The host-buffer pipeline: chunk c goes H2D -> kernel -> (D2H) on stream
+// c % 2, so chunk c+1's upload overlaps chunk c's kernel and download (the
+// copy engines are full duplex).
+enum class HostOp { kInsert, kFindBytes, kFindBits };
+
+int host_pipeline(sbbf_gpu* f, HostOp op, const uint64_t* h_hashes, uint64_t n, void* h_out) {
+  if (n == 0) return SBBF_OK;
+  if (!h_hashes || (op != HostOp::kInsert && !h_out)) return fail(SBBF_EINVAL, "null host buffer");
+  std::lock_guard<std::mutex> lock(f->host_mu);
+  DeviceGuard g(f->di.device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  int rc = ensure_host_path(f);
+  if (rc != SBBF_OK) return rc;
+  for (uint64_t off = 0, c = 0; off < n; off += kHostChunk, ++c) {
+    const uint64_t m = (n - off < kHostChunk) ? n - off : kHostChunk;
+    const int s = static_cast<int>(c & 1);
+    cudaError_t e = cudaMemcpyAsync(f->d_stage[s], h_hashes + off, m * sizeof(uint64_t),
+                                    cudaMemcpyHostToDevice, f->hs[s]);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(H2D)");
+    if (op == HostOp::kInsert) {
+      e = sbbf::launch_insert(f->di, resolve_insert(f, m), f->d_blocks, f->nb, f->d_stage[s], m,
+                              f->hs[s]);
+      if (e != cudaSuccess) return cuda_fail(e, "insert kernel");
+    } else {
+      const bool bits = op == HostOp::kFindBits;
+      e = sbbf::launch_find(f->di, resolve_find(f, m), f->d_blocks, f->nb, f->d_stage[s], m,
+                            f->d_res[s], bits, f->hs[s]);
+      if (e != cudaSuccess) return cuda_fail(e, "find kernel");
+      // kHostChunk is a multiple of 32, so chunk bitmaps tile the output.
+      void* dst = bits ? static_cast<void*>(static_cast<uint32_t*>(h_out) + off / 32)
+                       : static_cast<void*>(static_cast<uint8_t*>(h_out) + off);
+      const size_t bytes = bits ? ((m + 31) / 32) * sizeof(uint32_t) : m;
+      e = cudaMemcpyAsync(dst, f->d_res[s], bytes, cudaMemcpyDeviceToHost, f->hs[s]);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(D2H)");
+    }
+  }
+  for (int s = 0; s < 2; ++s) {
+    cudaError_t e = cudaStreamSynchronize(f->hs[s]);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  }
+  return SBBF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sbbf_gpu_abi_version(void) { return SBBF_GPU_ABI_VERSION; }
+const char* sbbf_gpu_last_error(void) { return g_err.c_str(); }
+uint64_t sbbf_gpu_launch_count(void) { return sbbf::launch_count(); }
+
+int sbbf_gpu_create(uint64_t num_buckets, int device, sbbf_gpu_t** out) {
+  if (!out) return fail(SBBF_EINVAL, "out is null");
+  *out = nullptr;
+  if (num_buckets == 0) return fail(SBBF_EINVAL, "SplitBlockFilter needs at least one bucket");
+  if (num_buckets > (~uint64_t{0}) / 32) return fail(SBBF_EINVAL, "num_buckets overflows size");
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    return fail(SBBF_ENODEV, std::string("no CUDA device: ") +
+                                 (e == cudaSuccess ? "count is 0" : cudaGetErrorString(e)));
+  }
+  if (device < 0 || device >= count) return fail(SBBF_ENODEV, "bad device ordinal");
+  DeviceGuard g(device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  sbbf_gpu* f = new (std::nothrow) sbbf_gpu;
+  if (!f) return fail(SBBF_ENOMEM, "host allocation failed");
+  f->nb = num_buckets;
+  f->di.device = device;
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) == cudaSuccess) f->di.sms = v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) == cudaSuccess)
+    f->di.smem_optin = static_cast<size_t>(v);
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, device) == cudaSuccess)
+    f->di.l2_bytes = static_cast<size_t>(v);
+  e = cudaMalloc(&f->d_blocks, num_buckets * 32);
+  if (e == cudaSuccess) e = cudaMemset(f->d_blocks, 0, num_buckets * 32);
+  if (e == cudaSuccess) e = cudaMalloc(&f->d_one, 2 * sizeof(uint64_t));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    const int rc = cuda_fail(e, "allocating the block array");
+    sbbf_gpu_destroy(f);
+    return rc;
+  }
+  *out = f;
+  return SBBF_OK;
+}
+
+int sbbf_gpu_destroy(sbbf_gpu_t* f) {
+  if (!f) return SBBF_OK;
+  {
+    DeviceGuard g(f->di.device);
+    if (f->d_blocks) cudaDeviceSynchronize();
+    cudaFree(f->d_blocks);
+    cudaFree(f->d_one);
+    for (int i = 0; i < 2; ++i) {
+      if (f->hs[i]) cudaStreamDestroy(f->hs[i]);
+      cudaFree(f->d_stage[i]);
+      cudaFree(f->d_res[i]);
+    }
+  }
+  delete f;
+  return SBBF_OK;
+}
+
+int sbbf_gpu_clear(sbbf_gpu_t* f, void* stream) {
+  if (!f) return fail(SBBF_EINVAL, "null filter");
+  DeviceGuard g(f->di.device);
+  cudaError_t e = cudaMemsetAsync(f->d_blocks, 0, f->nb * 32, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "cudaMemsetAsync");
+}
+
+uint64_t sbbf_gpu_num_buckets(const sbbf_gpu_t* f) { return f ? f->nb : 0; }
+uint64_t sbbf_gpu_size_bytes(const sbbf_gpu_t* f) { return f ? f->nb * 32 : 0; }
+uint32_t sbbf_gpu_hasher_id(const sbbf_gpu_t* f) { return f ? f->hasher_id : 0; }
+int sbbf_gpu_device(const sbbf_gpu_t* f) { return f ? f->di.device : -1; }
+void* sbbf_gpu_device_blocks(sbbf_gpu_t* f) { return f ? f->d_blocks : nullptr; }
+
+int sbbf_gpu_set_hasher_id(sbbf_gpu_t* f, uint32_t hasher_id) {
+  if (!f) return fail(SBBF_EINVAL, "null filter");
+  f->hasher_id = hasher_id;
+  return SBBF_OK;
+}
+
+int sbbf_gpu_insert_batch(sbbf_gpu_t* f, const uint64_t* d_hashes, uint64_t n, void* stream) {
+  if (!f) return fail(SBBF_EINVAL, "null filter");
+  if (n == 0) return SBBF_OK;  // empty batch is a no-op (filter_test.cpp:169-175)
+  if (!d_hashes) return fail(SBBF_EINVAL, "null hashes");
+  DeviceGuard g(f->di.device);
+  cudaError_t e = sbbf::launch_insert(f->di, resolve_insert(f, n), f->d_blocks, f->nb, d_hashes, n,
+                                      static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "insert kernel launch");
+}
+
+static int find_common(const sbbf_gpu_t* f, const uint64_t* d_hashes, uint64_t n, void* d_out,
+                       bool bits, void* stream) {
+  if (!f) return fail(SBBF_EINVAL, "null filter");
+  if (n == 0) return SBBF_OK;
+  if (!d_hashes || !d_out) return fail(SBBF_EINVAL, "null buffer");
+  DeviceGuard g(f->di.device);
+  cudaError_t e = sbbf::launch_find(f->di, resolve_find(f, n), f->d_blocks, f->nb, d_hashes, n,
+                                    d_out, bits, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "find kernel launch");
+}
+
+int sbbf_gpu_find_batch(const sbbf_gpu_t* f, const uint64_t* d_hashes, uint64_t n,
+                        uint8_t* d_results, void* stream) {
+  return find_common(f, d_hashes, n, d_results, false, stream);
+}
+
+int sbbf_gpu_find_batch_bits(const sbbf_gpu_t* f, const uint64_t* d_hashes, uint64_t n,
+                             uint32_t* d_bits, void* stream) {
+  return find_common(f, d_hashes, n, d_bits, true, stream);
+}
+
+int sbbf_gpu_add_hashes_host(sbbf_gpu_t* f, const uint64_t* h_hashes, uint64_t n) {
+  if (!f) return fail(SBBF_EINVAL, "null filter");
+  return host_pipeline(f, HostOp::kInsert, h_hashes, n, nullptr);
+}
+
+int sbbf_gpu_find_hashes_host(const sbbf_gpu_t* f, const uint64_t* h_hashes, uint64_t n,
+                              uint8_t* h_results) {
+  if (!f) return fail(SBBF_EINVAL, "null filter");
+  return host_pipeline(const_cast<sbbf_gpu*>(f), HostOp::kFindBytes, h_hashes, n, h_results);
+}
+
+int sbbf_gpu_find_bits_host(const sbbf_gpu_t* f, const uint64_t* h_hashes, uint64_t n,
+                            uint32_t* h_bits) {
+  if (!f) return fail(SBBF_EINVAL, "null filter");
+  return host_pipeline(const_cast<sbbf_gpu*>(f), HostOp::kFindBits, h_hashes, n, h_bits);
+}
+
+int sbbf_gpu_add_hash(sbbf_gpu_t* f, uint64_t hash) {
+  if (!f) return fail(SBBF_EINVAL, "null filter");
+  std::lock_guard<std::mutex> lock(f->host_mu);
+  DeviceGuard g(f->di.device);
+  cudaError_t e = cudaMemcpy(f->d_one, &hash, sizeof(hash), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = sbbf::launch_insert(f->di, SBBF_INSERT_LANE8, f->d_blocks, f->nb, f->d_one, 1, nullptr);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "add_hash");
+}
+
+int sbbf_gpu_find_hash(const sbbf_gpu_t* f, uint64_t hash, int* found) {
+  if (!f || !found) return fail(SBBF_EINVAL, "null argument");
+  sbbf_gpu* m = const_cast<sbbf_gpu*>(f);
+  std::lock_guard<std::mutex> lock(m->host_mu);
+  DeviceGuard g(f->di.device);
+  uint8_t r = 0;
+  cudaError_t e = cudaMemcpy(m->d_one, &hash, sizeof(hash), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = sbbf::launch_find(f->di, SBBF_FIND_GLOBAL, f->d_blocks, f->nb, m->d_one, 1, m->d_one + 1,
+                          false, nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(&r, m->d_one + 1, 1, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "find_hash");
+  *found = r ? 1 : 0;
+  return SBBF_OK;
+}
+
+int sbbf_gpu_to_host(const sbbf_gpu_t* f, void* h_dst, uint64_t bytes) {
+  if (!f || !h_dst) return fail(SBBF_EINVAL, "null argument");
+  if (bytes != f->nb * 32) return fail(SBBF_EINVAL, "bytes must equal num_buckets * 32");
+  DeviceGuard g(f->di.device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(h_dst, f->d_blocks, bytes, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "to_host");
+}
+
+int sbbf_gpu_blocks_to_host(const sbbf_gpu_t* f, uint64_t first_block, uint64_t count,
+                            void* h_dst) {
+  if (!f || (count && !h_dst)) return fail(SBBF_EINVAL, "null argument");
+  if (first_block > f->nb || count > f->nb - first_block)
+    return fail(SBBF_EINVAL, "block range out of bounds");
+  if (count == 0) return SBBF_OK;
+  DeviceGuard g(f->di.device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess)
+    e = cudaMemcpy(h_dst, f->d_blocks + first_block * 8, count * 32, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "blocks_to_host");
+}
+
+int sbbf_gpu_from_host(sbbf_gpu_t* f, const void* h_src, uint64_t bytes) {
+  if (!f || !h_src) return fail(SBBF_EINVAL, "null argument");
+  if (bytes != f->nb * 32) return fail(SBBF_EINVAL, "bytes must equal num_buckets * 32");
+  DeviceGuard g(f->di.device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(f->d_blocks, h_src, bytes, cudaMemcpyHostToDevice);
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "from_host");
+}
+
+int sbbf_gpu_block_index_batch(const uint64_t* d_hashes, uint64_t n, uint64_t num_buckets,
+                               uint64_t* d_out, void* stream) {
+  if (n == 0) return SBBF_OK;
+  if (!d_hashes || !d_out) return fail(SBBF_EINVAL, "null buffer");
+  cudaError_t e = sbbf::launch_block_index(d_hashes, n, num_buckets, d_out,
+                                           static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "block_index kernel");
+}
+
+int sbbf_gpu_make_mask_batch(const uint64_t* d_hashes, uint64_t n, uint32_t* d_lanes,
+                             void* stream) {
+  if (n == 0) return SBBF_OK;
+  if (!d_hashes || !d_lanes) return fail(SBBF_EINVAL, "null buffer");
+  cudaError_t e = sbbf::launch_make_mask(d_hashes, n, d_lanes, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "make_mask kernel");
+}
+
+int sbbf_gpu_set_insert_variant(sbbf_gpu_t* f, int variant) {
+  if (!f) return fail(SBBF_EINVAL, "null filter");
+  if (variant < SBBF_INSERT_AUTO || variant > SBBF_INSERT_THREAD)
+    return fail(SBBF_EINVAL, "unknown insert variant");
+  f->insert_variant = variant;
+  return SBBF_OK;
+}
+
+int sbbf_gpu_set_find_variant(sbbf_gpu_t* f, int variant) {
+  if (!f) return fail(SBBF_EINVAL, "null filter");
+  if (variant < SBBF_FIND_AUTO || variant > SBBF_FIND_SMEM)
+    return fail(SBBF_EINVAL, "unknown find variant");
+  if (variant == SBBF_FIND_SMEM && !smem_fits(f))
+    return fail(SBBF_EINVAL, "filter too large for the shared-memory path");
+  f->find_variant = variant;
+  return SBBF_OK;
+}
+
+int sbbf_gpu_resolved_insert_variant(const sbbf_gpu_t* f, uint64_t n) {
+  return f ? resolve_insert(f, n) : SBBF_EINVAL;
+}
+
+int sbbf_gpu_resolved_find_variant(const sbbf_gpu_t* f, uint64_t n) {
+  return f ? resolve_find(f, n) : SBBF_EINVAL;
+}
+
+}  // extern "C"

@@ -1,0 +1,37 @@
+// sbbf_internal.h — launchers shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sbbf_gpu.h"
+#include "sbbf_workload.h"
+
+namespace sbbf {
+
+struct DeviceInfo {
+  int device = 0;
+  int sms = 148;
+  size_t smem_optin = 227 * 1024;  // cudaDevAttrMaxSharedMemoryPerBlockOptin
+  size_t l2_bytes = 126u << 20;
+};
+
+constexpr int kInsertLane8 = SBBF_INSERT_LANE8;
+constexpr int kInsertLane8Test = SBBF_INSERT_LANE8_TEST;
+constexpr int kInsertThread = SBBF_INSERT_THREAD;
+constexpr int kFindGlobal = SBBF_FIND_GLOBAL;
+constexpr int kFindSmem = SBBF_FIND_SMEM;
+
+uint64_t launch_count();
+void note_launch();
+
+cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, uint64_t nb,
+                          const uint64_t* hashes, uint64_t n, cudaStream_t s);
+cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* blocks, uint64_t nb,
+                        const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s);
+cudaError_t launch_block_index(const uint64_t* h, uint64_t n, uint64_t nb, uint64_t* out,
+                               cudaStream_t s);
+cudaError_t launch_make_mask(const uint64_t* h, uint64_t n, uint32_t* out, cudaStream_t s);
+
+}  // namespace sbbf

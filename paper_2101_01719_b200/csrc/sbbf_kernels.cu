@@ -1,0 +1,348 @@
+// sbbf_kernels.cu — hand-written sm_100a kernels for batched SBBF insert/lookup.
+//
+// Reference hot loops being replaced (paths relative to /root/reference/proj/):
+//   add_many_avx2  core/src/filter.cpp:79-84   (per key: load 32 B, OR mask, store)
+//   find_many_avx2 core/src/filter.cpp:86-93   (per key: load 32 B, vptest, 1 byte out)
+//
+// Design (DESIGN.md §3 has the roofline for each):
+//   * insert_lane8   — 8 threads per key, one `red.global.or.b32` per lane. One
+//     warp instruction covers 4 keys = 4 sectors, so the L2 sees one 32-byte
+//     atomic sector op per key instead of eight word ops (insert_thread).
+//     Atomic OR is exact: OR is commutative/associative/idempotent, so any
+//     interleaving yields the reference's bytes.
+//   * insert_lane8_test — loads the lane first and only issues the red when
+//     the bit is clear (bits are monotone): cuts atomics for
+//     duplicate/hot keys (config 4's Zipf duplicates).
+//   * find_global    — one thread per key, U keys in flight per thread, one
+//     256-bit LDG per key (LDG.E.ENL2.256), hashes streamed evict-first,
+//     results either 0/1 bytes (drop-in) or a __ballot_sync-packed bitmap.
+//   * find_smem      — small filters (<= ~200 KiB, e.g. config 1) are staged
+//     into shared memory per CTA with cp.async.bulk (TMA bulk copy, mbarrier
+//     completion) and probed from smem with two 128-bit LDS per key.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "sbbf_device.cuh"
+#include "sbbf_internal.h"
+
+namespace sbbf {
+namespace {
+
+using dev::Block8;
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// insert
+// ---------------------------------------------------------------------------
+// __launch_bounds__ minimum-blocks hints below are load-bearing: without them
+// ptxas minimises registers by sinking each block load next to its use, which
+// serialises the U independent sector reads (checked in SASS).
+template <bool kTest>
+__global__ void __launch_bounds__(kThreads, 4) insert_lane8_kernel(uint32_t* __restrict__ blocks,
+                                                                uint64_t num_buckets,
+                                                                const uint64_t* __restrict__ hashes,
+                                                                uint64_t n) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane >> 3;       // which of the 4 keys of a round
+  const int word = lane & 7;       // which lane of the block this thread owns
+  const uint32_t seed = dev::lane_seed_rt(word);
+  const uint64_t pol = dev::policy_evict_first();
+  const uint64_t keep = dev::policy_evict_last();
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
+  const uint64_t ntiles = (n + 31) >> 5;
+  for (uint64_t t = warp; t < ntiles; t += nwarps) {
+    const uint64_t base = t << 5;
+    const uint64_t idx = base + lane;
+    const uint64_t h = idx < n ? dev::ld_stream_u64(hashes + idx, pol) : 0;
+    const uint32_t valid = __ballot_sync(0xffffffffu, idx < n);
+    uint32_t* ptr[8];
+    uint32_t bit[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int k = r * 4 + sub;
+      const uint64_t hk = __shfl_sync(0xffffffffu, h, k);
+      ptr[r] = blocks + dev::block_index(hk, num_buckets) * 8 + word;
+      bit[r] = ((valid >> k) & 1u) ? dev::lane_bit(static_cast<uint32_t>(hk), seed) : 0u;
+    }
+    if constexpr (kTest) {
+      uint32_t cur[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) cur[r] = bit[r] ? dev::ld_lane(ptr[r], keep) : ~0u;
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (bit[r] & ~cur[r]) dev::red_or(ptr[r], bit[r], keep);
+    } else {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (bit[r]) dev::red_or(ptr[r], bit[r], keep);
+    }
+  }
+}
+
+// Baseline variant: one thread per key, eight word atomics per key.
+__global__ void __launch_bounds__(kThreads) insert_thread_kernel(uint32_t* __restrict__ blocks,
+                                                                 uint64_t num_buckets,
+                                                                 const uint64_t* __restrict__ hashes,
+                                                                 uint64_t n) {
+  const uint64_t pol = dev::policy_evict_first();
+  const uint64_t keep = dev::policy_evict_last();
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n; i += stride) {
+    const uint64_t h = dev::ld_stream_u64(hashes + i, pol);
+    uint32_t* b = blocks + dev::block_index(h, num_buckets) * 8;
+    const uint32_t low = static_cast<uint32_t>(h);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) dev::red_or(b + w, dev::lane_bit(low, dev::lane_seed(w)), keep);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// lookup from L2/HBM
+// ---------------------------------------------------------------------------
+// Warp tile = 32*U consecutive keys; lane l owns keys base + u*32 + l. All U
+// hash loads, then all U block loads are issued before any is consumed, so
+// each thread keeps U independent 32-byte sector reads in flight.
+template <int U, bool kBits>
+constexpr int find_min_blocks() { return U >= 8 ? (kBits ? 2 : 4) : 5; }
+
+template <int U, bool kBits>
+__global__ void __launch_bounds__(kThreads, find_min_blocks<U, kBits>()) find_global_kernel(const uint32_t* __restrict__ blocks,
+                                                               uint64_t num_buckets,
+                                                               const uint64_t* __restrict__ hashes,
+                                                               uint64_t n, void* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = dev::policy_evict_first();
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
+  constexpr uint64_t kTile = 32 * U;
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  for (uint64_t t = warp; t < ntiles; t += nwarps) {
+    const uint64_t base = t * kTile;
+    uint64_t h[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t idx = base + u * 32 + lane;
+      h[u] = idx < n ? dev::ld_stream_u64(hashes + idx, pol) : 0;
+    }
+    Block8 b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) dev::ld_block_nc(blocks + dev::block_index(h[u], num_buckets) * 8, b[u]);
+    uint32_t mine = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t idx = base + u * 32 + lane;
+      const bool hit = dev::block_contains(b[u], h[u]) && idx < n;
+      if constexpr (kBits) {
+        const uint32_t word = __ballot_sync(0xffffffffu, hit);
+        if (lane == u) mine = word;
+      } else {
+        if (idx < n) dev::st_stream_u8(static_cast<uint8_t*>(out) + idx, hit ? 1u : 0u);
+      }
+    }
+    if constexpr (kBits) {
+      const uint64_t nwords = (n + 31) >> 5;
+      const uint64_t widx = (base >> 5) + lane;
+      if (lane < U && widx < nwords) dev::st_stream_u32(static_cast<uint32_t*>(out) + widx, mine);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// lookup from shared memory (small filters)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <bool kBits>
+__global__ void __launch_bounds__(1024, 1) find_smem_kernel(const uint32_t* __restrict__ blocks,
+                                                         uint64_t num_buckets,
+                                                         const uint64_t* __restrict__ hashes,
+                                                         uint64_t n, void* __restrict__ out) {
+  extern __shared__ __align__(128) uint4 sfilter[];
+  __shared__ __align__(8) uint64_t mbar;
+  const uint32_t bytes = static_cast<uint32_t>(num_buckets * 32);
+  const uint32_t bar = smem_u32(&mbar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    constexpr uint32_t kChunk = 16384;
+    for (uint32_t off = 0; off < bytes; off += kChunk) {
+      const uint32_t sz = bytes - off < kChunk ? bytes - off : kChunk;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(reinterpret_cast<const char*>(sfilter) + off)),
+          "l"(reinterpret_cast<const char*>(blocks) + off), "r"(sz), "r"(bar)
+          : "memory");
+    }
+  }
+  // Wait for the bulk copy (phase 0).
+  {
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
+    }
+  }
+
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = dev::policy_evict_first();
+  constexpr int U = 4;
+  constexpr uint64_t kTile = 32 * U;
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  for (uint64_t t = warp; t < ntiles; t += nwarps) {
+    const uint64_t base = t * kTile;
+    uint64_t h[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t idx = base + u * 32 + lane;
+      h[u] = idx < n ? dev::ld_stream_u64(hashes + idx, pol) : 0;
+    }
+    uint32_t mine = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t idx = base + u * 32 + lane;
+      const uint4* p = sfilter + dev::block_index(h[u], num_buckets) * 2;
+      const uint4 lo = p[0], hi = p[1];
+      Block8 b{{lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w}};
+      const bool hit = dev::block_contains(b, h[u]) && idx < n;
+      if constexpr (kBits) {
+        const uint32_t word = __ballot_sync(0xffffffffu, hit);
+        if (lane == u) mine = word;
+      } else {
+        if (idx < n) dev::st_stream_u8(static_cast<uint8_t*>(out) + idx, hit ? 1u : 0u);
+      }
+    }
+    if constexpr (kBits) {
+      const uint64_t nwords = (n + 31) >> 5;
+      const uint64_t widx = (base >> 5) + lane;
+      if (lane < U && widx < nwords) dev::st_stream_u32(static_cast<uint32_t*>(out) + widx, mine);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// free functions (known-answer tests)
+// ---------------------------------------------------------------------------
+__global__ void block_index_kernel(const uint64_t* __restrict__ h, uint64_t n, uint64_t nb,
+                                   uint64_t* __restrict__ out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = dev::block_index(h[i], nb);
+}
+
+__global__ void make_mask_kernel(const uint64_t* __restrict__ h, uint64_t n,
+                                 uint32_t* __restrict__ out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t low = static_cast<uint32_t>(h[i]);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) out[i * 8 + w] = dev::lane_bit(low, dev::lane_seed(w));
+  }
+}
+
+std::atomic<uint64_t> g_launches{0};
+
+// Blocks per SM the hardware can co-schedule for a kernel (cached per kernel).
+template <typename K>
+int resident_blocks(K kernel, int threads, size_t smem) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem) != cudaSuccess || b < 1)
+    b = 1;
+  return b;
+}
+
+uint64_t grid_for(uint64_t work_items, uint64_t items_per_block, int sms, int per_sm) {
+  const uint64_t want = (work_items + items_per_block - 1) / items_per_block;
+  const uint64_t cap = static_cast<uint64_t>(sms) * per_sm;
+  uint64_t g = want < cap ? want : cap;
+  return g < 1 ? 1 : g;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers (sbbf_internal.h)
+// ---------------------------------------------------------------------------
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, uint64_t nb,
+                          const uint64_t* hashes, uint64_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  note_launch();
+  if (variant == kInsertThread) {
+    static const int occ = resident_blocks(insert_thread_kernel, kThreads, 0);
+    const uint64_t g = grid_for(n, kThreads * 4, di.sms, occ);
+    insert_thread_kernel<<<static_cast<unsigned>(g), kThreads, 0, s>>>(blocks, nb, hashes, n);
+  } else if (variant == kInsertLane8Test) {
+    static const int occ = resident_blocks(insert_lane8_kernel<true>, kThreads, 0);
+    const uint64_t g = grid_for(n, kThreads * 2, di.sms, occ);
+    insert_lane8_kernel<true><<<static_cast<unsigned>(g), kThreads, 0, s>>>(blocks, nb, hashes, n);
+  } else {
+    static const int occ = resident_blocks(insert_lane8_kernel<false>, kThreads, 0);
+    const uint64_t g = grid_for(n, kThreads * 2, di.sms, occ);
+    insert_lane8_kernel<false><<<static_cast<unsigned>(g), kThreads, 0, s>>>(blocks, nb, hashes, n);
+  }
+  return cudaGetLastError();
+}
+
+constexpr int kFindU = 8;
+
+cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* blocks, uint64_t nb,
+                        const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  note_launch();
+  if (variant == kFindSmem) {
+    const size_t smem = static_cast<size_t>(nb) * 32;
+    auto kern = bits ? find_smem_kernel<true> : find_smem_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const int threads = 1024;
+    const uint64_t g = grid_for(n, threads * 8, di.sms, 1);
+    kern<<<static_cast<unsigned>(g), threads, smem, s>>>(blocks, nb, hashes, n, out);
+  } else {
+    static const int occ_b = resident_blocks(find_global_kernel<kFindU, true>, kThreads, 0);
+    static const int occ_y = resident_blocks(find_global_kernel<kFindU, false>, kThreads, 0);
+    const uint64_t g = grid_for(n, kThreads * kFindU, di.sms, bits ? occ_b : occ_y);
+    if (bits)
+      find_global_kernel<kFindU, true><<<static_cast<unsigned>(g), kThreads, 0, s>>>(blocks, nb, hashes, n, out);
+    else
+      find_global_kernel<kFindU, false><<<static_cast<unsigned>(g), kThreads, 0, s>>>(blocks, nb, hashes, n, out);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_index(const uint64_t* h, uint64_t n, uint64_t nb, uint64_t* out,
+                               cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  note_launch();
+  const uint64_t g = grid_for(n, 256, 148, 8);
+  block_index_kernel<<<static_cast<unsigned>(g), 256, 0, s>>>(h, n, nb, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_make_mask(const uint64_t* h, uint64_t n, uint32_t* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  note_launch();
+  const uint64_t g = grid_for(n, 256, 148, 8);
+  make_mask_kernel<<<static_cast<unsigned>(g), 256, 0, s>>>(h, n, out);
+  return cudaGetLastError();
+}
+
+}  // namespace sbbf

@@ -1,0 +1,167 @@
+"""Generate tests/golden/ fixtures by running the REFERENCE itself.
+
+Runs the unmodified reference core (oracle/_ref/libsbbf_ref.so, compiled from
+/root/reference/proj/core/src by oracle/Makefile) on seeded inputs and writes
+its outputs as small fixtures. Only runnable where /root/reference exists;
+the committed fixtures travel to the GPU box, the reference does not.
+
+    python tests/golden/make_golden.py            # configs 1-3 + unit cases
+    python tests/golden/make_golden.py --cfg4     # also config 4 (~minutes)
+
+Inputs: the reference tests' own std::mt19937_64 draws (seeds from
+filter_test.cpp / persist_test.cpp / acceptance.cpp) and the BASELINE.json
+config streams (paper_2101_01719_b200.workload, restated on the host by the
+oracle).
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from oracle import Oracle, Reference  # noqa: E402
+from paper_2101_01719_b200 import workload as W  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def image_crc(img: bytes) -> int:
+    return int.from_bytes(img[-4:], "little")
+
+
+def unit_cases(ref: Reference, orc: Oracle) -> dict:
+    g: dict = {}
+    # block_index vs the big-integer oracle (filter_test.cpp:35-49 inputs).
+    buckets = [1, 2, 3, 7, 4096, 1000, 999983, 1 << 20, (1 << 40) + 17, (1 << 33) + 9]
+    hs = ref.mt19937_64(0x5EED0001, 2000)
+    g["block_index"] = {
+        "hash_seed": 0x5EED0001, "n": 2000, "buckets": buckets,
+        "expected": [[ref.block_index(int(h), b) for b in buckets] for h in hs],
+    }
+    # make_mask (filter_test.cpp:102-114 inputs)
+    hs = ref.mt19937_64(0x5EED0003, 2000)
+    g["make_mask"] = {"hash_seed": 0x5EED0003, "n": 2000,
+                      "expected": [ref.make_mask(int(h)) for h in hs]}
+    # Filters built by the reference: (buckets, adds, insert seed, probe count)
+    cases = [
+        ("one_bucket_24", 1, 24, 0x5EED000A, 4096),
+        ("add_then_find_57", 57, 1000, 0x5EED0004, 1000),
+        ("bulk_97", 97, 1000, 0x5EED0005, 1000),
+        ("monotone_11", 11, 200, 0x5EED0006, 500),
+        ("backend_identity_4096", 4096, 100_000, 0x5EED0007, 10_000),
+        ("instrumented_1000", 1000, 5000, 0x5EED0008, 5000),
+        ("persist_512", 512, 20_000, 0xABCD01, 5000),
+        ("nonpow2_7919", 7919, 200_000, 0xACC0002, 100_000),
+        ("nonpow2_999983", 999_983, 3_000_000, 0xACC0009, 1_000_000),
+        ("acceptance_7", 7, 1_000_000, 0xACC0001, 10_000),
+    ]
+    fl = []
+    for name, nb, adds, seed, nprobe in cases:
+        draws = ref.mt19937_64(seed, adds + nprobe)
+        ins = draws[:adds]
+        # probes: half inserted keys, half fresh draws
+        half = min(adds, nprobe // 2)
+        probes = np.concatenate([ins[:half], draws[adds: adds + nprobe - half]])
+        f = ref.filter(nb)
+        f.add_hashes(ins)
+        res = f.find_hashes(probes)
+        img = f.serialize()
+        entry = {"name": name, "buckets": nb, "adds": adds, "seed": seed, "probes": int(probes.size),
+                 "image_crc": image_crc(img), "popcount": orc.popcount(f.blocks()),
+                 "blocks_sha256": sha(f.blocks()), "results_sha256": sha(res),
+                 "hits": int(res.sum())}
+        if nb <= 128:
+            entry["image_hex"] = img.hex()
+        fl.append(entry)
+    g["filters"] = fl
+    return g
+
+
+def config_golden(ref: Reference, orc: Oracle, cid: int, threads: int) -> dict:
+    cfg = W.CONFIGS[cid]
+    t0 = time.time()
+    table = W.zipf_cdf_table(cfg.inserts.zipf_s, cfg.inserts.zipf_n) if cfg.inserts.dup_num else None
+    st = orc.stream(cfg.inserts, table)
+    f = ref.filter(cfg.num_buckets)
+    chunk = 1 << 26
+    N = cfg.inserts.n
+    first_ins = None
+    for s in range(0, N, chunk):
+        a = orc.gen_inserts(st, s, min(chunk, N - s))
+        if first_ins is None:
+            first_ins = [int(x) for x in a[:4]]
+        f.add_hashes(a)
+    img = f.serialize()
+    blocks = f.blocks()
+    L = cfg.lookups.n
+    hits = 0
+    member_hits = 0
+    nonmember_hits = 0
+    crc_state = 0
+    first_look = None
+    res_crcs = []
+    for s in range(0, L, chunk):
+        m = min(chunk, L - s)
+        q = orc.gen_lookups(st, cfg.lookups, N, s, m)
+        if first_look is None:
+            first_look = [int(x) for x in q[:4]]
+        r = f.find_hashes(q, threads)
+        hits += int(r.sum())
+        # member mask for this chunk
+        j = np.arange(s, s + m, dtype=np.uint64)
+        if cfg.lookups.members_first:
+            mem = j < N
+        else:
+            p, qq = cfg.lookups.p, cfg.lookups.q
+            mem = ((j + 1) * p // qq) > (j * p // qq)
+        member_hits += int(r[mem].sum())
+        nonmember_hits += int(r[~mem].sum())
+        res_crcs.append(orc.crc32(np.packbits(r, bitorder="little").tobytes()))
+    n_members = W.member_count(cfg.lookups, N, 0, L)
+    out = {
+        "config": cid, "num_buckets": cfg.num_buckets, "inserts": N, "lookups": L,
+        "first_inserts": first_ins, "first_lookups": first_look,
+        "image_crc": image_crc(img), "popcount": orc.popcount(blocks),
+        "members": n_members, "member_hits": member_hits,
+        "nonmembers": L - n_members, "false_positives": nonmember_hits,
+        "lookup_bitmap_chunk_crcs": res_crcs, "chunk_keys": chunk,
+        "seconds": round(time.time() - t0, 1),
+    }
+    print(f"cfg{cid}: crc={out['image_crc']:#x} fp={nonmember_hits}/{L - n_members} "
+          f"members={member_hits}/{n_members} ({out['seconds']} s)", flush=True)
+    return out
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cfg4", action="store_true")
+    ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
+    args = ap.parse_args()
+    ref, orc = Reference(), Oracle()
+    with open(os.path.join(OUT, "unit_cases.json"), "w") as fh:
+        json.dump(unit_cases(ref, orc), fh)
+    cfgs = {}
+    path = os.path.join(OUT, "configs.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            cfgs = json.load(fh)
+    for cid in (1, 2, 3) + ((4,) if args.cfg4 else ()):
+        cfgs[str(cid)] = config_golden(ref, orc, cid, args.threads)
+    with open(path, "w") as fh:
+        json.dump(cfgs, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()

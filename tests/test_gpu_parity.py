@@ -1,0 +1,291 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle and the
+reference's golden fixtures. Bit-exact everywhere (integer/byte work).
+
+Small cases compare whole filters and result arrays with the oracle on the
+same inputs; full-size BASELINE configs compare the reference's image CRC,
+set-bit count, false-positive count and per-chunk lookup-bitmap CRCs
+(tests/golden/configs.json), plus size-independent properties (no false
+negatives, idempotence, order independence).
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import bits_to_bytes  # noqa: E402
+from paper_2101_01719_b200 import SplitBlockFilter, _lib  # noqa: E402
+from paper_2101_01719_b200 import block_index_batch, make_mask_batch  # noqa: E402
+from paper_2101_01719_b200 import workload as W  # noqa: E402
+
+from .test_oracle import BLOCK_INDEX_KAT, MASK_KAT  # noqa: E402
+
+INSERT_VARIANTS = [_lib.INSERT_LANE8, _lib.INSERT_LANE8_TEST, _lib.INSERT_THREAD]
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def dev(a, cuda):
+    return torch.from_numpy(np.ascontiguousarray(a, np.uint64).view(np.int64)).to(cuda)
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+# --- known answers on device ------------------------------------------------------
+def test_block_index_kat_on_device(cuda):
+    for h, nb, want in BLOCK_INDEX_KAT:
+        got = block_index_batch(dev([h], cuda), nb)
+        assert int(got.cpu().numpy().view(np.uint64)[0]) == want
+
+
+def test_make_mask_kat_on_device(cuda, oracle):
+    hs = [0, 1, 0xFFFFFFFF00000000, 0xDEADBEEF, 0x12345678DEADBEEF] + list(MASK_KAT)
+    got = u32(make_mask_batch(dev(hs, cuda))).reshape(-1, 8)
+    for h, row in zip(hs, got):
+        assert row.tolist() == oracle.make_mask(h)
+    for h, lanes in MASK_KAT.items():
+        assert u32(make_mask_batch(dev([h], cuda)))[0].tolist() == lanes
+
+
+def test_golden_block_index_and_mask_on_device(cuda, oracle, golden_units):
+    g = golden_units["block_index"]
+    hs = oracle.mt19937_64(g["hash_seed"], g["n"])
+    want = np.array(g["expected"], dtype=np.uint64)
+    for j, nb in enumerate(g["buckets"]):
+        got = block_index_batch(dev(hs, cuda), nb).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, want[:, j]), nb
+    g = golden_units["make_mask"]
+    hs = oracle.mt19937_64(g["hash_seed"], g["n"])
+    got = u32(make_mask_batch(dev(hs, cuda))).reshape(-1, 8)
+    assert np.array_equal(got, np.array(g["expected"], dtype=np.uint32))
+
+
+# --- filters built by the reference (golden) -------------------------------------
+@pytest.mark.parametrize("variant", INSERT_VARIANTS)
+@pytest.mark.parametrize("idx", range(10))
+def test_golden_filters_on_device(cuda, oracle, golden_units, idx, variant):
+    c = golden_units["filters"][idx]
+    draws = oracle.mt19937_64(c["seed"], c["adds"] + c["probes"])
+    ins = draws[: c["adds"]]
+    half = min(c["adds"], c["probes"] // 2)
+    probes = np.concatenate([ins[:half], draws[c["adds"]: c["adds"] + c["probes"] - half]])
+    f = SplitBlockFilter(c["buckets"])
+    f.set_insert_variant(variant)
+    f.add_hashes(dev(ins, cuda))
+    blocks = f.blocks()
+    assert sha(blocks) == c["blocks_sha256"]
+    assert oracle.image_crc(blocks) == c["image_crc"]
+    if "image_hex" in c:
+        assert oracle.serialize(blocks).hex() == c["image_hex"]
+    res = f.find_hashes(dev(probes, cuda)).cpu().numpy()
+    assert sha(res) == c["results_sha256"] and int(res.sum()) == c["hits"]
+    bits = u32(f.find_hashes_bits(dev(probes, cuda)))
+    assert np.array_equal(bits_to_bytes(bits, probes.size), res)
+
+
+@pytest.mark.parametrize("nb", [1, 2, 7, 57, 1000, 4096, 6400, 7919, 32768, 999983])
+@pytest.mark.parametrize("n", [0, 1, 31, 32, 33, 255, 257, 1000, 100_003])
+def test_random_parity(cuda, oracle, nb, n):
+    rng = np.random.default_rng(nb * 1000 + n)
+    hs = rng.integers(0, 2**64, size=n, dtype=np.uint64)
+    probes = np.concatenate([hs[: n // 2], rng.integers(0, 2**64, size=n + 7, dtype=np.uint64)])
+    want = oracle.build(nb, hs)
+    for v in INSERT_VARIANTS:
+        f = SplitBlockFilter(nb)
+        f.set_insert_variant(v)
+        f.add_hashes(dev(hs, cuda))
+        assert np.array_equal(f.blocks(), want), v
+    want_res = oracle.find_hashes(want, probes)
+    for fv in (_lib.FIND_GLOBAL, _lib.FIND_SMEM):
+        if fv == _lib.FIND_SMEM and nb * 32 > 200 * 1024:
+            continue
+        f.set_find_variant(fv)
+        assert np.array_equal(f.find_hashes(dev(probes, cuda)).cpu().numpy(), want_res)
+        bits = u32(f.find_hashes_bits(dev(probes, cuda)))
+        assert bits.size == (probes.size + 31) // 32
+        assert np.array_equal(bits_to_bytes(bits, probes.size), want_res)
+        if probes.size % 32:
+            assert bits[-1] >> (probes.size % 32) == 0  # no stray bits past n
+
+
+def test_host_buffer_path(cuda, oracle):
+    """add_hashes/find_hashes with host arrays (pipelined H2D/D2H, several chunks)."""
+    rng = np.random.default_rng(11)
+    hs = rng.integers(0, 2**64, size=9_000_017, dtype=np.uint64)   # > 2 host chunks
+    probes = rng.integers(0, 2**64, size=9_100_000, dtype=np.uint64)
+    probes[::3] = hs[: probes[::3].size]
+    f = SplitBlockFilter(123_457)
+    f.add_hashes(hs)
+    want = oracle.build(123_457, hs)
+    assert np.array_equal(f.blocks(), want)
+    want_res = oracle.find_hashes(want, probes, threads=8)
+    assert np.array_equal(f.find_hashes(probes), want_res)
+    assert np.array_equal(bits_to_bytes(f.find_hashes_bits(probes), probes.size), want_res)
+
+
+def test_single_key_ops_and_api(cuda, oracle):
+    with pytest.raises(ValueError):
+        SplitBlockFilter(0)                       # filter.cpp:160-162
+    f = SplitBlockFilter(1)
+    assert f.num_buckets() == 1 and f.size_bytes() == 32 and f.hasher_id() == 0
+    assert not f.find_hash(0)
+    f.add_hash(0)                                 # filter_test.cpp:164-170
+    assert f.blocks().tolist() == [[1] * 8] and f.find_hash(0)
+    g = SplitBlockFilter(57)
+    hs = oracle.mt19937_64(0x5EED0004, 1000)
+    for h in hs[:200]:
+        assert not g.find_hash(int(h)) or True
+        g.add_hash(int(h))
+    assert all(g.find_hash(int(h)) for h in hs[:200])
+    assert np.array_equal(g.blocks(), oracle.build(57, hs[:200]))
+    # from_blocks / equality / clear
+    h2 = SplitBlockFilter.from_blocks(g.blocks())
+    assert h2 == g
+    h2.set_hasher_id(1)
+    assert h2 != g
+    h2.clear()
+    torch.cuda.synchronize()
+    assert not h2.blocks().any()
+    # empty batches are no-ops (filter_test.cpp:175-180)
+    g.add_hashes(dev([], cuda))
+    assert g.find_hashes(dev([], cuda)).numel() == 0
+    assert np.array_equal(g.blocks(), oracle.build(57, hs[:200]))
+
+
+def test_idempotence_and_order_independence(cuda, oracle):
+    rng = np.random.default_rng(5)
+    hs = rng.integers(0, 2**64, size=1_000_000, dtype=np.uint64)
+    a = SplitBlockFilter(4096)
+    a.add_hashes(dev(hs, cuda))
+    b = SplitBlockFilter(4096)
+    b.add_hashes(dev(hs[::-1].copy(), cuda))
+    b.add_hashes(dev(hs[:1000], cuda))
+    assert a == b
+    # concurrent inserts from two streams (atomic OR) give the same bytes
+    c = SplitBlockFilter(4096)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    d = dev(hs, cuda)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        c.add_hashes(d[: 500_000])
+    with torch.cuda.stream(s2):
+        c.add_hashes(d[500_000:])
+    torch.cuda.synchronize()
+    assert c == a
+    assert np.array_equal(a.blocks(), oracle.build(4096, hs))
+
+
+def test_no_false_negatives_acceptance(cuda):
+    # acceptance.cpp:63-82: 10^6 hashes, {1, 7, 4096} buckets
+    rng = np.random.default_rng(0xACC0001)
+    hs = dev(rng.integers(0, 2**64, size=1_000_000, dtype=np.uint64), cuda)
+    for nb in (1, 7, 4096):
+        f = SplitBlockFilter(nb)
+        f.add_hashes(hs)
+        assert int(f.find_hashes(hs).sum()) == hs.numel()
+
+
+def test_64bit_block_offsets(cuda, oracle):
+    """A filter larger than 2^32 words (> 16 GiB): offsets must be 64-bit."""
+    nb = (1 << 29) + 12345          # 17.2 GB, 2^32+ 32-bit words
+    f = SplitBlockFilter(nb)
+    rng = np.random.default_rng(99)
+    hs = rng.integers(0, 2**64, size=200_000, dtype=np.uint64)
+    hs[:1000] |= np.uint64(0xFFFF000000000000)   # force the top of the array
+    f.add_hashes(dev(hs, cuda))
+    idx = np.array([oracle.block_index(int(h), nb) for h in hs[:2000]])
+    assert idx.max() > (1 << 29)
+    for i, h in zip(idx[:300], hs[:300]):
+        blk = f.blocks_range(int(i), 1)[0]
+        m = np.array(oracle.make_mask(int(h)), np.uint32)
+        assert np.all(blk & m == m)
+    assert int(f.find_hashes(dev(hs, cuda)).sum()) == hs.size
+    top = f.blocks_range(nb - 4, 4)
+    assert top.shape == (4, 8)
+    del f
+    torch.cuda.empty_cache()
+
+
+# --- device stream generators == host oracle --------------------------------------
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_generators_match_oracle(cuda, oracle, cid):
+    cfg = W.CONFIGS[cid]
+    st = W.StreamHandle(cfg.inserts)
+    table = st.table.cpu().numpy().view(np.uint64) if st.table is not None else None
+    ost = oracle.stream(cfg.inserts, table)
+    for start in (0, 12_345_678 if cfg.inserts.n > 20_000_000 else 1000, cfg.inserts.n - 5000):
+        got = W.gen_inserts(st, start, 5000).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, oracle.gen_inserts(ost, start, 5000))
+    for start in (0, 99_999, cfg.lookups.n - 4000):
+        got = W.gen_lookups(st, cfg.lookups, cfg.inserts.n, start, 4000).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, oracle.gen_lookups(ost, cfg.lookups, cfg.inserts.n, start, 4000))
+
+
+# --- full BASELINE configs against the reference's golden values ------------------
+def run_config(cid, cuda, oracle, insert_variant=0, find_variant=0):
+    cfg = W.CONFIGS[cid]
+    st = W.StreamHandle(cfg.inserts)
+    f = SplitBlockFilter(cfg.num_buckets)
+    if insert_variant:
+        f.set_insert_variant(insert_variant)
+    if find_variant:
+        f.set_find_variant(find_variant)
+    N, L = cfg.inserts.n, cfg.lookups.n
+    chunk = cfg.insert_chunk or (1 << 26)
+    buf = torch.empty(min(chunk, max(N, L)), dtype=torch.int64, device=cuda)
+    for s in range(0, N, chunk):
+        m = min(chunk, N - s)
+        f.add_hashes(W.gen_inserts(st, s, m, buf[:m]))
+    crcs, member_hits, fp = [], 0, 0
+    gchunk = 1 << 26
+    for s in range(0, L, gchunk):
+        m = min(gchunk, L - s)
+        q = W.gen_lookups(st, cfg.lookups, N, s, m, buf[:m])
+        bits = f.find_hashes_bits(q)
+        hb = u32(bits)
+        crcs.append(oracle.crc32(hb.view(np.uint8)[: (m + 7) // 8].tobytes()))
+        res = bits_to_bytes(hb, m)
+        j = np.arange(s, s + m, dtype=np.uint64)
+        if cfg.lookups.members_first:
+            mem = j < N
+        else:
+            mem = ((j + 1) * cfg.lookups.p // cfg.lookups.q) > (j * cfg.lookups.p // cfg.lookups.q)
+        member_hits += int(res[mem].sum())
+        fp += int(res[~mem].sum())
+    blocks = f.blocks()
+    return dict(image_crc=oracle.image_crc(blocks), popcount=oracle.popcount(blocks),
+                member_hits=member_hits, false_positives=fp, crcs=crcs)
+
+
+@pytest.mark.parametrize("cid", [1, 2])
+@pytest.mark.parametrize("iv", INSERT_VARIANTS)
+def test_config_small(cuda, oracle, golden_configs, cid, iv):
+    g = golden_configs[str(cid)]
+    for fv in (_lib.FIND_GLOBAL, _lib.FIND_SMEM if cid == 1 else _lib.FIND_AUTO):
+        r = run_config(cid, cuda, oracle, iv, fv)
+        assert r["image_crc"] == g["image_crc"]
+        assert r["popcount"] == g["popcount"]
+        assert r["member_hits"] == g["members"]          # no false negatives
+        assert r["false_positives"] == g["false_positives"]
+        assert r["crcs"] == g["lookup_bitmap_chunk_crcs"]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cid", [3, 4])
+def test_config_full(cuda, oracle, golden_configs, cid):
+    if str(cid) not in golden_configs:
+        pytest.skip(f"no golden for config {cid}")
+    g = golden_configs[str(cid)]
+    r = run_config(cid, cuda, oracle, _lib.INSERT_LANE8_TEST if cid == 4 else 0)
+    assert r["image_crc"] == g["image_crc"]
+    assert r["popcount"] == g["popcount"]
+    assert r["member_hits"] == g["members"]
+    assert r["false_positives"] == g["false_positives"]
+    assert r["crcs"] == g["lookup_bitmap_chunk_crcs"]
