@@ -58,7 +58,9 @@ enum {
   SBBF_INSERT_AUTO = 0,
   SBBF_INSERT_LANE8 = 1,      /* 8 threads per key, one red.or per lane: 1 sector op / key */
   SBBF_INSERT_LANE8_TEST = 2, /* as LANE8, but skip lanes whose bit is already set (hot keys) */
-  SBBF_INSERT_THREAD = 3      /* 1 thread per key, 8 red.or per key (baseline variant) */
+  SBBF_INSERT_THREAD = 3,     /* 1 thread per key, 8 red.or per key (baseline variant) */
+  SBBF_INSERT_WIDE = 4,       /* 4 threads per key, one 64-bit red.or per lane pair */
+  SBBF_INSERT_WIDE_TEST = 5   /* as WIDE, skipping lane pairs whose bits are all set */
 };
 
 /* Lookup strategies (sbbf_gpu_set_find_variant). AUTO picks per call. */
@@ -142,6 +144,41 @@ int sbbf_gpu_set_find_variant(sbbf_gpu_t* f, int variant);
 /* Variant the AUTO policy would use for a batch of n keys (for reporting). */
 int sbbf_gpu_resolved_insert_variant(const sbbf_gpu_t* f, uint64_t n);
 int sbbf_gpu_resolved_find_variant(const sbbf_gpu_t* f, uint64_t n);
+
+/* --- multi-GPU shards (no reference counterpart: the reference has no
+ *     distributed mode) -----------------------------------
+ * Rank r of P owns global blocks [floor(r*B/P), floor((r+1)*B/P)). A shard
+ * keeps the global block_index (taken against total_buckets), so the shards
+ * concatenated in rank order are byte-identical to one B-bucket filter.
+ * Shard kernels ignore (insert) / answer 0 for (find) keys it does not own. */
+int sbbf_gpu_create_shard(uint64_t total_buckets, uint64_t first_block, uint64_t num_buckets,
+                          int device, sbbf_gpu_t** out);
+uint64_t sbbf_gpu_total_buckets(const sbbf_gpu_t* f);
+uint64_t sbbf_gpu_first_block(const sbbf_gpu_t* f);
+/* h_bounds[0..parts] = floor(r * total_buckets / parts) (host). */
+int sbbf_shard_bounds(uint64_t total_buckets, uint32_t parts, uint64_t* h_bounds);
+/* d_counts[r] = number of keys whose block falls in shard r (parts <= 1024;
+ * d_bounds = the first `parts` entries of sbbf_shard_bounds, on device). */
+int sbbf_shard_count(const uint64_t* d_hashes, uint64_t n, uint64_t total_buckets,
+                     const uint64_t* d_bounds, uint32_t parts, uint64_t* d_counts, void* stream);
+/* Group keys by destination shard: segment r of d_out starts at d_offsets[r]
+ * (exclusive prefix sum of the counts). d_pos (optional, n < 2^32) gets each
+ * key's source index; d_cursor is parts u64 of scratch. Order inside a
+ * segment is unspecified. */
+int sbbf_shard_scatter(const uint64_t* d_hashes, uint64_t n, uint64_t total_buckets,
+                       const uint64_t* d_bounds, uint32_t parts, const uint64_t* d_offsets,
+                       uint64_t* d_cursor, uint64_t* d_out, uint32_t* d_pos, void* stream);
+/* d_dst[d_pos[i]] = d_src[i]: lookup answers back to source order. */
+int sbbf_scatter_u8(const uint8_t* d_src, const uint32_t* d_pos, uint64_t n, uint8_t* d_dst,
+                    void* stream);
+/* Pack 0/1 bytes into an LSB-first bitmap of ceil(n/32) words. */
+int sbbf_pack_bits(const uint8_t* d_src, uint64_t n, uint32_t* d_bits, void* stream);
+
+/* L2 fetch-granularity hint for `device` (cudaLimitMaxL2FetchGranularity,
+ * 0..128 bytes; process-wide for that device). 32 makes a random 32-byte
+ * block miss fetch one sector from HBM instead of a wider line. *old (if
+ * non-NULL) receives the previous value. */
+int sbbf_gpu_set_l2_fetch_granularity(int device, int bytes, int* old);
 
 /* --- diagnostics ------------------------------------------------------ */
 const char* sbbf_gpu_last_error(void);

@@ -21,7 +21,7 @@ SBBF_ECUDA = -3
 SBBF_ENODEV = -4
 SBBF_EFORMAT = -5
 
-INSERT_AUTO, INSERT_LANE8, INSERT_LANE8_TEST, INSERT_THREAD = 0, 1, 2, 3
+INSERT_AUTO, INSERT_LANE8, INSERT_LANE8_TEST, INSERT_THREAD, INSERT_WIDE, INSERT_WIDE_TEST = 0, 1, 2, 3, 4, 5
 FIND_AUTO, FIND_GLOBAL, FIND_SMEM = 0, 1, 2
 
 # Every symbol include/sbbf_gpu.h and include/sbbf_workload.h declare, with
@@ -55,6 +55,15 @@ PROTOTYPES = {
     "sbbf_gpu_set_find_variant": (_i, [_vp, _i]),
     "sbbf_gpu_resolved_insert_variant": (_i, [_vp, _u64]),
     "sbbf_gpu_resolved_find_variant": (_i, [_vp, _u64]),
+    "sbbf_gpu_set_l2_fetch_granularity": (_i, [_i, _i, C.POINTER(_i)]),
+    "sbbf_gpu_create_shard": (_i, [_u64, _u64, _u64, _i, C.POINTER(_vp)]),
+    "sbbf_gpu_total_buckets": (_u64, [_vp]),
+    "sbbf_gpu_first_block": (_u64, [_vp]),
+    "sbbf_shard_bounds": (_i, [_u64, _u32, _u64p]),
+    "sbbf_shard_count": (_i, [_vp, _u64, _u64, _vp, _u32, _vp, _vp]),
+    "sbbf_shard_scatter": (_i, [_vp, _u64, _u64, _vp, _u32, _vp, _vp, _vp, _vp, _vp]),
+    "sbbf_scatter_u8": (_i, [_vp, _vp, _u64, _vp, _vp]),
+    "sbbf_pack_bits": (_i, [_vp, _u64, _vp, _vp]),
     "sbbf_gpu_last_error": (C.c_char_p, []),
     "sbbf_gpu_abi_version": (_i, []),
     "sbbf_gpu_launch_count": (_u64, []),

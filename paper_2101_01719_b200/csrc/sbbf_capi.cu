@@ -54,7 +54,8 @@ constexpr uint64_t kHostChunk = uint64_t{1} << 22;  // keys per pipelined host c
 
 struct sbbf_gpu {
   sbbf::DeviceInfo di;
-  uint64_t nb = 0;
+  uint64_t nb = 0;                    // local block count (== geom.nb_local)
+  sbbf::Geom geom{0, 0, 0};           // global bucket count / first block of this shard
   uint32_t* d_blocks = nullptr;
   uint32_t hasher_id = 0;
   int insert_variant = SBBF_INSERT_AUTO;
@@ -73,7 +74,11 @@ namespace {
 int resolve_insert(const sbbf_gpu* f, uint64_t n) {
   (void)n;
   if (f->insert_variant != SBBF_INSERT_AUTO) return f->insert_variant;
-  return SBBF_INSERT_LANE8;
+  // L2-resident filters are bound by the L2 atomic unit (op count): plain
+  // 64-bit reds. Larger filters: load the lane pair first (the read path
+  // fills L2 faster than a missing atomic does, and duplicates/hot keys skip
+  // the atomic entirely).
+  return f->nb * 32 <= f->di.l2_bytes / 2 ? SBBF_INSERT_WIDE : SBBF_INSERT_WIDE_TEST;
 }
 
 bool smem_fits(const sbbf_gpu* f) {
@@ -124,12 +129,12 @@ int host_pipeline(sbbf_gpu* f, HostOp op, const uint64_t* h_hashes, uint64_t n, 
                                     cudaMemcpyHostToDevice, f->hs[s]);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(H2D)");
     if (op == HostOp::kInsert) {
-      e = sbbf::launch_insert(f->di, resolve_insert(f, m), f->d_blocks, f->nb, f->d_stage[s], m,
+      e = sbbf::launch_insert(f->di, resolve_insert(f, m), f->d_blocks, f->geom, f->d_stage[s], m,
                               f->hs[s]);
       if (e != cudaSuccess) return cuda_fail(e, "insert kernel");
     } else {
       const bool bits = op == HostOp::kFindBits;
-      e = sbbf::launch_find(f->di, resolve_find(f, m), f->d_blocks, f->nb, f->d_stage[s], m,
+      e = sbbf::launch_find(f->di, resolve_find(f, m), f->d_blocks, f->geom, f->d_stage[s], m,
                             f->d_res[s], bits, f->hs[s]);
       if (e != cudaSuccess) return cuda_fail(e, "find kernel");
       // kHostChunk is a multiple of 32, so chunk bitmaps tile the output.
@@ -156,10 +161,17 @@ const char* sbbf_gpu_last_error(void) { return g_err.c_str(); }
 uint64_t sbbf_gpu_launch_count(void) { return sbbf::launch_count(); }
 
 int sbbf_gpu_create(uint64_t num_buckets, int device, sbbf_gpu_t** out) {
+  return sbbf_gpu_create_shard(num_buckets, 0, num_buckets, device, out);
+}
+
+int sbbf_gpu_create_shard(uint64_t total_buckets, uint64_t first_block, uint64_t num_buckets,
+                          int device, sbbf_gpu_t** out) {
   if (!out) return fail(SBBF_EINVAL, "out is null");
   *out = nullptr;
   if (num_buckets == 0) return fail(SBBF_EINVAL, "SplitBlockFilter needs at least one bucket");
   if (num_buckets > (~uint64_t{0}) / 32) return fail(SBBF_EINVAL, "num_buckets overflows size");
+  if (first_block > total_buckets || num_buckets > total_buckets - first_block)
+    return fail(SBBF_EINVAL, "shard range exceeds total_buckets");
   int count = 0;
   cudaError_t e = cudaGetDeviceCount(&count);
   if (e != cudaSuccess || count == 0) {
@@ -172,6 +184,7 @@ int sbbf_gpu_create(uint64_t num_buckets, int device, sbbf_gpu_t** out) {
   sbbf_gpu* f = new (std::nothrow) sbbf_gpu;
   if (!f) return fail(SBBF_ENOMEM, "host allocation failed");
   f->nb = num_buckets;
+  f->geom = sbbf::Geom{total_buckets, first_block, num_buckets};
   f->di.device = device;
   int v = 0;
   if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) == cudaSuccess) f->di.sms = v;
@@ -217,6 +230,8 @@ int sbbf_gpu_clear(sbbf_gpu_t* f, void* stream) {
 }
 
 uint64_t sbbf_gpu_num_buckets(const sbbf_gpu_t* f) { return f ? f->nb : 0; }
+uint64_t sbbf_gpu_total_buckets(const sbbf_gpu_t* f) { return f ? f->geom.nb_global : 0; }
+uint64_t sbbf_gpu_first_block(const sbbf_gpu_t* f) { return f ? f->geom.first : 0; }
 uint64_t sbbf_gpu_size_bytes(const sbbf_gpu_t* f) { return f ? f->nb * 32 : 0; }
 uint32_t sbbf_gpu_hasher_id(const sbbf_gpu_t* f) { return f ? f->hasher_id : 0; }
 int sbbf_gpu_device(const sbbf_gpu_t* f) { return f ? f->di.device : -1; }
@@ -233,7 +248,7 @@ int sbbf_gpu_insert_batch(sbbf_gpu_t* f, const uint64_t* d_hashes, uint64_t n, v
   if (n == 0) return SBBF_OK;  // empty batch is a no-op (filter_test.cpp:169-175)
   if (!d_hashes) return fail(SBBF_EINVAL, "null hashes");
   DeviceGuard g(f->di.device);
-  cudaError_t e = sbbf::launch_insert(f->di, resolve_insert(f, n), f->d_blocks, f->nb, d_hashes, n,
+  cudaError_t e = sbbf::launch_insert(f->di, resolve_insert(f, n), f->d_blocks, f->geom, d_hashes, n,
                                       static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "insert kernel launch");
 }
@@ -244,7 +259,7 @@ static int find_common(const sbbf_gpu_t* f, const uint64_t* d_hashes, uint64_t n
   if (n == 0) return SBBF_OK;
   if (!d_hashes || !d_out) return fail(SBBF_EINVAL, "null buffer");
   DeviceGuard g(f->di.device);
-  cudaError_t e = sbbf::launch_find(f->di, resolve_find(f, n), f->d_blocks, f->nb, d_hashes, n,
+  cudaError_t e = sbbf::launch_find(f->di, resolve_find(f, n), f->d_blocks, f->geom, d_hashes, n,
                                     d_out, bits, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "find kernel launch");
 }
@@ -282,7 +297,7 @@ int sbbf_gpu_add_hash(sbbf_gpu_t* f, uint64_t hash) {
   DeviceGuard g(f->di.device);
   cudaError_t e = cudaMemcpy(f->d_one, &hash, sizeof(hash), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
-    e = sbbf::launch_insert(f->di, SBBF_INSERT_LANE8, f->d_blocks, f->nb, f->d_one, 1, nullptr);
+    e = sbbf::launch_insert(f->di, SBBF_INSERT_WIDE, f->d_blocks, f->geom, f->d_one, 1, nullptr);
   if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
   return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "add_hash");
 }
@@ -295,7 +310,7 @@ int sbbf_gpu_find_hash(const sbbf_gpu_t* f, uint64_t hash, int* found) {
   uint8_t r = 0;
   cudaError_t e = cudaMemcpy(m->d_one, &hash, sizeof(hash), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
-    e = sbbf::launch_find(f->di, SBBF_FIND_GLOBAL, f->d_blocks, f->nb, m->d_one, 1, m->d_one + 1,
+    e = sbbf::launch_find(f->di, SBBF_FIND_GLOBAL, f->d_blocks, f->geom, m->d_one, 1, m->d_one + 1,
                           false, nullptr);
   if (e == cudaSuccess) e = cudaMemcpy(&r, m->d_one + 1, 1, cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "find_hash");
@@ -351,9 +366,21 @@ int sbbf_gpu_make_mask_batch(const uint64_t* d_hashes, uint64_t n, uint32_t* d_l
   return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "make_mask kernel");
 }
 
+int sbbf_gpu_set_l2_fetch_granularity(int device, int bytes, int* old) {
+  if (bytes < 0 || bytes > 128) return fail(SBBF_EINVAL, "granularity must be 0..128 bytes");
+  DeviceGuard g(device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  size_t prev = 0;
+  cudaError_t e = cudaDeviceGetLimit(&prev, cudaLimitMaxL2FetchGranularity);
+  if (e == cudaSuccess) e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(bytes));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaLimitMaxL2FetchGranularity");
+  if (old) *old = static_cast<int>(prev);
+  return SBBF_OK;
+}
+
 int sbbf_gpu_set_insert_variant(sbbf_gpu_t* f, int variant) {
   if (!f) return fail(SBBF_EINVAL, "null filter");
-  if (variant < SBBF_INSERT_AUTO || variant > SBBF_INSERT_THREAD)
+  if (variant < SBBF_INSERT_AUTO || variant > SBBF_INSERT_WIDE_TEST)
     return fail(SBBF_EINVAL, "unknown insert variant");
   f->insert_variant = variant;
   return SBBF_OK;

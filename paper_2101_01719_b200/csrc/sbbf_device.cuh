@@ -121,6 +121,18 @@ __device__ __forceinline__ void red_or(uint32_t* p, uint32_t v, uint64_t policy)
                : "memory");
 }
 
+__device__ __forceinline__ void red_or64(uint64_t* p, uint64_t v, uint64_t policy) {
+  asm volatile("red.relaxed.gpu.global.or.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(v),
+               "l"(policy)
+               : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_pair(const uint64_t* p, uint64_t policy) {
+  uint64_t v;
+  asm volatile("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(policy));
+  return v;
+}
+
 __device__ __forceinline__ void st_stream_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.global.L1::no_allocate.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 
+#include "sbbf_bench.h"
 #include "sbbf_gpu.h"
 #include "sbbf_workload.h"
 
@@ -17,18 +18,30 @@ struct DeviceInfo {
   size_t l2_bytes = 126u << 20;
 };
 
+// Filter geometry: block_index is taken against nb_global (the whole
+// filter's bucket count), then offset by the shard's first block. A
+// single-GPU filter is the shard {nb, 0, nb}.
+struct Geom {
+  uint64_t nb_global;
+  uint64_t first;
+  uint64_t nb_local;
+};
+
 constexpr int kInsertLane8 = SBBF_INSERT_LANE8;
 constexpr int kInsertLane8Test = SBBF_INSERT_LANE8_TEST;
 constexpr int kInsertThread = SBBF_INSERT_THREAD;
+constexpr int kInsertWide = SBBF_INSERT_WIDE;
+constexpr int kInsertWideTest = SBBF_INSERT_WIDE_TEST;
 constexpr int kFindGlobal = SBBF_FIND_GLOBAL;
 constexpr int kFindSmem = SBBF_FIND_SMEM;
 
 uint64_t launch_count();
 void note_launch();
+uint64_t grid_for(uint64_t work_items, uint64_t items_per_block, int sms, int per_sm);
 
-cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, uint64_t nb,
+cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, const Geom& g,
                           const uint64_t* hashes, uint64_t n, cudaStream_t s);
-cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* blocks, uint64_t nb,
+cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* blocks, const Geom& g,
                         const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s);
 cudaError_t launch_block_index(const uint64_t* h, uint64_t n, uint64_t nb, uint64_t* out,
                                cudaStream_t s);

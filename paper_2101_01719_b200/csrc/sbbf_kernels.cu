@@ -5,20 +5,26 @@
 //   find_many_avx2 core/src/filter.cpp:86-93   (per key: load 32 B, vptest, 1 byte out)
 //
 // Design (DESIGN.md §3 has the roofline for each):
-//   * insert_lane8   — 8 threads per key, one `red.global.or.b32` per lane. One
-//     warp instruction covers 4 keys = 4 sectors, so the L2 sees one 32-byte
-//     atomic sector op per key instead of eight word ops (insert_thread).
-//     Atomic OR is exact: OR is commutative/associative/idempotent, so any
-//     interleaving yields the reference's bytes.
-//   * insert_lane8_test — loads the lane first and only issues the red when
-//     the bit is clear (bits are monotone): cuts atomics for
-//     duplicate/hot keys (config 4's Zipf duplicates).
-//   * find_global    — one thread per key, U keys in flight per thread, one
-//     256-bit LDG per key (LDG.E.ENL2.256), hashes streamed evict-first,
-//     results either 0/1 bytes (drop-in) or a __ballot_sync-packed bitmap.
-//   * find_smem      — small filters (<= ~200 KiB, e.g. config 1) are staged
+//   * insert_wide     — 4 threads per key, one `red.global.or.b64` per lane pair.
+//     The L2 atomic unit is op-bound, so 4 ops/key beat 8 (insert_lane8) and
+//     32 scattered ops/warp-instruction (insert_thread). Atomic OR is exact:
+//     OR is commutative/associative/idempotent, so any interleaving yields the
+//     reference's bytes.
+//   * insert_*_test   — load first, red only lanes whose bits are missing (bits
+//     are monotone): a miss is filled by the faster read path and
+//     duplicate/hot keys (config 4's Zipf) skip the atomic.
+//   * find_global     — one thread per key, U keys in flight per thread, one
+//     256-bit LDG per key (LDG.E.256), hashes streamed evict-first, results
+//     either 0/1 bytes (drop-in) or a __ballot_sync-packed bitmap.
+//   * find_smem       — small filters (<= ~200 KiB, e.g. config 1) are staged
 //     into shared memory per CTA with cp.async.bulk (TMA bulk copy, mbarrier
-//     completion) and probed from smem with two 128-bit LDS per key.
+//     completion) and probed with two 128-bit LDS per key.
+//
+// Every kernel takes a Geom: the block index is computed against the GLOBAL
+// bucket count and offset by the shard's first block, so a shard of a
+// multi-GPU filter (sharded.py) keeps the reference's block_index exactly.
+// Keys outside [first, first + nb_local) are ignored by inserts and answer 0
+// in lookups (the router never sends them).
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -34,20 +40,26 @@ using dev::Block8;
 
 constexpr int kThreads = 256;
 
+// Local block of `h` and whether this shard owns it.
+__device__ __forceinline__ uint64_t local_block(uint64_t h, const Geom& g, bool& ok) {
+  const uint64_t b = dev::block_index(h, g.nb_global) - g.first;
+  ok = b < g.nb_local;
+  return ok ? b : 0;
+}
+
 // ---------------------------------------------------------------------------
 // insert
 // ---------------------------------------------------------------------------
 // __launch_bounds__ minimum-blocks hints below are load-bearing: without them
-// ptxas minimises registers by sinking each block load next to its use, which
-// serialises the U independent sector reads (checked in SASS).
+// ptxas minimises registers by sinking each load next to its use, which
+// serialises the independent sector accesses (checked in SASS).
 template <bool kTest>
-__global__ void __launch_bounds__(kThreads, 4) insert_lane8_kernel(uint32_t* __restrict__ blocks,
-                                                                uint64_t num_buckets,
-                                                                const uint64_t* __restrict__ hashes,
-                                                                uint64_t n) {
+__global__ void __launch_bounds__(kThreads, 4) insert_lane8_kernel(uint32_t* __restrict__ blocks, Geom g,
+                                                                   const uint64_t* __restrict__ hashes,
+                                                                   uint64_t n) {
   const int lane = threadIdx.x & 31;
-  const int sub = lane >> 3;       // which of the 4 keys of a round
-  const int word = lane & 7;       // which lane of the block this thread owns
+  const int sub = lane >> 3;  // which of the 4 keys of a round
+  const int word = lane & 7;  // which lane of the block this thread owns
   const uint32_t seed = dev::lane_seed_rt(word);
   const uint64_t pol = dev::policy_evict_first();
   const uint64_t keep = dev::policy_evict_last();
@@ -65,8 +77,9 @@ __global__ void __launch_bounds__(kThreads, 4) insert_lane8_kernel(uint32_t* __r
     for (int r = 0; r < 8; ++r) {
       const int k = r * 4 + sub;
       const uint64_t hk = __shfl_sync(0xffffffffu, h, k);
-      ptr[r] = blocks + dev::block_index(hk, num_buckets) * 8 + word;
-      bit[r] = ((valid >> k) & 1u) ? dev::lane_bit(static_cast<uint32_t>(hk), seed) : 0u;
+      bool ok;
+      ptr[r] = blocks + local_block(hk, g, ok) * 8 + word;
+      bit[r] = (((valid >> k) & 1u) && ok) ? dev::lane_bit(static_cast<uint32_t>(hk), seed) : 0u;
     }
     if constexpr (kTest) {
       uint32_t cur[8];
@@ -83,9 +96,69 @@ __global__ void __launch_bounds__(kThreads, 4) insert_lane8_kernel(uint32_t* __r
   }
 }
 
+// 4 threads per key, one 64-bit `red.global.or.b64` per lane pair: half the
+// L2 atomic operations of insert_lane8 (120 vs 85 G keys/s on an L2-resident
+// buffer, scripts/microbench.cu). Lane 2w is the low half of u64 word w
+// (little-endian lanes, filter.hpp:23-24).
+template <bool kTest>
+__global__ void __launch_bounds__(kThreads, 4) insert_wide_kernel(uint32_t* __restrict__ blocks, Geom g,
+                                                                  const uint64_t* __restrict__ hashes,
+                                                                  uint64_t n) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane >> 2;   // which of the 8 keys of a round
+  const int pair = lane & 3;   // which 64-bit lane pair of the block this thread owns
+  const uint32_t seed_lo = dev::lane_seed_rt(2 * pair), seed_hi = dev::lane_seed_rt(2 * pair + 1);
+  const uint64_t pol = dev::policy_evict_first();
+  const uint64_t keep = dev::policy_evict_last();
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
+  // A warp step covers kT tiles of 32 keys: the kT hash loads are issued
+  // together so one DRAM round trip feeds 4*kT atomic rounds.
+  constexpr int kT = 4;
+  const uint64_t nsteps = (n + 32 * kT - 1) / (32 * kT);
+  for (uint64_t t = warp; t < nsteps; t += nwarps) {
+    const uint64_t base = t * (32 * kT);
+    uint64_t h[kT];
+#pragma unroll
+    for (int j = 0; j < kT; ++j) {
+      const uint64_t idx = base + j * 32 + lane;
+      h[j] = idx < n ? dev::ld_stream_u64(hashes + idx, pol) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kT; ++j) {
+      const uint32_t valid = __ballot_sync(0xffffffffu, base + j * 32 + lane < n);
+      if (valid == 0) break;
+      uint64_t* ptr[4];
+      uint64_t mask[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int k = r * 8 + sub;
+        const uint64_t hk = __shfl_sync(0xffffffffu, h[j], k);
+        const uint32_t low = static_cast<uint32_t>(hk);
+        bool ok;
+        ptr[r] = reinterpret_cast<uint64_t*>(blocks + local_block(hk, g, ok) * 8) + pair;
+        mask[r] = (((valid >> k) & 1u) && ok)
+                      ? (static_cast<uint64_t>(dev::lane_bit(low, seed_hi)) << 32) | dev::lane_bit(low, seed_lo)
+                      : 0ull;
+      }
+      if constexpr (kTest) {
+        uint64_t cur[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) cur[r] = mask[r] ? dev::ld_pair(ptr[r], keep) : ~0ull;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (mask[r] & ~cur[r]) dev::red_or64(ptr[r], mask[r], keep);
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (mask[r]) dev::red_or64(ptr[r], mask[r], keep);
+      }
+    }
+  }
+}
+
 // Baseline variant: one thread per key, eight word atomics per key.
-__global__ void __launch_bounds__(kThreads) insert_thread_kernel(uint32_t* __restrict__ blocks,
-                                                                 uint64_t num_buckets,
+__global__ void __launch_bounds__(kThreads) insert_thread_kernel(uint32_t* __restrict__ blocks, Geom g,
                                                                  const uint64_t* __restrict__ hashes,
                                                                  uint64_t n) {
   const uint64_t pol = dev::policy_evict_first();
@@ -93,7 +166,9 @@ __global__ void __launch_bounds__(kThreads) insert_thread_kernel(uint32_t* __res
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n; i += stride) {
     const uint64_t h = dev::ld_stream_u64(hashes + i, pol);
-    uint32_t* b = blocks + dev::block_index(h, num_buckets) * 8;
+    bool ok;
+    uint32_t* b = blocks + local_block(h, g, ok) * 8;
+    if (!ok) continue;
     const uint32_t low = static_cast<uint32_t>(h);
 #pragma unroll
     for (int w = 0; w < 8; ++w) dev::red_or(b + w, dev::lane_bit(low, dev::lane_seed(w)), keep);
@@ -110,10 +185,9 @@ template <int U, bool kBits>
 constexpr int find_min_blocks() { return U >= 8 ? (kBits ? 2 : 4) : 5; }
 
 template <int U, bool kBits>
-__global__ void __launch_bounds__(kThreads, find_min_blocks<U, kBits>()) find_global_kernel(const uint32_t* __restrict__ blocks,
-                                                               uint64_t num_buckets,
-                                                               const uint64_t* __restrict__ hashes,
-                                                               uint64_t n, void* __restrict__ out) {
+__global__ void __launch_bounds__(kThreads, find_min_blocks<U, kBits>())
+    find_global_kernel(const uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ hashes,
+                       uint64_t n, void* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const uint64_t pol = dev::policy_evict_first();
   const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
@@ -129,13 +203,18 @@ __global__ void __launch_bounds__(kThreads, find_min_blocks<U, kBits>()) find_gl
       h[u] = idx < n ? dev::ld_stream_u64(hashes + idx, pol) : 0;
     }
     Block8 b[U];
+    uint32_t owned = 0;
 #pragma unroll
-    for (int u = 0; u < U; ++u) dev::ld_block_nc(blocks + dev::block_index(h[u], num_buckets) * 8, b[u]);
+    for (int u = 0; u < U; ++u) {
+      bool ok;
+      dev::ld_block_nc(blocks + local_block(h[u], g, ok) * 8, b[u]);
+      owned |= static_cast<uint32_t>(ok) << u;
+    }
     uint32_t mine = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t idx = base + u * 32 + lane;
-      const bool hit = dev::block_contains(b[u], h[u]) && idx < n;
+      const bool hit = dev::block_contains(b[u], h[u]) && ((owned >> u) & 1u) && idx < n;
       if constexpr (kBits) {
         const uint32_t word = __ballot_sync(0xffffffffu, hit);
         if (lane == u) mine = word;
@@ -159,13 +238,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 template <bool kBits>
-__global__ void __launch_bounds__(1024, 1) find_smem_kernel(const uint32_t* __restrict__ blocks,
-                                                         uint64_t num_buckets,
-                                                         const uint64_t* __restrict__ hashes,
-                                                         uint64_t n, void* __restrict__ out) {
+__global__ void __launch_bounds__(1024, 1) find_smem_kernel(const uint32_t* __restrict__ blocks, Geom g,
+                                                            const uint64_t* __restrict__ hashes,
+                                                            uint64_t n, void* __restrict__ out) {
   extern __shared__ __align__(128) uint4 sfilter[];
   __shared__ __align__(8) uint64_t mbar;
-  const uint32_t bytes = static_cast<uint32_t>(num_buckets * 32);
+  const uint32_t bytes = static_cast<uint32_t>(g.nb_local * 32);
   const uint32_t bar = smem_u32(&mbar);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
@@ -216,10 +294,11 @@ __global__ void __launch_bounds__(1024, 1) find_smem_kernel(const uint32_t* __re
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t idx = base + u * 32 + lane;
-      const uint4* p = sfilter + dev::block_index(h[u], num_buckets) * 2;
+      bool ok;
+      const uint4* p = sfilter + local_block(h[u], g, ok) * 2;
       const uint4 lo = p[0], hi = p[1];
       Block8 b{{lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w}};
-      const bool hit = dev::block_contains(b, h[u]) && idx < n;
+      const bool hit = dev::block_contains(b, h[u]) && ok && idx < n;
       if constexpr (kBits) {
         const uint32_t word = __ballot_sync(0xffffffffu, hit);
         if (lane == u) mine = word;
@@ -257,7 +336,14 @@ __global__ void make_mask_kernel(const uint64_t* __restrict__ h, uint64_t n,
 
 std::atomic<uint64_t> g_launches{0};
 
-// Blocks per SM the hardware can co-schedule for a kernel (cached per kernel).
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers (sbbf_internal.h)
+// ---------------------------------------------------------------------------
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 template <typename K>
 int resident_blocks(K kernel, int threads, size_t smem) {
   int b = 0;
@@ -273,57 +359,57 @@ uint64_t grid_for(uint64_t work_items, uint64_t items_per_block, int sms, int pe
   return g < 1 ? 1 : g;
 }
 
-}  // namespace
-
-// ---------------------------------------------------------------------------
-// launchers (sbbf_internal.h)
-// ---------------------------------------------------------------------------
-uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
-void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
-
-cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, uint64_t nb,
+cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, const Geom& g,
                           const uint64_t* hashes, uint64_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   note_launch();
   if (variant == kInsertThread) {
     static const int occ = resident_blocks(insert_thread_kernel, kThreads, 0);
-    const uint64_t g = grid_for(n, kThreads * 4, di.sms, occ);
-    insert_thread_kernel<<<static_cast<unsigned>(g), kThreads, 0, s>>>(blocks, nb, hashes, n);
+    const uint64_t grid = grid_for(n, kThreads * 4, di.sms, occ);
+    insert_thread_kernel<<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n);
   } else if (variant == kInsertLane8Test) {
     static const int occ = resident_blocks(insert_lane8_kernel<true>, kThreads, 0);
-    const uint64_t g = grid_for(n, kThreads * 2, di.sms, occ);
-    insert_lane8_kernel<true><<<static_cast<unsigned>(g), kThreads, 0, s>>>(blocks, nb, hashes, n);
-  } else {
+    const uint64_t grid = grid_for(n, kThreads * 2, di.sms, occ);
+    insert_lane8_kernel<true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n);
+  } else if (variant == kInsertLane8) {
     static const int occ = resident_blocks(insert_lane8_kernel<false>, kThreads, 0);
-    const uint64_t g = grid_for(n, kThreads * 2, di.sms, occ);
-    insert_lane8_kernel<false><<<static_cast<unsigned>(g), kThreads, 0, s>>>(blocks, nb, hashes, n);
+    const uint64_t grid = grid_for(n, kThreads * 2, di.sms, occ);
+    insert_lane8_kernel<false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n);
+  } else if (variant == kInsertWideTest) {
+    static const int occ = resident_blocks(insert_wide_kernel<true>, kThreads, 0);
+    const uint64_t grid = grid_for(n, kThreads * 4, di.sms, occ);
+    insert_wide_kernel<true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n);
+  } else {
+    static const int occ = resident_blocks(insert_wide_kernel<false>, kThreads, 0);
+    const uint64_t grid = grid_for(n, kThreads * 4, di.sms, occ);
+    insert_wide_kernel<false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n);
   }
   return cudaGetLastError();
 }
 
 constexpr int kFindU = 8;
 
-cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* blocks, uint64_t nb,
+cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* blocks, const Geom& g,
                         const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   note_launch();
   if (variant == kFindSmem) {
-    const size_t smem = static_cast<size_t>(nb) * 32;
+    const size_t smem = static_cast<size_t>(g.nb_local) * 32;
     auto kern = bits ? find_smem_kernel<true> : find_smem_kernel<false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const int threads = 1024;
-    const uint64_t g = grid_for(n, threads * 8, di.sms, 1);
-    kern<<<static_cast<unsigned>(g), threads, smem, s>>>(blocks, nb, hashes, n, out);
+    const uint64_t grid = grid_for(n, threads * 8, di.sms, 1);
+    kern<<<static_cast<unsigned>(grid), threads, smem, s>>>(blocks, g, hashes, n, out);
   } else {
     static const int occ_b = resident_blocks(find_global_kernel<kFindU, true>, kThreads, 0);
     static const int occ_y = resident_blocks(find_global_kernel<kFindU, false>, kThreads, 0);
-    const uint64_t g = grid_for(n, kThreads * kFindU, di.sms, bits ? occ_b : occ_y);
+    const uint64_t grid = grid_for(n, kThreads * kFindU, di.sms, bits ? occ_b : occ_y);
     if (bits)
-      find_global_kernel<kFindU, true><<<static_cast<unsigned>(g), kThreads, 0, s>>>(blocks, nb, hashes, n, out);
+      find_global_kernel<kFindU, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n, out);
     else
-      find_global_kernel<kFindU, false><<<static_cast<unsigned>(g), kThreads, 0, s>>>(blocks, nb, hashes, n, out);
+      find_global_kernel<kFindU, false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n, out);
   }
   return cudaGetLastError();
 }
@@ -332,16 +418,16 @@ cudaError_t launch_block_index(const uint64_t* h, uint64_t n, uint64_t nb, uint6
                                cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   note_launch();
-  const uint64_t g = grid_for(n, 256, 148, 8);
-  block_index_kernel<<<static_cast<unsigned>(g), 256, 0, s>>>(h, n, nb, out);
+  const uint64_t grid = grid_for(n, 256, 148, 8);
+  block_index_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(h, n, nb, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_make_mask(const uint64_t* h, uint64_t n, uint32_t* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   note_launch();
-  const uint64_t g = grid_for(n, 256, 148, 8);
-  make_mask_kernel<<<static_cast<unsigned>(g), 256, 0, s>>>(h, n, out);
+  const uint64_t grid = grid_for(n, 256, 148, 8);
+  make_mask_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(h, n, out);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,309 @@
+"""Multi-GPU sharded SBBF: one process per GPU, filter partitioned by
+contiguous block range, keys routed to their owner with an all-to-all
+(the reference itself has no distributed mode).
+
+Rank r of P owns global blocks ``[floor(r*B/P), floor((r+1)*B/P))`` and keeps
+the global ``block_index`` (``mulhi(hash, B)``), so the shards concatenated in
+rank order are byte-identical to the reference's single B-bucket filter.
+
+insert: partition (``sbbf_shard_count`` + ``sbbf_shard_scatter``) ->
+        counts all-to-all -> keys all-to-all (NCCL over NVLink) -> local insert
+find:   same forward exchange (keeping source positions) -> local find (one
+        byte per key, receive order) -> reverse all-to-all of the answers ->
+        ``sbbf_scatter_u8`` back to source order (-> ``sbbf_pack_bits``).
+
+``torch.distributed`` is the plumbing (NCCL on GPUs, gloo in the CPU tests);
+the per-rank compute goes through ``ShardOps`` — ``CudaShardOps`` (the C ABI)
+in the product. Tests inject a host restatement to exercise the exchange
+logic on CPU with world_size 2.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import statistics
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+
+try:
+    import torch
+    import torch.distributed as dist
+except ImportError:  # pragma: no cover
+    torch = None
+    dist = None
+
+
+def shard_bounds(total_buckets: int, parts: int) -> list[int]:
+    """bounds[r] = floor(r * B / P), r = 0..P (the shard of rank r is [bounds[r], bounds[r+1]))."""
+    if parts < 1 or total_buckets < parts:
+        raise ValueError("need 1 <= parts <= total_buckets")
+    return [(total_buckets * r) // parts for r in range(parts + 1)]
+
+
+def owner_of_block(b: int, total_buckets: int, parts: int) -> int:
+    """Rank owning global block b: floor(((b+1)P - 1) / B)."""
+    return ((b + 1) * parts - 1) // total_buckets
+
+
+class ShardOps:
+    """Per-rank compute used by ShardedFilter (device- or host-resident)."""
+
+    def create(self, total: int, first: int, count: int):
+        raise NotImplementedError
+
+    def partition(self, keys, total: int, bounds: list[int], with_pos: bool):
+        """-> (counts: list[int], routed keys grouped by owner, positions or None)."""
+        raise NotImplementedError
+
+    def insert(self, shard, keys) -> None:
+        raise NotImplementedError
+
+    def find(self, shard, keys):
+        """-> one 0/1 byte per key (same device/type family as keys)."""
+        raise NotImplementedError
+
+    def scatter_back(self, answers, pos, n: int):
+        raise NotImplementedError
+
+    def pack_bits(self, answers):
+        raise NotImplementedError
+
+    def blocks(self, shard) -> np.ndarray:
+        raise NotImplementedError
+
+    def empty(self, n: int, dtype):
+        raise NotImplementedError
+
+
+class CudaShardOps(ShardOps):
+    """The product path: sm_100a kernels behind the C ABI."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.dev = torch.device("cuda", device)
+        self._bounds_cache: dict = {}
+
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream(self.dev).cuda_stream)
+
+    def create(self, total, first, count):
+        from .filter import SplitBlockFilter
+        f = SplitBlockFilter.__new__(SplitBlockFilter)
+        f._h = C.c_void_p()
+        check(_lib.lib().sbbf_gpu_create_shard(total, first, count, self.device, C.byref(f._h)),
+              "sbbf_gpu_create_shard")
+        f._device = self.device
+        return f
+
+    def _dev_bounds(self, bounds):
+        key = tuple(bounds)
+        if key not in self._bounds_cache:
+            self._bounds_cache[key] = torch.tensor(bounds[:-1], dtype=torch.int64, device=self.dev)
+        return self._bounds_cache[key]
+
+    def partition(self, keys, total, bounds, with_pos):
+        L = _lib.lib()
+        parts = len(bounds) - 1
+        n = keys.numel()
+        db = self._dev_bounds(bounds)
+        counts = torch.empty(parts, dtype=torch.int64, device=self.dev)
+        s = self._stream()
+        check(L.sbbf_shard_count(C.c_void_p(keys.data_ptr()), n, total, C.c_void_p(db.data_ptr()),
+                                 parts, C.c_void_p(counts.data_ptr()), s), "sbbf_shard_count")
+        offsets = torch.cumsum(counts, 0) - counts
+        cursor = torch.empty(parts, dtype=torch.int64, device=self.dev)
+        routed = torch.empty(n, dtype=torch.int64, device=self.dev)
+        pos = torch.empty(n, dtype=torch.int32, device=self.dev) if with_pos else None
+        check(L.sbbf_shard_scatter(C.c_void_p(keys.data_ptr()), n, total, C.c_void_p(db.data_ptr()),
+                                   parts, C.c_void_p(offsets.data_ptr()), C.c_void_p(cursor.data_ptr()),
+                                   C.c_void_p(routed.data_ptr()),
+                                   C.c_void_p(pos.data_ptr()) if with_pos else None, s),
+              "sbbf_shard_scatter")
+        return counts.tolist(), routed, pos
+
+    def insert(self, shard, keys):
+        check(_lib.lib().sbbf_gpu_insert_batch(shard.handle, C.c_void_p(keys.data_ptr()), keys.numel(),
+                                               self._stream()), "sbbf_gpu_insert_batch")
+
+    def find(self, shard, keys):
+        out = torch.empty(keys.numel(), dtype=torch.uint8, device=self.dev)
+        check(_lib.lib().sbbf_gpu_find_batch(shard.handle, C.c_void_p(keys.data_ptr()), keys.numel(),
+                                             C.c_void_p(out.data_ptr()), self._stream()),
+              "sbbf_gpu_find_batch")
+        return out
+
+    def scatter_back(self, answers, pos, n):
+        out = torch.empty(n, dtype=torch.uint8, device=self.dev)
+        check(_lib.lib().sbbf_scatter_u8(C.c_void_p(answers.data_ptr()), C.c_void_p(pos.data_ptr()), n,
+                                         C.c_void_p(out.data_ptr()), self._stream()), "sbbf_scatter_u8")
+        return out
+
+    def pack_bits(self, answers):
+        n = answers.numel()
+        out = torch.empty((n + 31) // 32, dtype=torch.int32, device=self.dev)
+        check(_lib.lib().sbbf_pack_bits(C.c_void_p(answers.data_ptr()), n, C.c_void_p(out.data_ptr()),
+                                        self._stream()), "sbbf_pack_bits")
+        return out
+
+    def blocks(self, shard):
+        return shard.blocks()
+
+    def empty(self, n, dtype):
+        return torch.empty(n, dtype=dtype, device=self.dev)
+
+
+class ShardedFilter:
+    """One rank's view of a P-way sharded filter of ``total_buckets`` buckets."""
+
+    def __init__(self, total_buckets: int, ops: ShardOps | None = None, group=None,
+                 rank: int | None = None, world: int | None = None):
+        if total_buckets <= 0:
+            raise ValueError("SplitBlockFilter needs at least one bucket")
+        self.group = group
+        init = dist is not None and dist.is_available() and dist.is_initialized()
+        self.rank = rank if rank is not None else (dist.get_rank(group) if init else 0)
+        self.world = world if world is not None else (dist.get_world_size(group) if init else 1)
+        self.total = int(total_buckets)
+        self.bounds = shard_bounds(self.total, self.world)
+        self.first = self.bounds[self.rank]
+        self.count = self.bounds[self.rank + 1] - self.first
+        if ops is None:
+            ops = CudaShardOps(torch.cuda.current_device())
+        self.ops = ops
+        self.shard = ops.create(self.total, self.first, self.count)
+        self.last_exchange: dict = {}
+
+    # -- exchange ---------------------------------------------------------------
+    def _exchange(self, payload, send_counts: list[int], recv_counts: list[int] | None = None):
+        """all-to-all with uneven splits; returns (received, recv_counts)."""
+        if not (dist is not None and dist.is_available() and dist.is_initialized()):
+            assert self.world == 1
+            return payload, send_counts
+        if recv_counts is None:
+            sc = torch.tensor(send_counts, dtype=torch.int64, device=payload.device)
+            rc = torch.empty_like(sc)
+            dist.all_to_all_single(rc, sc, group=self.group)
+            recv_counts = rc.tolist()
+        out = torch.empty(sum(recv_counts), dtype=payload.dtype, device=payload.device)
+        dist.all_to_all_single(out, payload, output_split_sizes=recv_counts,
+                               input_split_sizes=send_counts, group=self.group)
+        return out, recv_counts
+
+    # -- hot path -----------------------------------------------------------------
+    def add_hashes(self, keys) -> None:
+        """Insert this rank's batch (any keys; each is routed to its owner)."""
+        counts, routed, _ = self.ops.partition(keys, self.total, self.bounds, with_pos=False)
+        recv, rc = self._exchange(routed, counts)
+        self.last_exchange = {"sent": counts, "received": rc}
+        self.ops.insert(self.shard, recv)
+
+    def find_hashes(self, keys):
+        """0/1 byte per key of this rank's batch, in the batch's order."""
+        n = keys.numel()
+        counts, routed, pos = self.ops.partition(keys, self.total, self.bounds, with_pos=True)
+        recv, rc = self._exchange(routed, counts)
+        answers = self.ops.find(self.shard, recv)
+        back, _ = self._exchange(answers, rc, counts)
+        self.last_exchange = {"sent": counts, "received": rc}
+        return self.ops.scatter_back(back, pos, n)
+
+    def find_hashes_bits(self, keys):
+        return self.ops.pack_bits(self.find_hashes(keys))
+
+    # -- inspection -----------------------------------------------------------------
+    def local_blocks(self) -> np.ndarray:
+        return self.ops.blocks(self.shard)
+
+    def gather_blocks(self, dst: int = 0):
+        """Whole filter (num_buckets, 8) on rank `dst` (None elsewhere): the shards
+        in rank order, which must equal the single-filter bytes."""
+        mine = self.local_blocks()
+        if self.world == 1:
+            return mine
+        t = torch.from_numpy(mine.view(np.int32).reshape(-1).copy())
+        backend = dist.get_backend(self.group)
+        if backend == "nccl":
+            t = t.to(torch.device("cuda", torch.cuda.current_device()))
+        sizes = [(self.bounds[r + 1] - self.bounds[r]) * 8 for r in range(self.world)]
+        buf = [torch.empty(max(sizes), dtype=torch.int32, device=t.device) for _ in range(self.world)]
+        padded = torch.zeros(max(sizes), dtype=torch.int32, device=t.device)
+        padded[: t.numel()] = t
+        dist.all_gather(buf, padded, group=self.group)
+        if self.rank != dst:
+            return None
+        parts = [b[:s].cpu().numpy() for b, s in zip(buf, sizes)]
+        return np.concatenate(parts).view(np.uint32).reshape(-1, 8)
+
+
+# ---------------------------------------------------------------------------------
+# bench.py --gpus N (torchrun): weak scaling, one rank per GPU
+# ---------------------------------------------------------------------------------
+def bench_main(args) -> None:
+    """Each rank originates a config-2-sized batch (1M inserts, 10M lookups);
+    the filter is P x 1 MiB sharded by block range; keys cross NVLink to their
+    owner. value = all ranks' keys / max-over-ranks device time."""
+    from . import workload as W
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    cfg = W.CONFIGS[args.config]
+    N, L = cfg.inserts.n, cfg.lookups.n
+    total = cfg.num_buckets * world
+    # rank r originates insert positions [rN, (r+1)N) of one world-wide stream
+    spec = W.InsertSpec(seed=cfg.inserts.seed, n=N * world)
+    st = W.StreamHandle(spec, local)
+    ins = W.gen_inserts(st, rank * N, N, device=local)
+    look = W.gen_lookups(st, cfg.lookups, N * world, rank * L, L, device=local)
+    f = ShardedFilter(total)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    from ._lib import launch_count
+
+    def step():
+        f.add_hashes(ins)
+        return f.find_hashes_bits(look)
+
+    for _ in range(max(args.warmup, 3)):
+        f.shard.clear()
+        flush.zero_()
+        step()
+    torch.cuda.synchronize(dev)
+    times = []
+    l0 = launch_count()
+    for _ in range(args.steps):
+        f.shard.clear()
+        flush.zero_()
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        times.append(float(t.item()))
+    launches = launch_count() - l0
+    ms = statistics.mean(times)
+    if rank == 0:
+        line = {
+            "metric": "SBBF insert/lookup Gkeys/s (device-timed) vs random-32B-sector roofline",
+            "value": world * (N + L) / (ms * 1e-3) / 1e9, "unit": "Gkeys/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded splitmix64 hash streams, generated in HBM)",
+            "config": {"workload": f"sharded: per rank BASELINE config {args.config} batch "
+                                   f"({N:,} inserts + {L:,} lookups) into a {world}-way block-range "
+                                   f"sharded filter of {total} blocks; keys routed by NCCL all-to-all",
+                       "parallelism": f"shard{world}", "l2": "flushed between timed steps"},
+            "gpu_launches": launches, "time": "max over ranks of CUDA-event step time",
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()

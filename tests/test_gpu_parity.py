@@ -23,7 +23,8 @@ from paper_2101_01719_b200 import workload as W  # noqa: E402
 
 from .test_oracle import BLOCK_INDEX_KAT, MASK_KAT  # noqa: E402
 
-INSERT_VARIANTS = [_lib.INSERT_LANE8, _lib.INSERT_LANE8_TEST, _lib.INSERT_THREAD]
+INSERT_VARIANTS = [_lib.INSERT_LANE8, _lib.INSERT_LANE8_TEST, _lib.INSERT_THREAD,
+                   _lib.INSERT_WIDE, _lib.INSERT_WIDE_TEST]
 
 
 def sha(a):
@@ -283,7 +284,7 @@ def test_config_full(cuda, oracle, golden_configs, cid):
     if str(cid) not in golden_configs:
         pytest.skip(f"no golden for config {cid}")
     g = golden_configs[str(cid)]
-    r = run_config(cid, cuda, oracle, _lib.INSERT_LANE8_TEST if cid == 4 else 0)
+    r = run_config(cid, cuda, oracle)
     assert r["image_crc"] == g["image_crc"]
     assert r["popcount"] == g["popcount"]
     assert r["member_hits"] == g["members"]

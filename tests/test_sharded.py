@@ -1,0 +1,240 @@
+"""Sharded (multi-GPU) filter: exchange logic on CPU with gloo (world_size 2
+and 3), routing kernels and the NCCL self-exchange on one GPU.
+
+The CPU tests run the real ShardedFilter (paper_2101_01719_b200/sharded.py)
+with an injected host restatement of the per-rank compute (numpy), and check
+the gathered shards and every lookup answer against the oracle's
+single-filter result. Only the exchange/partition logic is under test there;
+the GPU tests cover the CUDA routing kernels.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2101_01719_b200 import sharded as S
+
+SEEDS = np.array([0x44974D91, 0x47B6137B, 0xA2B7289D, 0x8824AD5B,
+                  0x2DF1424B, 0x705495C7, 0x5C6BFB31, 0x9EFC4947], dtype=np.uint32)
+
+
+def mulhi64(a: np.ndarray, b: int) -> np.ndarray:
+    """floor(a*b / 2^64) with 32-bit limbs (vectorised)."""
+    a = a.astype(np.uint64)
+    M = np.uint64(0xFFFFFFFF)
+    al, ah = a & M, a >> np.uint64(32)
+    bl, bh = np.uint64(b & 0xFFFFFFFF), np.uint64(b >> 32)
+    ll, lh, hl, hh = al * bl, al * bh, ah * bl, ah * bh
+    mid = (ll >> np.uint64(32)) + (lh & M) + (hl & M)
+    return hh + (lh >> np.uint64(32)) + (hl >> np.uint64(32)) + (mid >> np.uint64(32))
+
+
+def masks(h: np.ndarray) -> np.ndarray:
+    low = (h & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    return (np.uint32(1) << ((low[:, None] * SEEDS[None, :]) >> np.uint32(27))).astype(np.uint32)
+
+
+class HostShardOps(S.ShardOps):
+    """Numpy restatement of the per-rank compute (test double for CudaShardOps)."""
+
+    def create(self, total, first, count):
+        return {"total": total, "first": first, "count": count,
+                "blocks": np.zeros((count, 8), np.uint32)}
+
+    def partition(self, keys, total, bounds, with_pos):
+        h = keys.numpy().view(np.uint64)
+        b = mulhi64(h, total)
+        owner = np.searchsorted(np.array(bounds[:-1], np.uint64), b, side="right") - 1
+        order = np.argsort(owner, kind="stable")
+        counts = np.bincount(owner, minlength=len(bounds) - 1).tolist()
+        routed = torch.from_numpy(h[order].view(np.int64).copy())
+        pos = torch.from_numpy(order.astype(np.int32)) if with_pos else None
+        return counts, routed, pos
+
+    def _local(self, shard, h):
+        b = mulhi64(h, shard["total"]) - np.uint64(shard["first"])
+        assert np.all(b < np.uint64(shard["count"])), "a key reached the wrong shard"
+        return b.astype(np.int64)
+
+    def insert(self, shard, keys):
+        h = keys.numpy().view(np.uint64)
+        if h.size:
+            np.bitwise_or.at(shard["blocks"], self._local(shard, h), masks(h))
+
+    def find(self, shard, keys):
+        h = keys.numpy().view(np.uint64)
+        if not h.size:
+            return torch.zeros(0, dtype=torch.uint8)
+        blk = shard["blocks"][self._local(shard, h)]
+        m = masks(h)
+        return torch.from_numpy(np.all((blk & m) == m, axis=1).astype(np.uint8))
+
+    def scatter_back(self, answers, pos, n):
+        out = np.zeros(n, np.uint8)
+        out[pos.numpy()] = answers.numpy()
+        return torch.from_numpy(out)
+
+    def pack_bits(self, answers):
+        a = answers.numpy()
+        return torch.from_numpy(np.packbits(a, bitorder="little").view(np.uint8))
+
+    def blocks(self, shard):
+        return shard["blocks"]
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, total, n_ins, n_look, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(1000 + rank)
+        ins = rng.integers(0, 2**64, size=n_ins, dtype=np.uint64)
+        f = S.ShardedFilter(total, ops=HostShardOps())
+        f.add_hashes(torch.from_numpy(ins.view(np.int64)))
+        dist.barrier()
+        look = np.concatenate([ins[: n_look // 2], rng.integers(0, 2**64, size=n_look - n_look // 2,
+                                                                  dtype=np.uint64)])
+        ans = f.find_hashes(torch.from_numpy(look.view(np.int64))).numpy()
+        full = f.gather_blocks(0)
+        q.put((rank, ins, look, ans, full, f.first, f.count, f.last_exchange))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,total", [(2, 4096), (2, 1001), (3, 7919)])
+def test_gloo_sharded_matches_oracle(oracle, world, total):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, total, 20_000, 10_000, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    got.sort(key=lambda x: x[0])
+    all_ins = np.concatenate([g[1] for g in got])
+    want = oracle.build(total, all_ins)
+    full = got[0][4]
+    assert full.shape == (total, 8)
+    assert np.array_equal(full, want)                     # shards concatenate to the reference filter
+    assert oracle.image_crc(full) == oracle.image_crc(want)
+    for rank, ins, look, ans, *_ in got:
+        assert np.array_equal(ans, oracle.find_hashes(want, look)), rank
+        assert ans[: len(look) // 2].all()               # no false negatives across ranks
+    bounds = S.shard_bounds(total, world)
+    for rank, *_rest in got:
+        first, count = got[rank][5], got[rank][6]
+        assert (first, count) == (bounds[rank], bounds[rank + 1] - bounds[rank])
+    # exchange bookkeeping: what rank a sent to b is what b received from a
+    for a in range(world):
+        for b in range(world):
+            assert got[a][7]["sent"][b] == got[b][7]["received"][a]
+
+
+def test_bounds_and_owner():
+    for total in (1, 7, 4096, 1001, 2**28, 2**28 + 3):
+        for parts in (1, 2, 3, 4, 8):
+            if parts > total:
+                continue
+            b = S.shard_bounds(total, parts)
+            assert b[0] == 0 and b[-1] == total and all(x <= y for x, y in zip(b, b[1:]))
+            for blk in {0, total - 1, total // 2, total // 3, max(0, b[min(1, parts)] - 1)}:
+                r = S.owner_of_block(blk, total, parts)
+                assert b[r] <= blk < b[r + 1]
+
+
+# ---------------------------------------------------------------------------------
+# GPU: routing kernels, multi-shard on one device, NCCL self-exchange
+# ---------------------------------------------------------------------------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts", [1, 2, 3, 8])
+def test_cuda_partition_kernels(cuda, parts):
+    ops = S.CudaShardOps(0)
+    total = 2**20 + 17
+    rng = np.random.default_rng(parts)
+    h = rng.integers(0, 2**64, size=1_000_003, dtype=np.uint64)
+    d = torch.from_numpy(h.view(np.int64)).to(cuda)
+    bounds = S.shard_bounds(total, parts)
+    counts, routed, pos = ops.partition(d, total, bounds, with_pos=True)
+    host = HostShardOps()
+    want_counts, _, _ = host.partition(torch.from_numpy(h.view(np.int64)), total, bounds, True)
+    assert counts == want_counts
+    r = routed.cpu().numpy().view(np.uint64)
+    p = pos.cpu().numpy().astype(np.int64)
+    assert np.array_equal(np.sort(p), np.arange(h.size))         # a permutation
+    assert np.array_equal(r, h[p])                               # routed[i] = h[pos[i]]
+    off = np.concatenate([[0], np.cumsum(counts)])
+    blk = mulhi64(r, total)
+    for k in range(parts):
+        seg = blk[off[k]:off[k + 1]]
+        assert np.all(seg >= bounds[k]) and np.all(seg < bounds[k + 1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts", [2, 4, 8])
+def test_multi_shard_one_gpu(cuda, oracle, parts):
+    """P shards on one GPU fed by the routing kernels (no collective): the
+    concatenated shards equal the single filter; lookups agree."""
+    ops = S.CudaShardOps(0)
+    total = 32768 * parts
+    rng = np.random.default_rng(77)
+    h = rng.integers(0, 2**64, size=2_000_000, dtype=np.uint64)
+    look = np.concatenate([h[:500_000], rng.integers(0, 2**64, size=500_000, dtype=np.uint64)])
+    bounds = S.shard_bounds(total, parts)
+    shards = [ops.create(total, bounds[r], bounds[r + 1] - bounds[r]) for r in range(parts)]
+    counts, routed, _ = ops.partition(torch.from_numpy(h.view(np.int64)).to(cuda), total, bounds, False)
+    off = np.concatenate([[0], np.cumsum(counts)])
+    for r in range(parts):
+        ops.insert(shards[r], routed[off[r]:off[r + 1]])
+    full = np.concatenate([s.blocks() for s in shards])
+    want = oracle.build(total, h)
+    assert np.array_equal(full, want)
+    dl = torch.from_numpy(look.view(np.int64)).to(cuda)
+    counts, routed, pos = ops.partition(dl, total, bounds, True)
+    off = np.concatenate([[0], np.cumsum(counts)])
+    answers = torch.cat([ops.find(shards[r], routed[off[r]:off[r + 1]]) for r in range(parts)])
+    back = ops.scatter_back(answers, pos, look.size).cpu().numpy()
+    assert np.array_equal(back, oracle.find_hashes(want, look))
+    bits = ops.pack_bits(ops.scatter_back(answers, pos, look.size)).cpu().numpy().view(np.uint32)
+    from oracle import bits_to_bytes
+    assert np.array_equal(bits_to_bytes(bits, look.size), back)
+    # keys a shard does not own: ignored by insert, answer 0 in find
+    before = shards[0].blocks()
+    ops.insert(shards[0], routed[off[-2]:off[-1]])
+    assert np.array_equal(shards[0].blocks(), before)
+    assert int(ops.find(shards[0], routed[off[-2]:off[-1]]).sum()) == 0
+
+
+@pytest.mark.gpu
+def test_nccl_self_exchange(cuda, oracle):
+    """The full ShardedFilter path over NCCL at world_size 1 (self-exchange)."""
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=cuda)
+    try:
+        rng = np.random.default_rng(5)
+        h = rng.integers(0, 2**64, size=1_000_000, dtype=np.uint64)
+        f = S.ShardedFilter(32768)
+        f.add_hashes(torch.from_numpy(h.view(np.int64)).to(cuda))
+        want = oracle.build(32768, h)
+        assert np.array_equal(f.gather_blocks(), want)
+        look = np.concatenate([h[:1000], rng.integers(0, 2**64, size=100_000, dtype=np.uint64)])
+        ans = f.find_hashes(torch.from_numpy(look.view(np.int64)).to(cuda)).cpu().numpy()
+        assert np.array_equal(ans, oracle.find_hashes(want, look))
+    finally:
+        dist.destroy_process_group()
