@@ -1,0 +1,73 @@
+// C++ drop-in test: the reference's call pattern (tools/harness.cpp:160-171:
+// construct, add_hashes(span), find_hashes(span, uint8_t*)) against
+// sbbf::gpu::SplitBlockFilter, checked byte-for-byte with the oracle.
+// Built and run by tests/test_cpp_dropin.py.
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <vector>
+
+#include "sbbf_gpu.hpp"
+
+extern "C" {
+void oracle_gen_splitmix(uint64_t seed, uint64_t start, uint64_t n, uint64_t* out);
+void oracle_add_hashes(uint32_t* blocks, uint64_t num_buckets, const uint64_t* hashes, uint64_t n);
+void oracle_find_hashes(const uint32_t* blocks, uint64_t num_buckets, const uint64_t* hashes,
+                        uint64_t n, uint8_t* results);
+uint32_t oracle_image_crc(const uint32_t* blocks, uint64_t num_buckets, uint32_t hasher_id);
+}
+
+#define REQUIRE(c)                                                     \
+  do {                                                                 \
+    if (!(c)) {                                                        \
+      std::fprintf(stderr, "FAILED %s at line %d\n", #c, __LINE__);   \
+      return 1;                                                        \
+    }                                                                  \
+  } while (0)
+
+int main() {
+  // config 1: 100k keys (splitmix64 seed 1) into 4096 blocks
+  const uint64_t nb = 4096;
+  std::vector<uint64_t> ins(100000), non(1000000);
+  oracle_gen_splitmix(1, 0, ins.size(), ins.data());
+  oracle_gen_splitmix(2, 0, non.size(), non.data());
+
+  sbbf::gpu::SplitBlockFilter f(nb);
+  REQUIRE(f.num_buckets() == nb && f.size_bytes() == nb * 32 && f.hasher_id() == 0);
+  f.add_hashes(ins);
+  const auto blocks = f.blocks();
+
+  std::vector<uint32_t> want(nb * 8, 0);
+  oracle_add_hashes(want.data(), nb, ins.data(), ins.size());
+  REQUIRE(std::memcmp(blocks.data(), want.data(), nb * 32) == 0);
+  REQUIRE(oracle_image_crc(reinterpret_cast<const uint32_t*>(blocks.data()), nb, 0) == 0xe34f8befu);
+
+  std::vector<uint8_t> got(non.size()), ref(non.size());
+  f.find_hashes(non, got.data());
+  oracle_find_hashes(want.data(), nb, non.data(), non.size(), ref.data());
+  REQUIRE(got == ref);
+  uint64_t fp = 0;
+  for (uint8_t r : got) fp += r;
+  REQUIRE(fp == 10190);  // SURVEY.md §8(c) golden FP count
+  const auto mem = f.find_hashes(ins);
+  for (uint8_t r : mem) REQUIRE(r == 1);
+
+  // error behaviour mirrors filter.cpp:160-162
+  bool threw = false;
+  try {
+    sbbf::gpu::SplitBlockFilter bad(0);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  REQUIRE(threw);
+
+  // from_blocks / operator== / single-key ops
+  auto g = sbbf::gpu::SplitBlockFilter::from_blocks(blocks);
+  REQUIRE(g == f);
+  sbbf::gpu::SplitBlockFilter one(1);
+  one.add_hash(0);
+  REQUIRE(one.find_hash(0));
+  for (uint32_t lane : one.blocks()[0].lanes) REQUIRE(lane == 1u);
+  std::printf("cpp drop-in ok: crc 0xe34f8bef, %llu false positives\n", (unsigned long long)fp);
+  return 0;
+}
