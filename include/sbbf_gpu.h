@@ -60,14 +60,17 @@ enum {
   SBBF_INSERT_LANE8_TEST = 2, /* as LANE8, but skip lanes whose bit is already set (hot keys) */
   SBBF_INSERT_THREAD = 3,     /* 1 thread per key, 8 red.or per key (baseline variant) */
   SBBF_INSERT_WIDE = 4,       /* 4 threads per key, one 64-bit red.or per lane pair */
-  SBBF_INSERT_WIDE_TEST = 5   /* as WIDE, skipping lane pairs whose bits are all set */
+  SBBF_INSERT_WIDE_TEST = 5,  /* as WIDE, skipping lane pairs whose bits are all set */
+  SBBF_INSERT_BLOCKED = 6     /* group the batch by filter slice first, then insert slice by
+                                 slice so the atomics hit L2 (filters beyond L2) */
 };
 
 /* Lookup strategies (sbbf_gpu_set_find_variant). AUTO picks per call. */
 enum {
   SBBF_FIND_AUTO = 0,
   SBBF_FIND_GLOBAL = 1, /* one 256-bit LDG per key from L2/HBM */
-  SBBF_FIND_SMEM = 2    /* filter staged into shared memory per CTA (small filters only) */
+  SBBF_FIND_SMEM = 2,   /* filter staged into shared memory per CTA (small filters only) */
+  SBBF_FIND_BLOCKED = 3 /* group the batch by filter slice, probe slice by slice from L2 */
 };
 
 typedef struct sbbf_gpu sbbf_gpu_t;

@@ -21,8 +21,9 @@ SBBF_ECUDA = -3
 SBBF_ENODEV = -4
 SBBF_EFORMAT = -5
 
-INSERT_AUTO, INSERT_LANE8, INSERT_LANE8_TEST, INSERT_THREAD, INSERT_WIDE, INSERT_WIDE_TEST = 0, 1, 2, 3, 4, 5
-FIND_AUTO, FIND_GLOBAL, FIND_SMEM = 0, 1, 2
+(INSERT_AUTO, INSERT_LANE8, INSERT_LANE8_TEST, INSERT_THREAD, INSERT_WIDE, INSERT_WIDE_TEST,
+ INSERT_BLOCKED) = range(7)
+FIND_AUTO, FIND_GLOBAL, FIND_SMEM, FIND_BLOCKED = range(4)
 
 # Every symbol include/sbbf_gpu.h and include/sbbf_workload.h declare, with
 # (restype, argtypes). tests/test_abi.py checks the .so exports all of them.

@@ -13,6 +13,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "sbbf_internal.h"
 
@@ -67,18 +68,27 @@ struct sbbf_gpu {
   uint64_t* d_stage[2] = {nullptr, nullptr};
   void* d_res[2] = {nullptr, nullptr};
   uint64_t* d_one = nullptr;  // single-key scratch: [hash, result]
+  // L2-blocked path: filter slice bounds (global block ids), created lazily.
+  std::mutex plan_mu;
+  sbbf::BlockedPlan plan;
+  uint64_t* d_plan_bounds = nullptr;
 };
 
 namespace {
 
+constexpr uint64_t kSliceBytes = 24ull << 20;  // blocked path: one slice + chunk bitmap stay in L2
+
+bool beyond_l2(const sbbf_gpu* f) { return f->nb * 32 > f->di.l2_bytes / 2; }
+
 int resolve_insert(const sbbf_gpu* f, uint64_t n) {
-  (void)n;
   if (f->insert_variant != SBBF_INSERT_AUTO) return f->insert_variant;
   // L2-resident filters are bound by the L2 atomic unit (op count): plain
-  // 64-bit reds. Larger filters: load the lane pair first (the read path
-  // fills L2 faster than a missing atomic does, and duplicates/hot keys skip
-  // the atomic entirely).
-  return f->nb * 32 <= f->di.l2_bytes / 2 ? SBBF_INSERT_WIDE : SBBF_INSERT_WIDE_TEST;
+  // 64-bit reds. Beyond L2, a batch of at least half a key per block is
+  // grouped by filter slice first (blocked path, sbbf_blocked.cu); smaller
+  // batches load the lane pair first (a load fills L2 faster than a missing
+  // atomic, and duplicates/hot keys skip the atomic entirely).
+  if (!beyond_l2(f)) return SBBF_INSERT_WIDE;
+  return n >= f->nb / 2 ? SBBF_INSERT_BLOCKED : SBBF_INSERT_WIDE_TEST;
 }
 
 bool smem_fits(const sbbf_gpu* f) {
@@ -88,11 +98,62 @@ bool smem_fits(const sbbf_gpu* f) {
 
 int resolve_find(const sbbf_gpu* f, uint64_t n) {
   if (f->find_variant == SBBF_FIND_SMEM && smem_fits(f)) return SBBF_FIND_SMEM;
+  if (f->find_variant == SBBF_FIND_BLOCKED) return SBBF_FIND_BLOCKED;
   if (f->find_variant != SBBF_FIND_AUTO) return SBBF_FIND_GLOBAL;
   // Staging the filter costs one filter-size copy per CTA; it pays once each
   // SM probes enough keys to amortise it.
   if (smem_fits(f) && n >= 64 * f->nb) return SBBF_FIND_SMEM;
+  if (beyond_l2(f) && n >= f->nb / 2) return SBBF_FIND_BLOCKED;
   return SBBF_FIND_GLOBAL;
+}
+
+// Slice bounds for the blocked path: parts slices of ~kSliceBytes over this
+// shard's blocks, as global block ids (the partition kernel compares
+// block_index against them).
+int ensure_plan(sbbf_gpu* f) {
+  std::lock_guard<std::mutex> lock(f->plan_mu);
+  if (f->d_plan_bounds) return SBBF_OK;
+  uint64_t parts = (f->nb * 32 + kSliceBytes - 1) / kSliceBytes;
+  parts = parts < 2 ? 2 : (parts > 1024 ? 1024 : parts);
+  if (parts > f->nb) parts = f->nb;
+  std::vector<uint64_t> b(parts);
+  for (uint64_t k = 0; k < parts; ++k)
+    b[k] = f->geom.first + static_cast<uint64_t>((static_cast<unsigned __int128>(f->nb) * k) / parts);
+  cudaError_t e = cudaMalloc(&f->d_plan_bounds, parts * sizeof(uint64_t));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(f->d_plan_bounds, b.data(), parts * sizeof(uint64_t), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(f->d_plan_bounds);
+    f->d_plan_bounds = nullptr;
+    return cuda_fail(e, "blocked plan");
+  }
+  // Keep freed scratch in the stream-ordered pool between calls.
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, f->di.device) == cudaSuccess) {
+    uint64_t keep = ~uint64_t{0};
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  f->plan.parts = static_cast<uint32_t>(parts);
+  f->plan.d_bounds = f->d_plan_bounds;
+  return SBBF_OK;
+}
+
+// One dispatch point for every insert / find launch of the ABI.
+cudaError_t do_insert(sbbf_gpu* f, int variant, const uint64_t* h, uint64_t n, cudaStream_t s) {
+  if (variant == SBBF_INSERT_BLOCKED) {
+    if (ensure_plan(f) != SBBF_OK) return cudaErrorMemoryAllocation;
+    return sbbf::blocked_insert(f->di, f->d_blocks, f->geom, f->plan, h, n, s);
+  }
+  return sbbf::launch_insert(f->di, variant, f->d_blocks, f->geom, h, n, s);
+}
+
+cudaError_t do_find(sbbf_gpu* f, int variant, const uint64_t* h, uint64_t n, void* out, bool bits,
+                    cudaStream_t s) {
+  if (variant == SBBF_FIND_BLOCKED) {
+    if (ensure_plan(f) != SBBF_OK) return cudaErrorMemoryAllocation;
+    return sbbf::blocked_find(f->di, f->d_blocks, f->geom, f->plan, h, n, out, bits, s);
+  }
+  return sbbf::launch_find(f->di, variant, f->d_blocks, f->geom, h, n, out, bits, s);
 }
 
 int ensure_host_path(sbbf_gpu* f) {
@@ -129,13 +190,11 @@ int host_pipeline(sbbf_gpu* f, HostOp op, const uint64_t* h_hashes, uint64_t n, 
                                     cudaMemcpyHostToDevice, f->hs[s]);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(H2D)");
     if (op == HostOp::kInsert) {
-      e = sbbf::launch_insert(f->di, resolve_insert(f, m), f->d_blocks, f->geom, f->d_stage[s], m,
-                              f->hs[s]);
+      e = do_insert(f, resolve_insert(f, m), f->d_stage[s], m, f->hs[s]);
       if (e != cudaSuccess) return cuda_fail(e, "insert kernel");
     } else {
       const bool bits = op == HostOp::kFindBits;
-      e = sbbf::launch_find(f->di, resolve_find(f, m), f->d_blocks, f->geom, f->d_stage[s], m,
-                            f->d_res[s], bits, f->hs[s]);
+      e = do_find(f, resolve_find(f, m), f->d_stage[s], m, f->d_res[s], bits, f->hs[s]);
       if (e != cudaSuccess) return cuda_fail(e, "find kernel");
       // kHostChunk is a multiple of 32, so chunk bitmaps tile the output.
       void* dst = bits ? static_cast<void*>(static_cast<uint32_t*>(h_out) + off / 32)
@@ -212,6 +271,7 @@ int sbbf_gpu_destroy(sbbf_gpu_t* f) {
     if (f->d_blocks) cudaDeviceSynchronize();
     cudaFree(f->d_blocks);
     cudaFree(f->d_one);
+    cudaFree(f->d_plan_bounds);
     for (int i = 0; i < 2; ++i) {
       if (f->hs[i]) cudaStreamDestroy(f->hs[i]);
       cudaFree(f->d_stage[i]);
@@ -248,8 +308,7 @@ int sbbf_gpu_insert_batch(sbbf_gpu_t* f, const uint64_t* d_hashes, uint64_t n, v
   if (n == 0) return SBBF_OK;  // empty batch is a no-op (filter_test.cpp:169-175)
   if (!d_hashes) return fail(SBBF_EINVAL, "null hashes");
   DeviceGuard g(f->di.device);
-  cudaError_t e = sbbf::launch_insert(f->di, resolve_insert(f, n), f->d_blocks, f->geom, d_hashes, n,
-                                      static_cast<cudaStream_t>(stream));
+  cudaError_t e = do_insert(f, resolve_insert(f, n), d_hashes, n, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "insert kernel launch");
 }
 
@@ -259,8 +318,8 @@ static int find_common(const sbbf_gpu_t* f, const uint64_t* d_hashes, uint64_t n
   if (n == 0) return SBBF_OK;
   if (!d_hashes || !d_out) return fail(SBBF_EINVAL, "null buffer");
   DeviceGuard g(f->di.device);
-  cudaError_t e = sbbf::launch_find(f->di, resolve_find(f, n), f->d_blocks, f->geom, d_hashes, n,
-                                    d_out, bits, static_cast<cudaStream_t>(stream));
+  sbbf_gpu* m = const_cast<sbbf_gpu*>(f);  // the blocked plan is created lazily
+  cudaError_t e = do_find(m, resolve_find(f, n), d_hashes, n, d_out, bits, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "find kernel launch");
 }
 
@@ -380,7 +439,7 @@ int sbbf_gpu_set_l2_fetch_granularity(int device, int bytes, int* old) {
 
 int sbbf_gpu_set_insert_variant(sbbf_gpu_t* f, int variant) {
   if (!f) return fail(SBBF_EINVAL, "null filter");
-  if (variant < SBBF_INSERT_AUTO || variant > SBBF_INSERT_WIDE_TEST)
+  if (variant < SBBF_INSERT_AUTO || variant > SBBF_INSERT_BLOCKED)
     return fail(SBBF_EINVAL, "unknown insert variant");
   f->insert_variant = variant;
   return SBBF_OK;
@@ -388,7 +447,7 @@ int sbbf_gpu_set_insert_variant(sbbf_gpu_t* f, int variant) {
 
 int sbbf_gpu_set_find_variant(sbbf_gpu_t* f, int variant) {
   if (!f) return fail(SBBF_EINVAL, "null filter");
-  if (variant < SBBF_FIND_AUTO || variant > SBBF_FIND_SMEM)
+  if (variant < SBBF_FIND_AUTO || variant > SBBF_FIND_BLOCKED)
     return fail(SBBF_EINVAL, "unknown find variant");
   if (variant == SBBF_FIND_SMEM && !smem_fits(f))
     return fail(SBBF_EINVAL, "filter too large for the shared-memory path");

@@ -96,6 +96,15 @@ __device__ __forceinline__ void ld_block_nc(const uint32_t* p, Block8& b) {
       : "l"(p));
 }
 
+// Same without the L2 priority hint (blocked path: the working slice changes
+// as the batch advances, so no line should outlive its slice).
+__device__ __forceinline__ void ld_block_nc_normal(const uint32_t* p, Block8& b) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(b.w[0]), "=r"(b.w[1]), "=r"(b.w[2]), "=r"(b.w[3]), "=r"(b.w[4]),
+                 "=r"(b.w[5]), "=r"(b.w[6]), "=r"(b.w[7])
+               : "l"(p));
+}
+
 // Same, but L1-allocating (L2-resident filters get some L1 reuse).
 __device__ __forceinline__ void ld_block_l1(const uint32_t* p, Block8& b) {
   asm volatile("ld.global.nc.L2::evict_last.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"

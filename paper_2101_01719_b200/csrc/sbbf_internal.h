@@ -43,6 +43,29 @@ cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, c
                           const uint64_t* hashes, uint64_t n, cudaStream_t s);
 cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* blocks, const Geom& g,
                         const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s);
+// Bucket `hashes` by block range: bucket k holds the keys whose block_index
+// (against `total`) lies in [d_bounds[k], d_bounds[k+1]). Writes the counts,
+// their exclusive prefix sum, the grouped keys and (optionally) each key's
+// source index. All stream-ordered, no host sync. parts <= 1024.
+cudaError_t launch_partition(const uint64_t* hashes, uint64_t n, uint64_t total, const uint64_t* d_bounds,
+                             uint32_t parts, uint64_t* d_counts, uint64_t* d_offsets, uint64_t* d_cursor,
+                             uint64_t* d_out, uint32_t* d_pos, int sms, cudaStream_t s);
+
+// insert_wide over `n` keys with one warp step per 128 keys and the grid
+// covering the batch once, so CTAs run in key order (blocked path).
+cudaError_t launch_insert_ordered(const DeviceInfo& di, uint32_t* blocks, const Geom& g,
+                                  const uint64_t* hashes, uint64_t n, cudaStream_t s);
+
+// L2-blocked paths for filters larger than L2 (sbbf_blocked.cu).
+struct BlockedPlan {
+  uint32_t parts = 0;             // filter slices
+  const uint64_t* d_bounds = nullptr;  // parts entries, global block ids
+};
+cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
+                           const uint64_t* hashes, uint64_t n, cudaStream_t s);
+cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
+                         const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s);
+
 cudaError_t launch_block_index(const uint64_t* h, uint64_t n, uint64_t nb, uint64_t* out,
                                cudaStream_t s);
 cudaError_t launch_make_mask(const uint64_t* h, uint64_t n, uint32_t* out, cudaStream_t s);

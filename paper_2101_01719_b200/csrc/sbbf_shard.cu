@@ -132,7 +132,45 @@ __global__ void pack_bits_kernel(const uint8_t* __restrict__ src, uint64_t n, ui
 
 int shard_rc(cudaError_t e) { return e == cudaSuccess ? SBBF_OK : SBBF_ECUDA; }
 
+// Exclusive prefix sum of parts (<= 1024) counts in one CTA.
+__global__ void __launch_bounds__(1024) exclusive_scan_kernel(const unsigned long long* __restrict__ counts,
+                                                              uint32_t parts,
+                                                              unsigned long long* __restrict__ offsets) {
+  __shared__ unsigned long long buf[2][kMaxParts];
+  const uint32_t t = threadIdx.x;
+  int cur = 0;
+  buf[0][t] = (t > 0 && t <= parts) ? counts[t - 1] : 0ull;
+  __syncthreads();
+  for (uint32_t d = 1; d < kMaxParts; d <<= 1) {
+    buf[cur ^ 1][t] = buf[cur][t] + (t >= d ? buf[cur][t - d] : 0ull);
+    cur ^= 1;
+    __syncthreads();
+  }
+  if (t < parts) offsets[t] = buf[cur][t];
+}
+
 }  // namespace
+
+cudaError_t launch_partition(const uint64_t* hashes, uint64_t n, uint64_t total, const uint64_t* d_bounds,
+                             uint32_t parts, uint64_t* d_counts, uint64_t* d_offsets, uint64_t* d_cursor,
+                             uint64_t* d_out, uint32_t* d_pos, int sms, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(d_counts, 0, parts * sizeof(uint64_t), s);
+  if (e != cudaSuccess || n == 0) return e;
+  const uint64_t grid = grid_for(n, kChunk, sms, 8);
+  note_launch();
+  shard_count_kernel<<<static_cast<unsigned>(grid), kShardThreads, 0, s>>>(
+      hashes, n, total, d_bounds, parts, reinterpret_cast<unsigned long long*>(d_counts));
+  note_launch();
+  exclusive_scan_kernel<<<1, kMaxParts, 0, s>>>(reinterpret_cast<unsigned long long*>(d_counts), parts,
+                                                reinterpret_cast<unsigned long long*>(d_offsets));
+  e = cudaMemcpyAsync(d_cursor, d_offsets, parts * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return e;
+  note_launch();
+  shard_scatter_kernel<<<static_cast<unsigned>(grid), kShardThreads, 0, s>>>(
+      hashes, n, total, d_bounds, parts, reinterpret_cast<unsigned long long*>(d_cursor), d_out, d_pos);
+  return cudaGetLastError();
+}
+
 }  // namespace sbbf
 
 extern "C" {

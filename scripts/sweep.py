@@ -90,7 +90,8 @@ def variants():
         byts = torch.empty(Lk, dtype=torch.uint8, device=DEV)
         f = SplitBlockFilter(cfg.num_buckets)
         chunk = cfg.insert_chunk or N
-        for iv, name in ((1, "lane8"), (2, "lane8_test"), (3, "thread"), (4, "wide"), (5, "wide_test")):
+        for iv, name in ((1, "lane8"), (2, "lane8_test"), (3, "thread"), (4, "wide"), (5, "wide_test"),
+                         (6, "blocked")):
             f.set_insert_variant(iv)
 
             def ins_fn():
@@ -106,7 +107,7 @@ def variants():
         f.clear()
         for s0 in range(0, N, chunk):
             f.add_hashes(ins[s0:s0 + chunk])
-        fvs = [(1, "global")] + ([(2, "smem")] if cfg.filter_bytes <= 200 * 1024 else [])
+        fvs = [(1, "global"), (3, "blocked")] + ([(2, "smem")] if cfg.filter_bytes <= 200 * 1024 else [])
         for fv, name in fvs:
             f.set_find_variant(fv)
             for kind, fn in (("bits", lambda: f.find_hashes_bits(look, bits)),

@@ -24,7 +24,8 @@ from paper_2101_01719_b200 import workload as W  # noqa: E402
 from .test_oracle import BLOCK_INDEX_KAT, MASK_KAT  # noqa: E402
 
 INSERT_VARIANTS = [_lib.INSERT_LANE8, _lib.INSERT_LANE8_TEST, _lib.INSERT_THREAD,
-                   _lib.INSERT_WIDE, _lib.INSERT_WIDE_TEST]
+                   _lib.INSERT_WIDE, _lib.INSERT_WIDE_TEST, _lib.INSERT_BLOCKED]
+FIND_VARIANTS = [_lib.FIND_GLOBAL, _lib.FIND_SMEM, _lib.FIND_BLOCKED]
 
 
 def sha(a):
@@ -104,11 +105,11 @@ def test_random_parity(cuda, oracle, nb, n):
         f.add_hashes(dev(hs, cuda))
         assert np.array_equal(f.blocks(), want), v
     want_res = oracle.find_hashes(want, probes)
-    for fv in (_lib.FIND_GLOBAL, _lib.FIND_SMEM):
+    for fv in FIND_VARIANTS:
         if fv == _lib.FIND_SMEM and nb * 32 > 200 * 1024:
             continue
         f.set_find_variant(fv)
-        assert np.array_equal(f.find_hashes(dev(probes, cuda)).cpu().numpy(), want_res)
+        assert np.array_equal(f.find_hashes(dev(probes, cuda)).cpu().numpy(), want_res), fv
         bits = u32(f.find_hashes_bits(dev(probes, cuda)))
         assert bits.size == (probes.size + 31) // 32
         assert np.array_equal(bits_to_bytes(bits, probes.size), want_res)
@@ -269,7 +270,7 @@ def run_config(cid, cuda, oracle, insert_variant=0, find_variant=0):
 @pytest.mark.parametrize("iv", INSERT_VARIANTS)
 def test_config_small(cuda, oracle, golden_configs, cid, iv):
     g = golden_configs[str(cid)]
-    for fv in (_lib.FIND_GLOBAL, _lib.FIND_SMEM if cid == 1 else _lib.FIND_AUTO):
+    for fv in (_lib.FIND_GLOBAL, _lib.FIND_SMEM if cid == 1 else _lib.FIND_BLOCKED):
         r = run_config(cid, cuda, oracle, iv, fv)
         assert r["image_crc"] == g["image_crc"]
         assert r["popcount"] == g["popcount"]
@@ -279,12 +280,15 @@ def test_config_small(cuda, oracle, golden_configs, cid, iv):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cid", [3, 4])
-def test_config_full(cuda, oracle, golden_configs, cid):
+@pytest.mark.parametrize("cid,iv,fv", [(3, 0, 0), (4, 0, 0),
+                                       (3, _lib.INSERT_WIDE_TEST, _lib.FIND_GLOBAL),
+                                       (4, _lib.INSERT_WIDE_TEST, _lib.FIND_GLOBAL)])
+def test_config_full(cuda, oracle, golden_configs, cid, iv, fv):
+    """Full configs 3 and 4: AUTO (the L2-blocked path) and the direct path."""
     if str(cid) not in golden_configs:
         pytest.skip(f"no golden for config {cid}")
     g = golden_configs[str(cid)]
-    r = run_config(cid, cuda, oracle)
+    r = run_config(cid, cuda, oracle, iv, fv)
     assert r["image_crc"] == g["image_crc"]
     assert r["popcount"] == g["popcount"]
     assert r["member_hits"] == g["members"]
