@@ -5,17 +5,17 @@
 // rate tops out at 37-43 G/s whatever the access path (LSU, TMA, gather4;
 // profiles/r1_microbench_*.log). The blocked path trades that for streaming:
 //
-//   1. partition the batch by filter slice (launch_partition: CTA-chunked
-//      histogram + reservation scatter, 8 B in / 12 B out per key),
+//   1. bucket the batch by filter slice (bucket_count + bucket_scatter:
+//      8 B in, 8 B (+4 B source position) out per key),
 //   2. process the grouped keys in slice order — CTAs are dispatched in
 //      blockIdx order, so the keys in flight at any moment fall in one or two
-//      slices (<= ~24 MiB each) and their probes/atomics hit L2; every filter
+//      slices (~16 MiB each) and their probes/atomics hit L2; every filter
 //      line is fetched from HBM about once per chunk,
 //   3. lookups set their answer bit at the key's source position with a red
 //      into a chunk bitmap that stays L2-resident.
 //
-// Per-key HBM traffic ~ 8 (read) + 12 (grouped write) + 12 (grouped read)
-// + filter_bytes / chunk_keys, instead of a ~128-byte random line fill.
+// Per-key HBM traffic ~ 8 (count) + 8 + 12 (scatter) + 12 (probe) +
+// filter_bytes / chunk_keys, instead of a ~128-byte random line fill.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -31,18 +31,257 @@ constexpr int kProbeU = 8;
 constexpr int kProbeThreads = 256;
 constexpr uint64_t kProbeTile = kProbeThreads * kProbeU;
 
+// ---------------------------------------------------------------------------
+// bucket partition
+// ---------------------------------------------------------------------------
+// Bucket of a key = its local block scaled to [0, S) by a 32.32 fixed-point
+// multiply: monotone in the block, so bucket k is a contiguous block range of
+// ~nb/S blocks (neighbouring buckets may share a boundary block — harmless,
+// each key is still handled on its own). S <= 64.
+//
+// Ranking inside a warp is a ballot "multisplit": for a BITS-bit bucket id,
+// BITS ballots give every lane the mask of lanes holding its bucket (AND of
+// ballot or ~ballot per bit). Per-warp running counts live in registers —
+// lane l owns buckets l and l+32 — so there are no per-key shared-memory
+// atomics (~2 cycles per lane on this part) and no __match_any_sync (which
+// measured slower still: profiles/r1_blocked_partition.md).
+constexpr int kPartThreads = 512;
+constexpr int kPartWarps = kPartThreads / 32;
+constexpr int kPartPerThread = 8;
+constexpr uint64_t kPartChunk = kPartThreads * kPartPerThread;
+constexpr int kMaxBuckets = 64;
+constexpr int kMaxBits = 6;
+
+struct BucketMap {
+  uint64_t nb_global, first, nb_local, mult;  // mult = floor(S * 2^32 / nb_local)
+  uint32_t S, bits;
+};
+
+__device__ __forceinline__ uint32_t bucket_of(uint64_t h, const BucketMap& bm) {
+  const uint64_t b = dev::block_index(h, bm.nb_global) - bm.first;
+  const uint64_t q = (b < bm.nb_local ? b : 0) * bm.mult >> 32;
+  return q < bm.S ? static_cast<uint32_t>(q) : bm.S - 1;
+}
+
+// Lanes whose bucket equals `v`, given the per-bit ballots of the warp.
+__device__ __forceinline__ uint32_t lanes_with(uint32_t v, const uint32_t (&bal)[kMaxBits], uint32_t bits,
+                                               uint32_t active) {
+  uint32_t m = active;
+#pragma unroll
+  for (int k = 0; k < kMaxBits; ++k)
+    if (k < static_cast<int>(bits)) m &= ((v >> k) & 1u) ? bal[k] : ~bal[k];
+  return m;
+}
+
+// One warp step over 32 keys: rank of each lane inside its bucket group and
+// the per-bucket counts added to the lane-owned counters c0 (bucket = lane)
+// and c1 (bucket = lane + 32).
+__device__ __forceinline__ uint32_t warp_rank(uint32_t bk, bool valid, uint32_t bits, uint32_t lane,
+                                              uint32_t& c0, uint32_t& c1) {
+  const uint32_t active = __ballot_sync(0xffffffffu, valid);
+  uint32_t bal[kMaxBits];
+#pragma unroll
+  for (int k = 0; k < kMaxBits; ++k) bal[k] = (k < static_cast<int>(bits)) ? __ballot_sync(0xffffffffu, (bk >> k) & 1u) : 0u;
+  const uint32_t peers = lanes_with(bk, bal, bits, active);
+  // prior count of my bucket in this warp, from the lane that owns it
+  const uint32_t p0 = __shfl_sync(0xffffffffu, c0, bk & 31);
+  const uint32_t p1 = __shfl_sync(0xffffffffu, c1, bk & 31);
+  const uint32_t prior = (bk & 32) ? p1 : p0;
+  c0 += __popc(lanes_with(lane, bal, bits, active));
+  if (bits > 5) c1 += __popc(lanes_with(lane + 32, bal, bits, active));
+  return prior + __popc(peers & ((1u << lane) - 1u));
+}
+
+__global__ void __launch_bounds__(kPartThreads, 2) bucket_count_kernel(const uint64_t* __restrict__ hashes,
+                                                                       uint64_t n, BucketMap bm,
+                                                                       unsigned long long* __restrict__ counts) {
+  __shared__ unsigned int cta[kMaxBuckets];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t pol = dev::policy_evict_first();
+  if (threadIdx.x < kMaxBuckets) cta[threadIdx.x] = 0;
+  uint32_t c0 = 0, c1 = 0;
+  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kPartChunk; base < n;
+       base += static_cast<uint64_t>(gridDim.x) * kPartChunk) {
+    uint64_t h[kPartPerThread];
+#pragma unroll
+    for (int j = 0; j < kPartPerThread; ++j) {
+      const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
+      h[j] = i < n ? dev::ld_stream_u64(hashes + i, pol) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kPartPerThread; ++j) {
+      const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
+      const uint32_t bk = i < n ? bucket_of(h[j], bm) : 0u;
+      const uint32_t active = __ballot_sync(0xffffffffu, i < n);
+      uint32_t bal[kMaxBits];
+#pragma unroll
+      for (int k = 0; k < kMaxBits; ++k)
+        bal[k] = (k < static_cast<int>(bm.bits)) ? __ballot_sync(0xffffffffu, (bk >> k) & 1u) : 0u;
+      c0 += __popc(lanes_with(lane, bal, bm.bits, active));
+      if (bm.bits > 5) c1 += __popc(lanes_with(lane + 32, bal, bm.bits, active));
+    }
+  }
+  __syncthreads();
+  if (lane < bm.S && c0) atomicAdd(&cta[lane], c0);
+  if (lane + 32 < bm.S && c1) atomicAdd(&cta[lane + 32], c1);
+  __syncthreads();
+  if (threadIdx.x < bm.S && cta[threadIdx.x])
+    atomicAdd(&counts[threadIdx.x], static_cast<unsigned long long>(cta[threadIdx.x]));
+}
+
+// Scatter through shared memory: each chunk is first placed bucket-major in
+// smem (ballot ranks, no atomics), then copied out so that consecutive
+// threads write consecutive slots of one bucket run — coalesced stores
+// instead of one scattered 8-byte store per key.
+struct ScatterSmem {
+  uint64_t key[kPartChunk];
+  uint32_t pos[kPartChunk];
+  uint8_t bk[kPartChunk];
+  uint32_t wcnt[kPartWarps][kMaxBuckets];  // per-warp counts -> exclusive prefix over warps
+  uint32_t boff[kMaxBuckets];              // exclusive prefix over buckets (CTA-local)
+  unsigned long long gbase[kMaxBuckets];   // global slot of the CTA's run, per bucket
+};
+
+__global__ void __launch_bounds__(kPartThreads, 2) bucket_scatter_kernel(
+    const uint64_t* __restrict__ hashes, uint64_t n, BucketMap bm, unsigned long long* __restrict__ cursor,
+    uint64_t* __restrict__ out, uint32_t* __restrict__ pos) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ScatterSmem& sm = *reinterpret_cast<ScatterSmem*>(smem_raw);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t pol = dev::policy_evict_first();
+  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kPartChunk; base < n;
+       base += static_cast<uint64_t>(gridDim.x) * kPartChunk) {
+    const uint32_t cnt = static_cast<uint32_t>(n - base < kPartChunk ? n - base : kPartChunk);
+    uint64_t h[kPartPerThread];
+    uint32_t bk[kPartPerThread], off[kPartPerThread];
+#pragma unroll
+    for (int j = 0; j < kPartPerThread; ++j) {
+      const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
+      h[j] = i < n ? dev::ld_stream_u64(hashes + i, pol) : 0;
+    }
+    uint32_t c0 = 0, c1 = 0;
+#pragma unroll
+    for (int j = 0; j < kPartPerThread; ++j) {
+      const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
+      const bool valid = i < n;
+      bk[j] = valid ? bucket_of(h[j], bm) : 0u;
+      off[j] = warp_rank(bk[j], valid, bm.bits, lane, c0, c1);
+      if (!valid) bk[j] = 0xffffffffu;
+    }
+    sm.wcnt[warp][lane] = c0;
+    sm.wcnt[warp][lane + 32] = c1;
+    __syncthreads();
+    if (warp == 0) {
+      // bucket totals (lane owns buckets lane, lane+32), warp prefixes, then a
+      // warp-wide exclusive scan over the 64 buckets
+      uint32_t t0 = 0, t1 = 0;
+#pragma unroll
+      for (int w = 0; w < kPartWarps; ++w) {
+        const uint32_t a = sm.wcnt[w][lane], b = sm.wcnt[w][lane + 32];
+        sm.wcnt[w][lane] = t0;
+        sm.wcnt[w][lane + 32] = t1;
+        t0 += a;
+        t1 += b;
+      }
+      uint32_t s0 = t0, s1 = t1;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y0 = __shfl_up_sync(0xffffffffu, s0, d), y1 = __shfl_up_sync(0xffffffffu, s1, d);
+        if (lane >= static_cast<uint32_t>(d)) {
+          s0 += y0;
+          s1 += y1;
+        }
+      }
+      const uint32_t sum0 = __shfl_sync(0xffffffffu, s0, 31);
+      sm.boff[lane] = s0 - t0;
+      sm.boff[lane + 32] = sum0 + s1 - t1;
+      sm.gbase[lane] = (lane < bm.S && t0) ? atomicAdd(&cursor[lane], static_cast<unsigned long long>(t0)) : 0ull;
+      sm.gbase[lane + 32] =
+          (lane + 32 < bm.S && t1) ? atomicAdd(&cursor[lane + 32], static_cast<unsigned long long>(t1)) : 0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPartPerThread; ++j) {
+      if (bk[j] != 0xffffffffu) {
+        const uint32_t loc = sm.boff[bk[j]] + sm.wcnt[warp][bk[j]] + off[j];
+        sm.key[loc] = h[j];
+        sm.pos[loc] = static_cast<uint32_t>(base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x);
+        sm.bk[loc] = static_cast<uint8_t>(bk[j]);
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < cnt; i += kPartThreads) {
+      const uint32_t b = sm.bk[i];
+      const uint64_t slot = sm.gbase[b] + (i - sm.boff[b]);
+      out[slot] = sm.key[i];
+      if (pos) pos[slot] = sm.pos[i];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void bucket_scan_kernel(const unsigned long long* __restrict__ counts, uint32_t S,
+                                   unsigned long long* __restrict__ cursor) {
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0;
+    for (uint32_t b = 0; b < S; ++b) {
+      cursor[b] = s;
+      s += counts[b];
+    }
+  }
+}
+
+BucketMap make_map(const Geom& g, uint32_t S) {
+  BucketMap bm;
+  bm.nb_global = g.nb_global;
+  bm.first = g.first;
+  bm.nb_local = g.nb_local;
+  bm.S = S;
+  bm.bits = 0;
+  while ((1u << bm.bits) < S) ++bm.bits;
+  bm.mult = static_cast<uint64_t>((static_cast<unsigned __int128>(S) << 32) / g.nb_local);
+  return bm;
+}
+
+// Group `m` keys by bucket: d_out (and d_pos) receive them bucket-major.
+cudaError_t bucket_partition(const DeviceInfo& di, const Geom& g, uint32_t S, const uint64_t* hashes,
+                             uint64_t m, uint64_t* d_counts, uint64_t* d_cursor, uint64_t* d_out,
+                             uint32_t* d_pos, cudaStream_t s) {
+  const BucketMap bm = make_map(g, S);
+  cudaError_t e = cudaMemsetAsync(d_counts, 0, S * sizeof(uint64_t), s);
+  if (e != cudaSuccess) return e;
+  const uint64_t grid = grid_for(m, kPartChunk, di.sms, 2);
+  note_launch();
+  bucket_count_kernel<<<static_cast<unsigned>(grid), kPartThreads, 0, s>>>(
+      hashes, m, bm, reinterpret_cast<unsigned long long*>(d_counts));
+  note_launch();
+  bucket_scan_kernel<<<1, 32, 0, s>>>(reinterpret_cast<unsigned long long*>(d_counts), S,
+                                      reinterpret_cast<unsigned long long*>(d_cursor));
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(ScatterSmem)));
+  if (attr != cudaSuccess) return attr;
+  note_launch();
+  bucket_scatter_kernel<<<static_cast<unsigned>(grid), kPartThreads, sizeof(ScatterSmem), s>>>(
+      hashes, m, bm, reinterpret_cast<unsigned long long*>(d_cursor), d_out, d_pos);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// grouped probe
+// ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kProbeThreads, 2) probe_grouped_kernel(
     const uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
     const uint32_t* __restrict__ pos, uint64_t m, uint32_t* __restrict__ bitmap) {
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kProbeTile + threadIdx.x;
   const uint64_t pol = dev::policy_evict_first();
+  const uint64_t keep = dev::policy_evict_last();
   uint64_t h[kProbeU];
   uint32_t p[kProbeU];
 #pragma unroll
   for (int u = 0; u < kProbeU; ++u) {
     const uint64_t i = base + static_cast<uint64_t>(u) * kProbeThreads;
     h[u] = i < m ? dev::ld_stream_u64(keys + i, pol) : 0;
-    p[u] = i < m ? pos[i] : 0;
+    p[u] = i < m ? dev::ld_stream_u32(pos + i, pol) : 0;
   }
   dev::Block8 b[kProbeU];
   uint32_t ok_mask = 0;
@@ -57,7 +296,7 @@ __global__ void __launch_bounds__(kProbeThreads, 2) probe_grouped_kernel(
   for (int u = 0; u < kProbeU; ++u) {
     const uint64_t i = base + static_cast<uint64_t>(u) * kProbeThreads;
     if (i < m && ((ok_mask >> u) & 1u) && dev::block_contains(b[u], h[u]))
-      atomicOr(bitmap + (p[u] >> 5), 1u << (p[u] & 31));
+      dev::red_or(bitmap + (p[u] >> 5), 1u << (p[u] & 31), keep);  // chunk bitmap stays in L2
   }
 }
 
@@ -70,7 +309,7 @@ __global__ void expand_bits_kernel(const uint32_t* __restrict__ bits, uint64_t n
 struct Scratch {
   uint64_t* keys = nullptr;
   uint32_t* pos = nullptr;
-  uint64_t* counts = nullptr;  // [3][parts]: counts, offsets, cursor
+  uint64_t* counts = nullptr;  // [2][S]: counts, cursor
   uint32_t* bits = nullptr;
 };
 
@@ -78,7 +317,7 @@ cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, uint32_t parts, bool with_p
                           cudaStream_t s) {
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&sc.keys), cap * sizeof(uint64_t), s);
   if (e == cudaSuccess)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&sc.counts), 3 * parts * sizeof(uint64_t), s);
+    e = cudaMallocAsync(reinterpret_cast<void**>(&sc.counts), 2 * parts * sizeof(uint64_t), s);
   if (e == cudaSuccess && with_pos) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.pos), cap * sizeof(uint32_t), s);
   if (e == cudaSuccess && with_bits)
     e = cudaMallocAsync(reinterpret_cast<void**>(&sc.bits), ((cap + 31) / 32) * sizeof(uint32_t), s);
@@ -103,9 +342,11 @@ cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g
   cudaError_t e = alloc_scratch(sc, cap, plan.parts, false, false, s);
   for (uint64_t off = 0; e == cudaSuccess && off < n; off += cap) {
     const uint64_t m = n - off < cap ? n - off : cap;
-    e = launch_partition(hashes + off, m, g.nb_global, plan.d_bounds, plan.parts, sc.counts,
-                         sc.counts + plan.parts, sc.counts + 2 * plan.parts, sc.keys, nullptr, di.sms, s);
-    if (e == cudaSuccess) e = launch_insert_ordered(di, blocks, g, sc.keys, m, s);
+    e = bucket_partition(di, g, plan.parts, hashes + off, m, sc.counts, sc.counts + plan.parts, sc.keys,
+                         nullptr, s);
+    // test-before-set: grouped duplicates (config 4's hot keys arrive back to
+    // back) skip the atomic once their bits are in.
+    if (e == cudaSuccess) e = launch_insert_ordered(di, blocks, g, sc.keys, m, /*test=*/true, s);
   }
   free_scratch(sc, s);
   return e == cudaSuccess ? cudaGetLastError() : e;
@@ -122,8 +363,8 @@ cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geo
     uint32_t* bm = bits ? static_cast<uint32_t*>(out) + off / 32 : sc.bits;
     e = cudaMemsetAsync(bm, 0, ((m + 31) / 32) * sizeof(uint32_t), s);
     if (e == cudaSuccess)
-      e = launch_partition(hashes + off, m, g.nb_global, plan.d_bounds, plan.parts, sc.counts,
-                           sc.counts + plan.parts, sc.counts + 2 * plan.parts, sc.keys, sc.pos, di.sms, s);
+      e = bucket_partition(di, g, plan.parts, hashes + off, m, sc.counts, sc.counts + plan.parts, sc.keys,
+                           sc.pos, s);
     if (e != cudaSuccess) break;
     note_launch();
     probe_grouped_kernel<<<static_cast<unsigned>((m + kProbeTile - 1) / kProbeTile), kProbeThreads, 0, s>>>(

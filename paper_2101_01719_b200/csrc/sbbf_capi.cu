@@ -76,9 +76,15 @@ struct sbbf_gpu {
 
 namespace {
 
-constexpr uint64_t kSliceBytes = 24ull << 20;  // blocked path: one slice + chunk bitmap stay in L2
+constexpr uint64_t kSliceBytes = 16ull << 20;  // blocked path: one slice + chunk bitmap stay in L2
 
 bool beyond_l2(const sbbf_gpu* f) { return f->nb * 32 > f->di.l2_bytes / 2; }
+// Blocking pays once random probes mostly miss L2: a ~L2-sized filter (config
+// 3) already hits L2 often enough that the partition passes cost more than
+// they save (profiles/r1_blocked_partition.md).
+bool blocked_pays(const sbbf_gpu* f, uint64_t n) {
+  return f->nb * 32 > 2 * static_cast<uint64_t>(f->di.l2_bytes) && n >= f->nb / 2;
+}
 
 int resolve_insert(const sbbf_gpu* f, uint64_t n) {
   if (f->insert_variant != SBBF_INSERT_AUTO) return f->insert_variant;
@@ -88,7 +94,7 @@ int resolve_insert(const sbbf_gpu* f, uint64_t n) {
   // batches load the lane pair first (a load fills L2 faster than a missing
   // atomic, and duplicates/hot keys skip the atomic entirely).
   if (!beyond_l2(f)) return SBBF_INSERT_WIDE;
-  return n >= f->nb / 2 ? SBBF_INSERT_BLOCKED : SBBF_INSERT_WIDE_TEST;
+  return blocked_pays(f, n) ? SBBF_INSERT_BLOCKED : SBBF_INSERT_WIDE_TEST;
 }
 
 bool smem_fits(const sbbf_gpu* f) {
@@ -103,7 +109,7 @@ int resolve_find(const sbbf_gpu* f, uint64_t n) {
   // Staging the filter costs one filter-size copy per CTA; it pays once each
   // SM probes enough keys to amortise it.
   if (smem_fits(f) && n >= 64 * f->nb) return SBBF_FIND_SMEM;
-  if (beyond_l2(f) && n >= f->nb / 2) return SBBF_FIND_BLOCKED;
+  if (blocked_pays(f, n)) return SBBF_FIND_BLOCKED;
   return SBBF_FIND_GLOBAL;
 }
 
@@ -114,7 +120,7 @@ int ensure_plan(sbbf_gpu* f) {
   std::lock_guard<std::mutex> lock(f->plan_mu);
   if (f->d_plan_bounds) return SBBF_OK;
   uint64_t parts = (f->nb * 32 + kSliceBytes - 1) / kSliceBytes;
-  parts = parts < 2 ? 2 : (parts > 1024 ? 1024 : parts);
+  parts = parts < 2 ? 2 : (parts > 64 ? 64 : parts);  // bucket ids are <= 6 bits
   if (parts > f->nb) parts = f->nb;
   std::vector<uint64_t> b(parts);
   for (uint64_t k = 0; k < parts; ++k)

@@ -74,6 +74,14 @@ __device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t* p, uint64_t po
   return v;
 }
 
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t policy) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(p), "l"(policy));
+  return v;
+}
+
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

@@ -54,7 +54,7 @@ cudaError_t launch_partition(const uint64_t* hashes, uint64_t n, uint64_t total,
 // insert_wide over `n` keys with one warp step per 128 keys and the grid
 // covering the batch once, so CTAs run in key order (blocked path).
 cudaError_t launch_insert_ordered(const DeviceInfo& di, uint32_t* blocks, const Geom& g,
-                                  const uint64_t* hashes, uint64_t n, cudaStream_t s);
+                                  const uint64_t* hashes, uint64_t n, bool test, cudaStream_t s);
 
 // L2-blocked paths for filters larger than L2 (sbbf_blocked.cu).
 struct BlockedPlan {

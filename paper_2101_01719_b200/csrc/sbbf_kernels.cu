@@ -388,12 +388,15 @@ cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, c
 }
 
 cudaError_t launch_insert_ordered(const DeviceInfo& di, uint32_t* blocks, const Geom& g,
-                                  const uint64_t* hashes, uint64_t n, cudaStream_t s) {
+                                  const uint64_t* hashes, uint64_t n, bool test, cudaStream_t s) {
   (void)di;
   if (n == 0) return cudaSuccess;
   note_launch();
   const uint64_t grid = (n + kThreads * 4 - 1) / (kThreads * 4);  // 8 warps x 128 keys per CTA
-  insert_wide_kernel<false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n);
+  if (test)
+    insert_wide_kernel<true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n);
+  else
+    insert_wide_kernel<false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n);
   return cudaGetLastError();
 }
 

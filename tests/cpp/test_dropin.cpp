@@ -67,7 +67,8 @@ int main() {
   sbbf::gpu::SplitBlockFilter one(1);
   one.add_hash(0);
   REQUIRE(one.find_hash(0));
-  for (uint32_t lane : one.blocks()[0].lanes) REQUIRE(lane == 1u);
+  const auto one_blocks = one.blocks();  // keep the temporary alive for the loop
+  for (uint32_t lane : one_blocks[0].lanes) REQUIRE(lane == 1u);
   std::printf("cpp drop-in ok: crc 0xe34f8bef, %llu false positives\n", (unsigned long long)fp);
   return 0;
 }
