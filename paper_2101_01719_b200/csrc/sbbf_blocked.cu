@@ -64,34 +64,42 @@ __device__ __forceinline__ uint32_t bucket_of(uint64_t h, const BucketMap& bm) {
 }
 
 // Lanes whose bucket equals `v`, given the per-bit ballots of the warp.
-__device__ __forceinline__ uint32_t lanes_with(uint32_t v, const uint32_t (&bal)[kMaxBits], uint32_t bits,
-                                               uint32_t active) {
+template <int BITS>
+__device__ __forceinline__ uint32_t lanes_with(uint32_t v, const uint32_t (&bal)[kMaxBits], uint32_t active) {
   uint32_t m = active;
 #pragma unroll
-  for (int k = 0; k < kMaxBits; ++k)
-    if (k < static_cast<int>(bits)) m &= ((v >> k) & 1u) ? bal[k] : ~bal[k];
+  for (int k = 0; k < BITS; ++k) m &= ((v >> k) & 1u) ? bal[k] : ~bal[k];
   return m;
+}
+
+template <int BITS>
+__device__ __forceinline__ void bit_ballots(uint32_t bk, uint32_t (&bal)[kMaxBits]) {
+#pragma unroll
+  for (int k = 0; k < BITS; ++k) bal[k] = __ballot_sync(0xffffffffu, (bk >> k) & 1u);
 }
 
 // One warp step over 32 keys: rank of each lane inside its bucket group and
 // the per-bucket counts added to the lane-owned counters c0 (bucket = lane)
 // and c1 (bucket = lane + 32).
-__device__ __forceinline__ uint32_t warp_rank(uint32_t bk, bool valid, uint32_t bits, uint32_t lane,
-                                              uint32_t& c0, uint32_t& c1) {
+template <int BITS>
+__device__ __forceinline__ uint32_t warp_rank(uint32_t bk, bool valid, uint32_t lane, uint32_t& c0,
+                                              uint32_t& c1) {
   const uint32_t active = __ballot_sync(0xffffffffu, valid);
   uint32_t bal[kMaxBits];
-#pragma unroll
-  for (int k = 0; k < kMaxBits; ++k) bal[k] = (k < static_cast<int>(bits)) ? __ballot_sync(0xffffffffu, (bk >> k) & 1u) : 0u;
-  const uint32_t peers = lanes_with(bk, bal, bits, active);
+  bit_ballots<BITS>(bk, bal);
+  const uint32_t peers = lanes_with<BITS>(bk, bal, active);
   // prior count of my bucket in this warp, from the lane that owns it
-  const uint32_t p0 = __shfl_sync(0xffffffffu, c0, bk & 31);
-  const uint32_t p1 = __shfl_sync(0xffffffffu, c1, bk & 31);
-  const uint32_t prior = (bk & 32) ? p1 : p0;
-  c0 += __popc(lanes_with(lane, bal, bits, active));
-  if (bits > 5) c1 += __popc(lanes_with(lane + 32, bal, bits, active));
+  uint32_t prior = __shfl_sync(0xffffffffu, c0, bk & 31);
+  if constexpr (BITS > 5) {
+    const uint32_t p1 = __shfl_sync(0xffffffffu, c1, bk & 31);
+    prior = (bk & 32) ? p1 : prior;
+    c1 += __popc(lanes_with<BITS>(lane + 32, bal, active));
+  }
+  c0 += __popc(lanes_with<BITS>(lane, bal, active));
   return prior + __popc(peers & ((1u << lane) - 1u));
 }
 
+template <int BITS>
 __global__ void __launch_bounds__(kPartThreads, 2) bucket_count_kernel(const uint64_t* __restrict__ hashes,
                                                                        uint64_t n, BucketMap bm,
                                                                        unsigned long long* __restrict__ counts) {
@@ -100,13 +108,23 @@ __global__ void __launch_bounds__(kPartThreads, 2) bucket_count_kernel(const uin
   const uint64_t pol = dev::policy_evict_first();
   if (threadIdx.x < kMaxBuckets) cta[threadIdx.x] = 0;
   uint32_t c0 = 0, c1 = 0;
-  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kPartChunk; base < n;
-       base += static_cast<uint64_t>(gridDim.x) * kPartChunk) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kPartChunk;
+  uint64_t base = static_cast<uint64_t>(blockIdx.x) * kPartChunk;
+  // Software pipeline: the next chunk's loads are in flight while this
+  // chunk's ballots run (the kernel is otherwise latency bound).
+  uint64_t nxt[kPartPerThread];
+#pragma unroll
+  for (int j = 0; j < kPartPerThread; ++j) {
+    const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
+    nxt[j] = i < n ? dev::ld_stream_u64(hashes + i, pol) : 0;
+  }
+  for (; base < n; base += stride) {
     uint64_t h[kPartPerThread];
 #pragma unroll
     for (int j = 0; j < kPartPerThread; ++j) {
-      const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
-      h[j] = i < n ? dev::ld_stream_u64(hashes + i, pol) : 0;
+      h[j] = nxt[j];
+      const uint64_t i = base + stride + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
+      nxt[j] = i < n ? dev::ld_stream_u64(hashes + i, pol) : 0;
     }
 #pragma unroll
     for (int j = 0; j < kPartPerThread; ++j) {
@@ -114,11 +132,9 @@ __global__ void __launch_bounds__(kPartThreads, 2) bucket_count_kernel(const uin
       const uint32_t bk = i < n ? bucket_of(h[j], bm) : 0u;
       const uint32_t active = __ballot_sync(0xffffffffu, i < n);
       uint32_t bal[kMaxBits];
-#pragma unroll
-      for (int k = 0; k < kMaxBits; ++k)
-        bal[k] = (k < static_cast<int>(bm.bits)) ? __ballot_sync(0xffffffffu, (bk >> k) & 1u) : 0u;
-      c0 += __popc(lanes_with(lane, bal, bm.bits, active));
-      if (bm.bits > 5) c1 += __popc(lanes_with(lane + 32, bal, bm.bits, active));
+      bit_ballots<BITS>(bk, bal);
+      c0 += __popc(lanes_with<BITS>(lane, bal, active));
+      if constexpr (BITS > 5) c1 += __popc(lanes_with<BITS>(lane + 32, bal, active));
     }
   }
   __syncthreads();
@@ -142,6 +158,7 @@ struct ScatterSmem {
   unsigned long long gbase[kMaxBuckets];   // global slot of the CTA's run, per bucket
 };
 
+template <int BITS>
 __global__ void __launch_bounds__(kPartThreads, 2) bucket_scatter_kernel(
     const uint64_t* __restrict__ hashes, uint64_t n, BucketMap bm, unsigned long long* __restrict__ cursor,
     uint64_t* __restrict__ out, uint32_t* __restrict__ pos) {
@@ -165,7 +182,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) bucket_scatter_kernel(
       const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
       const bool valid = i < n;
       bk[j] = valid ? bucket_of(h[j], bm) : 0u;
-      off[j] = warp_rank(bk[j], valid, bm.bits, lane, c0, c1);
+      off[j] = warp_rank<BITS>(bk[j], valid, lane, c0, c1);
       if (!valid) bk[j] = 0xffffffffu;
     }
     sm.wcnt[warp][lane] = c0;
@@ -239,8 +256,29 @@ BucketMap make_map(const Geom& g, uint32_t S) {
   bm.S = S;
   bm.bits = 0;
   while ((1u << bm.bits) < S) ++bm.bits;
+  if (bm.bits == 0) bm.bits = 1;  // a single bucket still needs a 1-bit id
   bm.mult = static_cast<uint64_t>((static_cast<unsigned __int128>(S) << 32) / g.nb_local);
   return bm;
+}
+
+template <int BITS>
+cudaError_t bucket_partition_bits(uint64_t grid, const BucketMap& bm, const uint64_t* hashes, uint64_t m,
+                                  uint64_t* d_counts, uint64_t* d_cursor, uint64_t* d_out, uint32_t* d_pos,
+                                  cudaStream_t s) {
+  note_launch();
+  bucket_count_kernel<BITS><<<static_cast<unsigned>(grid), kPartThreads, 0, s>>>(
+      hashes, m, bm, reinterpret_cast<unsigned long long*>(d_counts));
+  note_launch();
+  bucket_scan_kernel<<<1, 32, 0, s>>>(reinterpret_cast<unsigned long long*>(d_counts), bm.S,
+                                      reinterpret_cast<unsigned long long*>(d_cursor));
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      bucket_scatter_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      static_cast<int>(sizeof(ScatterSmem)));
+  if (attr != cudaSuccess) return attr;
+  note_launch();
+  bucket_scatter_kernel<BITS><<<static_cast<unsigned>(grid), kPartThreads, sizeof(ScatterSmem), s>>>(
+      hashes, m, bm, reinterpret_cast<unsigned long long*>(d_cursor), d_out, d_pos);
+  return cudaGetLastError();
 }
 
 // Group `m` keys by bucket: d_out (and d_pos) receive them bucket-major.
@@ -251,19 +289,15 @@ cudaError_t bucket_partition(const DeviceInfo& di, const Geom& g, uint32_t S, co
   cudaError_t e = cudaMemsetAsync(d_counts, 0, S * sizeof(uint64_t), s);
   if (e != cudaSuccess) return e;
   const uint64_t grid = grid_for(m, kPartChunk, di.sms, 2);
-  note_launch();
-  bucket_count_kernel<<<static_cast<unsigned>(grid), kPartThreads, 0, s>>>(
-      hashes, m, bm, reinterpret_cast<unsigned long long*>(d_counts));
-  note_launch();
-  bucket_scan_kernel<<<1, 32, 0, s>>>(reinterpret_cast<unsigned long long*>(d_counts), S,
-                                      reinterpret_cast<unsigned long long*>(d_cursor));
-  static const cudaError_t attr = cudaFuncSetAttribute(
-      bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(ScatterSmem)));
-  if (attr != cudaSuccess) return attr;
-  note_launch();
-  bucket_scatter_kernel<<<static_cast<unsigned>(grid), kPartThreads, sizeof(ScatterSmem), s>>>(
-      hashes, m, bm, reinterpret_cast<unsigned long long*>(d_cursor), d_out, d_pos);
-  return cudaGetLastError();
+  switch (bm.bits) {
+    case 1: return bucket_partition_bits<1>(grid, bm, hashes, m, d_counts, d_cursor, d_out, d_pos, s);
+    case 2: return bucket_partition_bits<2>(grid, bm, hashes, m, d_counts, d_cursor, d_out, d_pos, s);
+    case 3: return bucket_partition_bits<3>(grid, bm, hashes, m, d_counts, d_cursor, d_out, d_pos, s);
+    case 4: return bucket_partition_bits<4>(grid, bm, hashes, m, d_counts, d_cursor, d_out, d_pos, s);
+    case 5: return bucket_partition_bits<5>(grid, bm, hashes, m, d_counts, d_cursor, d_out, d_pos, s);
+    case 6: return bucket_partition_bits<6>(grid, bm, hashes, m, d_counts, d_cursor, d_out, d_pos, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 // ---------------------------------------------------------------------------
