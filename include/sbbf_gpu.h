@@ -148,6 +148,23 @@ int sbbf_gpu_set_find_variant(sbbf_gpu_t* f, int variant);
 int sbbf_gpu_resolved_insert_variant(const sbbf_gpu_t* f, uint64_t n);
 int sbbf_gpu_resolved_find_variant(const sbbf_gpu_t* f, uint64_t n);
 
+/* --- XXH64 key frontend: kHasherXxh64 (hash.hpp:12), hash_key /
+ *     hash_u64_key (hash.hpp:20-25, hash.cpp:100-114) ----------------------
+ * u64 keys hash as their 8 little-endian bytes; byte-string key i is
+ * d_data[d_offsets[i], d_offsets[i+1]) (n+1 offsets). The *_keys_u64 calls
+ * hash inside the insert / lookup kernel (no hash array in HBM); pair them
+ * with sbbf_gpu_set_hasher_id(f, 1) so images record the frontend. */
+int sbbf_gpu_hash_u64_keys(const uint64_t* d_keys, uint64_t n, uint64_t seed, uint64_t* d_hashes,
+                           void* stream);
+int sbbf_gpu_hash_bytes(const uint8_t* d_data, const uint64_t* d_offsets, uint64_t n, uint64_t seed,
+                        uint64_t* d_hashes, void* stream);
+int sbbf_gpu_insert_keys_u64(sbbf_gpu_t* f, const uint64_t* d_keys, uint64_t n, uint64_t seed,
+                             void* stream);
+int sbbf_gpu_find_keys_u64(const sbbf_gpu_t* f, const uint64_t* d_keys, uint64_t n, uint64_t seed,
+                           uint8_t* d_results, void* stream);
+int sbbf_gpu_find_keys_u64_bits(const sbbf_gpu_t* f, const uint64_t* d_keys, uint64_t n, uint64_t seed,
+                                uint32_t* d_bits, void* stream);
+
 /* --- multi-GPU shards (no reference counterpart: the reference has no
  *     distributed mode) -----------------------------------
  * Rank r of P owns global blocks [floor(r*B/P), floor((r+1)*B/P)). A shard

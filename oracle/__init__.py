@@ -255,6 +255,8 @@ class Reference:
         L.ref_hash_u64_key.restype = C.c_uint64
         L.ref_hash_u64_key.argtypes = [C.c_uint64, C.c_uint64]
         L.ref_mt19937_64.argtypes = [C.c_uint64, C.c_uint64, _u64p]
+        L.ref_fpp_sim.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _u64p,
+                                  C.POINTER(C.c_uint32)]
         L.ref_time_build_probe.argtypes = [C.c_uint64, _u64p, C.c_uint64, _u64p, C.c_uint64, _u8p,
                                            C.c_int, C.c_int, C.POINTER(C.c_double),
                                            C.POINTER(C.c_double), C.POINTER(C.c_void_p)]
@@ -279,6 +281,13 @@ class Reference:
         out = np.empty(n, np.uint64)
         self.lib.ref_mt19937_64(seed, n, _p(out, _u64p))
         return out
+
+    def fpp_sim(self, ndv: int, filter_bytes: int, queries: int, seed: int):
+        """(false positives, image CRC) of the reference's run_fpp_sim loop."""
+        fp = C.c_uint64(0)
+        crc = C.c_uint32(0)
+        self.lib.ref_fpp_sim(ndv, filter_bytes // 32, queries, seed, C.byref(fp), C.byref(crc))
+        return int(fp.value), int(crc.value)
 
     def crc32(self, data: bytes) -> int:
         a = np.frombuffer(data, np.uint8) if len(data) else np.zeros(1, np.uint8)

@@ -139,6 +139,23 @@ void ref_mt19937_64(uint64_t seed, uint64_t n, uint64_t* out) {
   for (uint64_t i = 0; i < n; ++i) out[i] = rng();
 }
 
+// run_fpp_sim's loop (tools/harness.cpp:84-97) with the reference's own
+// hash_u64_key / add_hash / find_hash: counters [0, ndv) inserted, counters
+// [2^32, 2^32 + queries) probed. Writes the false-positive count and the
+// image CRC of the built filter (hasher id kHasherXxh64).
+void ref_fpp_sim(uint64_t ndv, uint64_t num_buckets, uint64_t queries, uint64_t seed, uint64_t* fp,
+                 uint32_t* image_crc) {
+  SplitBlockFilter filter(num_buckets, sbbf::kHasherXxh64);
+  for (uint64_t c = 0; c < ndv; ++c) filter.add_hash(sbbf::hash_u64_key(c, seed));
+  uint64_t hits = 0;
+  for (uint64_t i = 0; i < queries; ++i)
+    hits += filter.find_hash(sbbf::hash_u64_key((uint64_t{1} << 32) + i, seed)) ? 1 : 0;
+  *fp = hits;
+  const std::vector<uint8_t> img = sbbf::serialize(filter);
+  *image_crc = static_cast<uint32_t>(img[img.size() - 4]) | (static_cast<uint32_t>(img[img.size() - 3]) << 8) |
+               (static_cast<uint32_t>(img[img.size() - 2]) << 16) | (static_cast<uint32_t>(img[img.size() - 1]) << 24);
+}
+
 // ---- CPU baseline timing (harness.cpp:160-201) ---------------------------
 // Each rep builds a fresh zeroed filter untimed, times add_hashes over the
 // whole batch, then times find_hashes over the lookup batch with `threads`

@@ -57,6 +57,11 @@ PROTOTYPES = {
     "sbbf_gpu_resolved_insert_variant": (_i, [_vp, _u64]),
     "sbbf_gpu_resolved_find_variant": (_i, [_vp, _u64]),
     "sbbf_gpu_set_l2_fetch_granularity": (_i, [_i, _i, C.POINTER(_i)]),
+    "sbbf_gpu_hash_u64_keys": (_i, [_vp, _u64, _u64, _vp, _vp]),
+    "sbbf_gpu_hash_bytes": (_i, [_vp, _vp, _u64, _u64, _vp, _vp]),
+    "sbbf_gpu_insert_keys_u64": (_i, [_vp, _vp, _u64, _u64, _vp]),
+    "sbbf_gpu_find_keys_u64": (_i, [_vp, _vp, _u64, _u64, _vp, _vp]),
+    "sbbf_gpu_find_keys_u64_bits": (_i, [_vp, _vp, _u64, _u64, _vp, _vp]),
     "sbbf_gpu_create_shard": (_i, [_u64, _u64, _u64, _i, C.POINTER(_vp)]),
     "sbbf_gpu_total_buckets": (_u64, [_vp]),
     "sbbf_gpu_first_block": (_u64, [_vp]),

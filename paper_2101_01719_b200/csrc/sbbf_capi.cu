@@ -10,6 +10,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <new>
 #include <string>
@@ -467,6 +468,79 @@ int sbbf_gpu_resolved_insert_variant(const sbbf_gpu_t* f, uint64_t n) {
 
 int sbbf_gpu_resolved_find_variant(const sbbf_gpu_t* f, uint64_t n) {
   return f ? resolve_find(f, n) : SBBF_EINVAL;
+}
+
+// ---- XXH64 key frontend (hash.hpp:11-25, hash.cpp:100-114) -----------------
+int sbbf_gpu_hash_u64_keys(const uint64_t* d_keys, uint64_t n, uint64_t seed, uint64_t* d_hashes,
+                           void* stream) {
+  if (n == 0) return SBBF_OK;
+  if (!d_keys || !d_hashes) return fail(SBBF_EINVAL, "null buffer");
+  cudaError_t e = sbbf::launch_hash_u64(d_keys, n, seed, d_hashes, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "hash kernel");
+}
+
+int sbbf_gpu_hash_bytes(const uint8_t* d_data, const uint64_t* d_offsets, uint64_t n, uint64_t seed,
+                        uint64_t* d_hashes, void* stream) {
+  if (n == 0) return SBBF_OK;
+  if (!d_offsets || !d_hashes) return fail(SBBF_EINVAL, "null buffer");
+  cudaError_t e =
+      sbbf::launch_hash_bytes(d_data, d_offsets, n, seed, d_hashes, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "hash kernel");
+}
+
+// Hash-then-dispatch for the paths without a fused kernel (blocked, forced
+// variants): the hashes go to stream-ordered scratch.
+static cudaError_t with_hashed(const uint64_t* keys, uint64_t n, uint64_t seed, cudaStream_t s,
+                               const std::function<cudaError_t(const uint64_t*)>& body) {
+  uint64_t* tmp = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&tmp), n * sizeof(uint64_t), s);
+  if (e == cudaSuccess) e = sbbf::launch_hash_u64(keys, n, seed, tmp, s);
+  if (e == cudaSuccess) e = body(tmp);
+  if (tmp) cudaFreeAsync(tmp, s);
+  return e;
+}
+
+int sbbf_gpu_insert_keys_u64(sbbf_gpu_t* f, const uint64_t* d_keys, uint64_t n, uint64_t seed,
+                             void* stream) {
+  if (!f) return fail(SBBF_EINVAL, "null filter");
+  if (n == 0) return SBBF_OK;
+  if (!d_keys) return fail(SBBF_EINVAL, "null keys");
+  DeviceGuard g(f->di.device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int v = resolve_insert(f, n);
+  cudaError_t e;
+  if (v == SBBF_INSERT_WIDE || v == SBBF_INSERT_WIDE_TEST)
+    e = sbbf::launch_insert_keys(f->di, v == SBBF_INSERT_WIDE_TEST, f->d_blocks, f->geom, d_keys, n, seed, s);
+  else
+    e = with_hashed(d_keys, n, seed, s, [&](const uint64_t* h) { return do_insert(f, v, h, n, s); });
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "insert_keys");
+}
+
+static int find_keys_common(const sbbf_gpu_t* f, const uint64_t* d_keys, uint64_t n, uint64_t seed,
+                            void* d_out, bool bits, void* stream) {
+  if (!f) return fail(SBBF_EINVAL, "null filter");
+  if (n == 0) return SBBF_OK;
+  if (!d_keys || !d_out) return fail(SBBF_EINVAL, "null buffer");
+  DeviceGuard g(f->di.device);
+  sbbf_gpu* m = const_cast<sbbf_gpu*>(f);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int v = resolve_find(f, n);
+  cudaError_t e;
+  if (v == SBBF_FIND_GLOBAL)
+    e = sbbf::launch_find_keys(f->di, f->d_blocks, f->geom, d_keys, n, seed, d_out, bits, s);
+  else
+    e = with_hashed(d_keys, n, seed, s, [&](const uint64_t* h) { return do_find(m, v, h, n, d_out, bits, s); });
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "find_keys");
+}
+
+int sbbf_gpu_find_keys_u64(const sbbf_gpu_t* f, const uint64_t* d_keys, uint64_t n, uint64_t seed,
+                           uint8_t* d_results, void* stream) {
+  return find_keys_common(f, d_keys, n, seed, d_results, false, stream);
+}
+
+int sbbf_gpu_find_keys_u64_bits(const sbbf_gpu_t* f, const uint64_t* d_keys, uint64_t n, uint64_t seed,
+                                uint32_t* d_bits, void* stream) {
+  return find_keys_common(f, d_keys, n, seed, d_bits, true, stream);
 }
 
 }  // extern "C"

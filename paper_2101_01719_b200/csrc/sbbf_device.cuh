@@ -63,6 +63,77 @@ __device__ __forceinline__ bool block_contains(const Block8& b, uint64_t hash) {
   return missing == 0;
 }
 
+// ---- XXH64 key frontend (kHasherXxh64 = 1, hash.hpp:12; hash.cpp:45-114) ---
+// The published XXH64 algorithm. hash_u64_key hashes the key's 8
+// little-endian bytes (hash.cpp:108-114), which on device is the u64 itself.
+constexpr uint64_t kXP1 = 0x9E3779B185EBCA87ull, kXP2 = 0xC2B2AE3D27D4EB4Full,
+                   kXP3 = 0x165667B19E3779F9ull, kXP4 = 0x85EBCA77C2B2AE63ull,
+                   kXP5 = 0x27D4EB2F165667C5ull;
+
+__host__ __device__ __forceinline__ uint64_t xxh_rotl(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+__host__ __device__ __forceinline__ uint64_t xxh_round(uint64_t acc, uint64_t in) {
+  return xxh_rotl(acc + in * kXP2, 31) * kXP1;
+}
+__host__ __device__ __forceinline__ uint64_t xxh_avalanche(uint64_t h) {
+  h ^= h >> 33;
+  h *= kXP2;
+  h ^= h >> 29;
+  h *= kXP3;
+  return h ^ (h >> 32);
+}
+
+__host__ __device__ __forceinline__ uint64_t xxh64_u64(uint64_t key, uint64_t seed) {
+  uint64_t h = seed + kXP5 + 8;
+  h ^= xxh_round(0, key);
+  h = xxh_rotl(h, 27) * kXP1 + kXP4;
+  return xxh_avalanche(h);
+}
+
+__device__ __forceinline__ uint64_t xxh_load(const uint8_t* p, int bytes) {
+  uint64_t v = 0;
+  for (int i = bytes - 1; i >= 0; --i) v = (v << 8) | p[i];
+  return v;
+}
+
+// Arbitrary byte string (hash_key, hash.cpp:100-106).
+__device__ inline uint64_t xxh64_bytes(const uint8_t* p, uint64_t len, uint64_t seed) {
+  const uint8_t* end = p + len;
+  uint64_t h;
+  if (len >= 32) {
+    uint64_t v1 = seed + kXP1 + kXP2, v2 = seed + kXP2, v3 = seed, v4 = seed - kXP1;
+    do {
+      v1 = xxh_round(v1, xxh_load(p, 8));
+      v2 = xxh_round(v2, xxh_load(p + 8, 8));
+      v3 = xxh_round(v3, xxh_load(p + 16, 8));
+      v4 = xxh_round(v4, xxh_load(p + 24, 8));
+      p += 32;
+    } while (p + 32 <= end);
+    h = xxh_rotl(v1, 1) + xxh_rotl(v2, 7) + xxh_rotl(v3, 12) + xxh_rotl(v4, 18);
+    h = (h ^ xxh_round(0, v1)) * kXP1 + kXP4;
+    h = (h ^ xxh_round(0, v2)) * kXP1 + kXP4;
+    h = (h ^ xxh_round(0, v3)) * kXP1 + kXP4;
+    h = (h ^ xxh_round(0, v4)) * kXP1 + kXP4;
+  } else {
+    h = seed + kXP5;
+  }
+  h += len;
+  for (; p + 8 <= end; p += 8) h = xxh_rotl(h ^ xxh_round(0, xxh_load(p, 8)), 27) * kXP1 + kXP4;
+  if (p + 4 <= end) {
+    h = xxh_rotl(h ^ (xxh_load(p, 4) * kXP1), 23) * kXP2 + kXP3;
+    p += 4;
+  }
+  for (; p < end; ++p) h = xxh_rotl(h ^ (*p * kXP5), 11) * kXP1;
+  return xxh_avalanche(h);
+}
+
+// Key handling of the fused kernels: raw 64-bit hashes (kHasherRaw) or u64
+// keys hashed on the fly with XXH64 (kHasherXxh64).
+template <bool kKeys>
+__device__ __forceinline__ uint64_t to_hash(uint64_t v, uint64_t seed) {
+  if constexpr (kKeys) return xxh64_u64(v, seed);
+  else return v;
+}
+
 // ---- memory primitives ---------------------------------------------------
 // Streamed once (hash arrays): skip L1, evict-first in L2 so the stream does
 // not push the filter out of L2.

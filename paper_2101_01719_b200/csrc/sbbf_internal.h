@@ -66,6 +66,15 @@ cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g
 cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
                          const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s);
 
+// XXH64 key frontend (kHasherXxh64): hashing kernels and fused insert/find.
+cudaError_t launch_hash_u64(const uint64_t* keys, uint64_t n, uint64_t seed, uint64_t* out, cudaStream_t s);
+cudaError_t launch_hash_bytes(const uint8_t* data, const uint64_t* offsets, uint64_t n, uint64_t seed,
+                              uint64_t* out, cudaStream_t s);
+cudaError_t launch_insert_keys(const DeviceInfo& di, bool test, uint32_t* blocks, const Geom& g,
+                               const uint64_t* keys, uint64_t n, uint64_t seed, cudaStream_t s);
+cudaError_t launch_find_keys(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const uint64_t* keys,
+                             uint64_t n, uint64_t seed, void* out, bool bits, cudaStream_t s);
+
 cudaError_t launch_block_index(const uint64_t* h, uint64_t n, uint64_t nb, uint64_t* out,
                                cudaStream_t s);
 cudaError_t launch_make_mask(const uint64_t* h, uint64_t n, uint32_t* out, cudaStream_t s);

@@ -100,10 +100,12 @@ __global__ void __launch_bounds__(kThreads, 4) insert_lane8_kernel(uint32_t* __r
 // L2 atomic operations of insert_lane8 (120 vs 85 G keys/s on an L2-resident
 // buffer, scripts/microbench.cu). Lane 2w is the low half of u64 word w
 // (little-endian lanes, filter.hpp:23-24).
-template <bool kTest>
+// kKeys: the input is u64 keys, hashed on the fly with XXH64(seed) (the
+// reference's kHasherXxh64 frontend fused into the insert).
+template <bool kTest, bool kKeys = false>
 __global__ void __launch_bounds__(kThreads, 4) insert_wide_kernel(uint32_t* __restrict__ blocks, Geom g,
                                                                   const uint64_t* __restrict__ hashes,
-                                                                  uint64_t n) {
+                                                                  uint64_t n, uint64_t seed = 0) {
   const int lane = threadIdx.x & 31;
   const int sub = lane >> 2;   // which of the 8 keys of a round
   const int pair = lane & 3;   // which 64-bit lane pair of the block this thread owns
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, 4) insert_wide_kernel(uint32_t* __re
 #pragma unroll
     for (int j = 0; j < kT; ++j) {
       const uint64_t idx = base + j * 32 + lane;
-      h[j] = idx < n ? dev::ld_stream_u64(hashes + idx, pol) : 0;
+      h[j] = idx < n ? dev::to_hash<kKeys>(dev::ld_stream_u64(hashes + idx, pol), seed) : 0;
     }
 #pragma unroll
     for (int j = 0; j < kT; ++j) {
@@ -184,10 +186,10 @@ __global__ void __launch_bounds__(kThreads) insert_thread_kernel(uint32_t* __res
 template <int U, bool kBits>
 constexpr int find_min_blocks() { return U >= 8 ? (kBits ? 2 : 4) : 5; }
 
-template <int U, bool kBits>
+template <int U, bool kBits, bool kKeys = false>
 __global__ void __launch_bounds__(kThreads, find_min_blocks<U, kBits>())
     find_global_kernel(const uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ hashes,
-                       uint64_t n, void* __restrict__ out) {
+                       uint64_t n, void* __restrict__ out, uint64_t seed = 0) {
   const int lane = threadIdx.x & 31;
   const uint64_t pol = dev::policy_evict_first();
   const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, find_min_blocks<U, kBits>())
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t idx = base + u * 32 + lane;
-      h[u] = idx < n ? dev::ld_stream_u64(hashes + idx, pol) : 0;
+      h[u] = idx < n ? dev::to_hash<kKeys>(dev::ld_stream_u64(hashes + idx, pol), seed) : 0;
     }
     Block8 b[U];
     uint32_t owned = 0;
@@ -334,9 +336,43 @@ __global__ void make_mask_kernel(const uint64_t* __restrict__ h, uint64_t n,
   }
 }
 
+// XXH64 of u64 keys (hash_u64_key, hash.cpp:108-114) and of byte strings
+// (hash_key, hash.cpp:100-106; key i = data[offsets[i], offsets[i+1])).
+__global__ void hash_u64_kernel(const uint64_t* __restrict__ keys, uint64_t n, uint64_t seed,
+                                uint64_t* __restrict__ out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = dev::xxh64_u64(keys[i], seed);
+}
+
+__global__ void hash_bytes_kernel(const uint8_t* __restrict__ data, const uint64_t* __restrict__ offsets,
+                                  uint64_t n, uint64_t seed, uint64_t* __restrict__ out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t b = offsets[i], e = offsets[i + 1];
+    out[i] = dev::xxh64_bytes(data + b, e - b, seed);
+  }
+}
+
 std::atomic<uint64_t> g_launches{0};
 
 }  // namespace
+
+cudaError_t launch_hash_u64(const uint64_t* keys, uint64_t n, uint64_t seed, uint64_t* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  note_launch();
+  hash_u64_kernel<<<static_cast<unsigned>(grid_for(n, 1024, 148, 16)), 256, 0, s>>>(keys, n, seed, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hash_bytes(const uint8_t* data, const uint64_t* offsets, uint64_t n, uint64_t seed,
+                              uint64_t* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  note_launch();
+  hash_bytes_kernel<<<static_cast<unsigned>(grid_for(n, 256, 148, 16)), 128, 0, s>>>(data, offsets, n, seed,
+                                                                                       out);
+  return cudaGetLastError();
+}
 
 // ---------------------------------------------------------------------------
 // launchers (sbbf_internal.h)
@@ -401,6 +437,39 @@ cudaError_t launch_insert_ordered(const DeviceInfo& di, uint32_t* blocks, const 
 }
 
 constexpr int kFindU = 8;
+
+// Fused XXH64 frontends: u64 keys hashed inside the insert / lookup kernel.
+cudaError_t launch_insert_keys(const DeviceInfo& di, bool test, uint32_t* blocks, const Geom& g,
+                               const uint64_t* keys, uint64_t n, uint64_t seed, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  note_launch();
+  if (test) {
+    static const int occ = resident_blocks(insert_wide_kernel<true, true>, kThreads, 0);
+    const uint64_t grid = grid_for(n, kThreads * 4, di.sms, occ);
+    insert_wide_kernel<true, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, keys, n, seed);
+  } else {
+    static const int occ = resident_blocks(insert_wide_kernel<false, true>, kThreads, 0);
+    const uint64_t grid = grid_for(n, kThreads * 4, di.sms, occ);
+    insert_wide_kernel<false, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, keys, n, seed);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_find_keys(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const uint64_t* keys,
+                             uint64_t n, uint64_t seed, void* out, bool bits, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  note_launch();
+  static const int occ_b = resident_blocks(find_global_kernel<kFindU, true, true>, kThreads, 0);
+  static const int occ_y = resident_blocks(find_global_kernel<kFindU, false, true>, kThreads, 0);
+  const uint64_t grid = grid_for(n, kThreads * kFindU, di.sms, bits ? occ_b : occ_y);
+  if (bits)
+    find_global_kernel<kFindU, true, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, keys, n,
+                                                                                           out, seed);
+  else
+    find_global_kernel<kFindU, false, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, keys, n,
+                                                                                            out, seed);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* blocks, const Geom& g,
                         const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s) {

@@ -220,6 +220,60 @@ class SplitBlockFilter:
                                         o.ctypes.data_as(C.c_void_p)), "sbbf_gpu_find_bits_host")
         return o
 
+    # -- XXH64 key frontend (kHasherXxh64, hash.hpp:12): u64 keys hashed in-kernel --
+    def _dev_keys(self, keys):
+        if _is_cuda_tensor(keys):
+            return _dev_u64(keys)
+        a = _host_u64(keys)
+        return torch.from_numpy(a.view(np.int64)).to(torch.device("cuda", self._device))
+
+    def add_keys(self, keys, seed: int = 0) -> None:
+        """Insert u64 keys hashed with hash_u64_key(key, seed) (hash.cpp:108-114)."""
+        t = self._dev_keys(keys)
+        check(_lib.lib().sbbf_gpu_insert_keys_u64(self._h, C.c_void_p(t.data_ptr()), t.numel(), seed,
+                                                  _stream_ptr(self._device)), "sbbf_gpu_insert_keys_u64")
+
+    def find_keys(self, keys, seed: int = 0, results=None):
+        t = self._dev_keys(keys)
+        out = results if results is not None else torch.empty(t.numel(), dtype=torch.uint8, device=t.device)
+        check(_lib.lib().sbbf_gpu_find_keys_u64(self._h, C.c_void_p(t.data_ptr()), t.numel(), seed,
+                                                C.c_void_p(out.data_ptr()), _stream_ptr(self._device)),
+              "sbbf_gpu_find_keys_u64")
+        return out
+
+    def find_keys_bits(self, keys, seed: int = 0, out=None):
+        t = self._dev_keys(keys)
+        o = out if out is not None else torch.empty((t.numel() + 31) // 32, dtype=torch.int32, device=t.device)
+        check(_lib.lib().sbbf_gpu_find_keys_u64_bits(self._h, C.c_void_p(t.data_ptr()), t.numel(), seed,
+                                                     C.c_void_p(o.data_ptr()), _stream_ptr(self._device)),
+              "sbbf_gpu_find_keys_u64_bits")
+        return o
+
+
+def hash_u64_keys(keys: "torch.Tensor", seed: int = 0) -> "torch.Tensor":
+    """hash_u64_key (hash.cpp:108-114) on device: XXH64 of each key's 8 LE bytes."""
+    t = _dev_u64(keys)
+    out = torch.empty(t.numel(), dtype=torch.int64, device=t.device)
+    check(_lib.lib().sbbf_gpu_hash_u64_keys(C.c_void_p(t.data_ptr()), t.numel(), seed,
+                                            C.c_void_p(out.data_ptr()), _stream_ptr(t.device.index or 0)),
+          "sbbf_gpu_hash_u64_keys")
+    return out
+
+
+def hash_keys(keys, seed: int = 0, device: int = 0) -> "torch.Tensor":
+    """hash_key (hash.cpp:100-106) on device for a list of byte strings."""
+    blobs = [k.encode() if isinstance(k, str) else bytes(k) for k in keys]
+    offsets = np.zeros(len(blobs) + 1, np.uint64)
+    offsets[1:] = np.cumsum([len(b) for b in blobs], dtype=np.uint64)
+    dev = torch.device("cuda", device)
+    data = torch.frombuffer(bytearray(b"".join(blobs)) or bytearray(1), dtype=torch.uint8).to(dev)
+    offs = torch.from_numpy(offsets.view(np.int64)).to(dev)
+    out = torch.empty(len(blobs), dtype=torch.int64, device=dev)
+    check(_lib.lib().sbbf_gpu_hash_bytes(C.c_void_p(data.data_ptr()), C.c_void_p(offs.data_ptr()), len(blobs),
+                                         seed, C.c_void_p(out.data_ptr()), _stream_ptr(device)),
+          "sbbf_gpu_hash_bytes")
+    return out
+
 
 def block_index_batch(hashes: "torch.Tensor", num_buckets: int) -> "torch.Tensor":
     """filter.hpp:42 on device, for known-answer tests."""

@@ -144,6 +144,30 @@ def config_golden(ref: Reference, orc: Oracle, cid: int, threads: int) -> dict:
     return out
 
 
+def frontend_cases(ref: Reference) -> dict:
+    """XXH64 frontend (hash.cpp) and run_fpp_sim (harness.cpp:67-109) goldens."""
+    g: dict = {}
+    keys = ref.mt19937_64(0xF00D, 256)
+    g["u64"] = {"key_seed": 0xF00D, "n": 256, "seeds": [0, 1, 20160216],
+                "expected": [[int(ref.lib.ref_hash_u64_key(int(k), s)) for s in (0, 1, 20160216)]
+                             for k in keys]}
+    rng = np.random.default_rng(0xBEEF)
+    strings = [rng.integers(0, 256, size=int(rng.integers(0, 100)), dtype=np.uint8).tobytes()
+               for _ in range(64)]
+    g["bytes"] = {"hex": [s.hex() for s in strings],
+                  "expected": [ref.hash_key(s, 7) for s in strings], "seed": 7}
+    # acceptance.cpp:168-181,354-366 (criteria 4a-4c) and the README example
+    runs = []
+    for ndv, nbytes, seed in ((100_000, 131_072, 20160216), (1_000_000, 1_048_576, 20160216),
+                              (100_000_000, 134_217_728, 20160216), (100_000, 131_072, 1)):
+        fp, crc = ref.fpp_sim(ndv, nbytes, 1_000_000, seed)
+        runs.append({"ndv": ndv, "filter_bytes": nbytes, "queries": 1_000_000, "seed": seed,
+                     "false_positives": fp, "image_crc": crc})
+        print(f"fpp-sim ndv={ndv} bytes={nbytes} seed={seed}: fp={fp} crc={crc:#x}", flush=True)
+    g["fpp_sim"] = runs
+    return g
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg4", action="store_true")
@@ -152,6 +176,8 @@ def main() -> None:
     ref, orc = Reference(), Oracle()
     with open(os.path.join(OUT, "unit_cases.json"), "w") as fh:
         json.dump(unit_cases(ref, orc), fh)
+    with open(os.path.join(OUT, "frontend.json"), "w") as fh:
+        json.dump(frontend_cases(ref), fh)
     cfgs = {}
     path = os.path.join(OUT, "configs.json")
     if os.path.exists(path):
