@@ -148,6 +148,20 @@ int sbbf_gpu_set_find_variant(sbbf_gpu_t* f, int variant);
 int sbbf_gpu_resolved_insert_variant(const sbbf_gpu_t* f, uint64_t n);
 int sbbf_gpu_resolved_find_variant(const sbbf_gpu_t* f, uint64_t n);
 
+/* --- FilterImage v1: serialize / deserialize / save_filter / load_filter
+ *     (persist.hpp:14-31,50-66; persist.cpp:72-157). The image is
+ *     "SBBF" | version 1 | hasher id (u32 LE) | bucket count (u64 LE) |
+ *     blocks | CRC-32 (IEEE) of everything before it. The CRC of the block
+ *     array is computed on the GPU. Format errors return SBBF_EFORMAT with
+ *     *errc = 1 + PersistErrc: 1 truncated, 2 bad magic, 3 bad version,
+ *     4 zero buckets, 5 bad checksum, 6 I/O. --------------------------- */
+uint64_t sbbf_gpu_image_size(uint64_t num_buckets);
+int sbbf_gpu_image_crc(const sbbf_gpu_t* f, uint32_t* crc);
+int sbbf_gpu_serialize(const sbbf_gpu_t* f, void* h_dst, uint64_t cap, uint64_t* written);
+int sbbf_gpu_deserialize(const void* h_img, uint64_t len, int device, sbbf_gpu_t** out, int* errc);
+int sbbf_gpu_save(const sbbf_gpu_t* f, const char* path, int* errc);
+int sbbf_gpu_load(const char* path, int device, sbbf_gpu_t** out, int* errc);
+
 /* --- XXH64 key frontend: kHasherXxh64 (hash.hpp:12), hash_key /
  *     hash_u64_key (hash.hpp:20-25, hash.cpp:100-114) ----------------------
  * u64 keys hash as their 8 little-endian bytes; byte-string key i is

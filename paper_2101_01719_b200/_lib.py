@@ -57,6 +57,12 @@ PROTOTYPES = {
     "sbbf_gpu_resolved_insert_variant": (_i, [_vp, _u64]),
     "sbbf_gpu_resolved_find_variant": (_i, [_vp, _u64]),
     "sbbf_gpu_set_l2_fetch_granularity": (_i, [_i, _i, C.POINTER(_i)]),
+    "sbbf_gpu_image_size": (_u64, [_u64]),
+    "sbbf_gpu_image_crc": (_i, [_vp, C.POINTER(_u32)]),
+    "sbbf_gpu_serialize": (_i, [_vp, _vp, _u64, C.POINTER(_u64)]),
+    "sbbf_gpu_deserialize": (_i, [_vp, _u64, _i, C.POINTER(_vp), C.POINTER(_i)]),
+    "sbbf_gpu_save": (_i, [_vp, C.c_char_p, C.POINTER(_i)]),
+    "sbbf_gpu_load": (_i, [C.c_char_p, _i, C.POINTER(_vp), C.POINTER(_i)]),
     "sbbf_gpu_hash_u64_keys": (_i, [_vp, _u64, _u64, _vp, _vp]),
     "sbbf_gpu_hash_bytes": (_i, [_vp, _vp, _u64, _u64, _vp, _vp]),
     "sbbf_gpu_insert_keys_u64": (_i, [_vp, _vp, _u64, _u64, _vp]),

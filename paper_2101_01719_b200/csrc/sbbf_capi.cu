@@ -470,6 +470,128 @@ int sbbf_gpu_resolved_find_variant(const sbbf_gpu_t* f, uint64_t n) {
   return f ? resolve_find(f, n) : SBBF_EINVAL;
 }
 
+// ---- FilterImage v1 (persist.hpp:14-31, persist.cpp:72-157) -----------------
+static void image_header(uint8_t hdr[17], uint64_t nb, uint32_t hasher_id) {
+  hdr[0] = 'S';
+  hdr[1] = 'B';
+  hdr[2] = 'B';
+  hdr[3] = 'F';
+  hdr[4] = 1;  // kImageVersion, persist.hpp:21
+  for (int i = 0; i < 4; ++i) hdr[5 + i] = static_cast<uint8_t>(hasher_id >> (8 * i));
+  for (int i = 0; i < 8; ++i) hdr[9 + i] = static_cast<uint8_t>(nb >> (8 * i));
+}
+
+uint64_t sbbf_gpu_image_size(uint64_t num_buckets) { return 17 + 32 * num_buckets + 4; }
+
+int sbbf_gpu_image_crc(const sbbf_gpu_t* f, uint32_t* crc) {
+  if (!f || !crc) return fail(SBBF_EINVAL, "null argument");
+  DeviceGuard g(f->di.device);
+  uint8_t hdr[17];
+  image_header(hdr, f->nb, f->hasher_id);
+  cudaError_t e = cudaDeviceSynchronize();
+  uint32_t body = 0;
+  if (e == cudaSuccess) e = sbbf::device_crc32(f->d_blocks, f->nb * 32, &body, nullptr);
+  if (e != cudaSuccess) return cuda_fail(e, "image crc");
+  *crc = sbbf::crc32_combine(sbbf::crc32_host_update(0, hdr, 17), body, f->nb * 32);
+  return SBBF_OK;
+}
+
+int sbbf_gpu_serialize(const sbbf_gpu_t* f, void* h_dst, uint64_t cap, uint64_t* written) {
+  if (!f || !h_dst) return fail(SBBF_EINVAL, "null argument");
+  const uint64_t size = sbbf_gpu_image_size(f->nb);
+  if (cap < size) return fail(SBBF_EINVAL, "destination smaller than the image");
+  uint8_t* out = static_cast<uint8_t*>(h_dst);
+  image_header(out, f->nb, f->hasher_id);
+  int rc = sbbf_gpu_to_host(f, out + 17, f->nb * 32);  // lanes are little-endian in HBM already
+  uint32_t crc = 0;
+  if (rc == SBBF_OK) rc = sbbf_gpu_image_crc(f, &crc);
+  if (rc != SBBF_OK) return rc;
+  for (int i = 0; i < 4; ++i) out[size - 4 + i] = static_cast<uint8_t>(crc >> (8 * i));
+  if (written) *written = size;
+  return SBBF_OK;
+}
+
+static uint64_t get_le(const uint8_t* p, int n) {
+  uint64_t v = 0;
+  for (int i = n - 1; i >= 0; --i) v = (v << 8) | p[i];
+  return v;
+}
+
+// persist.cpp:90-126: same checks, same order, same codes (errc = 1 + PersistErrc).
+int sbbf_gpu_deserialize(const void* h_img, uint64_t len, int device, sbbf_gpu_t** out, int* errc) {
+  if (!out) return fail(SBBF_EINVAL, "out is null");
+  *out = nullptr;
+  auto bad = [&](int code, const char* msg) {
+    if (errc) *errc = code;
+    return fail(SBBF_EFORMAT, msg);
+  };
+  if (errc) *errc = 0;
+  const uint8_t* b = static_cast<const uint8_t*>(h_img);
+  if (!b || len < 21) return bad(1, "filter image shorter than fixed fields");
+  if (b[0] != 'S' || b[1] != 'B' || b[2] != 'B' || b[3] != 'F') return bad(2, "not a filter image (bad magic)");
+  if (b[4] != 1) return bad(3, "unsupported filter image version");
+  const uint32_t hid = static_cast<uint32_t>(get_le(b + 5, 4));
+  const uint64_t nb = get_le(b + 9, 8);
+  if (nb == 0) return bad(4, "filter image declares zero buckets");
+  if (nb > (~uint64_t{0} - 21) / 32 || len != sbbf_gpu_image_size(nb))
+    return bad(1, "filter image length does not match its bucket count");
+  sbbf_gpu_t* f = nullptr;
+  int rc = sbbf_gpu_create(nb, device, &f);
+  if (rc != SBBF_OK) return rc;
+  rc = sbbf_gpu_from_host(f, b + 17, nb * 32);
+  if (rc == SBBF_OK) rc = sbbf_gpu_set_hasher_id(f, hid);
+  uint32_t crc = 0;
+  if (rc == SBBF_OK) rc = sbbf_gpu_image_crc(f, &crc);
+  if (rc != SBBF_OK) {
+    sbbf_gpu_destroy(f);
+    return rc;
+  }
+  if (crc != static_cast<uint32_t>(get_le(b + len - 4, 4))) {
+    sbbf_gpu_destroy(f);
+    return bad(5, "filter image checksum mismatch");
+  }
+  *out = f;
+  return SBBF_OK;
+}
+
+// save_filter / load_filter (persist.cpp:128-157); I/O failures -> errc 6 (kIo).
+int sbbf_gpu_save(const sbbf_gpu_t* f, const char* path, int* errc) {
+  if (!f || !path) return fail(SBBF_EINVAL, "null argument");
+  if (errc) *errc = 0;
+  std::vector<uint8_t> img(sbbf_gpu_image_size(f->nb));
+  int rc = sbbf_gpu_serialize(f, img.data(), img.size(), nullptr);
+  if (rc != SBBF_OK) return rc;
+  FILE* fp = std::fopen(path, "wb");
+  const bool ok = fp && std::fwrite(img.data(), 1, img.size(), fp) == img.size() && std::fflush(fp) == 0;
+  if (fp) std::fclose(fp);
+  if (!ok) {
+    if (errc) *errc = 6;
+    return fail(SBBF_EFORMAT, std::string("cannot write ") + path);
+  }
+  return SBBF_OK;
+}
+
+int sbbf_gpu_load(const char* path, int device, sbbf_gpu_t** out, int* errc) {
+  if (!path || !out) return fail(SBBF_EINVAL, "null argument");
+  *out = nullptr;
+  FILE* fp = std::fopen(path, "rb");
+  if (!fp) {
+    if (errc) *errc = 6;
+    return fail(SBBF_EFORMAT, std::string("cannot open ") + path);
+  }
+  std::vector<uint8_t> bytes;
+  uint8_t chunk[1 << 16];
+  size_t got;
+  while ((got = std::fread(chunk, 1, sizeof(chunk), fp)) > 0) bytes.insert(bytes.end(), chunk, chunk + got);
+  const bool err = std::ferror(fp) != 0;
+  std::fclose(fp);
+  if (err) {
+    if (errc) *errc = 6;
+    return fail(SBBF_EFORMAT, std::string("read failed for ") + path);
+  }
+  return sbbf_gpu_deserialize(bytes.data(), bytes.size(), device, out, errc);
+}
+
 // ---- XXH64 key frontend (hash.hpp:11-25, hash.cpp:100-114) -----------------
 int sbbf_gpu_hash_u64_keys(const uint64_t* d_keys, uint64_t n, uint64_t seed, uint64_t* d_hashes,
                            void* stream) {

@@ -75,6 +75,12 @@ cudaError_t launch_insert_keys(const DeviceInfo& di, bool test, uint32_t* blocks
 cudaError_t launch_find_keys(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const uint64_t* keys,
                              uint64_t n, uint64_t seed, void* out, bool bits, cudaStream_t s);
 
+// FilterImage CRC-32 (sbbf_image.cu): standard CRC-32 of `bytes` device
+// bytes (synchronises `s`), and host helpers to extend / combine CRCs.
+cudaError_t device_crc32(const void* d_data, uint64_t bytes, uint32_t* crc_out, cudaStream_t s);
+uint32_t crc32_host_update(uint32_t crc, const uint8_t* p, uint64_t n);
+uint32_t crc32_combine(uint32_t crc1, uint32_t crc2, uint64_t len2);
+
 cudaError_t launch_block_index(const uint64_t* h, uint64_t n, uint64_t nb, uint64_t* out,
                                cudaStream_t s);
 cudaError_t launch_make_mask(const uint64_t* h, uint64_t n, uint32_t* out, cudaStream_t s);

@@ -40,6 +40,19 @@ except ImportError:  # pragma: no cover
     torch = None
 
 
+PERSIST_ERRC = {1: "kTruncated", 2: "kBadMagic", 3: "kBadVersion", 4: "kBadBucketCount",
+                5: "kBadChecksum", 6: "kIo"}  # persist.hpp:33-40 (value + 1)
+
+
+class PersistError(ValueError):
+    """PersistError (persist.hpp:42-51): .code is the PersistErrc name."""
+
+    def __init__(self, errc: int, what: str):
+        super().__init__(what)
+        self.errc = errc
+        self.code = PERSIST_ERRC.get(errc, str(errc))
+
+
 def _is_cuda_tensor(x) -> bool:
     return torch is not None and isinstance(x, torch.Tensor) and x.is_cuda
 
@@ -219,6 +232,62 @@ class SplitBlockFilter:
         check(L.sbbf_gpu_find_bits_host(self._h, a.ctypes.data_as(C.c_void_p), a.size,
                                         o.ctypes.data_as(C.c_void_p)), "sbbf_gpu_find_bits_host")
         return o
+
+    # -- FilterImage v1 (persist.hpp:14-66, persist.cpp:72-157) ----------------------
+    def image_crc(self) -> int:
+        """The image trailer CRC-32 (computed on the GPU)."""
+        crc = C.c_uint32(0)
+        check(_lib.lib().sbbf_gpu_image_crc(self._h, C.byref(crc)), "sbbf_gpu_image_crc")
+        return int(crc.value)
+
+    def serialize(self) -> bytes:
+        """serialize() (persist.cpp:72-88): the canonical v1 image."""
+        L = _lib.lib()
+        out = np.empty(int(L.sbbf_gpu_image_size(self.num_buckets())), np.uint8)
+        written = C.c_uint64(0)
+        check(L.sbbf_gpu_serialize(self._h, out.ctypes.data_as(C.c_void_p), out.size, C.byref(written)),
+              "sbbf_gpu_serialize")
+        return out.tobytes()
+
+    @classmethod
+    def _adopt(cls, h: C.c_void_p, device: int) -> "SplitBlockFilter":
+        f = cls.__new__(cls)
+        f._h = h
+        f._device = device
+        return f
+
+    @classmethod
+    def deserialize(cls, image: bytes, device: int = 0) -> "SplitBlockFilter":
+        """deserialize() (persist.cpp:90-126); raises PersistError with the
+        reference's error code on malformed images."""
+        a = np.frombuffer(image, np.uint8) if len(image) else np.zeros(1, np.uint8)
+        h = C.c_void_p()
+        errc = C.c_int(0)
+        rc = _lib.lib().sbbf_gpu_deserialize(a.ctypes.data_as(C.c_void_p), len(image), device, C.byref(h),
+                                             C.byref(errc))
+        if rc == _lib.SBBF_EFORMAT:
+            raise PersistError(errc.value, _lib.last_error())
+        check(rc, "sbbf_gpu_deserialize")
+        return cls._adopt(h, device)
+
+    def save(self, path: str) -> None:
+        """save_filter (persist.cpp:128-142)."""
+        errc = C.c_int(0)
+        rc = _lib.lib().sbbf_gpu_save(self._h, str(path).encode(), C.byref(errc))
+        if rc == _lib.SBBF_EFORMAT:
+            raise PersistError(errc.value, _lib.last_error())
+        check(rc, "sbbf_gpu_save")
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "SplitBlockFilter":
+        """load_filter (persist.cpp:144-157)."""
+        h = C.c_void_p()
+        errc = C.c_int(0)
+        rc = _lib.lib().sbbf_gpu_load(str(path).encode(), device, C.byref(h), C.byref(errc))
+        if rc == _lib.SBBF_EFORMAT:
+            raise PersistError(errc.value, _lib.last_error())
+        check(rc, "sbbf_gpu_load")
+        return cls._adopt(h, device)
 
     # -- XXH64 key frontend (kHasherXxh64, hash.hpp:12): u64 keys hashed in-kernel --
     def _dev_keys(self, keys):
