@@ -257,6 +257,10 @@ class Reference:
         L.ref_mt19937_64.argtypes = [C.c_uint64, C.c_uint64, _u64p]
         L.ref_fpp_sim.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _u64p,
                                   C.POINTER(C.c_uint32)]
+        L.ref_sbbf_fpp.restype = C.c_double
+        L.ref_sbbf_fpp.argtypes = [C.c_double]
+        L.ref_size_for.restype = C.c_uint64
+        L.ref_size_for.argtypes = [C.c_uint64, C.c_double]
         L.ref_time_build_probe.argtypes = [C.c_uint64, _u64p, C.c_uint64, _u64p, C.c_uint64, _u8p,
                                            C.c_int, C.c_int, C.POINTER(C.c_double),
                                            C.POINTER(C.c_double), C.POINTER(C.c_void_p)]

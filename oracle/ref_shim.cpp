@@ -21,6 +21,7 @@
 
 #include "sbbf/filter.hpp"
 #include "sbbf/hash.hpp"
+#include "sbbf/model.hpp"
 #include "sbbf/persist.hpp"
 
 using sbbf::SplitBlockFilter;
@@ -154,6 +155,17 @@ void ref_fpp_sim(uint64_t ndv, uint64_t num_buckets, uint64_t queries, uint64_t 
   const std::vector<uint8_t> img = sbbf::serialize(filter);
   *image_crc = static_cast<uint32_t>(img[img.size() - 4]) | (static_cast<uint32_t>(img[img.size() - 3]) << 8) |
                (static_cast<uint32_t>(img[img.size() - 2]) << 16) | (static_cast<uint32_t>(img[img.size() - 1]) << 24);
+}
+
+// model.cpp:78-103,187-212 (sbbf_fpp, size_for) for the build tool's sizing.
+double ref_sbbf_fpp(double a) { return sbbf::sbbf_fpp(a); }
+
+uint64_t ref_size_for(uint64_t ndv, double target_fpp) {
+  try {
+    return sbbf::size_for(ndv, target_fpp).num_buckets;
+  } catch (...) {
+    return 0;
+  }
 }
 
 // ---- CPU baseline timing (harness.cpp:160-201) ---------------------------

@@ -10,10 +10,10 @@ bit-identical to the reference's for the same arguments (tests).
 """
 from __future__ import annotations
 
-import math
 import time
 
 from .filter import SplitBlockFilter
+from .tools import sbbf_fpp  # noqa: F401  (model.cpp:78-103, bit-exact restatement)
 
 try:
     import torch
@@ -23,22 +23,6 @@ except ImportError:  # pragma: no cover
 NEGATIVE_COUNTER_BASE = 1 << 32      # harness.cpp:31
 HUGE_NDV_THRESHOLD = 10_000_000      # harness.hpp:85
 KHASHER_XXH64 = 1                    # hash.hpp:12
-
-
-def sbbf_fpp(a: float) -> float:
-    """Expected FPP at a keys per block: sum_i Poisson(i; a) * (1 - (31/32)^i)^8
-    (the paper's formula; model.cpp:78-103 evaluates the same series)."""
-    if not math.isfinite(a) or a < 0:
-        raise ValueError("per-block density a must be finite and nonnegative")
-    if a == 0:
-        return 0.0
-    total, keep, i = 0.0, 1.0, 0
-    cap = int(math.ceil(a + 40.0 * math.sqrt(a) + 64.0))
-    while i <= cap:
-        total += math.exp(i * math.log(a) - a - math.lgamma(i + 1.0)) * (1.0 - keep) ** 8
-        keep *= 31.0 / 32.0
-        i += 1
-    return min(total, 1.0)
 
 
 def fpp_sim(ndv: int, filter_bytes: int, negative_queries: int = 1_000_000, seed: int = 1,

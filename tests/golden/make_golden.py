@@ -165,7 +165,30 @@ def frontend_cases(ref: Reference) -> dict:
                      "false_positives": fp, "image_crc": crc})
         print(f"fpp-sim ndv={ndv} bytes={nbytes} seed={seed}: fp={fp} crc={crc:#x}", flush=True)
     g["fpp_sim"] = runs
+    # sbbf build / query (harness.cpp:262-304) on a deterministic key file
+    keys, probes = build_query_inputs()
+    hashes = np.array([ref.hash_key(k, 0) for k in keys], np.uint64)
+    distinct = int(np.unique(hashes).size)
+    g_build = {}
+    for fpp in (0.01, 0.001, 0.2):
+        nb = int(ref.lib.ref_size_for(max(1, distinct), fpp))
+        f = ref.filter(nb, 1)
+        f.add_hashes(hashes)
+        ph = np.array([ref.hash_key(k, 0) for k in probes], np.uint64)
+        res = f.find_hashes(ph)
+        g_build[str(fpp)] = {"num_buckets": nb, "image_crc": image_crc(f.serialize()),
+                             "maybe": int(res.sum()), "answers_sha256": sha(res)}
+    g["build_query"] = {"keys_read": len(keys), "distinct": distinct, "runs": g_build}
     return g
+
+
+def build_query_inputs():
+    """Key file lines for the build/query golden: 20k keys with duplicates
+    and an empty line; probes = every other key plus absent ones."""
+    keys = [f"key-{i}".encode() for i in range(20_000)] + [f"key-{i}".encode() for i in range(0, 20_000, 7)]
+    keys.append(b"")
+    probes = keys[::2] + [f"absent-{i}".encode() for i in range(30_000)]
+    return keys, probes
 
 
 def main() -> None:
