@@ -50,7 +50,8 @@ struct DeviceGuard {
   }
 };
 
-constexpr uint64_t kHostChunk = uint64_t{1} << 22;  // keys per pipelined host chunk (32 MiB)
+constexpr uint64_t kHostChunk = uint64_t{1} << 20;  // keys per pipelined host chunk (8 MiB)
+constexpr int kHostStreams = 3;                      // chunks in flight: H2D / kernel / D2H
 
 }  // namespace
 
@@ -65,9 +66,9 @@ struct sbbf_gpu {
   // Host-buffer path resources, created on first use.
   std::mutex host_mu;
   bool host_ready = false;
-  cudaStream_t hs[2] = {nullptr, nullptr};
-  uint64_t* d_stage[2] = {nullptr, nullptr};
-  void* d_res[2] = {nullptr, nullptr};
+  cudaStream_t hs[kHostStreams] = {};
+  uint64_t* d_stage[kHostStreams] = {};
+  void* d_res[kHostStreams] = {};
   uint64_t* d_one = nullptr;  // single-key scratch: [hash, result]
   // L2-blocked path: filter slice bounds (global block ids), created lazily.
   std::mutex plan_mu;
@@ -165,7 +166,7 @@ cudaError_t do_find(sbbf_gpu* f, int variant, const uint64_t* h, uint64_t n, voi
 
 int ensure_host_path(sbbf_gpu* f) {
   if (f->host_ready) return SBBF_OK;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kHostStreams; ++i) {
     cudaError_t e = cudaStreamCreateWithFlags(&f->hs[i], cudaStreamNonBlocking);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
     e = cudaMalloc(&f->d_stage[i], kHostChunk * sizeof(uint64_t));
@@ -192,7 +193,7 @@ int host_pipeline(sbbf_gpu* f, HostOp op, const uint64_t* h_hashes, uint64_t n, 
   if (rc != SBBF_OK) return rc;
   for (uint64_t off = 0, c = 0; off < n; off += kHostChunk, ++c) {
     const uint64_t m = (n - off < kHostChunk) ? n - off : kHostChunk;
-    const int s = static_cast<int>(c & 1);
+    const int s = static_cast<int>(c % kHostStreams);
     cudaError_t e = cudaMemcpyAsync(f->d_stage[s], h_hashes + off, m * sizeof(uint64_t),
                                     cudaMemcpyHostToDevice, f->hs[s]);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(H2D)");
@@ -211,7 +212,7 @@ int host_pipeline(sbbf_gpu* f, HostOp op, const uint64_t* h_hashes, uint64_t n, 
       if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(D2H)");
     }
   }
-  for (int s = 0; s < 2; ++s) {
+  for (int s = 0; s < kHostStreams; ++s) {
     cudaError_t e = cudaStreamSynchronize(f->hs[s]);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
   }
@@ -279,7 +280,7 @@ int sbbf_gpu_destroy(sbbf_gpu_t* f) {
     cudaFree(f->d_blocks);
     cudaFree(f->d_one);
     cudaFree(f->d_plan_bounds);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kHostStreams; ++i) {
       if (f->hs[i]) cudaStreamDestroy(f->hs[i]);
       cudaFree(f->d_stage[i]);
       cudaFree(f->d_res[i]);

@@ -118,6 +118,10 @@ __global__ void __launch_bounds__(kThreads, 4) insert_wide_kernel(uint32_t* __re
   // together so one DRAM round trip feeds 4*kT atomic rounds.
   constexpr int kT = 4;
   const uint64_t nsteps = (n + 32 * kT - 1) / (32 * kT);
+  // Programmatic dependent launch: let a following lookup grid get scheduled
+  // now (it waits in griddepcontrol.wait for this grid to finish before it
+  // reads the filter) so its launch latency hides behind this kernel's tail.
+  asm volatile("griddepcontrol.launch_dependents;");
   for (uint64_t t = warp; t < nsteps; t += nwarps) {
     const uint64_t base = t * (32 * kT);
     uint64_t h[kT];
@@ -196,6 +200,17 @@ __global__ void __launch_bounds__(kThreads, find_min_blocks<U, kBits>())
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
   constexpr uint64_t kTile = 32 * U;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
+  // Launched as a programmatic dependent of a preceding insert: warm the
+  // first tile's hashes into L2 (they do not depend on the insert), then wait
+  // for the insert grid to complete before touching the filter.
+  if (warp < ntiles) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t idx = warp * kTile + u * 32 + lane;
+      if (idx < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(hashes + idx));
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (uint64_t t = warp; t < ntiles; t += nwarps) {
     const uint64_t base = t * kTile;
     uint64_t h[U];
@@ -488,10 +503,21 @@ cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* block
     static const int occ_b = resident_blocks(find_global_kernel<kFindU, true>, kThreads, 0);
     static const int occ_y = resident_blocks(find_global_kernel<kFindU, false>, kThreads, 0);
     const uint64_t grid = grid_for(n, kThreads * kFindU, di.sms, bits ? occ_b : occ_y);
+    // programmatic dependent launch (see find_global_kernel's prologue)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const uint64_t zero_seed = 0;
     if (bits)
-      find_global_kernel<kFindU, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n, out);
-    else
-      find_global_kernel<kFindU, false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n, out);
+      return cudaLaunchKernelEx(&cfg, find_global_kernel<kFindU, true>, blocks, g, hashes, n, out, zero_seed);
+    return cudaLaunchKernelEx(&cfg, find_global_kernel<kFindU, false>, blocks, g, hashes, n, out, zero_seed);
   }
   return cudaGetLastError();
 }
