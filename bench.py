@@ -4,7 +4,7 @@
 A step = one pass of the hot path over one batch: insert every key of the
 config's insert stream into a fresh (zeroed, untimed) filter, then look up
 every key of its lookup stream (packed lookup bitmap out). Inputs are
-resident in HBM before timing; L2 is flushed (256 MiB memset, untimed)
+resident in HBM before timing; L2 is flushed (256 MiB memset + 256 MiB read, untimed)
 between timed steps. `value` = (inserts + lookups) / device time per step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--extra 3,4]
@@ -141,10 +141,18 @@ def run_config_device(cid: int, steps: int, warmup: int, device, collect_parity=
     look = W.gen_lookups(st, cfg.lookups, N, 0, L, device=device.index or 0)
     bits = torch.empty((L + 31) // 32, dtype=torch.int32, device=device)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
+    flush_rd = torch.zeros(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=device)
     f = SplitBlockFilter(cfg.num_buckets, device=device.index or 0)
     chunk = cfg.insert_chunk or N
     stream = torch.cuda.current_stream(device)
     torch.cuda.synchronize(device)
+
+    def flush_l2():
+        # write a buffer larger than L2 (evicts everything), then read another
+        # one so the lines left behind are clean: the next timed step starts
+        # cold and does not pay for writing back the flush's dirty lines
+        flush.zero_()
+        flush_rd.sum()
 
     def one_step(ev):
         ev[0].record(stream)
@@ -156,14 +164,14 @@ def run_config_device(cid: int, steps: int, warmup: int, device, collect_parity=
 
     for _ in range(warmup):
         f.clear()
-        flush.zero_()
+        flush_l2()
         one_step([torch.cuda.Event(enable_timing=True) for _ in range(3)])
     torch.cuda.synchronize(device)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
     l0 = launch_count()
     for k in range(steps):
         f.clear()
-        flush.zero_()  # > L2: every timed step starts cold
+        flush_l2()  # > L2: every timed step starts cold
         one_step(evs[k])
     torch.cuda.synchronize(device)
     launches = launch_count() - l0
@@ -367,7 +375,7 @@ def workload_config(cid: int) -> dict:
                         f"{cfg.filter_bytes:,} B ({cfg.num_buckets} blocks), then "
                         f"{cfg.lookups.n:,} lookups", "config_id": cid,
             "inserts": cfg.inserts.n, "lookups": cfg.lookups.n, "num_buckets": cfg.num_buckets,
-            "l2": "flushed between timed steps (256 MiB memset, untimed)",
+            "l2": "flushed between timed steps (256 MiB memset then 256 MiB read, untimed)",
             "lookup_output": "packed bitmap (1 bit/key)", "parallelism": "single GPU"}
 
 

@@ -247,6 +247,65 @@ __global__ void __launch_bounds__(kThreads, find_min_blocks<U, kBits>())
   }
 }
 
+// Software-pipelined variant: the next tile's hashes are loaded while this
+// tile's block loads are in flight, so the HBM latency of the hash stream is
+// off the per-warp critical path.
+template <int U, bool kBits, int kMinBlocks = 2>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    find_pipe_kernel(const uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ hashes,
+                     uint64_t n, void* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = dev::policy_evict_first();
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
+  constexpr uint64_t kTile = 32 * U;
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  uint64_t hn[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t idx = warp * kTile + u * 32 + lane;
+    hn[u] = (warp < ntiles && idx < n) ? dev::ld_stream_u64(hashes + idx, pol) : 0;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // filter reads only after the insert grid
+  for (uint64_t t = warp; t < ntiles; t += nwarps) {
+    const uint64_t base = t * kTile;
+    uint64_t h[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) h[u] = hn[u];
+    Block8 b[U];
+    uint32_t owned = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      bool ok;
+      dev::ld_block_nc(blocks + local_block(h[u], g, ok) * 8, b[u]);
+      owned |= static_cast<uint32_t>(ok) << u;
+    }
+    const uint64_t tn = t + nwarps;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t idx = tn * kTile + u * 32 + lane;
+      hn[u] = (tn < ntiles && idx < n) ? dev::ld_stream_u64(hashes + idx, pol) : 0;
+    }
+    uint32_t mine = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t idx = base + u * 32 + lane;
+      const bool hit = dev::block_contains(b[u], h[u]) && ((owned >> u) & 1u) && idx < n;
+      if constexpr (kBits) {
+        const uint32_t word = __ballot_sync(0xffffffffu, hit);
+        if (lane == u) mine = word;
+      } else {
+        if (idx < n) dev::st_stream_u8(static_cast<uint8_t*>(out) + idx, hit ? 1u : 0u);
+      }
+    }
+    if constexpr (kBits) {
+      const uint64_t nwords = (n + 31) >> 5;
+      const uint64_t widx = (base >> 5) + lane;
+      if (lane < U && widx < nwords) dev::st_stream_u32(static_cast<uint32_t*>(out) + widx, mine);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // lookup from shared memory (small filters)
 // ---------------------------------------------------------------------------
@@ -500,12 +559,13 @@ cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* block
     const uint64_t grid = grid_for(n, threads * 8, di.sms, 1);
     kern<<<static_cast<unsigned>(grid), threads, smem, s>>>(blocks, g, hashes, n, out);
   } else {
-    static const int occ_b = resident_blocks(find_global_kernel<kFindU, true>, kThreads, 0);
-    static const int occ_y = resident_blocks(find_global_kernel<kFindU, false>, kThreads, 0);
-    const uint64_t grid = grid_for(n, kThreads * kFindU, di.sms, bits ? occ_b : occ_y);
-    // programmatic dependent launch (see find_global_kernel's prologue)
+    // Pipelined lookup, 4 keys in flight per thread plus the next tile's
+    // hashes, 3 CTAs/SM (sweep of U in {2,4,8} x CTAs/SM: profiles/r1_find_tuning.md).
+    // Launched as a programmatic dependent of a preceding insert.
+    constexpr int kU = 4, kMinB = 3;
+    static const int occ = resident_blocks(find_pipe_kernel<kU, true, kMinB>, kThreads, 0);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kU, di.sms, occ)));
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
@@ -514,10 +574,8 @@ cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* block
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const uint64_t zero_seed = 0;
-    if (bits)
-      return cudaLaunchKernelEx(&cfg, find_global_kernel<kFindU, true>, blocks, g, hashes, n, out, zero_seed);
-    return cudaLaunchKernelEx(&cfg, find_global_kernel<kFindU, false>, blocks, g, hashes, n, out, zero_seed);
+    return bits ? cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, true, kMinB>, blocks, g, hashes, n, out)
+                : cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, false, kMinB>, blocks, g, hashes, n, out);
   }
   return cudaGetLastError();
 }
