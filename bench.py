@@ -414,6 +414,8 @@ def main() -> None:
     ap.add_argument("--extra", default="3,4", help="extra configs reported under 'configs'")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the multi-GPU sharded path even at world size 1 (NCCL self-exchange)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -422,9 +424,16 @@ def main() -> None:
         return
 
     world = env_int("WORLD_SIZE", 1)
-    if world > 1:
+    if world > 1 or args.sharded:
         from paper_2101_01719_b200 import sharded
-        sharded.bench_main(args)
+        rank = env_int("RANK", 0)
+        clocks = ClockSampler(env_int("LOCAL_RANK", 0))
+        if rank == 0:
+            clocks.start()
+        line = sharded.bench_main(args)
+        if rank == 0:
+            line["clocks"] = clocks.stop()
+            print(json.dumps(line), flush=True)
         return
 
     import torch

@@ -202,6 +202,13 @@ int sbbf_shard_count(const uint64_t* d_hashes, uint64_t n, uint64_t total_bucket
 int sbbf_shard_scatter(const uint64_t* d_hashes, uint64_t n, uint64_t total_buckets,
                        const uint64_t* d_bounds, uint32_t parts, const uint64_t* d_offsets,
                        uint64_t* d_cursor, uint64_t* d_out, uint32_t* d_pos, void* stream);
+/* One call for count + scatter (parts <= 64): warp-ballot multisplit, shard
+ * segments staged through shared memory for coalesced stores, no host sync.
+ * d_counts[r] = keys for shard r; segment r of d_out starts at the exclusive
+ * prefix sum of d_counts; d_scratch is parts u64. */
+int sbbf_shard_partition(const uint64_t* d_hashes, uint64_t n, uint64_t total_buckets,
+                         const uint64_t* d_bounds, uint32_t parts, uint64_t* d_counts, uint64_t* d_scratch,
+                         uint64_t* d_out, uint32_t* d_pos, void* stream);
 /* d_dst[d_pos[i]] = d_src[i]: lookup answers back to source order. */
 int sbbf_scatter_u8(const uint8_t* d_src, const uint32_t* d_pos, uint64_t n, uint8_t* d_dst,
                     void* stream);

@@ -74,6 +74,7 @@ PROTOTYPES = {
     "sbbf_shard_bounds": (_i, [_u64, _u32, _u64p]),
     "sbbf_shard_count": (_i, [_vp, _u64, _u64, _vp, _u32, _vp, _vp]),
     "sbbf_shard_scatter": (_i, [_vp, _u64, _u64, _vp, _u32, _vp, _vp, _vp, _vp, _vp]),
+    "sbbf_shard_partition": (_i, [_vp, _u64, _u64, _vp, _u32, _vp, _vp, _vp, _vp, _vp]),
     "sbbf_scatter_u8": (_i, [_vp, _vp, _u64, _vp, _vp]),
     "sbbf_pack_bits": (_i, [_vp, _u64, _vp, _vp]),
     "sbbf_gpu_last_error": (C.c_char_p, []),

@@ -18,6 +18,7 @@
 // filter_bytes / chunk_keys, instead of a ~128-byte random line fill.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "sbbf_device.cuh"
@@ -55,12 +56,25 @@ constexpr int kMaxBits = 6;
 struct BucketMap {
   uint64_t nb_global, first, nb_local, mult;  // mult = floor(S * 2^32 / nb_local)
   uint32_t S, bits;
+  const uint64_t* bounds;  // optional exact bucket starts (local block ids), S entries
+  bool top_bits;           // whole filter, S = 2^bits: bucket = top bits of the hash
 };
 
 __device__ __forceinline__ uint32_t bucket_of(uint64_t h, const BucketMap& bm) {
-  const uint64_t b = dev::block_index(h, bm.nb_global) - bm.first;
-  const uint64_t q = (b < bm.nb_local ? b : 0) * bm.mult >> 32;
-  return q < bm.S ? static_cast<uint32_t>(q) : bm.S - 1;
+  // block_index is monotone in the hash, so the hash's top bits split the
+  // filter into S contiguous block ranges without any 64-bit multiply
+  if (bm.top_bits) return static_cast<uint32_t>(h >> (64 - bm.bits));
+  uint64_t b = dev::block_index(h, bm.nb_global) - bm.first;
+  b = b < bm.nb_local ? b : 0;
+  uint64_t q = b * bm.mult >> 32;
+  q = q < bm.S ? q : bm.S - 1;
+  if (bm.bounds) {
+    // exact ranges (multi-GPU shards: [floor(rB/P), floor((r+1)B/P))): the
+    // fixed-point estimate is within one of the owner
+    while (q + 1 < bm.S && b >= __ldg(bm.bounds + q + 1)) ++q;
+    while (q > 0 && b < __ldg(bm.bounds + q)) --q;
+  }
+  return static_cast<uint32_t>(q);
 }
 
 // Lanes whose bucket equals `v`, given the per-bit ballots of the warp.
@@ -99,32 +113,43 @@ __device__ __forceinline__ uint32_t warp_rank(uint32_t bk, bool valid, uint32_t 
   return prior + __popc(peers & ((1u << lane) - 1u));
 }
 
+// Both passes give CTA c the same contiguous run of chunks, so the count
+// pass can hand each CTA exact per-bucket output offsets (after a tiny scan)
+// and the scatter pass needs no global atomics on its critical path.
+__device__ __forceinline__ void cta_chunk_range(uint64_t n, uint64_t& c0, uint64_t& c1) {
+  const uint64_t nchunks = (n + kPartChunk - 1) / kPartChunk;
+  const uint64_t per = (nchunks + gridDim.x - 1) / gridDim.x;
+  c0 = static_cast<uint64_t>(blockIdx.x) * per;
+  c1 = c0 + per < nchunks ? c0 + per : nchunks;
+}
+
 template <int BITS>
 __global__ void __launch_bounds__(kPartThreads, 2) bucket_count_kernel(const uint64_t* __restrict__ hashes,
                                                                        uint64_t n, BucketMap bm,
-                                                                       unsigned long long* __restrict__ counts) {
+                                                                       uint32_t* __restrict__ cta_hist) {
   __shared__ unsigned int cta[kMaxBuckets];
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t pol = dev::policy_evict_first();
   if (threadIdx.x < kMaxBuckets) cta[threadIdx.x] = 0;
   uint32_t c0 = 0, c1 = 0;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kPartChunk;
-  uint64_t base = static_cast<uint64_t>(blockIdx.x) * kPartChunk;
+  uint64_t ch0, ch1;
+  cta_chunk_range(n, ch0, ch1);
   // Software pipeline: the next chunk's loads are in flight while this
   // chunk's ballots run (the kernel is otherwise latency bound).
   uint64_t nxt[kPartPerThread];
 #pragma unroll
   for (int j = 0; j < kPartPerThread; ++j) {
-    const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
-    nxt[j] = i < n ? dev::ld_stream_u64(hashes + i, pol) : 0;
+    const uint64_t i = ch0 * kPartChunk + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
+    nxt[j] = (ch0 < ch1 && i < n) ? dev::ld_stream_u64(hashes + i, pol) : 0;
   }
-  for (; base < n; base += stride) {
+  for (uint64_t ch = ch0; ch < ch1; ++ch) {
+    const uint64_t base = ch * kPartChunk;
     uint64_t h[kPartPerThread];
 #pragma unroll
     for (int j = 0; j < kPartPerThread; ++j) {
       h[j] = nxt[j];
-      const uint64_t i = base + stride + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
-      nxt[j] = i < n ? dev::ld_stream_u64(hashes + i, pol) : 0;
+      const uint64_t i = base + kPartChunk + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
+      nxt[j] = (ch + 1 < ch1 && i < n) ? dev::ld_stream_u64(hashes + i, pol) : 0;
     }
 #pragma unroll
     for (int j = 0; j < kPartPerThread; ++j) {
@@ -141,8 +166,30 @@ __global__ void __launch_bounds__(kPartThreads, 2) bucket_count_kernel(const uin
   if (lane < bm.S && c0) atomicAdd(&cta[lane], c0);
   if (lane + 32 < bm.S && c1) atomicAdd(&cta[lane + 32], c1);
   __syncthreads();
-  if (threadIdx.x < bm.S && cta[threadIdx.x])
-    atomicAdd(&counts[threadIdx.x], static_cast<unsigned long long>(cta[threadIdx.x]));
+  if (threadIdx.x < kMaxBuckets) cta_hist[static_cast<uint64_t>(blockIdx.x) * kMaxBuckets + threadIdx.x] = cta[threadIdx.x];
+}
+
+// counts[b] = total of bucket b; cta_base[c][b] = first output slot of CTA c's
+// keys in bucket b (buckets are laid out in order, CTAs in order inside each).
+__global__ void bucket_scan_kernel(const uint32_t* __restrict__ cta_hist, uint32_t ctas, uint32_t S,
+                                   unsigned long long* __restrict__ counts,
+                                   unsigned long long* __restrict__ cta_base) {
+  __shared__ unsigned long long tot[kMaxBuckets];
+  const uint32_t b = threadIdx.x;  // one thread per bucket
+  unsigned long long t = 0;
+  if (b < S)
+    for (uint32_t c = 0; c < ctas; ++c) t += cta_hist[static_cast<uint64_t>(c) * kMaxBuckets + b];
+  tot[b] = t;
+  __syncthreads();
+  if (b < S) {
+    unsigned long long start = 0;
+    for (uint32_t k = 0; k < b; ++k) start += tot[k];
+    counts[b] = t;
+    for (uint32_t c = 0; c < ctas; ++c) {
+      cta_base[static_cast<uint64_t>(c) * kMaxBuckets + b] = start;
+      start += cta_hist[static_cast<uint64_t>(c) * kMaxBuckets + b];
+    }
+  }
 }
 
 // Scatter through shared memory: each chunk is first placed bucket-major in
@@ -154,20 +201,25 @@ struct ScatterSmem {
   uint32_t pos[kPartChunk];
   uint8_t bk[kPartChunk];
   uint32_t wcnt[kPartWarps][kMaxBuckets];  // per-warp counts -> exclusive prefix over warps
-  uint32_t boff[kMaxBuckets];              // exclusive prefix over buckets (CTA-local)
-  unsigned long long gbase[kMaxBuckets];   // global slot of the CTA's run, per bucket
+  uint32_t boff[kMaxBuckets];              // exclusive prefix over buckets (chunk-local)
+  unsigned long long gbase[kMaxBuckets];   // global slot of this chunk's run, per bucket
+  unsigned long long cursor[kMaxBuckets];  // this CTA's next slot per bucket
 };
 
 template <int BITS>
 __global__ void __launch_bounds__(kPartThreads, 2) bucket_scatter_kernel(
-    const uint64_t* __restrict__ hashes, uint64_t n, BucketMap bm, unsigned long long* __restrict__ cursor,
-    uint64_t* __restrict__ out, uint32_t* __restrict__ pos) {
+    const uint64_t* __restrict__ hashes, uint64_t n, BucketMap bm,
+    const unsigned long long* __restrict__ cta_base, uint64_t* __restrict__ out, uint32_t* __restrict__ pos) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ScatterSmem& sm = *reinterpret_cast<ScatterSmem*>(smem_raw);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t pol = dev::policy_evict_first();
-  for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * kPartChunk; base < n;
-       base += static_cast<uint64_t>(gridDim.x) * kPartChunk) {
+  if (threadIdx.x < kMaxBuckets)
+    sm.cursor[threadIdx.x] = cta_base[static_cast<uint64_t>(blockIdx.x) * kMaxBuckets + threadIdx.x];
+  uint64_t ch0, ch1;
+  cta_chunk_range(n, ch0, ch1);
+  for (uint64_t ch = ch0; ch < ch1; ++ch) {
+    const uint64_t base = ch * kPartChunk;
     const uint32_t cnt = static_cast<uint32_t>(n - base < kPartChunk ? n - base : kPartChunk);
     uint64_t h[kPartPerThread];
     uint32_t bk[kPartPerThread], off[kPartPerThread];
@@ -189,8 +241,9 @@ __global__ void __launch_bounds__(kPartThreads, 2) bucket_scatter_kernel(
     sm.wcnt[warp][lane + 32] = c1;
     __syncthreads();
     if (warp == 0) {
-      // bucket totals (lane owns buckets lane, lane+32), warp prefixes, then a
-      // warp-wide exclusive scan over the 64 buckets
+      // bucket totals (lane owns buckets lane, lane+32), warp prefixes, a
+      // warp-wide exclusive scan over the 64 buckets, and this CTA's own
+      // cursors (no global atomics: offsets came from the count pass)
       uint32_t t0 = 0, t1 = 0;
 #pragma unroll
       for (int w = 0; w < kPartWarps; ++w) {
@@ -212,9 +265,10 @@ __global__ void __launch_bounds__(kPartThreads, 2) bucket_scatter_kernel(
       const uint32_t sum0 = __shfl_sync(0xffffffffu, s0, 31);
       sm.boff[lane] = s0 - t0;
       sm.boff[lane + 32] = sum0 + s1 - t1;
-      sm.gbase[lane] = (lane < bm.S && t0) ? atomicAdd(&cursor[lane], static_cast<unsigned long long>(t0)) : 0ull;
-      sm.gbase[lane + 32] =
-          (lane + 32 < bm.S && t1) ? atomicAdd(&cursor[lane + 32], static_cast<unsigned long long>(t1)) : 0ull;
+      sm.gbase[lane] = sm.cursor[lane];
+      sm.gbase[lane + 32] = sm.cursor[lane + 32];
+      sm.cursor[lane] += t0;
+      sm.cursor[lane + 32] += t1;
     }
     __syncthreads();
 #pragma unroll
@@ -237,17 +291,6 @@ __global__ void __launch_bounds__(kPartThreads, 2) bucket_scatter_kernel(
   }
 }
 
-__global__ void bucket_scan_kernel(const unsigned long long* __restrict__ counts, uint32_t S,
-                                   unsigned long long* __restrict__ cursor) {
-  if (threadIdx.x == 0) {
-    unsigned long long s = 0;
-    for (uint32_t b = 0; b < S; ++b) {
-      cursor[b] = s;
-      s += counts[b];
-    }
-  }
-}
-
 BucketMap make_map(const Geom& g, uint32_t S) {
   BucketMap bm;
   bm.nb_global = g.nb_global;
@@ -258,44 +301,76 @@ BucketMap make_map(const Geom& g, uint32_t S) {
   while ((1u << bm.bits) < S) ++bm.bits;
   if (bm.bits == 0) bm.bits = 1;  // a single bucket still needs a 1-bit id
   bm.mult = static_cast<uint64_t>((static_cast<unsigned __int128>(S) << 32) / g.nb_local);
+  bm.bounds = nullptr;
+  bm.top_bits = g.first == 0 && g.nb_local == g.nb_global && (1u << bm.bits) == S;
   return bm;
+}
+
+// Scratch comes from the stream-ordered pool; keep freed blocks cached in the
+// pool (release threshold = max) so per-call allocations do not go back to
+// the driver at every synchronisation.
+void retain_pool() {
+  static std::atomic<uint64_t> done{0};  // bit per device ordinal < 64
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return;
+  const uint64_t bit = uint64_t{1} << dev;
+  if (done.load(std::memory_order_relaxed) & bit) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~uint64_t{0};
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done.fetch_or(bit, std::memory_order_relaxed);
 }
 
 template <int BITS>
 cudaError_t bucket_partition_bits(uint64_t grid, const BucketMap& bm, const uint64_t* hashes, uint64_t m,
-                                  uint64_t* d_counts, uint64_t* d_cursor, uint64_t* d_out, uint32_t* d_pos,
-                                  cudaStream_t s) {
-  note_launch();
-  bucket_count_kernel<BITS><<<static_cast<unsigned>(grid), kPartThreads, 0, s>>>(
-      hashes, m, bm, reinterpret_cast<unsigned long long*>(d_counts));
-  note_launch();
-  bucket_scan_kernel<<<1, 32, 0, s>>>(reinterpret_cast<unsigned long long*>(d_counts), bm.S,
-                                      reinterpret_cast<unsigned long long*>(d_cursor));
+                                  uint64_t* d_counts, uint64_t* d_out, uint32_t* d_pos, cudaStream_t s) {
+  retain_pool();
+  // per-CTA histograms and bases (grid x 64 entries) from the stream-ordered pool
+  uint32_t* hist = nullptr;
+  unsigned long long* bases = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&hist), grid * kMaxBuckets * sizeof(uint32_t), s);
+  if (e == cudaSuccess)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&bases), grid * kMaxBuckets * sizeof(unsigned long long), s);
   static const cudaError_t attr = cudaFuncSetAttribute(
       bucket_scatter_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
       static_cast<int>(sizeof(ScatterSmem)));
-  if (attr != cudaSuccess) return attr;
-  note_launch();
-  bucket_scatter_kernel<BITS><<<static_cast<unsigned>(grid), kPartThreads, sizeof(ScatterSmem), s>>>(
-      hashes, m, bm, reinterpret_cast<unsigned long long*>(d_cursor), d_out, d_pos);
-  return cudaGetLastError();
+  if (e == cudaSuccess) e = attr;
+  if (e == cudaSuccess) {
+    note_launch();
+    bucket_count_kernel<BITS><<<static_cast<unsigned>(grid), kPartThreads, 0, s>>>(hashes, m, bm, hist);
+    note_launch();
+    bucket_scan_kernel<<<1, kMaxBuckets, 0, s>>>(hist, static_cast<uint32_t>(grid), bm.S,
+                                                 reinterpret_cast<unsigned long long*>(d_counts), bases);
+    note_launch();
+    bucket_scatter_kernel<BITS><<<static_cast<unsigned>(grid), kPartThreads, sizeof(ScatterSmem), s>>>(
+        hashes, m, bm, bases, d_out, d_pos);
+    e = cudaGetLastError();
+  }
+  if (hist) cudaFreeAsync(hist, s);
+  if (bases) cudaFreeAsync(bases, s);
+  return e;
 }
 
 // Group `m` keys by bucket: d_out (and d_pos) receive them bucket-major.
 cudaError_t bucket_partition(const DeviceInfo& di, const Geom& g, uint32_t S, const uint64_t* hashes,
                              uint64_t m, uint64_t* d_counts, uint64_t* d_cursor, uint64_t* d_out,
-                             uint32_t* d_pos, cudaStream_t s) {
-  const BucketMap bm = make_map(g, S);
-  cudaError_t e = cudaMemsetAsync(d_counts, 0, S * sizeof(uint64_t), s);
-  if (e != cudaSuccess) return e;
+                             uint32_t* d_pos, cudaStream_t s, const uint64_t* d_bounds = nullptr) {
+  (void)d_cursor;
+  BucketMap bm = make_map(g, S);
+  bm.bounds = d_bounds;
+  // exact shard ranges: top hash bits equal the owner only when B is a power of two
+  if (d_bounds && (g.nb_global & (g.nb_global - 1)) != 0) bm.top_bits = false;
+  if (m == 0) return cudaMemsetAsync(d_counts, 0, S * sizeof(uint64_t), s);
   const uint64_t grid = grid_for(m, kPartChunk, di.sms, 2);
   switch (bm.bits) {
-    case 1: return bucket_partition_bits<1>(grid, bm, hashes, m, d_counts, d_cursor, d_out, d_pos, s);
-    case 2: return bucket_partition_bits<2>(grid, bm, hashes, m, d_counts, d_cursor, d_out, d_pos, s);
-    case 3: return bucket_partition_bits<3>(grid, bm, hashes, m, d_counts, d_cursor, d_out, d_pos, s);
-    case 4: return bucket_partition_bits<4>(grid, bm, hashes, m, d_counts, d_cursor, d_out, d_pos, s);
-    case 5: return bucket_partition_bits<5>(grid, bm, hashes, m, d_counts, d_cursor, d_out, d_pos, s);
-    case 6: return bucket_partition_bits<6>(grid, bm, hashes, m, d_counts, d_cursor, d_out, d_pos, s);
+    case 1: return bucket_partition_bits<1>(grid, bm, hashes, m, d_counts, d_out, d_pos, s);
+    case 2: return bucket_partition_bits<2>(grid, bm, hashes, m, d_counts, d_out, d_pos, s);
+    case 3: return bucket_partition_bits<3>(grid, bm, hashes, m, d_counts, d_out, d_pos, s);
+    case 4: return bucket_partition_bits<4>(grid, bm, hashes, m, d_counts, d_out, d_pos, s);
+    case 5: return bucket_partition_bits<5>(grid, bm, hashes, m, d_counts, d_out, d_pos, s);
+    case 6: return bucket_partition_bits<6>(grid, bm, hashes, m, d_counts, d_out, d_pos, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -367,6 +442,14 @@ void free_scratch(Scratch& sc, cudaStream_t s) {
 }
 
 }  // namespace
+
+cudaError_t shard_partition(const DeviceInfo& di, uint64_t total, uint32_t parts, const uint64_t* d_bounds,
+                            const uint64_t* hashes, uint64_t n, uint64_t* d_counts, uint64_t* d_cursor,
+                            uint64_t* d_out, uint32_t* d_pos, cudaStream_t s) {
+  if (n == 0) return cudaMemsetAsync(d_counts, 0, parts * sizeof(uint64_t), s);
+  const Geom whole{total, 0, total};
+  return bucket_partition(di, whole, parts, hashes, n, d_counts, d_cursor, d_out, d_pos, s, d_bounds);
+}
 
 cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
                            const uint64_t* hashes, uint64_t n, cudaStream_t s) {

@@ -123,6 +123,9 @@ int ensure_plan(sbbf_gpu* f) {
   if (f->d_plan_bounds) return SBBF_OK;
   uint64_t parts = (f->nb * 32 + kSliceBytes - 1) / kSliceBytes;
   parts = parts < 2 ? 2 : (parts > 64 ? 64 : parts);  // bucket ids are <= 6 bits
+  uint64_t pow2 = 1;
+  while (pow2 < parts) pow2 <<= 1;  // a power of two lets the partition use the hash's top bits
+  parts = pow2;
   if (parts > f->nb) parts = f->nb;
   std::vector<uint64_t> b(parts);
   for (uint64_t k = 0; k < parts; ++k)

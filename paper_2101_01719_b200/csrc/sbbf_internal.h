@@ -51,6 +51,13 @@ cudaError_t launch_partition(const uint64_t* hashes, uint64_t n, uint64_t total,
                              uint32_t parts, uint64_t* d_counts, uint64_t* d_offsets, uint64_t* d_cursor,
                              uint64_t* d_out, uint32_t* d_pos, int sms, cudaStream_t s);
 
+// Group keys by owning shard (parts <= 64, exact ranges d_bounds[0..parts)):
+// ballot-multisplit count + scan + shared-memory-staged scatter, no host
+// sync. d_counts receives the per-shard counts; d_cursor is scratch.
+cudaError_t shard_partition(const DeviceInfo& di, uint64_t total, uint32_t parts, const uint64_t* d_bounds,
+                            const uint64_t* hashes, uint64_t n, uint64_t* d_counts, uint64_t* d_cursor,
+                            uint64_t* d_out, uint32_t* d_pos, cudaStream_t s);
+
 // insert_wide over `n` keys with one warp step per 128 keys and the grid
 // covering the batch once, so CTAs run in key order (blocked path).
 cudaError_t launch_insert_ordered(const DeviceInfo& di, uint32_t* blocks, const Geom& g,

@@ -221,6 +221,22 @@ int sbbf_shard_scatter(const uint64_t* d_hashes, uint64_t n, uint64_t total_buck
   return sbbf::shard_rc(cudaGetLastError());
 }
 
+int sbbf_shard_partition(const uint64_t* d_hashes, uint64_t n, uint64_t total_buckets,
+                         const uint64_t* d_bounds, uint32_t parts, uint64_t* d_counts, uint64_t* d_scratch,
+                         uint64_t* d_out, uint32_t* d_pos, void* stream) {
+  if (!d_bounds || !d_counts || !d_scratch || parts == 0 || parts > 64 || (n && (!d_hashes || !d_out)) ||
+      n > 0xffffffffull)
+    return SBBF_EINVAL;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  sbbf::DeviceInfo di;
+  di.device = dev;
+  di.sms = sms;
+  return sbbf::shard_rc(sbbf::shard_partition(di, total_buckets, parts, d_bounds, d_hashes, n, d_counts,
+                                              d_scratch, d_out, d_pos, static_cast<cudaStream_t>(stream)));
+}
+
 int sbbf_scatter_u8(const uint8_t* d_src, const uint32_t* d_pos, uint64_t n, uint8_t* d_dst,
                     void* stream) {
   if (n == 0) return SBBF_OK;

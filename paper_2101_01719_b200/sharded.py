@@ -20,9 +20,9 @@ logic on CPU with world_size 2.
 from __future__ import annotations
 
 import ctypes as C
-import json
 import os
 import statistics
+import time
 
 import numpy as np
 
@@ -112,6 +112,17 @@ class CudaShardOps(ShardOps):
         db = self._dev_bounds(bounds)
         counts = torch.empty(parts, dtype=torch.int64, device=self.dev)
         s = self._stream()
+        if parts <= 64:
+            # one-call multisplit partition (count + scan + smem-staged scatter)
+            scratch = torch.empty(parts, dtype=torch.int64, device=self.dev)
+            routed = torch.empty(n, dtype=torch.int64, device=self.dev)
+            pos = torch.empty(n, dtype=torch.int32, device=self.dev) if with_pos else None
+            check(L.sbbf_shard_partition(C.c_void_p(keys.data_ptr()), n, total, C.c_void_p(db.data_ptr()),
+                                         parts, C.c_void_p(counts.data_ptr()), C.c_void_p(scratch.data_ptr()),
+                                         C.c_void_p(routed.data_ptr()),
+                                         C.c_void_p(pos.data_ptr()) if with_pos else None, s),
+                  "sbbf_shard_partition")
+            return counts.tolist(), routed, pos
         check(L.sbbf_shard_count(C.c_void_p(keys.data_ptr()), n, total, C.c_void_p(db.data_ptr()),
                                  parts, C.c_void_p(counts.data_ptr()), s), "sbbf_shard_count")
         offsets = torch.cumsum(counts, 0) - counts
@@ -242,18 +253,22 @@ class ShardedFilter:
 # ---------------------------------------------------------------------------------
 # bench.py --gpus N (torchrun): weak scaling, one rank per GPU
 # ---------------------------------------------------------------------------------
-def bench_main(args) -> None:
+def bench_main(args) -> dict | None:
     """Each rank originates a config-2-sized batch (1M inserts, 10M lookups);
     the filter is P x 1 MiB sharded by block range; keys cross NVLink to their
-    owner. value = all ranks' keys / max-over-ranks device time."""
+    owner. value = all ranks' keys / max-over-ranks device time. Returns the
+    JSON line on rank 0 (bench.py adds clocks and prints it), None elsewhere."""
     from . import workload as W
+    from ._lib import launch_count
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     cfg = W.CONFIGS[args.config]
     N, L = cfg.inserts.n, cfg.lookups.n
     total = cfg.num_buckets * world
@@ -264,27 +279,30 @@ def bench_main(args) -> None:
     look = W.gen_lookups(st, cfg.lookups, N * world, rank * L, L, device=local)
     f = ShardedFilter(total)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    from ._lib import launch_count
+    flush_rd = torch.zeros(64 << 20, dtype=torch.int32, device=dev)
 
-    def step():
-        f.add_hashes(ins)
-        return f.find_hashes_bits(look)
+    def step(k_ins, k_look):
+        f.add_hashes(k_ins)
+        return f.find_hashes_bits(k_look)
 
-    for _ in range(max(args.warmup, 3)):
+    def cold():
         f.shard.clear()
         flush.zero_()
-        step()
+        flush_rd.sum()
+
+    for _ in range(max(args.warmup, 3)):
+        cold()
+        step(ins, look)
     torch.cuda.synchronize(dev)
     times = []
     l0 = launch_count()
     for _ in range(args.steps):
-        f.shard.clear()
-        flush.zero_()
+        cold()
         dist.barrier()
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        step()
+        step(ins, look)
         e1.record()
         torch.cuda.synchronize(dev)
         t = torch.tensor([e0.elapsed_time(e1)], device=dev)
@@ -292,7 +310,29 @@ def bench_main(args) -> None:
         times.append(float(t.item()))
     launches = launch_count() - l0
     ms = statistics.mean(times)
+    sent = f.last_exchange.get("sent", [])
+
+    # e2e: hashes from pinned host memory, bitmap back to the host, every step
+    ins_h = ins.cpu().pin_memory()
+    look_h = look.cpu().pin_memory()
+    res_h = torch.empty((L + 31) // 32, dtype=torch.int32, pin_memory=True)
+    e2e = []
+    for k in range(args.steps + 2):
+        cold()
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        bits = step(ins_h.to(dev, non_blocking=True), look_h.to(dev, non_blocking=True))
+        res_h.copy_(bits)
+        torch.cuda.synchronize(dev)
+        t = torch.tensor([time.perf_counter() - t0], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if k >= 2:
+            e2e.append(float(t.item()))
+    line = None
     if rank == 0:
+        e2e_s = statistics.median(e2e)
+        fwd = 8.0 * (world - 1) / world  # bytes per key crossing NVLink (forward)
         line = {
             "metric": "SBBF insert/lookup Gkeys/s (device-timed) vs random-32B-sector roofline",
             "value": world * (N + L) / (ms * 1e-3) / 1e9, "unit": "Gkeys/s", "n_gpus": world,
@@ -302,8 +342,19 @@ def bench_main(args) -> None:
             "config": {"workload": f"sharded: per rank BASELINE config {args.config} batch "
                                    f"({N:,} inserts + {L:,} lookups) into a {world}-way block-range "
                                    f"sharded filter of {total} blocks; keys routed by NCCL all-to-all",
-                       "parallelism": f"shard{world}", "l2": "flushed between timed steps"},
+                       "parallelism": f"shard{world}", "l2": "flushed between timed steps (untimed)"},
+            "e2e": {"value": world * (N + L) / e2e_s / 1e9, "unit": "Gkeys/s",
+                    "h2d_bytes_per_step": 8 * (N + L), "d2h_bytes_per_step": 4 * ((L + 31) // 32),
+                    "ms_per_step": e2e_s * 1e3, "note": "per rank; max over ranks of wall time"},
+            "roofline": {"bound": "hbm", "kernel": "whole sharded step (partition + exchange + probe)",
+                         "achieved": (N + L) * 40.0 / (ms * 1e-3) / 1e9, "peak": 6523.3, "unit": "GB/s",
+                         "frac": (N + L) * 40.0 / (ms * 1e-3) / 1e9 / 6523.3, "traffic": None,
+                         "bytes_per_key": 40.0,
+                         "nvlink": {"bytes_per_key_forward": fwd,
+                                    "achieved_gbs": (N + L) * fwd / (ms * 1e-3) / 1e9,
+                                    "peer_peak_gbs": 770.0}},
             "gpu_launches": launches, "time": "max over ranks of CUDA-event step time",
+            "last_exchange_sent_keys": sent,
         }
-        print(json.dumps(line), flush=True)
     dist.destroy_process_group()
+    return line
