@@ -123,8 +123,72 @@ class SplitBlockFilter {
     return a.hasher_id() == b.hasher_id() && a.blocks() == b.blocks();
   }
 
+  // XXH64 frontend (kHasherXxh64, hash.hpp:12): u64 keys hashed in-kernel.
+  void add_keys_device(const std::uint64_t* d_keys, std::uint64_t n, std::uint64_t seed = 0,
+                       void* stream = nullptr) {
+    check(sbbf_gpu_insert_keys_u64(h_, d_keys, n, seed, stream), "insert_keys_u64");
+  }
+  void find_keys_device(const std::uint64_t* d_keys, std::uint64_t n, std::uint8_t* d_results,
+                        std::uint64_t seed = 0, void* stream = nullptr) const {
+    check(sbbf_gpu_find_keys_u64(h_, d_keys, n, seed, d_results, stream), "find_keys_u64");
+  }
+
+  static SplitBlockFilter adopt(sbbf_gpu_t* h) {
+    SplitBlockFilter f;
+    f.h_ = h;
+    return f;
+  }
+
  private:
+  SplitBlockFilter() = default;
   sbbf_gpu_t* h_ = nullptr;
 };
+
+// --- persist.hpp:33-66 mirror (FilterImage v1; CRC computed on the GPU) ----
+enum class PersistErrc { kTruncated, kBadMagic, kBadVersion, kBadBucketCount, kBadChecksum, kIo };
+
+class PersistError : public std::runtime_error {
+ public:
+  PersistError(PersistErrc code, const std::string& what) : std::runtime_error(what), code_(code) {}
+  PersistErrc code() const noexcept { return code_; }
+
+ private:
+  PersistErrc code_;
+};
+
+[[noreturn]] inline void throw_persist(int rc, int errc, const char* what) {
+  if (rc == SBBF_EFORMAT && errc >= 1 && errc <= 6)
+    throw PersistError(static_cast<PersistErrc>(errc - 1), std::string(what) + ": " + sbbf_gpu_last_error());
+  throw_status(rc, what);
+}
+
+inline std::vector<std::uint8_t> serialize(const SplitBlockFilter& f) {
+  std::vector<std::uint8_t> out(sbbf_gpu_image_size(f.num_buckets()));
+  std::uint64_t written = 0;
+  check(sbbf_gpu_serialize(f.handle(), out.data(), out.size(), &written), "serialize");
+  return out;
+}
+
+inline SplitBlockFilter deserialize(std::span<const std::uint8_t> bytes, int device = 0) {
+  sbbf_gpu_t* h = nullptr;
+  int errc = 0;
+  const int rc = sbbf_gpu_deserialize(bytes.data(), bytes.size(), device, &h, &errc);
+  if (rc != SBBF_OK) throw_persist(rc, errc, "deserialize");
+  return SplitBlockFilter::adopt(h);
+}
+
+inline void save_filter(const SplitBlockFilter& f, const std::string& path) {
+  int errc = 0;
+  const int rc = sbbf_gpu_save(f.handle(), path.c_str(), &errc);
+  if (rc != SBBF_OK) throw_persist(rc, errc, "save_filter");
+}
+
+inline SplitBlockFilter load_filter(const std::string& path, int device = 0) {
+  sbbf_gpu_t* h = nullptr;
+  int errc = 0;
+  const int rc = sbbf_gpu_load(path.c_str(), device, &h, &errc);
+  if (rc != SBBF_OK) throw_persist(rc, errc, "load_filter");
+  return SplitBlockFilter::adopt(h);
+}
 
 }  // namespace sbbf::gpu

@@ -69,6 +69,31 @@ int main() {
   REQUIRE(one.find_hash(0));
   const auto one_blocks = one.blocks();  // keep the temporary alive for the loop
   for (uint32_t lane : one_blocks[0].lanes) REQUIRE(lane == 1u);
+  // persist.hpp mirror: serialize -> deserialize round trip, CRC trailer,
+  // and the reference's error codes (persist_test.cpp:140-193)
+  const auto img = sbbf::gpu::serialize(f);
+  REQUIRE(img.size() == 17 + nb * 32 + 4);
+  const uint32_t trailer = img[img.size() - 4] | (img[img.size() - 3] << 8) | (img[img.size() - 2] << 16) |
+                           (static_cast<uint32_t>(img[img.size() - 1]) << 24);
+  REQUIRE(trailer == 0xe34f8befu);
+  auto back = sbbf::gpu::deserialize(img);
+  REQUIRE(back == f);
+  auto bad = img;
+  bad[100] ^= 1;
+  bool checksum = false;
+  try {
+    sbbf::gpu::deserialize(bad);
+  } catch (const sbbf::gpu::PersistError& e) {
+    checksum = e.code() == sbbf::gpu::PersistErrc::kBadChecksum;
+  }
+  REQUIRE(checksum);
+  bool io = false;
+  try {
+    sbbf::gpu::load_filter("/nonexistent/dir/f.sbbf");
+  } catch (const sbbf::gpu::PersistError& e) {
+    io = e.code() == sbbf::gpu::PersistErrc::kIo;
+  }
+  REQUIRE(io);
   std::printf("cpp drop-in ok: crc 0xe34f8bef, %llu false positives\n", (unsigned long long)fp);
   return 0;
 }
