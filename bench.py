@@ -441,7 +441,9 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
-                    help="run the multi-GPU sharded path even at world size 1 (NCCL self-exchange)")
+                    help="run the multi-GPU sharded path even at world size 1")
+    ap.add_argument("--route", default="auto", choices=["auto", "fused", "nccl"],
+                    help="sharded key routing: fused peer-memory dispatch or NCCL all-to-all")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

@@ -215,6 +215,36 @@ int sbbf_scatter_u8(const uint8_t* d_src, const uint32_t* d_pos, uint64_t n, uin
 /* Pack 0/1 bytes into an LSB-first bitmap of ceil(n/32) words. */
 int sbbf_pack_bits(const uint8_t* d_src, uint64_t n, uint32_t* d_bits, void* stream);
 
+/* --- fused multi-GPU dispatch over peer memory (SURVEY.md §8(e) "fused
+ *     option"; sbbf_route.cu) ---------------------------------------------
+ * Each rank owns a receive window (one cudaMalloc, exported by CUDA IPC
+ * handle) with a region per source rank and two parities. dispatch
+ * partitions a batch by owner shard and the scatter stores each owner's run
+ * straight into that owner's window over NVLink (no staging array, no
+ * counts exchange, no host sync). Per collective call, every rank runs:
+ *   insert: dispatch(keep_positions=0); barrier; insert_window
+ *   lookup: dispatch(keep_positions=1); barrier; find_window; barrier; combine
+ * where "barrier" is any stream-ordered collective (e.g. a 1-element NCCL
+ * all-reduce). Batches are <= max_batch keys per rank per call. */
+typedef struct sbbf_route sbbf_route_t;
+uint64_t sbbf_route_window_bytes(uint32_t parts, uint64_t max_batch);
+int sbbf_route_create(uint32_t parts, uint32_t rank, uint64_t max_batch, int device, sbbf_route_t** out);
+void sbbf_route_destroy(sbbf_route_t* rt);
+uint64_t sbbf_route_max_batch(const sbbf_route_t* rt);
+/* 64-byte CUDA IPC handle of this rank's window (exchange it out of band). */
+int sbbf_route_ipc_handle(const sbbf_route_t* rt, void* handle);
+/* Map peer `peer`'s window from its handle (another process). */
+int sbbf_route_open_peer(sbbf_route_t* rt, uint32_t peer, const void* handle);
+/* Same-process link (P shards driven by one process, e.g. tests). */
+int sbbf_route_link_local(sbbf_route_t* rt, uint32_t peer, const sbbf_route_t* other);
+int sbbf_route_ready(const sbbf_route_t* rt);
+int sbbf_route_dispatch(sbbf_route_t* rt, const uint64_t* d_hashes, uint64_t n, uint64_t total_buckets,
+                        const uint64_t* d_bounds, int keep_positions, void* stream);
+int sbbf_route_insert_window(sbbf_route_t* rt, sbbf_gpu_t* shard, void* stream);
+int sbbf_route_find_window(sbbf_route_t* rt, const sbbf_gpu_t* shard, void* stream);
+/* d_results[i] = answer for key i of the last lookup dispatch (0/1 bytes). */
+int sbbf_route_combine(sbbf_route_t* rt, uint8_t* d_results, void* stream);
+
 /* L2 fetch-granularity hint for `device` (cudaLimitMaxL2FetchGranularity,
  * 0..128 bytes; process-wide for that device). 32 makes a random 32-byte
  * block miss fetch one sector from HBM instead of a wider line. *old (if

@@ -77,6 +77,18 @@ PROTOTYPES = {
     "sbbf_shard_partition": (_i, [_vp, _u64, _u64, _vp, _u32, _vp, _vp, _vp, _vp, _vp]),
     "sbbf_scatter_u8": (_i, [_vp, _vp, _u64, _vp, _vp]),
     "sbbf_pack_bits": (_i, [_vp, _u64, _vp, _vp]),
+    "sbbf_route_window_bytes": (_u64, [_u32, _u64]),
+    "sbbf_route_create": (_i, [_u32, _u32, _u64, _i, C.POINTER(_vp)]),
+    "sbbf_route_destroy": (None, [_vp]),
+    "sbbf_route_max_batch": (_u64, [_vp]),
+    "sbbf_route_ipc_handle": (_i, [_vp, _vp]),
+    "sbbf_route_open_peer": (_i, [_vp, _u32, _vp]),
+    "sbbf_route_link_local": (_i, [_vp, _u32, _vp]),
+    "sbbf_route_ready": (_i, [_vp]),
+    "sbbf_route_dispatch": (_i, [_vp, _vp, _u64, _u64, _vp, _i, _vp]),
+    "sbbf_route_insert_window": (_i, [_vp, _vp, _vp]),
+    "sbbf_route_find_window": (_i, [_vp, _vp, _vp]),
+    "sbbf_route_combine": (_i, [_vp, _vp, _vp]),
     "sbbf_gpu_last_error": (C.c_char_p, []),
     "sbbf_gpu_abi_version": (_i, []),
     "sbbf_gpu_launch_count": (_u64, []),

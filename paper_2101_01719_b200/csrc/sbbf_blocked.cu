@@ -204,18 +204,39 @@ struct ScatterSmem {
   uint32_t boff[kMaxBuckets];              // exclusive prefix over buckets (chunk-local)
   unsigned long long gbase[kMaxBuckets];   // global slot of this chunk's run, per bucket
   unsigned long long cursor[kMaxBuckets];  // this CTA's next slot per bucket
+  unsigned long long bstart[kMaxBuckets];  // first slot of each bucket (routed mode)
+  uint64_t* dst[kMaxBuckets];              // routed mode: bucket b's run goes to dst[b][slot - bstart[b]]
+};
+
+// Routed mode of the scatter (fused multi-GPU dispatch, sbbf_route.cu): the
+// bucket-major run of bucket b is written straight into destination b's
+// window — a peer GPU's receive buffer mapped over NVLink — instead of a
+// local staging array, and block 0 publishes the per-bucket counts there.
+struct RouteOut {
+  uint64_t* const* dst = nullptr;                  // [S] window base for this source, per destination
+  unsigned long long* const* count_dst = nullptr;  // [S] where destination b expects this source's count
 };
 
 template <int BITS>
 __global__ void __launch_bounds__(kPartThreads, 2) bucket_scatter_kernel(
     const uint64_t* __restrict__ hashes, uint64_t n, BucketMap bm,
-    const unsigned long long* __restrict__ cta_base, uint64_t* __restrict__ out, uint32_t* __restrict__ pos) {
+    const unsigned long long* __restrict__ cta_base, uint64_t* __restrict__ out, uint32_t* __restrict__ pos,
+    RouteOut route = RouteOut{}, const unsigned long long* __restrict__ counts = nullptr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ScatterSmem& sm = *reinterpret_cast<ScatterSmem*>(smem_raw);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t pol = dev::policy_evict_first();
-  if (threadIdx.x < kMaxBuckets)
+  const bool routed = route.dst != nullptr;
+  if (threadIdx.x < kMaxBuckets) {
     sm.cursor[threadIdx.x] = cta_base[static_cast<uint64_t>(blockIdx.x) * kMaxBuckets + threadIdx.x];
+    if (routed) {
+      const bool used = threadIdx.x < bm.S;
+      sm.bstart[threadIdx.x] = cta_base[threadIdx.x];  // CTA 0's base = the bucket's first slot
+      sm.dst[threadIdx.x] = used ? route.dst[threadIdx.x] : nullptr;
+      // every destination learns how many keys this source sends it (zero included)
+      if (blockIdx.x == 0 && used) *route.count_dst[threadIdx.x] = counts[threadIdx.x];
+    }
+  }
   uint64_t ch0, ch1;
   cta_chunk_range(n, ch0, ch1);
   for (uint64_t ch = ch0; ch < ch1; ++ch) {
@@ -284,11 +305,17 @@ __global__ void __launch_bounds__(kPartThreads, 2) bucket_scatter_kernel(
     for (uint32_t i = threadIdx.x; i < cnt; i += kPartThreads) {
       const uint32_t b = sm.bk[i];
       const uint64_t slot = sm.gbase[b] + (i - sm.boff[b]);
-      out[slot] = sm.key[i];
+      if (routed)
+        sm.dst[b][slot - sm.bstart[b]] = sm.key[i];  // consecutive threads -> consecutive peer slots
+      else
+        out[slot] = sm.key[i];
       if (pos) pos[slot] = sm.pos[i];
     }
     __syncthreads();
   }
+  // peer stores are weakly ordered: make them visible system-wide before the
+  // grid completes (the host then orders the owner's read behind a collective)
+  if (routed) __threadfence_system();
 }
 
 BucketMap make_map(const Geom& g, uint32_t S) {
@@ -325,7 +352,8 @@ void retain_pool() {
 
 template <int BITS>
 cudaError_t bucket_partition_bits(uint64_t grid, const BucketMap& bm, const uint64_t* hashes, uint64_t m,
-                                  uint64_t* d_counts, uint64_t* d_out, uint32_t* d_pos, cudaStream_t s) {
+                                  uint64_t* d_counts, uint64_t* d_out, uint32_t* d_pos, cudaStream_t s,
+                                  RouteOut route = RouteOut{}) {
   retain_pool();
   // per-CTA histograms and bases (grid x 64 entries) from the stream-ordered pool
   uint32_t* hist = nullptr;
@@ -345,7 +373,7 @@ cudaError_t bucket_partition_bits(uint64_t grid, const BucketMap& bm, const uint
                                                  reinterpret_cast<unsigned long long*>(d_counts), bases);
     note_launch();
     bucket_scatter_kernel<BITS><<<static_cast<unsigned>(grid), kPartThreads, sizeof(ScatterSmem), s>>>(
-        hashes, m, bm, bases, d_out, d_pos);
+        hashes, m, bm, bases, d_out, d_pos, route, reinterpret_cast<const unsigned long long*>(d_counts));
     e = cudaGetLastError();
   }
   if (hist) cudaFreeAsync(hist, s);
@@ -356,21 +384,24 @@ cudaError_t bucket_partition_bits(uint64_t grid, const BucketMap& bm, const uint
 // Group `m` keys by bucket: d_out (and d_pos) receive them bucket-major.
 cudaError_t bucket_partition(const DeviceInfo& di, const Geom& g, uint32_t S, const uint64_t* hashes,
                              uint64_t m, uint64_t* d_counts, uint64_t* d_cursor, uint64_t* d_out,
-                             uint32_t* d_pos, cudaStream_t s, const uint64_t* d_bounds = nullptr) {
+                             uint32_t* d_pos, cudaStream_t s, const uint64_t* d_bounds = nullptr,
+                             RouteOut route = RouteOut{}) {
   (void)d_cursor;
   BucketMap bm = make_map(g, S);
   bm.bounds = d_bounds;
   // exact shard ranges: top hash bits equal the owner only when B is a power of two
   if (d_bounds && (g.nb_global & (g.nb_global - 1)) != 0) bm.top_bits = false;
-  if (m == 0) return cudaMemsetAsync(d_counts, 0, S * sizeof(uint64_t), s);
-  const uint64_t grid = grid_for(m, kPartChunk, di.sms, 2);
+  // an empty batch still runs the (tiny) grid in routed mode: every destination
+  // must receive this source's zero counts
+  if (m == 0 && !route.dst) return cudaMemsetAsync(d_counts, 0, S * sizeof(uint64_t), s);
+  const uint64_t grid = m ? grid_for(m, kPartChunk, di.sms, 2) : 1;
   switch (bm.bits) {
-    case 1: return bucket_partition_bits<1>(grid, bm, hashes, m, d_counts, d_out, d_pos, s);
-    case 2: return bucket_partition_bits<2>(grid, bm, hashes, m, d_counts, d_out, d_pos, s);
-    case 3: return bucket_partition_bits<3>(grid, bm, hashes, m, d_counts, d_out, d_pos, s);
-    case 4: return bucket_partition_bits<4>(grid, bm, hashes, m, d_counts, d_out, d_pos, s);
-    case 5: return bucket_partition_bits<5>(grid, bm, hashes, m, d_counts, d_out, d_pos, s);
-    case 6: return bucket_partition_bits<6>(grid, bm, hashes, m, d_counts, d_out, d_pos, s);
+    case 1: return bucket_partition_bits<1>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);
+    case 2: return bucket_partition_bits<2>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);
+    case 3: return bucket_partition_bits<3>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);
+    case 4: return bucket_partition_bits<4>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);
+    case 5: return bucket_partition_bits<5>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);
+    case 6: return bucket_partition_bits<6>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -449,6 +480,16 @@ cudaError_t shard_partition(const DeviceInfo& di, uint64_t total, uint32_t parts
   if (n == 0) return cudaMemsetAsync(d_counts, 0, parts * sizeof(uint64_t), s);
   const Geom whole{total, 0, total};
   return bucket_partition(di, whole, parts, hashes, n, d_counts, d_cursor, d_out, d_pos, s, d_bounds);
+}
+
+cudaError_t route_partition(const DeviceInfo& di, uint64_t total, uint32_t parts, const uint64_t* d_bounds,
+                            const uint64_t* hashes, uint64_t n, uint64_t* d_counts, uint32_t* d_pos,
+                            uint64_t* const* d_dst, unsigned long long* const* d_count_dst, cudaStream_t s) {
+  const Geom whole{total, 0, total};
+  RouteOut route;
+  route.dst = d_dst;
+  route.count_dst = d_count_dst;
+  return bucket_partition(di, whole, parts, hashes, n, d_counts, nullptr, nullptr, d_pos, s, d_bounds, route);
 }
 
 cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g, const BlockedPlan& plan,

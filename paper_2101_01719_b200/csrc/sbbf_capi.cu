@@ -27,6 +27,15 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+}  // namespace
+
+namespace sbbf {
+// Other translation units (sbbf_route.cu) report through sbbf_gpu_last_error.
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace sbbf
+
+namespace {
+
 int cuda_fail(cudaError_t e, const char* what) {
   const int code = (e == cudaErrorMemoryAllocation) ? SBBF_ENOMEM
                    : (e == cudaErrorNoDevice || e == cudaErrorInvalidDevice ||

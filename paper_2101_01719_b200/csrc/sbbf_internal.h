@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 
 #include "sbbf_bench.h"
 #include "sbbf_gpu.h"
@@ -36,6 +37,7 @@ constexpr int kFindGlobal = SBBF_FIND_GLOBAL;
 constexpr int kFindSmem = SBBF_FIND_SMEM;
 
 uint64_t launch_count();
+void set_last_error(const std::string& msg);  // what sbbf_gpu_last_error() returns on this thread
 void note_launch();
 uint64_t grid_for(uint64_t work_items, uint64_t items_per_block, int sms, int per_sm);
 
@@ -57,6 +59,15 @@ cudaError_t launch_partition(const uint64_t* hashes, uint64_t n, uint64_t total,
 cudaError_t shard_partition(const DeviceInfo& di, uint64_t total, uint32_t parts, const uint64_t* d_bounds,
                             const uint64_t* hashes, uint64_t n, uint64_t* d_counts, uint64_t* d_cursor,
                             uint64_t* d_out, uint32_t* d_pos, cudaStream_t s);
+
+// Fused dispatch (sbbf_route.cu): the shard partition whose scatter writes
+// bucket b's run straight to d_dst[b][0..count) — destination b's receive
+// window, a peer GPU's memory mapped over NVLink — and stores the count at
+// *d_count_dst[b]. d_counts receives the per-destination counts locally,
+// d_pos (optional) the source index of every routed slot (bucket-major).
+cudaError_t route_partition(const DeviceInfo& di, uint64_t total, uint32_t parts, const uint64_t* d_bounds,
+                            const uint64_t* hashes, uint64_t n, uint64_t* d_counts, uint32_t* d_pos,
+                            uint64_t* const* d_dst, unsigned long long* const* d_count_dst, cudaStream_t s);
 
 // insert_wide over `n` keys with one warp step per 128 keys and the grid
 // covering the batch once, so CTAs run in key order (blocked path).

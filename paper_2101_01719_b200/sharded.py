@@ -12,6 +12,15 @@ find:   same forward exchange (keeping source positions) -> local find (one
         byte per key, receive order) -> reverse all-to-all of the answers ->
         ``sbbf_scatter_u8`` back to source order (-> ``sbbf_pack_bits``).
 
+Fused mode (the default on GPUs, ``PeerRoute`` / ``csrc/sbbf_route.cu``):
+the partition's scatter writes each owner's run straight into that owner's
+receive window — its GPU memory mapped here by CUDA IPC, written over
+NVLink — so there is no staging array, no counts exchange and no host sync;
+a 1-element NCCL all-reduce orders the phases on the stream:
+
+insert: dispatch -> barrier -> insert_window
+find:   dispatch -> barrier -> find_window -> barrier -> combine
+
 ``torch.distributed`` is the plumbing (NCCL on GPUs, gloo in the CPU tests);
 the per-rank compute goes through ``ShardOps`` — ``CudaShardOps`` (the C ABI)
 in the product. Tests inject a host restatement to exercise the exchange
@@ -167,11 +176,89 @@ class CudaShardOps(ShardOps):
         return torch.empty(n, dtype=dtype, device=self.dev)
 
 
+class PeerRoute:
+    """This rank's receive window and its mappings of every peer's window
+    (``sbbf_route_*`` in include/sbbf_gpu.h). One collective call = one
+    ``dispatch`` on every rank, then the owner/source phases below."""
+
+    def __init__(self, parts: int, rank: int, max_batch: int, device: int):
+        self._h = C.c_void_p()
+        self.parts, self.rank, self.device = parts, rank, device
+        check(_lib.lib().sbbf_route_create(parts, rank, max_batch, device, C.byref(self._h)),
+              "sbbf_route_create")
+        self.max_batch = int(_lib.lib().sbbf_route_max_batch(self._h))
+
+    def close(self):
+        if self._h:
+            _lib.lib().sbbf_route_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def handle(self) -> bytes:
+        buf = (C.c_uint8 * 64)()
+        check(_lib.lib().sbbf_route_ipc_handle(self._h, buf), "sbbf_route_ipc_handle")
+        return bytes(buf)
+
+    def open_peer(self, peer: int, handle: bytes):
+        buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+        check(_lib.lib().sbbf_route_open_peer(self._h, peer, buf), "sbbf_route_open_peer")
+
+    def link_local(self, peer: int, other: "PeerRoute"):
+        check(_lib.lib().sbbf_route_link_local(self._h, peer, other._h), "sbbf_route_link_local")
+
+    def ready(self) -> bool:
+        return bool(_lib.lib().sbbf_route_ready(self._h))
+
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream(torch.device("cuda", self.device)).cuda_stream)
+
+    def dispatch(self, keys, total: int, d_bounds, keep_positions: bool):
+        n = keys.numel()
+        if n > self.max_batch:
+            raise ValueError(f"batch of {n} keys exceeds max_batch={self.max_batch}; split it "
+                             "identically on every rank")
+        check(_lib.lib().sbbf_route_dispatch(self._h, C.c_void_p(keys.data_ptr()) if n else None, n, total,
+                                             C.c_void_p(d_bounds.data_ptr()), int(keep_positions),
+                                             self._stream()), "sbbf_route_dispatch")
+
+    def insert_window(self, shard):
+        check(_lib.lib().sbbf_route_insert_window(self._h, shard.handle, self._stream()),
+              "sbbf_route_insert_window")
+
+    def find_window(self, shard):
+        check(_lib.lib().sbbf_route_find_window(self._h, shard.handle, self._stream()),
+              "sbbf_route_find_window")
+
+    def combine(self, out):
+        check(_lib.lib().sbbf_route_combine(self._h, C.c_void_p(out.data_ptr()) if out.numel() else None,
+                                            self._stream()), "sbbf_route_combine")
+
+
+def _peer_access_everywhere(devices: list[int]) -> bool:
+    for a in devices:
+        for b in devices:
+            if a != b and not torch.cuda.can_device_access_peer(a, b):
+                return False
+    return True
+
+
 class ShardedFilter:
-    """One rank's view of a P-way sharded filter of ``total_buckets`` buckets."""
+    """One rank's view of a P-way sharded filter of ``total_buckets`` buckets.
+
+    fused: route keys through peer-memory windows (``PeerRoute``) instead of
+    NCCL all-to-alls. None = on whenever the per-rank compute is the CUDA
+    library and every rank's GPU can map every other's (always at world 1).
+    max_batch: largest batch a rank passes per call in fused mode (window
+    capacity); larger batches must be split identically on every rank."""
 
     def __init__(self, total_buckets: int, ops: ShardOps | None = None, group=None,
-                 rank: int | None = None, world: int | None = None):
+                 rank: int | None = None, world: int | None = None, fused: bool | None = None,
+                 max_batch: int = 1 << 24):
         if total_buckets <= 0:
             raise ValueError("SplitBlockFilter needs at least one bucket")
         self.group = group
@@ -187,6 +274,40 @@ class ShardedFilter:
         self.ops = ops
         self.shard = ops.create(self.total, self.first, self.count)
         self.last_exchange: dict = {}
+        self.route = None
+        if fused is None:
+            fused = isinstance(ops, CudaShardOps) and self._peer_capable(init)
+        if fused:
+            if not isinstance(ops, CudaShardOps):
+                raise ValueError("fused routing needs the CUDA shard ops")
+            self._setup_route(init, max_batch)
+
+    def _peer_capable(self, init: bool) -> bool:
+        if self.world == 1:
+            return True
+        if not init or dist.get_backend(self.group) != "nccl":
+            return False
+        devs = [None] * self.world
+        dist.all_gather_object(devs, self.ops.device, group=self.group)
+        return _peer_access_everywhere(devs)
+
+    def _setup_route(self, init: bool, max_batch: int):
+        self.route = PeerRoute(self.world, self.rank, max_batch, self.ops.device)
+        if self.world > 1:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, self.route.handle(), group=self.group)
+            for peer, h in enumerate(handles):
+                if peer != self.rank:
+                    self.route.open_peer(peer, h)
+            dist.barrier(group=self.group)
+        assert self.route.ready()
+        self._flag = torch.zeros(1, dtype=torch.int32, device=self.ops.dev)
+
+    def _barrier(self):
+        """Stream-ordered: every rank's preceding kernels finish before any
+        rank's following kernels start (a 1-element NCCL all-reduce)."""
+        if self.world > 1:
+            dist.all_reduce(self._flag, group=self.group)
 
     # -- exchange ---------------------------------------------------------------
     def _exchange(self, payload, send_counts: list[int], recv_counts: list[int] | None = None):
@@ -207,6 +328,11 @@ class ShardedFilter:
     # -- hot path -----------------------------------------------------------------
     def add_hashes(self, keys) -> None:
         """Insert this rank's batch (any keys; each is routed to its owner)."""
+        if self.route is not None:
+            self.route.dispatch(keys, self.total, self.ops._dev_bounds(self.bounds), keep_positions=False)
+            self._barrier()
+            self.route.insert_window(self.shard)
+            return
         counts, routed, _ = self.ops.partition(keys, self.total, self.bounds, with_pos=False)
         recv, rc = self._exchange(routed, counts)
         self.last_exchange = {"sent": counts, "received": rc}
@@ -215,6 +341,14 @@ class ShardedFilter:
     def find_hashes(self, keys):
         """0/1 byte per key of this rank's batch, in the batch's order."""
         n = keys.numel()
+        if self.route is not None:
+            self.route.dispatch(keys, self.total, self.ops._dev_bounds(self.bounds), keep_positions=True)
+            self._barrier()
+            self.route.find_window(self.shard)
+            self._barrier()
+            out = self.ops.empty(n, torch.uint8)
+            self.route.combine(out)
+            return out
         counts, routed, pos = self.ops.partition(keys, self.total, self.bounds, with_pos=True)
         recv, rc = self._exchange(routed, counts)
         answers = self.ops.find(self.shard, recv)
@@ -277,7 +411,10 @@ def bench_main(args) -> dict | None:
     st = W.StreamHandle(spec, local)
     ins = W.gen_inserts(st, rank * N, N, device=local)
     look = W.gen_lookups(st, cfg.lookups, N * world, rank * L, L, device=local)
-    f = ShardedFilter(total)
+    route = getattr(args, "route", "auto")
+    f = ShardedFilter(total, fused=None if route == "auto" else route == "fused")
+    how = ("peer-memory windows over NVLink (fused dispatch, sbbf_route.cu)" if f.route is not None
+           else "NCCL all-to-all")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     flush_rd = torch.zeros(64 << 20, dtype=torch.int32, device=dev)
 
@@ -341,12 +478,12 @@ def bench_main(args) -> dict | None:
             "data": "synthetic (seeded splitmix64 hash streams, generated in HBM)",
             "config": {"workload": f"sharded: per rank BASELINE config {args.config} batch "
                                    f"({N:,} inserts + {L:,} lookups) into a {world}-way block-range "
-                                   f"sharded filter of {total} blocks; keys routed by NCCL all-to-all",
+                                   f"sharded filter of {total} blocks; keys routed by {how}",
                        "parallelism": f"shard{world}", "l2": "flushed between timed steps (untimed)"},
             "e2e": {"value": world * (N + L) / e2e_s / 1e9, "unit": "Gkeys/s",
                     "h2d_bytes_per_step": 8 * (N + L), "d2h_bytes_per_step": 4 * ((L + 31) // 32),
                     "ms_per_step": e2e_s * 1e3, "note": "per rank; max over ranks of wall time"},
-            "roofline": {"bound": "hbm", "kernel": "whole sharded step (partition + exchange + probe)",
+            "roofline": {"bound": "hbm", "kernel": "whole sharded step (partition + exchange + probe)", "routing": how,
                          "achieved": (N + L) * 40.0 / (ms * 1e-3) / 1e9, "peak": 6523.3, "unit": "GB/s",
                          "frac": (N + L) * 40.0 / (ms * 1e-3) / 1e9 / 6523.3, "traffic": None,
                          "bytes_per_key": 40.0,

@@ -229,12 +229,132 @@ def test_nccl_self_exchange(cuda, oracle):
     try:
         rng = np.random.default_rng(5)
         h = rng.integers(0, 2**64, size=1_000_000, dtype=np.uint64)
-        f = S.ShardedFilter(32768)
+        f = S.ShardedFilter(32768, fused=False)
+        assert f.route is None
         f.add_hashes(torch.from_numpy(h.view(np.int64)).to(cuda))
         want = oracle.build(32768, h)
         assert np.array_equal(f.gather_blocks(), want)
         look = np.concatenate([h[:1000], rng.integers(0, 2**64, size=100_000, dtype=np.uint64)])
         ans = f.find_hashes(torch.from_numpy(look.view(np.int64)).to(cuda)).cpu().numpy()
         assert np.array_equal(ans, oracle.find_hashes(want, look))
+    finally:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------------
+# GPU: fused dispatch over peer-memory windows (csrc/sbbf_route.cu)
+# ---------------------------------------------------------------------------------
+def _linked_routes(parts, max_batch):
+    routes = [S.PeerRoute(parts, r, max_batch, 0) for r in range(parts)]
+    for r in range(parts):
+        for q in range(parts):
+            routes[r].link_local(q, routes[q])
+        assert routes[r].ready()
+    return routes
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts,total", [(1, 32768), (2, 65536), (3, 7919 * 3), (8, 2**18 + 5)])
+def test_fused_route_multi_shard_one_gpu(cuda, oracle, parts, total):
+    """P ranks simulated by P route contexts + shards in one process: every
+    source's scatter writes into every owner's window; the concatenated
+    shards equal the single filter and every source gets the oracle's
+    answers. Ragged batches (one source empty), two calls of each kind so
+    both window parities are used."""
+    ops = S.CudaShardOps(0)
+    bounds = S.shard_bounds(total, parts)
+    db = ops._dev_bounds(bounds)
+    shards = [ops.create(total, bounds[r], bounds[r + 1] - bounds[r]) for r in range(parts)]
+    routes = _linked_routes(parts, 300_000)
+    rng = np.random.default_rng(parts * 31 + 1)
+    sizes = [0 if (parts > 1 and r == 1) else int(rng.integers(1, 250_000)) for r in range(parts)]
+    all_ins = []
+    for call in range(2):
+        batch = [rng.integers(0, 2**64, size=n, dtype=np.uint64) for n in sizes]
+        all_ins += batch
+        dev = [torch.from_numpy(b.view(np.int64)).to(cuda) for b in batch]
+        for r in range(parts):
+            routes[r].dispatch(dev[r], total, db, keep_positions=False)
+        for r in range(parts):
+            routes[r].insert_window(shards[r])
+        torch.cuda.synchronize()
+        want = oracle.build(total, np.concatenate(all_ins))
+        full = np.concatenate([s.blocks() for s in shards])
+        assert np.array_equal(full, want), f"call {call}"
+    hits = np.concatenate(all_ins)
+    for call in range(2):
+        looks = []
+        for r in range(parts):
+            m = int(rng.integers(0, 200_000)) if r != 0 else 1
+            half = min(m // 2, hits.size)
+            looks.append(np.concatenate([hits[rng.integers(0, hits.size, size=half)],
+                                         rng.integers(0, 2**64, size=m - half, dtype=np.uint64)]))
+        dev = [torch.from_numpy(x.view(np.int64)).to(cuda) for x in looks]
+        for r in range(parts):
+            routes[r].dispatch(dev[r], total, db, keep_positions=True)
+        for r in range(parts):
+            routes[r].find_window(shards[r])
+        outs = [torch.empty(x.size, dtype=torch.uint8, device=cuda) for x in looks]
+        for r in range(parts):
+            routes[r].combine(outs[r])
+        for r in range(parts):
+            assert np.array_equal(outs[r].cpu().numpy(), oracle.find_hashes(want, looks[r])), (call, r)
+    for rt in routes:
+        rt.close()
+
+
+@pytest.mark.gpu
+def test_fused_route_errors(cuda):
+    from paper_2101_01719_b200._lib import SbbfError
+    a = S.PeerRoute(2, 0, 1000, 0)
+    b = S.PeerRoute(2, 1, 5000, 0)
+    assert a.max_batch == 1024                      # rounded up to a multiple of 256
+    ops = S.CudaShardOps(0)
+    db = ops._dev_bounds(S.shard_bounds(4096, 2))
+    keys = torch.zeros(10, dtype=torch.int64, device=cuda)
+    with pytest.raises(SbbfError):                  # peer 1 not linked yet
+        a.dispatch(keys, 4096, db, False)
+    with pytest.raises(SbbfError):                  # capacities differ
+        a.link_local(1, b)
+    with pytest.raises(SbbfError):                  # bad geometry
+        S.PeerRoute(2, 2, 1000, 0)
+    with pytest.raises(ValueError):                 # over max_batch
+        a.dispatch(torch.zeros(2000, dtype=torch.int64, device=cuda), 4096, db, False)
+    with pytest.raises(SbbfError):                  # combine needs a lookup dispatch
+        a.combine(torch.empty(1, dtype=torch.uint8, device=cuda))
+    a.close()
+    b.close()
+
+
+@pytest.mark.gpu
+def test_fused_sharded_filter_world1(cuda, oracle):
+    """ShardedFilter picks the fused route by default; with and without an
+    NCCL process group it matches the oracle."""
+    rng = np.random.default_rng(9)
+    h = rng.integers(0, 2**64, size=700_000, dtype=np.uint64)
+    look = np.concatenate([h[:5000], rng.integers(0, 2**64, size=300_000, dtype=np.uint64)])
+    want = oracle.build(32768, h)
+    f = S.ShardedFilter(32768)
+    assert f.route is not None
+    f.add_hashes(torch.from_numpy(h.view(np.int64)).to(cuda))
+    assert np.array_equal(f.gather_blocks(), want)
+    ans = f.find_hashes(torch.from_numpy(look.view(np.int64)).to(cuda)).cpu().numpy()
+    assert np.array_equal(ans, oracle.find_hashes(want, look))
+    bits = f.find_hashes_bits(torch.from_numpy(look.view(np.int64)).to(cuda)).cpu().numpy().view(np.uint32)
+    from oracle import bits_to_bytes
+    assert np.array_equal(bits_to_bytes(bits, look.size), ans)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=cuda)
+    try:
+        g = S.ShardedFilter(32768)
+        assert g.route is not None
+        g.add_hashes(torch.from_numpy(h.view(np.int64)).to(cuda))
+        assert np.array_equal(g.gather_blocks(), want)
+        ans = g.find_hashes(torch.from_numpy(look.view(np.int64)).to(cuda)).cpu().numpy()
+        assert np.array_equal(ans, oracle.find_hashes(want, look))
+        n = S.ShardedFilter(32768, fused=False)     # the NCCL all-to-all path still works
+        n.add_hashes(torch.from_numpy(h.view(np.int64)).to(cuda))
+        assert np.array_equal(n.gather_blocks(), want)
     finally:
         dist.destroy_process_group()
