@@ -304,10 +304,16 @@ class ShardedFilter:
         self._flag = torch.zeros(1, dtype=torch.int32, device=self.ops.dev)
 
     def _barrier(self):
-        """Stream-ordered: every rank's preceding kernels finish before any
-        rank's following kernels start (a 1-element NCCL all-reduce)."""
-        if self.world > 1:
+        """Every rank's preceding kernels finish before any rank's following
+        kernels start: a 1-element NCCL all-reduce (stream-ordered, no host
+        sync); with a host backend (gloo), device sync + host barrier."""
+        if self.world == 1:
+            return
+        if dist.get_backend(self.group) == "nccl":
             dist.all_reduce(self._flag, group=self.group)
+        else:
+            torch.cuda.synchronize(self.ops.dev)
+            dist.barrier(group=self.group)
 
     # -- exchange ---------------------------------------------------------------
     def _exchange(self, payload, send_counts: list[int], recv_counts: list[int] | None = None):

@@ -358,3 +358,48 @@ def test_fused_sharded_filter_world1(cuda, oracle):
         assert np.array_equal(n.gather_blocks(), want)
     finally:
         dist.destroy_process_group()
+
+
+def _ipc_worker(rank, world, port, total, q):
+    """One process per rank on the same GPU: windows mapped across processes
+    with CUDA IPC handles (the multi-GPU plumbing), phases ordered by host
+    barriers (gloo); no kernel ever waits on another process."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
+        rng = np.random.default_rng(500 + rank)
+        ins = rng.integers(0, 2**64, size=150_000 + 1000 * rank, dtype=np.uint64)
+        f = S.ShardedFilter(total, fused=True, max_batch=1 << 18)
+        assert f.route is not None and f.route.ready()
+        f.add_hashes(torch.from_numpy(ins.view(np.int64)).to(dev))
+        look = np.concatenate([ins[:20_000], rng.integers(0, 2**64, size=60_000, dtype=np.uint64)])
+        ans = f.find_hashes(torch.from_numpy(look.view(np.int64)).to(dev)).cpu().numpy()
+        q.put((rank, ins, look, ans, f.local_blocks(), f.first))
+        dist.barrier()
+        f.route.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,total", [(2, 65536), (3, 7919 * 3)])
+def test_fused_ipc_processes(cuda, oracle, world, total):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, total, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    got.sort(key=lambda x: x[0])
+    want = oracle.build(total, np.concatenate([g[1] for g in got]))
+    full = np.concatenate([g[4] for g in got])
+    assert np.array_equal(full, want)
+    for rank, ins, look, ans, *_ in got:
+        assert np.array_equal(ans, oracle.find_hashes(want, look)), rank
