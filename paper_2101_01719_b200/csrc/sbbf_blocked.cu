@@ -1,21 +1,30 @@
-// sbbf_blocked.cu — L2-blocked insert/lookup for filters larger than L2.
+// sbbf_blocked.cu — multisplit partitions: the L2-blocked insert/lookup for
+// filters larger than L2, and the shard routing of the multi-GPU path.
 //
 // A random 32-byte probe that misses L2 costs a full DRAM line fill
 // (ncu: ~117 B of DRAM per key on a 1 GiB filter) and the HBM random-sector
 // rate tops out at 37-43 G/s whatever the access path (LSU, TMA, gather4;
 // profiles/r1_microbench_*.log). The blocked path trades that for streaming:
 //
-//   1. bucket the batch by filter slice (bucket_count + bucket_scatter:
-//      8 B in, 8 B (+4 B source position) out per key),
-//   2. process the grouped keys in slice order — CTAs are dispatched in
-//      blockIdx order, so the keys in flight at any moment fall in one or two
-//      slices (~16 MiB each) and their probes/atomics hit L2; every filter
-//      line is fetched from HBM about once per chunk,
-//   3. lookups set their answer bit at the key's source position with a red
-//      into a chunk bitmap that stays L2-resident.
+//   1. chunk_scatter: every 4096-key chunk of the batch is rewritten
+//      bucket-major (bucket = filter slice of ~16 MiB) inside its own region,
+//      with 16-bit bucket offsets per chunk (and, for lookups, each slot's
+//      16-bit source position): one read, coalesced writes, no count pass;
+//   2. segment_kernel: bucket by bucket over every chunk's run of that
+//      bucket; the keys in flight share one slice, so their probes /
+//      atomics are served by L2 and each filter line comes from HBM about
+//      once per batch chunk; lookups store an answer byte per routed slot;
+//   3. unpermute_kernel (lookups): each chunk's answers back to source order
+//      through shared memory, written as the caller's bits or bytes.
 //
-// Per-key HBM traffic ~ 8 (count) + 8 + 12 (scatter) + 12 (probe) +
-// filter_bytes / chunk_keys, instead of a ~128-byte random line fill.
+// Per-key HBM traffic ~ 8 + 10 (scatter) + 8 + 1 (probe) + 3 (unpermute) +
+// filter_bytes / batch-chunk keys, and no atomics besides the filter ORs
+// (profiles/r1_blocked_partition.md).
+//
+// The shard routing (shard_partition / route_partition) needs one
+// bucket-major layout over the whole batch instead: bucket_count ->
+// bucket_scan (per-CTA bases) -> bucket_scatter, which can also write each
+// destination's run straight into a peer GPU's window (sbbf_route.cu).
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -28,9 +37,6 @@ namespace sbbf {
 namespace {
 
 constexpr uint64_t kBlockedChunk = uint64_t{1} << 28;  // keys per partition round (3.1 GB scratch)
-constexpr int kProbeU = 8;
-constexpr int kProbeThreads = 256;
-constexpr uint64_t kProbeTile = kProbeThreads * kProbeU;
 
 // ---------------------------------------------------------------------------
 // bucket partition
@@ -47,6 +53,7 @@ constexpr uint64_t kProbeTile = kProbeThreads * kProbeU;
 // atomics (~2 cycles per lane on this part) and no __match_any_sync (which
 // measured slower still: profiles/r1_blocked_partition.md).
 constexpr int kPartThreads = 512;
+constexpr int kPartMinBlocks = 2;
 constexpr int kPartWarps = kPartThreads / 32;
 constexpr int kPartPerThread = 8;
 constexpr uint64_t kPartChunk = kPartThreads * kPartPerThread;
@@ -60,10 +67,12 @@ struct BucketMap {
   bool top_bits;           // whole filter, S = 2^bits: bucket = top bits of the hash
 };
 
+// kTop: the map is a whole filter split into S = 2^bits slices. block_index
+// is monotone in the hash, so the hash's top bits split the filter into S
+// contiguous block ranges without any 64-bit multiply.
+template <bool kTop>
 __device__ __forceinline__ uint32_t bucket_of(uint64_t h, const BucketMap& bm) {
-  // block_index is monotone in the hash, so the hash's top bits split the
-  // filter into S contiguous block ranges without any 64-bit multiply
-  if (bm.top_bits) return static_cast<uint32_t>(h >> (64 - bm.bits));
+  if constexpr (kTop) return static_cast<uint32_t>(h >> (64 - bm.bits));
   uint64_t b = dev::block_index(h, bm.nb_global) - bm.first;
   b = b < bm.nb_local ? b : 0;
   uint64_t q = b * bm.mult >> 32;
@@ -77,12 +86,16 @@ __device__ __forceinline__ uint32_t bucket_of(uint64_t h, const BucketMap& bm) {
   return static_cast<uint32_t>(q);
 }
 
-// Lanes whose bucket equals `v`, given the per-bit ballots of the warp.
+// Lanes whose bucket equals `v`, given the per-bit ballots of the warp:
+// AND over bits k of (bal[k] if bit k of v is set, else ~bal[k]), written as
+// bal[k] ^ flip_k(v) so each bit costs one LOP3.
+__device__ __forceinline__ uint32_t flip(uint32_t v, int k) { return ((v >> k) & 1u) - 1u; }
+
 template <int BITS>
 __device__ __forceinline__ uint32_t lanes_with(uint32_t v, const uint32_t (&bal)[kMaxBits], uint32_t active) {
   uint32_t m = active;
 #pragma unroll
-  for (int k = 0; k < BITS; ++k) m &= ((v >> k) & 1u) ? bal[k] : ~bal[k];
+  for (int k = 0; k < BITS; ++k) m &= bal[k] ^ flip(v, k);
   return m;
 }
 
@@ -92,12 +105,38 @@ __device__ __forceinline__ void bit_ballots(uint32_t bk, uint32_t (&bal)[kMaxBit
   for (int k = 0; k < BITS; ++k) bal[k] = __ballot_sync(0xffffffffu, (bk >> k) & 1u);
 }
 
+// Per-lane flip masks of the buckets lane l owns (l and l + 32), hoisted
+// out of the key loops: bits 0..4 are shared by both buckets.
+struct OwnerMasks {
+  uint32_t f[5];
+  __device__ __forceinline__ explicit OwnerMasks(uint32_t lane) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) f[k] = flip(lane, k);
+  }
+};
+
+// Add this warp step's counts of buckets lane and lane + 32 to c0 / c1.
+template <int BITS>
+__device__ __forceinline__ void owner_counts(const OwnerMasks& om, const uint32_t (&bal)[kMaxBits], uint32_t active,
+                                             uint32_t& c0, uint32_t& c1) {
+  constexpr int kLow = BITS < 5 ? BITS : 5;
+  uint32_t m = active;
+#pragma unroll
+  for (int k = 0; k < kLow; ++k) m &= bal[k] ^ om.f[k];
+  if constexpr (BITS > 5) {
+    c0 += __popc(m & ~bal[5]);
+    c1 += __popc(m & bal[5]);
+  } else {
+    c0 += __popc(m);
+  }
+}
+
 // One warp step over 32 keys: rank of each lane inside its bucket group and
 // the per-bucket counts added to the lane-owned counters c0 (bucket = lane)
 // and c1 (bucket = lane + 32).
 template <int BITS>
-__device__ __forceinline__ uint32_t warp_rank(uint32_t bk, bool valid, uint32_t lane, uint32_t& c0,
-                                              uint32_t& c1) {
+__device__ __forceinline__ uint32_t warp_rank(uint32_t bk, bool valid, uint32_t lane, const OwnerMasks& om,
+                                              uint32_t& c0, uint32_t& c1) {
   const uint32_t active = __ballot_sync(0xffffffffu, valid);
   uint32_t bal[kMaxBits];
   bit_ballots<BITS>(bk, bal);
@@ -107,9 +146,8 @@ __device__ __forceinline__ uint32_t warp_rank(uint32_t bk, bool valid, uint32_t 
   if constexpr (BITS > 5) {
     const uint32_t p1 = __shfl_sync(0xffffffffu, c1, bk & 31);
     prior = (bk & 32) ? p1 : prior;
-    c1 += __popc(lanes_with<BITS>(lane + 32, bal, active));
   }
-  c0 += __popc(lanes_with<BITS>(lane, bal, active));
+  owner_counts<BITS>(om, bal, active, c0, c1);
   return prior + __popc(peers & ((1u << lane) - 1u));
 }
 
@@ -123,12 +161,30 @@ __device__ __forceinline__ void cta_chunk_range(uint64_t n, uint64_t& c0, uint64
   c1 = c0 + per < nchunks ? c0 + per : nchunks;
 }
 
-template <int BITS>
-__global__ void __launch_bounds__(kPartThreads, 2) bucket_count_kernel(const uint64_t* __restrict__ hashes,
+// Loads of one partition chunk (8 keys per thread, coalesced). Chunks entirely
+// inside [0, n) skip the per-key bounds checks.
+__device__ __forceinline__ void load_chunk(const uint64_t* __restrict__ hashes, uint64_t n, uint64_t ch,
+                                           uint64_t pol, uint64_t (&dst)[kPartPerThread]) {
+  const uint64_t base = ch * kPartChunk + threadIdx.x;
+  if (base - threadIdx.x + kPartChunk <= n) {
+#pragma unroll
+    for (int j = 0; j < kPartPerThread; ++j) dst[j] = dev::ld_stream_u64(hashes + base + j * kPartThreads, pol);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kPartPerThread; ++j) {
+      const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads;
+      dst[j] = i < n ? dev::ld_stream_u64(hashes + i, pol) : 0;
+    }
+  }
+}
+
+template <int BITS, bool kTop>
+__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) bucket_count_kernel(const uint64_t* __restrict__ hashes,
                                                                        uint64_t n, BucketMap bm,
                                                                        uint32_t* __restrict__ cta_hist) {
   __shared__ unsigned int cta[kMaxBuckets];
   const uint32_t lane = threadIdx.x & 31;
+  const OwnerMasks om(lane);
   const uint64_t pol = dev::policy_evict_first();
   if (threadIdx.x < kMaxBuckets) cta[threadIdx.x] = 0;
   uint32_t c0 = 0, c1 = 0;
@@ -137,29 +193,30 @@ __global__ void __launch_bounds__(kPartThreads, 2) bucket_count_kernel(const uin
   // Software pipeline: the next chunk's loads are in flight while this
   // chunk's ballots run (the kernel is otherwise latency bound).
   uint64_t nxt[kPartPerThread];
-#pragma unroll
-  for (int j = 0; j < kPartPerThread; ++j) {
-    const uint64_t i = ch0 * kPartChunk + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
-    nxt[j] = (ch0 < ch1 && i < n) ? dev::ld_stream_u64(hashes + i, pol) : 0;
-  }
+  if (ch0 < ch1) load_chunk(hashes, n, ch0, pol, nxt);
   for (uint64_t ch = ch0; ch < ch1; ++ch) {
-    const uint64_t base = ch * kPartChunk;
     uint64_t h[kPartPerThread];
 #pragma unroll
-    for (int j = 0; j < kPartPerThread; ++j) {
-      h[j] = nxt[j];
-      const uint64_t i = base + kPartChunk + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
-      nxt[j] = (ch + 1 < ch1 && i < n) ? dev::ld_stream_u64(hashes + i, pol) : 0;
-    }
+    for (int j = 0; j < kPartPerThread; ++j) h[j] = nxt[j];
+    if (ch + 1 < ch1) load_chunk(hashes, n, ch + 1, pol, nxt);
+    const uint64_t base = ch * kPartChunk;
+    if (base + kPartChunk <= n) {
 #pragma unroll
-    for (int j = 0; j < kPartPerThread; ++j) {
-      const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
-      const uint32_t bk = i < n ? bucket_of(h[j], bm) : 0u;
-      const uint32_t active = __ballot_sync(0xffffffffu, i < n);
-      uint32_t bal[kMaxBits];
-      bit_ballots<BITS>(bk, bal);
-      c0 += __popc(lanes_with<BITS>(lane, bal, active));
-      if constexpr (BITS > 5) c1 += __popc(lanes_with<BITS>(lane + 32, bal, active));
+      for (int j = 0; j < kPartPerThread; ++j) {
+        uint32_t bal[kMaxBits];
+        bit_ballots<BITS>(bucket_of<kTop>(h[j], bm), bal);
+        owner_counts<BITS>(om, bal, 0xffffffffu, c0, c1);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kPartPerThread; ++j) {
+        const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
+        const uint32_t bk = i < n ? bucket_of<kTop>(h[j], bm) : 0u;
+        const uint32_t active = __ballot_sync(0xffffffffu, i < n);
+        uint32_t bal[kMaxBits];
+        bit_ballots<BITS>(bk, bal);
+        owner_counts<BITS>(om, bal, active, c0, c1);
+      }
     }
   }
   __syncthreads();
@@ -217,14 +274,15 @@ struct RouteOut {
   unsigned long long* const* count_dst = nullptr;  // [S] where destination b expects this source's count
 };
 
-template <int BITS>
-__global__ void __launch_bounds__(kPartThreads, 2) bucket_scatter_kernel(
+template <int BITS, bool kTop>
+__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) bucket_scatter_kernel(
     const uint64_t* __restrict__ hashes, uint64_t n, BucketMap bm,
     const unsigned long long* __restrict__ cta_base, uint64_t* __restrict__ out, uint32_t* __restrict__ pos,
     RouteOut route = RouteOut{}, const unsigned long long* __restrict__ counts = nullptr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ScatterSmem& sm = *reinterpret_cast<ScatterSmem*>(smem_raw);
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const OwnerMasks om(lane);
   const uint64_t pol = dev::policy_evict_first();
   const bool routed = route.dst != nullptr;
   if (threadIdx.x < kMaxBuckets) {
@@ -244,19 +302,23 @@ __global__ void __launch_bounds__(kPartThreads, 2) bucket_scatter_kernel(
     const uint32_t cnt = static_cast<uint32_t>(n - base < kPartChunk ? n - base : kPartChunk);
     uint64_t h[kPartPerThread];
     uint32_t bk[kPartPerThread], off[kPartPerThread];
-#pragma unroll
-    for (int j = 0; j < kPartPerThread; ++j) {
-      const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
-      h[j] = i < n ? dev::ld_stream_u64(hashes + i, pol) : 0;
-    }
+    load_chunk(hashes, n, ch, pol, h);
     uint32_t c0 = 0, c1 = 0;
+    if (cnt == kPartChunk) {
 #pragma unroll
-    for (int j = 0; j < kPartPerThread; ++j) {
-      const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
-      const bool valid = i < n;
-      bk[j] = valid ? bucket_of(h[j], bm) : 0u;
-      off[j] = warp_rank<BITS>(bk[j], valid, lane, c0, c1);
-      if (!valid) bk[j] = 0xffffffffu;
+      for (int j = 0; j < kPartPerThread; ++j) {
+        bk[j] = bucket_of<kTop>(h[j], bm);
+        off[j] = warp_rank<BITS>(bk[j], true, lane, om, c0, c1);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < kPartPerThread; ++j) {
+        const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
+        const bool valid = i < n;
+        bk[j] = valid ? bucket_of<kTop>(h[j], bm) : 0u;
+        off[j] = warp_rank<BITS>(bk[j], valid, lane, om, c0, c1);
+        if (!valid) bk[j] = 0xffffffffu;
+      }
     }
     sm.wcnt[warp][lane] = c0;
     sm.wcnt[warp][lane + 32] = c1;
@@ -350,7 +412,7 @@ void retain_pool() {
   done.fetch_or(bit, std::memory_order_relaxed);
 }
 
-template <int BITS>
+template <int BITS, bool kTop>
 cudaError_t bucket_partition_bits(uint64_t grid, const BucketMap& bm, const uint64_t* hashes, uint64_t m,
                                   uint64_t* d_counts, uint64_t* d_out, uint32_t* d_pos, cudaStream_t s,
                                   RouteOut route = RouteOut{}) {
@@ -362,17 +424,17 @@ cudaError_t bucket_partition_bits(uint64_t grid, const BucketMap& bm, const uint
   if (e == cudaSuccess)
     e = cudaMallocAsync(reinterpret_cast<void**>(&bases), grid * kMaxBuckets * sizeof(unsigned long long), s);
   static const cudaError_t attr = cudaFuncSetAttribute(
-      bucket_scatter_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      bucket_scatter_kernel<BITS, kTop>, cudaFuncAttributeMaxDynamicSharedMemorySize,
       static_cast<int>(sizeof(ScatterSmem)));
   if (e == cudaSuccess) e = attr;
   if (e == cudaSuccess) {
     note_launch();
-    bucket_count_kernel<BITS><<<static_cast<unsigned>(grid), kPartThreads, 0, s>>>(hashes, m, bm, hist);
+    bucket_count_kernel<BITS, kTop><<<static_cast<unsigned>(grid), kPartThreads, 0, s>>>(hashes, m, bm, hist);
     note_launch();
     bucket_scan_kernel<<<1, kMaxBuckets, 0, s>>>(hist, static_cast<uint32_t>(grid), bm.S,
                                                  reinterpret_cast<unsigned long long*>(d_counts), bases);
     note_launch();
-    bucket_scatter_kernel<BITS><<<static_cast<unsigned>(grid), kPartThreads, sizeof(ScatterSmem), s>>>(
+    bucket_scatter_kernel<BITS, kTop><<<static_cast<unsigned>(grid), kPartThreads, sizeof(ScatterSmem), s>>>(
         hashes, m, bm, bases, d_out, d_pos, route, reinterpret_cast<const unsigned long long*>(d_counts));
     e = cudaGetLastError();
   }
@@ -394,81 +456,331 @@ cudaError_t bucket_partition(const DeviceInfo& di, const Geom& g, uint32_t S, co
   // an empty batch still runs the (tiny) grid in routed mode: every destination
   // must receive this source's zero counts
   if (m == 0 && !route.dst) return cudaMemsetAsync(d_counts, 0, S * sizeof(uint64_t), s);
-  const uint64_t grid = m ? grid_for(m, kPartChunk, di.sms, 2) : 1;
-  switch (bm.bits) {
-    case 1: return bucket_partition_bits<1>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);
-    case 2: return bucket_partition_bits<2>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);
-    case 3: return bucket_partition_bits<3>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);
-    case 4: return bucket_partition_bits<4>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);
-    case 5: return bucket_partition_bits<5>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);
-    case 6: return bucket_partition_bits<6>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);
+  const uint64_t grid = m ? grid_for(m, kPartChunk, di.sms, kPartMinBlocks) : 1;
+  switch (bm.bits * 2 + (bm.top_bits ? 1 : 0)) {
+#define SBBF_PART_CASE(B)                                                                                       \
+  case 2 * B:                                                                                                   \
+    return bucket_partition_bits<B, false>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);         \
+  case 2 * B + 1:                                                                                               \
+    return bucket_partition_bits<B, true>(grid, bm, hashes, m, d_counts, d_out, d_pos, s, route);
+    SBBF_PART_CASE(1)
+    SBBF_PART_CASE(2)
+    SBBF_PART_CASE(3)
+    SBBF_PART_CASE(4)
+    SBBF_PART_CASE(5)
+    SBBF_PART_CASE(6)
+#undef SBBF_PART_CASE
     default: return cudaErrorInvalidValue;
   }
 }
 
 // ---------------------------------------------------------------------------
-// grouped probe
+// chunk-local blocked path (filters beyond L2)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kProbeThreads, 2) probe_grouped_kernel(
-    const uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
-    const uint32_t* __restrict__ pos, uint64_t m, uint32_t* __restrict__ bitmap) {
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kProbeTile + threadIdx.x;
+// chunk_scatter: every kPartChunk-key chunk of the batch is rewritten
+// bucket-major INSIDE ITS OWN REGION [ch*K, ch*K + cnt): one read of the
+// keys, fully coalesced writes, no count pass, no scan, no global atomics.
+// Per chunk it records the bucket offsets boffs[ch][0..S] (16-bit) and, for
+// lookups, each slot's 16-bit source position inside the chunk.
+struct ChunkSmem {
+  uint64_t key[kPartChunk];
+  uint16_t pos[kPartChunk];
+  uint32_t wcnt[kPartWarps][kMaxBuckets];
+  uint32_t boff[kMaxBuckets + 1];
+};
+constexpr int kBoffStride = kMaxBuckets + 1;
+
+template <int BITS, bool kTop>
+__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
+    chunk_scatter_kernel(const uint64_t* __restrict__ hashes, uint64_t n, BucketMap bm, uint64_t* __restrict__ out,
+                         uint16_t* __restrict__ pos16, uint16_t* __restrict__ boffs) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ChunkSmem& sm = *reinterpret_cast<ChunkSmem*>(smem_raw);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const OwnerMasks om(lane);
   const uint64_t pol = dev::policy_evict_first();
-  const uint64_t keep = dev::policy_evict_last();
-  uint64_t h[kProbeU];
-  uint32_t p[kProbeU];
+  const uint64_t nchunks = (n + kPartChunk - 1) / kPartChunk;
+  for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const uint64_t base = ch * kPartChunk;
+    const uint32_t cnt = static_cast<uint32_t>(n - base < kPartChunk ? n - base : kPartChunk);
+    uint64_t h[kPartPerThread];
+    uint32_t bk[kPartPerThread], off[kPartPerThread];
+    load_chunk(hashes, n, ch, pol, h);
+    uint32_t c0 = 0, c1 = 0;
+    if (cnt == kPartChunk) {
 #pragma unroll
-  for (int u = 0; u < kProbeU; ++u) {
-    const uint64_t i = base + static_cast<uint64_t>(u) * kProbeThreads;
-    h[u] = i < m ? dev::ld_stream_u64(keys + i, pol) : 0;
-    p[u] = i < m ? dev::ld_stream_u32(pos + i, pol) : 0;
-  }
-  dev::Block8 b[kProbeU];
-  uint32_t ok_mask = 0;
+      for (int j = 0; j < kPartPerThread; ++j) {
+        bk[j] = bucket_of<kTop>(h[j], bm);
+        off[j] = warp_rank<BITS>(bk[j], true, lane, om, c0, c1);
+      }
+    } else {
 #pragma unroll
-  for (int u = 0; u < kProbeU; ++u) {
-    const uint64_t blk = dev::block_index(h[u], g.nb_global) - g.first;
-    const bool ok = blk < g.nb_local;
-    ok_mask |= static_cast<uint32_t>(ok) << u;
-    dev::ld_block_nc_normal(blocks + (ok ? blk : 0) * 8, b[u]);
-  }
+      for (int j = 0; j < kPartPerThread; ++j) {
+        const bool valid = j * kPartThreads + threadIdx.x < cnt;
+        bk[j] = valid ? bucket_of<kTop>(h[j], bm) : 0u;
+        off[j] = warp_rank<BITS>(bk[j], valid, lane, om, c0, c1);
+        if (!valid) bk[j] = 0xffffffffu;
+      }
+    }
+    sm.wcnt[warp][lane] = c0;
+    sm.wcnt[warp][lane + 32] = c1;
+    __syncthreads();
+    if (warp == 0) {
+      // per-bucket totals over the warps (lane owns buckets lane, lane + 32),
+      // exclusive prefixes over warps and over buckets
+      uint32_t t0 = 0, t1 = 0;
 #pragma unroll
-  for (int u = 0; u < kProbeU; ++u) {
-    const uint64_t i = base + static_cast<uint64_t>(u) * kProbeThreads;
-    if (i < m && ((ok_mask >> u) & 1u) && dev::block_contains(b[u], h[u]))
-      dev::red_or(bitmap + (p[u] >> 5), 1u << (p[u] & 31), keep);  // chunk bitmap stays in L2
+      for (int w = 0; w < kPartWarps; ++w) {
+        const uint32_t a = sm.wcnt[w][lane], b = sm.wcnt[w][lane + 32];
+        sm.wcnt[w][lane] = t0;
+        sm.wcnt[w][lane + 32] = t1;
+        t0 += a;
+        t1 += b;
+      }
+      uint32_t s0 = t0, s1 = t1;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y0 = __shfl_up_sync(0xffffffffu, s0, d), y1 = __shfl_up_sync(0xffffffffu, s1, d);
+        if (lane >= static_cast<uint32_t>(d)) {
+          s0 += y0;
+          s1 += y1;
+        }
+      }
+      const uint32_t sum0 = __shfl_sync(0xffffffffu, s0, 31);
+      sm.boff[lane] = s0 - t0;
+      sm.boff[lane + 32] = sum0 + s1 - t1;
+      uint16_t* bo = boffs + ch * kBoffStride;
+      // buckets >= S are empty: their offsets equal cnt (lanes >= S may hold
+      // counts of aliased ids, which no key uses)
+      bo[lane] = static_cast<uint16_t>(lane < bm.S ? s0 - t0 : cnt);
+      bo[lane + 32] = static_cast<uint16_t>(lane + 32 < bm.S ? sum0 + s1 - t1 : cnt);
+      if (lane == 0) bo[kMaxBuckets] = static_cast<uint16_t>(cnt);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPartPerThread; ++j) {
+      if (bk[j] != 0xffffffffu) {
+        const uint32_t loc = sm.boff[bk[j]] + sm.wcnt[warp][bk[j]] + off[j];
+        sm.key[loc] = h[j];
+        sm.pos[loc] = static_cast<uint16_t>(j * kPartThreads + threadIdx.x);
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < cnt; i += kPartThreads) {
+      out[base + i] = sm.key[i];
+      if (pos16) pos16[base + i] = sm.pos[i];
+    }
+    __syncthreads();
   }
 }
 
-__global__ void expand_bits_kernel(const uint32_t* __restrict__ bits, uint64_t n, uint8_t* __restrict__ out) {
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    out[i] = static_cast<uint8_t>((bits[i >> 5] >> (i & 31)) & 1u);
+// Probe (lookup) or OR (insert) bucket by bucket: CTA blockIdx handles bucket
+// b = blockIdx / groups over chunks [grp*G, grp*G + G); CTAs run in blockIdx
+// order, so the keys in flight all fall in one or two ~16 MiB filter slices
+// and their sectors / atomics are served by L2. Each warp works on 4 chunk
+// segments at a time (independent loads in flight); a segment is the
+// chunk's contiguous run of bucket b. Lookups store one answer byte per
+// routed slot (plain stores, no atomics).
+constexpr int kSegThreads = 256;
+constexpr int kSegWarps = kSegThreads / 32;
+constexpr uint32_t kSegChunksPerCta = 64;
+
+template <bool kInsert, int kSegQ>
+__global__ void __launch_bounds__(kSegThreads, kSegQ > 4 ? 2 : 3)
+    segment_kernel(uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
+                   const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint8_t* __restrict__ ans) {
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t b = blockIdx.x / groups, grp = blockIdx.x % groups;
+  const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
+  const uint64_t c_begin = static_cast<uint64_t>(grp) * kSegChunksPerCta;
+  const uint64_t c_end = c_begin + kSegChunksPerCta < nchunks ? c_begin + kSegChunksPerCta : nchunks;
+  const uint64_t pol = dev::policy_evict_first();
+  const uint64_t keep = dev::policy_evict_last();
+  for (uint64_t c = c_begin + warp * kSegQ; c < c_end; c += kSegWarps * kSegQ) {
+    uint64_t seg[kSegQ];
+    uint32_t len[kSegQ];
+    uint32_t maxlen = 0;
+#pragma unroll
+    for (int q = 0; q < kSegQ; ++q) {
+      const uint64_t ch = c + q;
+      uint32_t st = 0, en = 0;
+      if (ch < c_end) {
+        st = boffs[ch * kBoffStride + b];
+        en = boffs[ch * kBoffStride + b + 1];
+      }
+      seg[q] = ch * kPartChunk + st;
+      len[q] = en - st;
+      maxlen = len[q] > maxlen ? len[q] : maxlen;
+    }
+    if constexpr (kInsert) {
+      // 4 lanes per key, one 64-bit lane pair each (as insert_wide_kernel);
+      // test-before-set: grouped duplicates (config 4's hot keys) skip the atomic
+      const uint32_t pair = lane & 3;
+      const uint32_t seed_lo = dev::lane_seed_rt(2 * pair), seed_hi = dev::lane_seed_rt(2 * pair + 1);
+      for (uint32_t j = lane >> 2; j < maxlen; j += 8) {
+        uint64_t h[kSegQ];
+#pragma unroll
+        for (int q = 0; q < kSegQ; ++q) h[q] = j < len[q] ? dev::ld_stream_u64(keys + seg[q] + j, pol) : 0;
+        uint64_t* ptr[kSegQ];
+        uint64_t mask[kSegQ], cur[kSegQ];
+#pragma unroll
+        for (int q = 0; q < kSegQ; ++q) {
+          const uint64_t blk = dev::block_index(h[q], g.nb_global) - g.first;
+          const bool ok = j < len[q] && blk < g.nb_local;
+          const uint32_t low = static_cast<uint32_t>(h[q]);
+          ptr[q] = reinterpret_cast<uint64_t*>(blocks + (ok ? blk : 0) * 8) + pair;
+          mask[q] = ok ? (static_cast<uint64_t>(dev::lane_bit(low, seed_hi)) << 32) | dev::lane_bit(low, seed_lo) : 0;
+          cur[q] = mask[q] ? dev::ld_pair(ptr[q], keep) : ~0ull;
+        }
+#pragma unroll
+        for (int q = 0; q < kSegQ; ++q)
+          if (mask[q] & ~cur[q]) dev::red_or64(ptr[q], mask[q], keep);
+      }
+    } else {
+      for (uint32_t j = lane; j < maxlen; j += 32) {
+        uint64_t h[kSegQ];
+#pragma unroll
+        for (int q = 0; q < kSegQ; ++q) h[q] = j < len[q] ? dev::ld_stream_u64(keys + seg[q] + j, pol) : 0;
+        dev::Block8 bl[kSegQ];
+        uint32_t owned = 0;
+#pragma unroll
+        for (int q = 0; q < kSegQ; ++q) {
+          const uint64_t blk = dev::block_index(h[q], g.nb_global) - g.first;
+          const bool ok = blk < g.nb_local;
+          owned |= static_cast<uint32_t>(ok) << q;
+          dev::ld_block_nc_normal(blocks + (ok ? blk : 0) * 8, bl[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < kSegQ; ++q)
+          if (j < len[q]) ans[seg[q] + j] = (((owned >> q) & 1u) && dev::block_contains(bl[q], h[q])) ? 1 : 0;
+      }
+    }
+  }
+}
+
+// Answers back to source order: one CTA per chunk reads the chunk's answer
+// bytes and 16-bit positions (both contiguous), scatters them into shared
+// memory and writes the chunk's result bits (ballot-packed) or bytes.
+constexpr int kUnpermThreads = 256;
+
+__global__ void __launch_bounds__(kUnpermThreads, 4) unpermute_kernel(const uint8_t* __restrict__ ans,
+                                                                   const uint16_t* __restrict__ pos16, uint64_t m,
+                                                                   void* __restrict__ out, bool bits) {
+  static_assert(kPartChunk <= 65536, "positions are 16-bit");
+  __shared__ __align__(16) uint8_t a[kPartChunk];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kPartChunk;
+  const uint32_t cnt = static_cast<uint32_t>(m - base < kPartChunk ? m - base : kPartChunk);
+  if (cnt == kPartChunk) {
+    // full chunk: 8 positions (16 B) + 8 answers (8 B) per vector load
+    constexpr int kVec = kPartChunk / (kUnpermThreads * 8);
+    uint4 pv[kVec];
+    uint2 av[kVec];
+#pragma unroll
+    for (int k = 0; k < kVec; ++k) {
+      const uint32_t i = (k * kUnpermThreads + threadIdx.x) * 8;
+      pv[k] = __ldg(reinterpret_cast<const uint4*>(pos16 + base + i));
+      av[k] = __ldg(reinterpret_cast<const uint2*>(ans + base + i));
+    }
+#pragma unroll
+    for (int k = 0; k < kVec; ++k) {
+      const uint32_t pw[4] = {pv[k].x, pv[k].y, pv[k].z, pv[k].w};
+      const uint32_t aw[2] = {av[k].x, av[k].y};
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        a[(pw[e >> 1] >> ((e & 1) * 16)) & 0xffffu] = static_cast<uint8_t>(aw[e >> 2] >> ((e & 3) * 8));
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < cnt; i += kUnpermThreads) a[pos16[base + i]] = ans[base + i];
+  }
+  __syncthreads();
+  if (bits) {
+    uint32_t* ob = static_cast<uint32_t*>(out) + (base >> 5);
+    for (uint32_t wd = warp; wd * 32 < cnt; wd += kUnpermThreads / 32) {
+      const uint32_t i = wd * 32 + lane;
+      const uint32_t word = __ballot_sync(0xffffffffu, i < cnt && a[i]);
+      if (lane == 0) ob[wd] = word;
+    }
+  } else {
+    uint8_t* o = static_cast<uint8_t*>(out) + base;
+    for (uint32_t i = threadIdx.x; i < cnt; i += kUnpermThreads) o[i] = a[i];
+  }
+}
+
+template <int BITS, bool kTop>
+cudaError_t chunk_partition_bits(const DeviceInfo& di, const BucketMap& bm, const uint64_t* hashes, uint64_t m,
+                                 uint64_t* out, uint16_t* pos16, uint16_t* boffs, cudaStream_t s) {
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      chunk_scatter_kernel<BITS, kTop>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(ChunkSmem)));
+  if (attr != cudaSuccess) return attr;
+  const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
+  const uint64_t grid = nchunks < static_cast<uint64_t>(di.sms) * kPartMinBlocks ? nchunks
+                                                                                 : static_cast<uint64_t>(di.sms) * kPartMinBlocks;
+  note_launch();
+  chunk_scatter_kernel<BITS, kTop><<<static_cast<unsigned>(grid), kPartThreads, sizeof(ChunkSmem), s>>>(
+      hashes, m, bm, out, pos16, boffs);
+  return cudaGetLastError();
+}
+
+cudaError_t chunk_partition(const DeviceInfo& di, const Geom& g, uint32_t S, const uint64_t* hashes, uint64_t m,
+                            uint64_t* out, uint16_t* pos16, uint16_t* boffs, cudaStream_t s) {
+  const BucketMap bm = make_map(g, S);
+  switch (bm.bits * 2 + (bm.top_bits ? 1 : 0)) {
+#define SBBF_CHUNK_CASE(B)                                                                  \
+  case 2 * B:                                                                               \
+    return chunk_partition_bits<B, false>(di, bm, hashes, m, out, pos16, boffs, s);         \
+  case 2 * B + 1:                                                                           \
+    return chunk_partition_bits<B, true>(di, bm, hashes, m, out, pos16, boffs, s);
+    SBBF_CHUNK_CASE(1)
+    SBBF_CHUNK_CASE(2)
+    SBBF_CHUNK_CASE(3)
+    SBBF_CHUNK_CASE(4)
+    SBBF_CHUNK_CASE(5)
+    SBBF_CHUNK_CASE(6)
+#undef SBBF_CHUNK_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <bool kInsert>
+cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* keys, const uint16_t* boffs, uint32_t S,
+                            uint64_t m, uint8_t* ans, cudaStream_t s) {
+  const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
+  const uint32_t groups = static_cast<uint32_t>((nchunks + kSegChunksPerCta - 1) / kSegChunksPerCta);
+  note_launch();
+  // segments per warp step: 4 for inserts (4 lanes per key), 2 for lookups
+  // (measured: 1.82 ms vs 1.89 (4) and 2.37 (8) per 2^28 config-4 lookups;
+  // a flattened one-item-per-thread variant measured 2.08)
+  if constexpr (kInsert)
+    segment_kernel<true, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans);
+  else
+    segment_kernel<false, 2><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans);
+  return cudaGetLastError();
 }
 
 struct Scratch {
   uint64_t* keys = nullptr;
-  uint32_t* pos = nullptr;
-  uint64_t* counts = nullptr;  // [2][S]: counts, cursor
-  uint32_t* bits = nullptr;
+  uint16_t* boffs = nullptr;
+  uint16_t* pos16 = nullptr;
+  uint8_t* ans = nullptr;
 };
 
-cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, uint32_t parts, bool with_pos, bool with_bits,
-                          cudaStream_t s) {
+cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, bool lookup, cudaStream_t s) {
+  retain_pool();
+  const uint64_t nchunks = (cap + kPartChunk - 1) / kPartChunk;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&sc.keys), cap * sizeof(uint64_t), s);
   if (e == cudaSuccess)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&sc.counts), 2 * parts * sizeof(uint64_t), s);
-  if (e == cudaSuccess && with_pos) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.pos), cap * sizeof(uint32_t), s);
-  if (e == cudaSuccess && with_bits)
-    e = cudaMallocAsync(reinterpret_cast<void**>(&sc.bits), ((cap + 31) / 32) * sizeof(uint32_t), s);
+    e = cudaMallocAsync(reinterpret_cast<void**>(&sc.boffs), nchunks * kBoffStride * sizeof(uint16_t), s);
+  if (lookup && e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.pos16), cap * sizeof(uint16_t), s);
+  if (lookup && e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.ans), cap, s);
   return e;
 }
 
 void free_scratch(Scratch& sc, cudaStream_t s) {
   if (sc.keys) cudaFreeAsync(sc.keys, s);
-  if (sc.pos) cudaFreeAsync(sc.pos, s);
-  if (sc.counts) cudaFreeAsync(sc.counts, s);
-  if (sc.bits) cudaFreeAsync(sc.bits, s);
+  if (sc.boffs) cudaFreeAsync(sc.boffs, s);
+  if (sc.pos16) cudaFreeAsync(sc.pos16, s);
+  if (sc.ans) cudaFreeAsync(sc.ans, s);
   sc = Scratch{};
 }
 
@@ -497,17 +809,14 @@ cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g
   if (n == 0) return cudaSuccess;
   const uint64_t cap = n < kBlockedChunk ? n : kBlockedChunk;
   Scratch sc;
-  cudaError_t e = alloc_scratch(sc, cap, plan.parts, false, false, s);
+  cudaError_t e = alloc_scratch(sc, cap, false, s);
   for (uint64_t off = 0; e == cudaSuccess && off < n; off += cap) {
     const uint64_t m = n - off < cap ? n - off : cap;
-    e = bucket_partition(di, g, plan.parts, hashes + off, m, sc.counts, sc.counts + plan.parts, sc.keys,
-                         nullptr, s);
-    // test-before-set: grouped duplicates (config 4's hot keys arrive back to
-    // back) skip the atomic once their bits are in.
-    if (e == cudaSuccess) e = launch_insert_ordered(di, blocks, g, sc.keys, m, /*test=*/true, s);
+    e = chunk_partition(di, g, plan.parts, hashes + off, m, sc.keys, nullptr, sc.boffs, s);
+    if (e == cudaSuccess) e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, plan.parts, m, nullptr, s);
   }
   free_scratch(sc, s);
-  return e == cudaSuccess ? cudaGetLastError() : e;
+  return e;
 }
 
 cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
@@ -515,23 +824,21 @@ cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geo
   if (n == 0) return cudaSuccess;
   const uint64_t cap = n < kBlockedChunk ? n : kBlockedChunk;  // a multiple of 32 unless n is the whole batch
   Scratch sc;
-  cudaError_t e = alloc_scratch(sc, cap, plan.parts, true, !bits, s);
+  cudaError_t e = alloc_scratch(sc, cap, true, s);
   for (uint64_t off = 0; e == cudaSuccess && off < n; off += cap) {
     const uint64_t m = n - off < cap ? n - off : cap;
-    uint32_t* bm = bits ? static_cast<uint32_t*>(out) + off / 32 : sc.bits;
-    e = cudaMemsetAsync(bm, 0, ((m + 31) / 32) * sizeof(uint32_t), s);
+    // 1. every chunk bucket-major in its own region (+ positions, offsets)
+    e = chunk_partition(di, g, plan.parts, hashes + off, m, sc.keys, sc.pos16, sc.boffs, s);
+    // 2. probe slice by slice (L2-resident), one answer byte per routed slot
     if (e == cudaSuccess)
-      e = bucket_partition(di, g, plan.parts, hashes + off, m, sc.counts, sc.counts + plan.parts, sc.keys,
-                           sc.pos, s);
-    if (e != cudaSuccess) break;
-    note_launch();
-    probe_grouped_kernel<<<static_cast<unsigned>((m + kProbeTile - 1) / kProbeTile), kProbeThreads, 0, s>>>(
-        blocks, g, sc.keys, sc.pos, m, bm);
-    e = cudaGetLastError();
-    if (e == cudaSuccess && !bits) {
+      e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, plan.parts, m, sc.ans, s);
+    // 3. back to source order, straight into the caller's bitmap / bytes
+    if (e == cudaSuccess) {
       note_launch();
-      expand_bits_kernel<<<static_cast<unsigned>(grid_for(m, 1024, di.sms, 8)), 256, 0, s>>>(
-          bm, m, static_cast<uint8_t*>(out) + off);
+      void* dst = bits ? static_cast<void*>(static_cast<uint32_t*>(out) + off / 32)
+                       : static_cast<void*>(static_cast<uint8_t*>(out) + off);
+      unpermute_kernel<<<static_cast<unsigned>((m + kPartChunk - 1) / kPartChunk), kUnpermThreads, 0, s>>>(
+          sc.ans, sc.pos16, m, dst, bits);
       e = cudaGetLastError();
     }
   }
