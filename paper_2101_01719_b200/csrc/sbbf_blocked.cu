@@ -585,8 +585,8 @@ constexpr int kSegThreads = 256;
 constexpr int kSegWarps = kSegThreads / 32;
 constexpr uint32_t kSegChunksPerCta = 64;
 
-template <bool kInsert, int kSegQ>
-__global__ void __launch_bounds__(kSegThreads, kSegQ > 4 ? 2 : 3)
+template <bool kInsert, int kSegQ, int kMinB = (kSegQ > 4 ? 2 : 3)>
+__global__ void __launch_bounds__(kSegThreads, kMinB)
     segment_kernel(uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
                    const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint8_t* __restrict__ ans) {
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -748,13 +748,14 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
   const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
   const uint32_t groups = static_cast<uint32_t>((nchunks + kSegChunksPerCta - 1) / kSegChunksPerCta);
   note_launch();
-  // segments per warp step: 4 for inserts (4 lanes per key), 2 for lookups
-  // (measured: 1.82 ms vs 1.89 (4) and 2.37 (8) per 2^28 config-4 lookups;
-  // a flattened one-item-per-thread variant measured 2.08)
+  // Segments per warp step / min CTAs per SM, measured on config 4
+  // (profiles/r1_blocked_partition.md): inserts 4 / 3 (4 lanes per key;
+  // 1 or 2 segments: same or slower); lookups 1 / 8 — 1.54 ms per 2^28 keys,
+  // vs 1.82 (2 segments), 1.89 (4), 2.37 (8): occupancy beats per-lane MLP.
   if constexpr (kInsert)
     segment_kernel<true, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans);
   else
-    segment_kernel<false, 2><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans);
+    segment_kernel<false, 1, 8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans);
   return cudaGetLastError();
 }
 
