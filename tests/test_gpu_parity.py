@@ -194,6 +194,37 @@ def test_no_false_negatives_acceptance(cuda):
         assert int(f.find_hashes(hs).sum()) == hs.numel()
 
 
+@pytest.mark.parametrize("nb", [2**20, 2**20 + 7, 3 * 2**19 + 1])
+@pytest.mark.parametrize("shape", ["one_slice", "one_key", "two_slices", "ragged_tail"])
+def test_blocked_path_skew(cuda, oracle, nb, shape):
+    """The L2-blocked path under skew: every key in one filter slice (one
+    4096-key run per chunk), one repeated key, two slices, and a batch whose
+    last partition chunk is partial. Bit-exact against the oracle."""
+    rng = np.random.default_rng(nb + len(shape))
+    n = 300_001
+    if shape == "one_slice":
+        hs = rng.integers(0, 2**58, size=n, dtype=np.uint64)          # top 6 bits zero
+    elif shape == "one_key":
+        hs = np.full(n, 0x123456789ABCDEF1, dtype=np.uint64)
+    elif shape == "two_slices":
+        hs = rng.integers(0, 2**58, size=n, dtype=np.uint64) | (rng.integers(0, 2, size=n).astype(np.uint64) << np.uint64(63))
+    else:
+        n = 4096 * 37 + 29
+        hs = rng.integers(0, 2**64, size=n, dtype=np.uint64)
+    probes = np.concatenate([hs[: n // 3], rng.integers(0, 2**58, size=n // 2, dtype=np.uint64),
+                             rng.integers(0, 2**64, size=1001, dtype=np.uint64)])
+    want = oracle.build(nb, hs)
+    f = SplitBlockFilter(nb)
+    f.set_insert_variant(_lib.INSERT_BLOCKED)
+    f.add_hashes(dev(hs, cuda))
+    assert np.array_equal(f.blocks(), want)
+    f.set_find_variant(_lib.FIND_BLOCKED)
+    want_res = oracle.find_hashes(want, probes)
+    assert np.array_equal(f.find_hashes(dev(probes, cuda)).cpu().numpy(), want_res)
+    bits = u32(f.find_hashes_bits(dev(probes, cuda)))
+    assert np.array_equal(bits_to_bytes(bits, probes.size), want_res)
+
+
 def test_64bit_block_offsets(cuda, oracle):
     """A filter larger than 2^32 words (> 16 GiB): offsets must be 64-bit."""
     nb = (1 << 29) + 12345          # 17.2 GB, 2^32+ 32-bit words
