@@ -275,12 +275,13 @@ class ShardedFilter:
         self.shard = ops.create(self.total, self.first, self.count)
         self.last_exchange: dict = {}
         self.route = None
+        fused_req = fused is True
         if fused is None:
             fused = isinstance(ops, CudaShardOps) and self._peer_capable(init)
         if fused:
             if not isinstance(ops, CudaShardOps):
                 raise ValueError("fused routing needs the CUDA shard ops")
-            self._setup_route(init, max_batch)
+            self._setup_route(init, max_batch, required=fused_req)
 
     def _peer_capable(self, init: bool) -> bool:
         if self.world == 1:
@@ -291,16 +292,37 @@ class ShardedFilter:
         dist.all_gather_object(devs, self.ops.device, group=self.group)
         return _peer_access_everywhere(devs)
 
-    def _setup_route(self, init: bool, max_batch: int):
-        self.route = PeerRoute(self.world, self.rank, max_batch, self.ops.device)
+    def _setup_route(self, init: bool, max_batch: int, required: bool = False):
+        """Map every peer's window. The ranks agree collectively: if any rank
+        cannot map a peer (e.g. GPUs hidden from each other), every rank falls
+        back to the NCCL path (or raises, when fused routing was required)."""
+        route, err = None, ""
+        try:
+            route = PeerRoute(self.world, self.rank, max_batch, self.ops.device)
+        except Exception as exc:  # noqa: BLE001 - reported below, collectively
+            err = repr(exc)
         if self.world > 1:
             handles = [None] * self.world
-            dist.all_gather_object(handles, self.route.handle(), group=self.group)
-            for peer, h in enumerate(handles):
-                if peer != self.rank:
-                    self.route.open_peer(peer, h)
-            dist.barrier(group=self.group)
-        assert self.route.ready()
+            dist.all_gather_object(handles, route.handle() if route is not None else None, group=self.group)
+            if route is not None and None not in handles:
+                try:
+                    for peer, h in enumerate(handles):
+                        if peer != self.rank:
+                            route.open_peer(peer, h)
+                except Exception as exc:  # noqa: BLE001
+                    err = repr(exc)
+            ok = [None] * self.world
+            dist.all_gather_object(ok, err, group=self.group)
+            err = next((e for e in ok if e), "")
+        if err or route is None or not route.ready():
+            if route is not None:
+                route.close()
+            if required:
+                raise RuntimeError(f"fused routing unavailable: {err}")
+            self.route = None
+            self.route_error = err
+            return
+        self.route = route
         self._flag = torch.zeros(1, dtype=torch.int32, device=self.ops.dev)
 
     def _barrier(self):
