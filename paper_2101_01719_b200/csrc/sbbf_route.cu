@@ -277,6 +277,9 @@ int sbbf_route_create(uint32_t parts, uint32_t rank, uint64_t max_batch, int dev
   rt->device = device;
   rt->di.device = device;
   cudaDeviceGetAttribute(&rt->di.sms, cudaDevAttrMultiProcessorCount, device);
+  int l2 = 0;
+  if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device) == cudaSuccess && l2 > 0)
+    rt->di.l2_bytes = static_cast<size_t>(l2);
   rt->R = sbbf::round_up(max_batch, 256);
   rt->window_bytes = sbbf_route_window_bytes(parts, max_batch);
   rt->peer.assign(parts, nullptr);
@@ -382,10 +385,63 @@ int sbbf_route_dispatch(sbbf_route_t* rt, const uint64_t* d_hashes, uint64_t n, 
                     "sbbf_route_dispatch");
 }
 
+}  // extern "C"
+
+namespace {
+// Shards beyond 2 x L2 (config 5's 1 GiB shards at P = 8): random probes
+// would be DRAM-bound, so each source region goes through the shard's own
+// AUTO dispatch (the L2-blocked path) instead of the direct window kernel.
+// That needs the region counts on the host: one small copy + stream sync.
+bool window_blocked(const sbbf_route* rt, const sbbf_gpu_t* shard) {
+  return sbbf_gpu_size_bytes(shard) > 2 * static_cast<uint64_t>(rt->di.l2_bytes);
+}
+
+int window_counts(const sbbf_route* rt, int p, cudaStream_t s, uint64_t* h) {
+  int rc = route_cuda(cudaMemcpyAsync(h, rt->window + count_off(p, 0), rt->parts * sizeof(uint64_t),
+                                      cudaMemcpyDeviceToHost, s),
+                      "window counts");
+  if (rc == SBBF_OK) rc = route_cuda(cudaStreamSynchronize(s), "window counts");
+  return rc;
+}
+
+// The source regions of window parity p copied back to back into one
+// stream-ordered allocation (*keys, *total keys).
+int gather_regions(const sbbf_route* rt, int p, const std::vector<uint64_t>& cnt, cudaStream_t s, uint64_t** keys,
+                   uint64_t* total) {
+  uint64_t t = 0;
+  for (uint64_t c : cnt) t += c;
+  *total = t;
+  *keys = nullptr;
+  if (t == 0) return SBBF_OK;
+  int rc = route_cuda(cudaMallocAsync(reinterpret_cast<void**>(keys), t * sizeof(uint64_t), s), "window gather");
+  for (uint64_t r = 0, off = 0; rc == SBBF_OK && r < rt->parts; off += cnt[r], ++r)
+    if (cnt[r])
+      rc = route_cuda(cudaMemcpyAsync(*keys + off, rt->window + keys_off(rt, p, static_cast<uint32_t>(r)),
+                                      cnt[r] * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s),
+                      "window gather");
+  return rc;
+}
+}  // namespace
+
+extern "C" {
+
 int sbbf_route_insert_window(sbbf_route_t* rt, sbbf_gpu_t* shard, void* stream) {
   if (!rt || !shard) return route_fail(SBBF_EINVAL, "sbbf_route_insert_window: null argument");
   DeviceGuard g(rt->device);
   const int p = rt->parity;
+  if (window_blocked(rt, shard)) {
+    std::vector<uint64_t> cnt(rt->parts);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int rc = window_counts(rt, p, s, cnt.data());
+    uint64_t* keys = nullptr;
+    uint64_t total = 0;
+    // one contiguous batch, so the blocked pass streams the shard through L2
+    // once per call rather than once per source region
+    if (rc == SBBF_OK) rc = gather_regions(rt, p, cnt, s, &keys, &total);
+    if (rc == SBBF_OK && total) rc = sbbf_gpu_insert_batch(shard, keys, total, stream);
+    if (keys) cudaFreeAsync(keys, s);
+    return rc;
+  }
   const sbbf::Geom geom{sbbf_gpu_total_buckets(shard), sbbf_gpu_first_block(shard), sbbf_gpu_num_buckets(shard)};
   sbbf::note_launch();
   // the window holds at most parts * R keys; the grid strides over the real count
@@ -401,6 +457,26 @@ int sbbf_route_find_window(sbbf_route_t* rt, const sbbf_gpu_t* shard, void* stre
   if (!rt || !shard) return route_fail(SBBF_EINVAL, "sbbf_route_find_window: null argument");
   DeviceGuard g(rt->device);
   const int p = rt->parity;
+  if (window_blocked(rt, shard)) {
+    std::vector<uint64_t> cnt(rt->parts);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int rc = window_counts(rt, p, s, cnt.data());
+    uint64_t* keys = nullptr;
+    uint64_t total = 0;
+    uint8_t* ans = nullptr;
+    if (rc == SBBF_OK) rc = gather_regions(rt, p, cnt, s, &keys, &total);
+    if (rc == SBBF_OK && total) rc = route_cuda(cudaMallocAsync(reinterpret_cast<void**>(&ans), total, s), "answers");
+    if (rc == SBBF_OK && total) rc = sbbf_gpu_find_batch(shard, keys, total, ans, stream);
+    // answers back next to each source region
+    for (uint64_t r = 0, off = 0; rc == SBBF_OK && r < rt->parts; off += cnt[r], ++r)
+      if (cnt[r])
+        rc = route_cuda(cudaMemcpyAsync(rt->window + res_off(rt, p, static_cast<uint32_t>(r)), ans + off, cnt[r],
+                                        cudaMemcpyDeviceToDevice, s),
+                        "answers");
+    if (keys) cudaFreeAsync(keys, s);
+    if (ans) cudaFreeAsync(ans, s);
+    return rc;
+  }
   const sbbf::Geom geom{sbbf_gpu_total_buckets(shard), sbbf_gpu_first_block(shard), sbbf_gpu_num_buckets(shard)};
   sbbf::note_launch();
   sbbf::window_find_kernel<<<static_cast<unsigned>(rt->di.sms * 3), sbbf::kWinThreads, 0,

@@ -416,10 +416,19 @@ class ShardedFilter:
 # bench.py --gpus N (torchrun): weak scaling, one rank per GPU
 # ---------------------------------------------------------------------------------
 def bench_main(args) -> dict | None:
-    """Each rank originates a config-2-sized batch (1M inserts, 10M lookups);
-    the filter is P x 1 MiB sharded by block range; keys cross NVLink to their
-    owner. value = all ranks' keys / max-over-ranks device time. Returns the
-    JSON line on rank 0 (bench.py adds clocks and prints it), None elsewhere."""
+    """The sharded bench. value = all ranks' keys / max-over-ranks device
+    time; returns the JSON line on rank 0 (bench.py adds clocks and prints
+    it), None elsewhere.
+
+    config 5 (the default under torchrun, BASELINE's sharded config): the
+    8 GiB filter (2^28 blocks) is split by block range over the P ranks;
+    every step each rank originates a bounded sample of config 5's streams —
+    ``--sample-keys`` inserts (positions [r*S, (r+1)*S) of splitmix64(9)) and
+    as many lookups (25 % members of the sampled inserts, non-members from
+    splitmix64(10)) — routed to their owners over NVLink.
+    config 2: each rank originates a config-2 batch (1M inserts, 10M
+    lookups) into a P x 1 MiB filter (routing overhead on L2-resident
+    shards)."""
     from . import workload as W
     from ._lib import launch_count
 
@@ -432,15 +441,24 @@ def bench_main(args) -> dict | None:
     os.environ.setdefault("MASTER_PORT", "29531")
     dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     cfg = W.CONFIGS[args.config]
-    N, L = cfg.inserts.n, cfg.lookups.n
-    total = cfg.num_buckets * world
+    if args.config == 5:
+        N = L = int(getattr(args, "sample_keys", 1 << 25))
+        total = cfg.num_buckets
+        workload = (f"BASELINE config 5 sample: 8 GiB filter ({total} blocks) sharded over {world} rank(s) "
+                    f"by block range; per rank per step {N:,} inserts (splitmix64(9) positions "
+                    f"[r*{N}, (r+1)*{N})) + {L:,} lookups (25% members)")
+    else:
+        N, L = cfg.inserts.n, cfg.lookups.n
+        total = cfg.num_buckets * world
+        workload = (f"sharded: per rank BASELINE config {args.config} batch ({N:,} inserts + {L:,} lookups) "
+                    f"into a {world}-way block-range sharded filter of {total} blocks")
     # rank r originates insert positions [rN, (r+1)N) of one world-wide stream
     spec = W.InsertSpec(seed=cfg.inserts.seed, n=N * world)
     st = W.StreamHandle(spec, local)
     ins = W.gen_inserts(st, rank * N, N, device=local)
     look = W.gen_lookups(st, cfg.lookups, N * world, rank * L, L, device=local)
     route = getattr(args, "route", "auto")
-    f = ShardedFilter(total, fused=None if route == "auto" else route == "fused")
+    f = ShardedFilter(total, fused=None if route == "auto" else route == "fused", max_batch=max(N, L))
     how = ("peer-memory windows over NVLink (fused dispatch, sbbf_route.cu)" if f.route is not None
            else "NCCL all-to-all")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -504,9 +522,7 @@ def bench_main(args) -> dict | None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (seeded splitmix64 hash streams, generated in HBM)",
-            "config": {"workload": f"sharded: per rank BASELINE config {args.config} batch "
-                                   f"({N:,} inserts + {L:,} lookups) into a {world}-way block-range "
-                                   f"sharded filter of {total} blocks; keys routed by {how}",
+            "config": {"workload": f"{workload}; keys routed by {how}", "config_id": args.config,
                        "parallelism": f"shard{world}", "l2": "flushed between timed steps (untimed)"},
             "e2e": {"value": world * (N + L) / e2e_s / 1e9, "unit": "Gkeys/s",
                     "h2d_bytes_per_step": 8 * (N + L), "d2h_bytes_per_step": 4 * ((L + 31) // 32),

@@ -403,3 +403,37 @@ def test_fused_ipc_processes(cuda, oracle, world, total):
     assert np.array_equal(full, want)
     for rank, ins, look, ans, *_ in got:
         assert np.array_equal(ans, oracle.find_hashes(want, look)), rank
+
+
+@pytest.mark.gpu
+def test_fused_route_big_shards(cuda, oracle):
+    """Shards beyond 2 x L2 (the config-5 regime): the owner's window ops go
+    through the L2-blocked path region by region; still bit-exact."""
+    parts, total = 2, 2 * (300 << 20) // 32 + 3
+    ops = S.CudaShardOps(0)
+    bounds = S.shard_bounds(total, parts)
+    db = ops._dev_bounds(bounds)
+    shards = [ops.create(total, bounds[r], bounds[r + 1] - bounds[r]) for r in range(parts)]
+    assert all(s.size_bytes() > 2 * (126 << 20) for s in shards)
+    routes = _linked_routes(parts, 1 << 21)
+    rng = np.random.default_rng(4242)
+    batch = [rng.integers(0, 2**64, size=1_500_000 + 77 * r, dtype=np.uint64) for r in range(parts)]
+    for r in range(parts):
+        routes[r].dispatch(torch.from_numpy(batch[r].view(np.int64)).to(cuda), total, db, keep_positions=False)
+    for r in range(parts):
+        routes[r].insert_window(shards[r])
+    want = oracle.build(total, np.concatenate(batch))
+    for r in range(parts):
+        assert np.array_equal(shards[r].blocks(), want[bounds[r]:bounds[r + 1]]), r
+    looks = [np.concatenate([batch[1 - r][:400_000], rng.integers(0, 2**64, size=900_000, dtype=np.uint64)])
+             for r in range(parts)]
+    for r in range(parts):
+        routes[r].dispatch(torch.from_numpy(looks[r].view(np.int64)).to(cuda), total, db, keep_positions=True)
+    for r in range(parts):
+        routes[r].find_window(shards[r])
+    for r in range(parts):
+        out = torch.empty(looks[r].size, dtype=torch.uint8, device=cuda)
+        routes[r].combine(out)
+        assert np.array_equal(out.cpu().numpy(), oracle.find_hashes(want, looks[r])), r
+    for rt in routes:
+        rt.close()
