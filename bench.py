@@ -455,7 +455,7 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=None,
                     help="2 (default, single GPU) / 3 / 4; under torchrun the default is 5 (sharded)")
-    ap.add_argument("--sample-keys", type=int, default=1 << 25,
+    ap.add_argument("--sample-keys", type=int, default=1 << 27,
                     help="config 5: inserts and lookups per rank per step (bounded sample)")
     ap.add_argument("--extra", default="3,4", help="extra configs reported under 'configs'")
     ap.add_argument("--no-cpu-baseline", action="store_true")

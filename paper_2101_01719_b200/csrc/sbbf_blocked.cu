@@ -29,6 +29,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <vector>
 
 #include "sbbf_device.cuh"
 #include "sbbf_internal.h"
@@ -805,18 +806,89 @@ cudaError_t route_partition(const DeviceInfo& di, uint64_t total, uint32_t parts
   return bucket_partition(di, whole, parts, hashes, n, d_counts, nullptr, nullptr, d_pos, s, d_bounds, route);
 }
 
+namespace {
+
+// One batch chunk (m <= kBlockedChunk keys) through the single-level path.
+cudaError_t insert_chunk(const DeviceInfo& di, uint32_t* blocks, const Geom& g, uint32_t parts, const uint64_t* keys,
+                         uint64_t m, Scratch& sc, cudaStream_t s) {
+  cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, nullptr, sc.boffs, s);
+  if (e == cudaSuccess) e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, parts, m, nullptr, s);
+  return e;
+}
+
+cudaError_t find_chunk(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, uint32_t parts,
+                       const uint64_t* keys, uint64_t m, Scratch& sc, void* dst, bool bits, cudaStream_t s) {
+  // 1. every chunk bucket-major in its own region (+ positions, offsets)
+  cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, sc.pos16, sc.boffs, s);
+  // 2. probe slice by slice (L2-resident), one answer byte per routed slot
+  if (e == cudaSuccess)
+    e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, parts, m, sc.ans, s);
+  // 3. back to source order, straight into the caller's bitmap / bytes
+  if (e == cudaSuccess) {
+    note_launch();
+    unpermute_kernel<<<static_cast<unsigned>((m + kPartChunk - 1) / kPartChunk), kUnpermThreads, 0, s>>>(
+        sc.ans, sc.pos16, m, dst, bits);
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+// Filters beyond kMaxBuckets slices (> ~1 GiB): a first partition groups the
+// batch chunk by "super-slice" (exact block ranges, global bucket-major
+// layout with source positions), then each super-slice runs the single-level
+// path on its sub-filter, so every slice the probes touch stays ~16 MiB.
+struct TwoLevel {
+  uint64_t* keys = nullptr;       // [m] grouped by super-slice
+  uint32_t* pos = nullptr;        // [m] source index (lookups)
+  uint8_t* ans = nullptr;         // [m] answers in grouped order (lookups)
+  uint8_t* bytes = nullptr;       // [m] answers in source order (bit output)
+  uint64_t* counts = nullptr;     // [2 * S]
+};
+
+cudaError_t super_counts(const DeviceInfo& di, const Geom& g, const BlockedPlan& plan, const uint64_t* keys,
+                         uint64_t m, TwoLevel& tl, bool lookup, cudaStream_t s, std::vector<uint64_t>& h) {
+  cudaError_t e = bucket_partition(di, g, plan.super_parts, keys, m, tl.counts, tl.counts + plan.super_parts, tl.keys,
+                                   lookup ? tl.pos : nullptr, s, plan.d_super_bounds);
+  h.assign(plan.super_parts, 0);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(h.data(), tl.counts, plan.super_parts * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return e;
+}
+
+Geom sub_geom(const Geom& g, const std::vector<uint64_t>& sb, uint32_t k) {
+  return Geom{g.nb_global, g.first + sb[k], sb[k + 1] - sb[k]};
+}
+
+}  // namespace
+
 cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
                            const uint64_t* hashes, uint64_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const uint64_t cap = n < kBlockedChunk ? n : kBlockedChunk;
   Scratch sc;
+  TwoLevel tl;
+  const bool two = plan.super_parts > 1;
   cudaError_t e = alloc_scratch(sc, cap, false, s);
+  if (e == cudaSuccess && two) e = cudaMallocAsync(reinterpret_cast<void**>(&tl.keys), cap * sizeof(uint64_t), s);
+  if (e == cudaSuccess && two)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&tl.counts), 2 * plan.super_parts * sizeof(uint64_t), s);
+  std::vector<uint64_t> cnt;
   for (uint64_t off = 0; e == cudaSuccess && off < n; off += cap) {
     const uint64_t m = n - off < cap ? n - off : cap;
-    e = chunk_partition(di, g, plan.parts, hashes + off, m, sc.keys, nullptr, sc.boffs, s);
-    if (e == cudaSuccess) e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, plan.parts, m, nullptr, s);
+    if (!two) {
+      e = insert_chunk(di, blocks, g, plan.parts, hashes + off, m, sc, s);
+      continue;
+    }
+    e = super_counts(di, g, plan, hashes + off, m, tl, false, s, cnt);
+    for (uint32_t k = 0, pre = 0; e == cudaSuccess && k < plan.super_parts; pre += cnt[k], ++k)
+      if (cnt[k])
+        e = insert_chunk(di, blocks + plan.h_super_bounds[k] * 8, sub_geom(g, plan.h_super_bounds, k), plan.parts,
+                         tl.keys + pre, cnt[k], sc, s);
   }
   free_scratch(sc, s);
+  if (tl.keys) cudaFreeAsync(tl.keys, s);
+  if (tl.counts) cudaFreeAsync(tl.counts, s);
   return e;
 }
 
@@ -825,25 +897,41 @@ cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geo
   if (n == 0) return cudaSuccess;
   const uint64_t cap = n < kBlockedChunk ? n : kBlockedChunk;  // a multiple of 32 unless n is the whole batch
   Scratch sc;
+  TwoLevel tl;
+  const bool two = plan.super_parts > 1;
   cudaError_t e = alloc_scratch(sc, cap, true, s);
+  if (e == cudaSuccess && two) e = cudaMallocAsync(reinterpret_cast<void**>(&tl.keys), cap * sizeof(uint64_t), s);
+  if (e == cudaSuccess && two) e = cudaMallocAsync(reinterpret_cast<void**>(&tl.pos), cap * sizeof(uint32_t), s);
+  if (e == cudaSuccess && two) e = cudaMallocAsync(reinterpret_cast<void**>(&tl.ans), cap, s);
+  if (e == cudaSuccess && two && bits) e = cudaMallocAsync(reinterpret_cast<void**>(&tl.bytes), cap, s);
+  if (e == cudaSuccess && two)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&tl.counts), 2 * plan.super_parts * sizeof(uint64_t), s);
+  std::vector<uint64_t> cnt;
   for (uint64_t off = 0; e == cudaSuccess && off < n; off += cap) {
     const uint64_t m = n - off < cap ? n - off : cap;
-    // 1. every chunk bucket-major in its own region (+ positions, offsets)
-    e = chunk_partition(di, g, plan.parts, hashes + off, m, sc.keys, sc.pos16, sc.boffs, s);
-    // 2. probe slice by slice (L2-resident), one answer byte per routed slot
-    if (e == cudaSuccess)
-      e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, plan.parts, m, sc.ans, s);
-    // 3. back to source order, straight into the caller's bitmap / bytes
-    if (e == cudaSuccess) {
-      note_launch();
-      void* dst = bits ? static_cast<void*>(static_cast<uint32_t*>(out) + off / 32)
-                       : static_cast<void*>(static_cast<uint8_t*>(out) + off);
-      unpermute_kernel<<<static_cast<unsigned>((m + kPartChunk - 1) / kPartChunk), kUnpermThreads, 0, s>>>(
-          sc.ans, sc.pos16, m, dst, bits);
-      e = cudaGetLastError();
+    void* dst = bits ? static_cast<void*>(static_cast<uint32_t*>(out) + off / 32)
+                     : static_cast<void*>(static_cast<uint8_t*>(out) + off);
+    if (!two) {
+      e = find_chunk(di, blocks, g, plan.parts, hashes + off, m, sc, dst, bits, s);
+      continue;
     }
+    e = super_counts(di, g, plan, hashes + off, m, tl, true, s, cnt);
+    for (uint32_t k = 0, pre = 0; e == cudaSuccess && k < plan.super_parts; pre += cnt[k], ++k)
+      if (cnt[k])
+        e = find_chunk(di, blocks + plan.h_super_bounds[k] * 8, sub_geom(g, plan.h_super_bounds, k), plan.parts,
+                       tl.keys + pre, cnt[k], sc, tl.ans + pre, false, s);
+    // grouped answers back to source order (then packed for bit output)
+    uint8_t* bytes = bits ? tl.bytes : static_cast<uint8_t*>(dst);
+    if (e == cudaSuccess && sbbf_scatter_u8(tl.ans, tl.pos, m, bytes, s) != SBBF_OK) e = cudaGetLastError();
+    if (e == cudaSuccess && bits && sbbf_pack_bits(tl.bytes, m, static_cast<uint32_t*>(dst), s) != SBBF_OK)
+      e = cudaGetLastError();
   }
   free_scratch(sc, s);
+  if (tl.keys) cudaFreeAsync(tl.keys, s);
+  if (tl.pos) cudaFreeAsync(tl.pos, s);
+  if (tl.ans) cudaFreeAsync(tl.ans, s);
+  if (tl.bytes) cudaFreeAsync(tl.bytes, s);
+  if (tl.counts) cudaFreeAsync(tl.counts, s);
   return e;
 }
 

@@ -83,6 +83,7 @@ struct sbbf_gpu {
   std::mutex plan_mu;
   sbbf::BlockedPlan plan;
   uint64_t* d_plan_bounds = nullptr;
+  uint64_t* d_super_bounds = nullptr;
 };
 
 namespace {
@@ -131,11 +132,31 @@ int ensure_plan(sbbf_gpu* f) {
   std::lock_guard<std::mutex> lock(f->plan_mu);
   if (f->d_plan_bounds) return SBBF_OK;
   uint64_t parts = (f->nb * 32 + kSliceBytes - 1) / kSliceBytes;
-  parts = parts < 2 ? 2 : (parts > 64 ? 64 : parts);  // bucket ids are <= 6 bits
+  // beyond 64 slices (bucket ids are <= 6 bits): super-slices of <= 64 slices
+  uint64_t super = (parts + 63) / 64;
+  super = super > 64 ? 64 : super;
+  if (super > 1) parts = (parts + super - 1) / super;
+  parts = parts < 2 ? 2 : (parts > 64 ? 64 : parts);
   uint64_t pow2 = 1;
   while (pow2 < parts) pow2 <<= 1;  // a power of two lets the partition use the hash's top bits
   parts = pow2;
   if (parts > f->nb) parts = f->nb;
+  if (super > 1) {
+    std::vector<uint64_t> sb(super + 1);
+    for (uint64_t k = 0; k <= super; ++k)
+      sb[k] = static_cast<uint64_t>((static_cast<unsigned __int128>(f->nb) * k) / super);
+    cudaError_t e = cudaMalloc(&f->d_super_bounds, super * sizeof(uint64_t));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(f->d_super_bounds, sb.data(), super * sizeof(uint64_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaFree(f->d_super_bounds);
+      f->d_super_bounds = nullptr;
+      return cuda_fail(e, "blocked plan");
+    }
+    f->plan.super_parts = static_cast<uint32_t>(super);
+    f->plan.d_super_bounds = f->d_super_bounds;
+    f->plan.h_super_bounds = sb;
+  }
   std::vector<uint64_t> b(parts);
   for (uint64_t k = 0; k < parts; ++k)
     b[k] = f->geom.first + static_cast<uint64_t>((static_cast<unsigned __int128>(f->nb) * k) / parts);
@@ -292,6 +313,7 @@ int sbbf_gpu_destroy(sbbf_gpu_t* f) {
     cudaFree(f->d_blocks);
     cudaFree(f->d_one);
     cudaFree(f->d_plan_bounds);
+    cudaFree(f->d_super_bounds);
     for (int i = 0; i < kHostStreams; ++i) {
       if (f->hs[i]) cudaStreamDestroy(f->hs[i]);
       cudaFree(f->d_stage[i]);

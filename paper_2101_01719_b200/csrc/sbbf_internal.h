@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "sbbf_bench.h"
 #include "sbbf_gpu.h"
@@ -76,8 +77,14 @@ cudaError_t launch_insert_ordered(const DeviceInfo& di, uint32_t* blocks, const 
 
 // L2-blocked paths for filters larger than L2 (sbbf_blocked.cu).
 struct BlockedPlan {
-  uint32_t parts = 0;             // filter slices
+  uint32_t parts = 0;             // filter slices (per super-slice when super_parts > 1)
   const uint64_t* d_bounds = nullptr;  // parts entries, global block ids
+  // Filters beyond 64 slices: super_parts exact block ranges, each blocked on
+  // its own (two-level path). Bounds are local block ids; the host copy has
+  // super_parts + 1 entries (the last = the shard's block count).
+  uint32_t super_parts = 1;
+  const uint64_t* d_super_bounds = nullptr;
+  std::vector<uint64_t> h_super_bounds;
 };
 cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
                            const uint64_t* hashes, uint64_t n, cudaStream_t s);

@@ -276,8 +276,10 @@ class ShardedFilter:
         self.last_exchange: dict = {}
         self.route = None
         fused_req = fused is True
+        # one rank owns every block: no routing at all unless asked for
+        self.direct = fused is None and self.world == 1 and isinstance(ops, CudaShardOps)
         if fused is None:
-            fused = isinstance(ops, CudaShardOps) and self._peer_capable(init)
+            fused = not self.direct and isinstance(ops, CudaShardOps) and self._peer_capable(init)
         if fused:
             if not isinstance(ops, CudaShardOps):
                 raise ValueError("fused routing needs the CUDA shard ops")
@@ -356,6 +358,9 @@ class ShardedFilter:
     # -- hot path -----------------------------------------------------------------
     def add_hashes(self, keys) -> None:
         """Insert this rank's batch (any keys; each is routed to its owner)."""
+        if self.direct:
+            self.ops.insert(self.shard, keys)
+            return
         if self.route is not None:
             self.route.dispatch(keys, self.total, self.ops._dev_bounds(self.bounds), keep_positions=False)
             self._barrier()
@@ -369,6 +374,8 @@ class ShardedFilter:
     def find_hashes(self, keys):
         """0/1 byte per key of this rank's batch, in the batch's order."""
         n = keys.numel()
+        if self.direct:
+            return self.ops.find(self.shard, keys)
         if self.route is not None:
             self.route.dispatch(keys, self.total, self.ops._dev_bounds(self.bounds), keep_positions=True)
             self._barrier()
@@ -442,7 +449,7 @@ def bench_main(args) -> dict | None:
     dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     cfg = W.CONFIGS[args.config]
     if args.config == 5:
-        N = L = int(getattr(args, "sample_keys", 1 << 25))
+        N = L = int(getattr(args, "sample_keys", 1 << 27))
         total = cfg.num_buckets
         workload = (f"BASELINE config 5 sample: 8 GiB filter ({total} blocks) sharded over {world} rank(s) "
                     f"by block range; per rank per step {N:,} inserts (splitmix64(9) positions "
@@ -460,7 +467,7 @@ def bench_main(args) -> dict | None:
     route = getattr(args, "route", "auto")
     f = ShardedFilter(total, fused=None if route == "auto" else route == "fused", max_batch=max(N, L))
     how = ("peer-memory windows over NVLink (fused dispatch, sbbf_route.cu)" if f.route is not None
-           else "NCCL all-to-all")
+           else "none (one rank owns every block)" if f.direct else "NCCL all-to-all")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     flush_rd = torch.zeros(64 << 20, dtype=torch.int32, device=dev)
 

@@ -225,6 +225,25 @@ def test_blocked_path_skew(cuda, oracle, nb, shape):
     assert np.array_equal(bits_to_bytes(bits, probes.size), want_res)
 
 
+@pytest.mark.parametrize("nb", [2**26, 2**26 + 12345])
+def test_blocked_two_level(cuda, oracle, nb):
+    """Filters beyond 64 slices of 16 MiB (> 1 GiB) take the two-level
+    blocked path: super-slices by exact block range, then slices."""
+    rng = np.random.default_rng(nb)
+    hs = rng.integers(0, 2**64, size=3_000_017, dtype=np.uint64)
+    probes = np.concatenate([hs[:500_000], rng.integers(0, 2**64, size=1_500_003, dtype=np.uint64)])
+    want = oracle.build(nb, hs)
+    f = SplitBlockFilter(nb)
+    f.set_insert_variant(_lib.INSERT_BLOCKED)
+    f.add_hashes(dev(hs, cuda))
+    assert np.array_equal(f.blocks(), want)
+    f.set_find_variant(_lib.FIND_BLOCKED)
+    want_res = oracle.find_hashes(want, probes)
+    assert np.array_equal(f.find_hashes(dev(probes, cuda)).cpu().numpy(), want_res)
+    bits = u32(f.find_hashes_bits(dev(probes, cuda)))
+    assert np.array_equal(bits_to_bytes(bits, probes.size), want_res)
+
+
 def test_64bit_block_offsets(cuda, oracle):
     """A filter larger than 2^32 words (> 16 GiB): offsets must be 64-bit."""
     nb = (1 << 29) + 12345          # 17.2 GB, 2^32+ 32-bit words

@@ -334,7 +334,13 @@ def test_fused_sharded_filter_world1(cuda, oracle):
     h = rng.integers(0, 2**64, size=700_000, dtype=np.uint64)
     look = np.concatenate([h[:5000], rng.integers(0, 2**64, size=300_000, dtype=np.uint64)])
     want = oracle.build(32768, h)
-    f = S.ShardedFilter(32768)
+    d = S.ShardedFilter(32768)                      # world 1 default: no routing at all
+    assert d.direct and d.route is None
+    d.add_hashes(torch.from_numpy(h.view(np.int64)).to(cuda))
+    assert np.array_equal(d.gather_blocks(), want)
+    assert np.array_equal(d.find_hashes(torch.from_numpy(look.view(np.int64)).to(cuda)).cpu().numpy(),
+                          oracle.find_hashes(want, look))
+    f = S.ShardedFilter(32768, fused=True)
     assert f.route is not None
     f.add_hashes(torch.from_numpy(h.view(np.int64)).to(cuda))
     assert np.array_equal(f.gather_blocks(), want)
@@ -347,7 +353,7 @@ def test_fused_sharded_filter_world1(cuda, oracle):
     os.environ["MASTER_PORT"] = str(free_port())
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=cuda)
     try:
-        g = S.ShardedFilter(32768)
+        g = S.ShardedFilter(32768, fused=True)
         assert g.route is not None
         g.add_hashes(torch.from_numpy(h.view(np.int64)).to(cuda))
         assert np.array_equal(g.gather_blocks(), want)
