@@ -172,6 +172,10 @@ int sbbf_gpu_hash_u64_keys(const uint64_t* d_keys, uint64_t n, uint64_t seed, ui
                            void* stream);
 int sbbf_gpu_hash_bytes(const uint8_t* d_data, const uint64_t* d_offsets, uint64_t n, uint64_t seed,
                         uint64_t* d_hashes, void* stream);
+/* hash_key(std::to_string(c), seed) for c = start .. start+n-1: the
+ * reference's byte-string experiment keys (KeyMode::kByteStrings,
+ * tools/harness.cpp:60-65), digits built on the device. */
+int sbbf_gpu_hash_counter_strings(uint64_t start, uint64_t n, uint64_t seed, uint64_t* d_hashes, void* stream);
 int sbbf_gpu_insert_keys_u64(sbbf_gpu_t* f, const uint64_t* d_keys, uint64_t n, uint64_t seed,
                              void* stream);
 int sbbf_gpu_find_keys_u64(const sbbf_gpu_t* f, const uint64_t* d_keys, uint64_t n, uint64_t seed,

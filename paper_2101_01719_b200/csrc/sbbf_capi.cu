@@ -645,6 +645,13 @@ int sbbf_gpu_hash_bytes(const uint8_t* d_data, const uint64_t* d_offsets, uint64
   return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "hash kernel");
 }
 
+int sbbf_gpu_hash_counter_strings(uint64_t start, uint64_t n, uint64_t seed, uint64_t* d_hashes, void* stream) {
+  if (n == 0) return SBBF_OK;
+  if (!d_hashes) return fail(SBBF_EINVAL, "null buffer");
+  cudaError_t e = sbbf::launch_hash_decimal(start, n, seed, d_hashes, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "hash kernel");
+}
+
 // Hash-then-dispatch for the paths without a fused kernel (blocked, forced
 // variants): the hashes go to stream-ordered scratch.
 static cudaError_t with_hashed(const uint64_t* keys, uint64_t n, uint64_t seed, cudaStream_t s,

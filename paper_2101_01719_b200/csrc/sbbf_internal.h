@@ -95,6 +95,7 @@ cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geo
 cudaError_t launch_hash_u64(const uint64_t* keys, uint64_t n, uint64_t seed, uint64_t* out, cudaStream_t s);
 cudaError_t launch_hash_bytes(const uint8_t* data, const uint64_t* offsets, uint64_t n, uint64_t seed,
                               uint64_t* out, cudaStream_t s);
+cudaError_t launch_hash_decimal(uint64_t start, uint64_t n, uint64_t seed, uint64_t* out, cudaStream_t s);
 cudaError_t launch_insert_keys(const DeviceInfo& di, bool test, uint32_t* blocks, const Geom& g,
                                const uint64_t* keys, uint64_t n, uint64_t seed, cudaStream_t s);
 cudaError_t launch_find_keys(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const uint64_t* keys,

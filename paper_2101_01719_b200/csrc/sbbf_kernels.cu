@@ -428,6 +428,24 @@ __global__ void hash_bytes_kernel(const uint8_t* __restrict__ data, const uint64
   }
 }
 
+// hash_key(std::to_string(counter), seed) for counters start .. start+n-1:
+// the reference's KeyMode::kByteStrings keys (tools/harness.cpp:60-65),
+// decimal digits built in registers, then XXH64 over them.
+__global__ void hash_decimal_kernel(uint64_t start, uint64_t n, uint64_t seed, uint64_t* __restrict__ out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint64_t c = start + i;
+    uint8_t rev[20], buf[24];
+    int len = 0;
+    do {
+      rev[len++] = static_cast<uint8_t>('0' + c % 10);
+      c /= 10;
+    } while (c);
+    for (int k = 0; k < len; ++k) buf[k] = rev[len - 1 - k];
+    out[i] = dev::xxh64_bytes(buf, static_cast<uint64_t>(len), seed);
+  }
+}
+
 std::atomic<uint64_t> g_launches{0};
 
 }  // namespace
@@ -445,6 +463,13 @@ cudaError_t launch_hash_bytes(const uint8_t* data, const uint64_t* offsets, uint
   note_launch();
   hash_bytes_kernel<<<static_cast<unsigned>(grid_for(n, 256, 148, 16)), 128, 0, s>>>(data, offsets, n, seed,
                                                                                        out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hash_decimal(uint64_t start, uint64_t n, uint64_t seed, uint64_t* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  note_launch();
+  hash_decimal_kernel<<<static_cast<unsigned>(grid_for(n, 256, 148, 16)), 128, 0, s>>>(start, n, seed, out);
   return cudaGetLastError();
 }
 

@@ -344,6 +344,16 @@ def hash_keys(keys, seed: int = 0, device: int = 0) -> "torch.Tensor":
     return out
 
 
+def hash_counter_strings(start: int, n: int, seed: int = 0, device: int = 0) -> "torch.Tensor":
+    """hash_key(std::to_string(c)) for c in [start, start + n) on device — the
+    reference's byte-string experiment keys (harness.cpp:60-65)."""
+    dev = torch.device("cuda", device)
+    out = torch.empty(n, dtype=torch.int64, device=dev)
+    check(_lib.lib().sbbf_gpu_hash_counter_strings(start, n, seed, C.c_void_p(out.data_ptr()) if n else None,
+                                                   _stream_ptr(device)), "sbbf_gpu_hash_counter_strings")
+    return out
+
+
 def block_index_batch(hashes: "torch.Tensor", num_buckets: int) -> "torch.Tensor":
     """filter.hpp:42 on device, for known-answer tests."""
     t = _dev_u64(hashes)

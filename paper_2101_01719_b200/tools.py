@@ -1,9 +1,14 @@
-"""Batch build / query from key files on the GPU — the reference's
-``sbbf build`` and ``sbbf query`` (tools/harness.cpp:247-304), plus the
-sizing model they use (core/src/model.cpp:78-103,170-212).
+"""The reference's ``sbbf`` toolkit commands on the GPU (tools/main.cpp,
+tools/harness.cpp): ``build`` / ``query`` from key files (harness.cpp:247-304),
+``fpp-sim`` (run_fpp_sim, harness.cpp:67-109), ``bench`` (run_bench,
+harness.cpp:132-245) and ``size`` (model.cpp:187-212), with the sizing model
+they use (model.cpp:78-103,170-212) restated bit-exactly.
 
     python -m paper_2101_01719_b200.tools build KEYS OUT.sbbf --fpp 0.01
     python -m paper_2101_01719_b200.tools query OUT.sbbf KEYS      # maybe/absent per line
+    python -m paper_2101_01719_b200.tools fpp-sim --ndv 1000000 --bytes 1048576 [--key-mode strings]
+    python -m paper_2101_01719_b200.tools bench --ndv 1000000 --bytes 1048576
+    python -m paper_2101_01719_b200.tools size --ndv 1000000 --fpp 0.01
 
 Keys are the newline-separated segments of the file (a final segment without
 a newline is a key; read_key_lines, harness.cpp:247-260), hashed with XXH64
@@ -18,7 +23,7 @@ import sys
 
 import numpy as np
 
-from .filter import SplitBlockFilter, hash_keys
+from .filter import PersistError, SplitBlockFilter, hash_keys
 
 KHASHER_XXH64 = 1
 
@@ -92,6 +97,80 @@ def size_for(ndv: int, target_fpp: float) -> int:
     return buckets
 
 
+EFFICIENT_FPP_MIN, EFFICIENT_FPP_MAX = 0.004, 0.19   # model.hpp:11-12
+
+
+def sizing(ndv: int, target_fpp: float) -> dict:
+    """model.cpp:187-212 SizingResult."""
+    if not (math.isfinite(target_fpp) and 0.0 < target_fpp < 1.0):
+        raise ValueError("target_fpp must lie strictly between 0 and 1")
+    buckets = size_for(ndv, target_fpp)
+    a = ndv / buckets
+    return {"num_buckets": buckets, "bytes": buckets * 32, "a": a, "predicted_fpp": sbbf_fpp(a),
+            "outside_efficient_range": target_fpp < EFFICIENT_FPP_MIN or target_fpp > EFFICIENT_FPP_MAX}
+
+
+def run_bench(ndv: int, filter_bytes: int, seed: int = 1, reps: int = 5, huge_ok: bool = False,
+              device: int = 0) -> dict:
+    """run_bench (harness.cpp:132-245) on the GPU: hashes of the counters
+    [0, ndv) pre-generated on the device, then `reps` fresh-filter inserts and
+    full lookups, device-timed (median); every inserted key must be found;
+    the fpp columns come from 100,000 negative probes."""
+    import statistics
+
+    import torch
+
+    from .fppsim import HUGE_NDV_THRESHOLD, NEGATIVE_COUNTER_BASE
+    from .filter import hash_u64_keys
+    if ndv > NEGATIVE_COUNTER_BASE:
+        raise ValueError("--ndv must not exceed 2^32 (the negative-query key space starts there)")
+    if ndv > HUGE_NDV_THRESHOLD and not huge_ok:
+        raise ValueError("--ndv beyond 10M is paper scale; pass --huge to allow it")
+    if reps < 3:
+        raise ValueError("--reps must be at least 3")
+    if ndv < 1:
+        raise ValueError("--ndv must be positive")
+    if filter_bytes < 32:
+        raise ValueError("--bytes must be at least 32 (one block)")
+    buckets = filter_bytes // 32
+    dev = torch.device("cuda", device)
+    hashes = hash_u64_keys(torch.arange(ndv, dtype=torch.int64, device=dev), seed)
+    results = torch.empty(ndv, dtype=torch.uint8, device=dev)
+    f = SplitBlockFilter(buckets, hasher_id=KHASHER_XXH64, device=device)
+    ti, tl = [], []
+    for _ in range(reps):
+        f.clear()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        f.add_hashes(hashes)
+        e[1].record()
+        f.find_hashes(hashes, results)
+        e[2].record()
+        torch.cuda.synchronize(dev)
+        ti.append(e[0].elapsed_time(e[1]) * 1e-3)
+        tl.append(e[1].elapsed_time(e[2]) * 1e-3)
+    found = int(results.sum(dtype=torch.int64).item())
+    if found != ndv:
+        raise RuntimeError("benchmark lookups lost inserted keys")
+    probes = hash_u64_keys(torch.arange(NEGATIVE_COUNTER_BASE, NEGATIVE_COUNTER_BASE + 100_000,
+                                        dtype=torch.int64, device=dev), seed)
+    fpp = int(f.find_hashes(probes).sum(dtype=torch.int64).item()) / 100_000
+    model = sbbf_fpp(ndv / buckets)
+    base = {"ndv": ndv, "filter_bytes": buckets * 32, "threads": 1, "measured_fpp": fpp, "model_fpp": model}
+    ins = dict(base, op="insert", wall_time_s=statistics.median(ti))
+    look = dict(base, op="lookup", wall_time_s=statistics.median(tl))
+    for r in (ins, look):
+        r["million_ops_per_sec"] = ndv / r["wall_time_s"] / 1e6
+    return {"insert": ins, "lookup": look, "device": torch.cuda.get_device_name(dev)}
+
+
+def _print_report(r: dict) -> None:
+    """main.cpp print_report format."""
+    print(f"{r['op']:<8} ndv={r['ndv']} bytes={r['filter_bytes']} threads={r['threads']} "
+          f"rate={r['million_ops_per_sec']:.1f} M/s measured_fpp={r['measured_fpp']:.6f} "
+          f"model_fpp={r['model_fpp']:.6f} wall={r['wall_time_s']:.3f}s")
+
+
 def read_key_lines(path: str) -> list[bytes]:
     """harness.cpp:247-260 (std::getline semantics)."""
     with open(path, "rb") as fh:
@@ -134,22 +213,83 @@ def run_query(filter_file: str, key_file: str, out=sys.stdout, device: int = 0) 
 
 
 def main(argv=None) -> int:
+    """Exit codes as main.cpp: 0 ok, 1 usage, 2 I/O."""
+    import json
+
     ap = argparse.ArgumentParser(prog="sbbf-b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
-    b = sub.add_parser("build")
+    b = sub.add_parser("build", help="hash a newline-delimited key file into a filter image")
     b.add_argument("keys")
     b.add_argument("out")
     b.add_argument("--fpp", type=float, default=0.01)
-    q = sub.add_parser("query")
+    q = sub.add_parser("query", help="print maybe/absent for each key in a file ('absent' is definitive)")
     q.add_argument("filter")
     q.add_argument("keys")
+    fs = sub.add_parser("fpp-sim", help="insert ndv keys, probe disjoint keys, compare measured vs model fpp")
+    fs.add_argument("--ndv", type=int, required=True)
+    fs.add_argument("--bytes", type=int)
+    fs.add_argument("--fpp", type=float)
+    fs.add_argument("--queries", type=int, default=1_000_000)
+    fs.add_argument("--seed", type=int, default=1)
+    fs.add_argument("--key-mode", default="random64")
+    fs.add_argument("--huge", action="store_true")
+    fs.add_argument("--json", action="store_true")
+    sz = sub.add_parser("size", help="smallest filter meeting a target fpp")
+    sz.add_argument("--ndv", type=int, required=True)
+    sz.add_argument("--fpp", type=float, required=True)
+    sz.add_argument("--json", action="store_true")
+    bn = sub.add_parser("bench", help="time bulk insert and lookup over pre-generated hashes (GPU)")
+    bn.add_argument("--ndv", type=int, required=True)
+    bn.add_argument("--bytes", type=int, required=True)
+    bn.add_argument("--seed", type=int, default=1)
+    bn.add_argument("--reps", type=int, default=5)
+    bn.add_argument("--huge", action="store_true")
+    bn.add_argument("--json", action="store_true")
     args = ap.parse_args(argv)
-    if args.cmd == "build":
-        r = run_build(args.keys, args.out, args.fpp)
-        print(f"built {r['num_buckets']} buckets ({r['bytes']} bytes) for {r['distinct_hashes']} distinct "
-              f"of {r['keys_read']} keys, predicted fpp {r['predicted_fpp']:.6g}", file=sys.stderr)
-    else:
-        run_query(args.filter, args.keys)
+    try:
+        if args.cmd == "build":
+            r = run_build(args.keys, args.out, args.fpp)
+            print(f"built {r['num_buckets']} buckets ({r['bytes']} bytes) for {r['distinct_hashes']} distinct "
+                  f"of {r['keys_read']} keys, predicted fpp {r['predicted_fpp']:.6g}", file=sys.stderr)
+        elif args.cmd == "query":
+            r = run_query(args.filter, args.keys)
+            print(f"{r['keys']} keys: {r['maybe']} maybe, {r['keys'] - r['maybe']} absent", file=sys.stderr)
+        elif args.cmd == "fpp-sim":
+            from .fppsim import fpp_sim
+            r = fpp_sim(args.ndv, args.bytes, args.queries, args.seed, huge_ok=args.huge, target_fpp=args.fpp,
+                        key_mode=args.key_mode)
+            r.pop("filter", None)
+            r["threads"] = 1
+            if args.json:
+                print(json.dumps(r, indent=2))
+            else:
+                _print_report(r)
+                ratio = r["measured_fpp"] / r["model_fpp"] if r["model_fpp"] > 0 else 0.0
+                print(f"measured/model fpp ratio: {ratio:.3f}")
+        elif args.cmd == "size":
+            r = sizing(args.ndv, args.fpp)
+            if args.json:
+                print(json.dumps(r, indent=2))
+            else:
+                print(f"ndv={args.ndv} target_fpp={args.fpp:g} -> buckets={r['num_buckets']} bytes={r['bytes']} "
+                      f"(a={r['a']:.3f}, predicted fpp={r['predicted_fpp']:.6f})")
+            if r["outside_efficient_range"]:
+                print(f"warning: target fpp {args.fpp:g} is outside the efficient range [0.4%, 19%] of the "
+                      "eight-lane layout; the filter will be correct but oversized relative to other designs",
+                      file=sys.stderr)
+        else:
+            r = run_bench(args.ndv, args.bytes, args.seed, args.reps, args.huge)
+            if args.json:
+                print(json.dumps(r, indent=2))
+            else:
+                _print_report(r["insert"])
+                _print_report(r["lookup"])
+    except (PersistError, OSError) as exc:  # main.cpp: PersistError -> kExitIo
+        print(f"error: {exc}", file=sys.stderr)
+        return 2
+    except ValueError as exc:                # UsageError / std::domain_error -> kExitUsage
+        print(f"error: {exc}", file=sys.stderr)
+        return 1
     return 0
 
 

@@ -104,3 +104,66 @@ def test_fpp_sim_matches_reference(cuda, oracle, golden, idx):
              (100_000_000, 134_217_728): (0.00728, 0.01092)}
     lo, hi = bands.get((r["ndv"], r["filter_bytes"]), (0.0, 1.0))
     assert lo <= out["measured_fpp"] <= hi
+
+
+def test_fppsim_sizing_arguments():
+    """harness.cpp:33-47: exactly one of --bytes / --fpp; --fpp in (0, 1);
+    --key-mode random64 | strings. All raised before any device work."""
+    from paper_2101_01719_b200.fppsim import fpp_sim, resolve_buckets
+    from paper_2101_01719_b200.tools import size_for
+    with pytest.raises(ValueError):
+        fpp_sim(10, 1 << 20, target_fpp=0.01)    # both
+    with pytest.raises(ValueError):
+        fpp_sim(10)                              # neither
+    with pytest.raises(ValueError):
+        fpp_sim(10, target_fpp=1.5)
+    with pytest.raises(ValueError):
+        fpp_sim(10, 1 << 20, key_mode="words")
+    assert resolve_buckets(100_000, None, 0.01) == size_for(100_000, 0.01)
+    assert resolve_buckets(0, None, 0.01) == 1
+    assert resolve_buckets(5, 100, None) == 3
+
+
+@pytest.mark.gpu
+def test_device_counter_strings(cuda, oracle):
+    """hash_key(std::to_string(c)) on the device (KeyMode::kByteStrings)."""
+    from paper_2101_01719_b200.filter import hash_counter_strings
+    for start in (0, 99_990, 2**32 - 5, 2**64 - 20):
+        for seed in (0, 1, 12345):
+            got = hash_counter_strings(start, 20, seed).cpu().numpy().view(np.uint64)
+            want = [oracle.xxh64(str(start + i).encode(), seed) for i in range(20)]
+            assert [int(x) for x in got] == want, (start, seed)
+
+
+@pytest.mark.gpu
+def test_fppsim_strings_and_target_fpp(cuda, oracle):
+    from paper_2101_01719_b200.fppsim import NEGATIVE_COUNTER_BASE, fpp_sim
+    from paper_2101_01719_b200.tools import size_for
+    ndv, q, seed = 20_000, 50_000, 3
+    r = fpp_sim(ndv, 65_536, q, seed, key_mode="strings")
+    ins = np.array([oracle.xxh64(str(c).encode(), seed) for c in range(ndv)], np.uint64)
+    probes = np.array([oracle.xxh64(str(NEGATIVE_COUNTER_BASE + i).encode(), seed) for i in range(q)], np.uint64)
+    blocks = oracle.build(65_536 // 32, ins)
+    assert r["false_positives"] == int(oracle.find_hashes(blocks, probes).sum())
+    assert np.array_equal(r["filter"].blocks(), blocks)
+    t = fpp_sim(100_000, None, 10_000, 1, target_fpp=0.01)
+    assert t["filter_bytes"] == size_for(100_000, 0.01) * 32
+
+
+@pytest.mark.gpu
+def test_tools_bench_and_cli(cuda, oracle, capsys):
+    from paper_2101_01719_b200 import tools
+    from paper_2101_01719_b200.fppsim import NEGATIVE_COUNTER_BASE
+    ndv, nbytes, seed = 200_000, 262_144, 7
+    r = tools.run_bench(ndv, nbytes, seed, reps=3)
+    ins = np.array([oracle.xxh64(c.to_bytes(8, "little"), seed) for c in range(ndv)], np.uint64)
+    probes = np.array([oracle.xxh64((NEGATIVE_COUNTER_BASE + i).to_bytes(8, "little"), seed)
+                       for i in range(100_000)], np.uint64)
+    fp = int(oracle.find_hashes(oracle.build(nbytes // 32, ins), probes).sum())
+    assert r["insert"]["measured_fpp"] == fp / 100_000 == r["lookup"]["measured_fpp"]
+    assert r["lookup"]["million_ops_per_sec"] > 0 and r["insert"]["op"] == "insert"
+    assert tools.main(["bench", "--ndv", "1000", "--bytes", "4096", "--reps", "3"]) == 0
+    assert tools.main(["fpp-sim", "--ndv", "1000", "--bytes", "4096", "--queries", "1000"]) == 0
+    out = capsys.readouterr().out
+    assert out.count("insert   ndv=1000") == 1 and "measured/model fpp ratio:" in out
+    assert tools.main(["bench", "--ndv", "1000", "--bytes", "4096", "--reps", "2"]) == 1

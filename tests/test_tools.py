@@ -66,3 +66,20 @@ def test_build_and_query_match_reference(cuda, oracle, golden, tmp_path, fpp):
     ans = np.array([1 if x == "maybe" else 0 for x in lines], np.uint8)
     assert q["maybe"] == run["maybe"] and len(lines) == len(probes)
     assert hashlib.sha256(ans.tobytes()).hexdigest() == run["answers_sha256"]
+
+
+def test_size_cli(reference, capsys):
+    """`sbbf size` (main.cpp cmd_size): bit-exact sizing, output format,
+    efficient-range warning, usage errors -> exit 1."""
+    from paper_2101_01719_b200 import tools
+    assert tools.main(["size", "--ndv", "1000000", "--fpp", "0.01"]) == 0
+    out = capsys.readouterr()
+    nb = tools.size_for(1_000_000, 0.01)
+    assert out.out.strip() == (f"ndv=1000000 target_fpp=0.01 -> buckets={nb} bytes={nb * 32} "
+                               f"(a={1_000_000 / nb:.3f}, predicted fpp={tools.sbbf_fpp(1_000_000 / nb):.6f})")
+    assert out.err == ""
+    assert tools.main(["size", "--ndv", "1000", "--fpp", "0.5"]) == 0
+    assert "outside the efficient range" in capsys.readouterr().err
+    assert tools.main(["size", "--ndv", "1000", "--fpp", "1.5"]) == 1
+    r = tools.sizing(123_457, 0.02)
+    assert r["num_buckets"] == reference.lib.ref_size_for(123_457, 0.02)
