@@ -176,6 +176,13 @@ int sbbf_gpu_hash_bytes(const uint8_t* d_data, const uint64_t* d_offsets, uint64
  * reference's byte-string experiment keys (KeyMode::kByteStrings,
  * tools/harness.cpp:60-65), digits built on the device. */
 int sbbf_gpu_hash_counter_strings(uint64_t start, uint64_t n, uint64_t seed, uint64_t* d_hashes, void* stream);
+/* Monte-Carlo false-positive oracle (sbbf_fpp_mc, model.cpp:105-128) on the
+ * GPU: `blocks` blocks each filled with Poisson(a) hashes from the block's
+ * preimage interval, then `trials` uniform probes; *fpp = hits / trials.
+ * Same distributions as the reference, counter-based per-block streams
+ * (seed-reproducible, not the reference's mt19937_64 draws). Errors as the
+ * reference's domain_error cases: a < 0, a > 500, blocks or trials == 0. */
+int sbbf_gpu_fpp_mc(double a, uint64_t blocks, uint64_t trials, uint64_t seed, int device, double* fpp);
 int sbbf_gpu_insert_keys_u64(sbbf_gpu_t* f, const uint64_t* d_keys, uint64_t n, uint64_t seed,
                              void* stream);
 int sbbf_gpu_find_keys_u64(const sbbf_gpu_t* f, const uint64_t* d_keys, uint64_t n, uint64_t seed,

@@ -78,6 +78,7 @@ PROTOTYPES = {
     "sbbf_scatter_u8": (_i, [_vp, _vp, _u64, _vp, _vp]),
     "sbbf_pack_bits": (_i, [_vp, _u64, _vp, _vp]),
     "sbbf_gpu_hash_counter_strings": (_i, [_u64, _u64, _u64, _vp, _vp]),
+    "sbbf_gpu_fpp_mc": (_i, [C.c_double, _u64, _u64, _u64, _i, C.POINTER(C.c_double)]),
     "sbbf_route_window_bytes": (_u64, [_u32, _u64]),
     "sbbf_route_create": (_i, [_u32, _u32, _u64, _i, C.POINTER(_vp)]),
     "sbbf_route_destroy": (None, [_vp]),

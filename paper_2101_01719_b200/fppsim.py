@@ -95,3 +95,20 @@ def fpp_sim(ndv: int, filter_bytes: int | None = None, negative_queries: int = 1
         "wall_time_s": wall,
         "filter": f,
     }
+
+
+def sbbf_fpp_mc(a: float, blocks: int, trials: int, seed: int = 0, device: int = 0) -> float:
+    """The reference's Monte-Carlo oracle (model.cpp:105-128) on the GPU:
+    Poisson(a) keys per block drawn from the block's preimage interval, then
+    `trials` uniform probes. Counter-based per-block streams (not the
+    reference's mt19937_64 draws): the same experiment, seed-reproducible.
+    Raises ValueError where the reference throws std::domain_error."""
+    import ctypes as C
+
+    from . import _lib
+    out = C.c_double(0.0)
+    rc = _lib.lib().sbbf_gpu_fpp_mc(float(a), int(blocks), int(trials), int(seed), int(device), C.byref(out))
+    if rc == _lib.SBBF_EINVAL:
+        raise ValueError(_lib.lib().sbbf_gpu_last_error().decode())
+    _lib.check(rc, "sbbf_gpu_fpp_mc")
+    return out.value

@@ -167,3 +167,26 @@ def test_tools_bench_and_cli(cuda, oracle, capsys):
     out = capsys.readouterr().out
     assert out.count("insert   ndv=1000") == 1 and "measured/model fpp ratio:" in out
     assert tools.main(["bench", "--ndv", "1000", "--bytes", "4096", "--reps", "2"]) == 1
+
+
+@pytest.mark.gpu
+def test_fpp_mc_oracle(cuda):
+    """The Monte-Carlo oracle on the GPU, checked the way the reference checks
+    its own (model_test.cpp:174-207), plus one run at scale."""
+    import math
+
+    from paper_2101_01719_b200.fppsim import sbbf_fpp, sbbf_fpp_mc
+    assert sbbf_fpp_mc(0.0, 64, 10_000, 1) == 0.0
+    assert sbbf_fpp_mc(26.0, 256, 20_000, 77) == sbbf_fpp_mc(26.0, 256, 20_000, 77)
+    for a in (20.0, 26.0):
+        series = sbbf_fpp(a)
+        mean = sum(sbbf_fpp_mc(a, 4096, 100_000, 1000 + r) for r in range(5)) / 5
+        se = math.sqrt(series * (1.0 - series) / 100_000)
+        assert abs(mean - series) <= 3.0 * se, (a, mean, series)
+    a = 24.4140625                     # config 1 density
+    got = sbbf_fpp_mc(a, 1 << 24, 100_000_000, 5)
+    se = math.sqrt(sbbf_fpp(a) * (1 - sbbf_fpp(a)) / 1e8)
+    assert abs(got - sbbf_fpp(a)) <= 4.0 * se, (got, sbbf_fpp(a))
+    for bad in ((-1.0, 16, 100), (5.0, 0, 100), (5.0, 16, 0), (501.0, 16, 100)):
+        with pytest.raises(ValueError):
+            sbbf_fpp_mc(*bad)
