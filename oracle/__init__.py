@@ -259,6 +259,10 @@ class Reference:
                                   C.POINTER(C.c_uint32)]
         L.ref_sbbf_fpp.restype = C.c_double
         L.ref_sbbf_fpp.argtypes = [C.c_double]
+        L.ref_standard_bloom_fpp.restype = C.c_double
+        L.ref_standard_bloom_fpp.argtypes = [C.c_double, C.c_uint]
+        L.ref_optimal_bloom_k.restype = C.c_uint
+        L.ref_optimal_bloom_k.argtypes = [C.c_double]
         L.ref_size_for.restype = C.c_uint64
         L.ref_size_for.argtypes = [C.c_uint64, C.c_double]
         L.ref_time_build_probe.argtypes = [C.c_uint64, _u64p, C.c_uint64, _u64p, C.c_uint64, _u8p,

@@ -159,6 +159,8 @@ void ref_fpp_sim(uint64_t ndv, uint64_t num_buckets, uint64_t queries, uint64_t 
 
 // model.cpp:78-103,187-212 (sbbf_fpp, size_for) for the build tool's sizing.
 double ref_sbbf_fpp(double a) { return sbbf::sbbf_fpp(a); }
+double ref_standard_bloom_fpp(double bits_per_key, unsigned k) { return sbbf::standard_bloom_fpp(bits_per_key, k); }
+unsigned ref_optimal_bloom_k(double bits_per_key) { return sbbf::optimal_bloom_k(bits_per_key); }
 
 uint64_t ref_size_for(uint64_t ndv, double target_fpp) {
   try {

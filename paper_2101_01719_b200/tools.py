@@ -1,8 +1,9 @@
 """The reference's ``sbbf`` toolkit commands on the GPU (tools/main.cpp,
 tools/harness.cpp): ``build`` / ``query`` from key files (harness.cpp:247-304),
 ``fpp-sim`` (run_fpp_sim, harness.cpp:67-109), ``bench`` (run_bench,
-harness.cpp:132-245) and ``size`` (model.cpp:187-212), with the sizing model
-they use (model.cpp:78-103,170-212) restated bit-exactly.
+harness.cpp:132-245), ``size`` (model.cpp:187-212) and ``model``
+(run_model, harness.cpp:110-129), with the model they use (model.cpp:78-236)
+restated bit-exactly.
 
     python -m paper_2101_01719_b200.tools build KEYS OUT.sbbf --fpp 0.01
     python -m paper_2101_01719_b200.tools query OUT.sbbf KEYS      # maybe/absent per line
@@ -108,6 +109,55 @@ def sizing(ndv: int, target_fpp: float) -> dict:
     a = ndv / buckets
     return {"num_buckets": buckets, "bytes": buckets * 32, "a": a, "predicted_fpp": sbbf_fpp(a),
             "outside_efficient_range": target_fpp < EFFICIENT_FPP_MIN or target_fpp > EFFICIENT_FPP_MAX}
+
+
+WITHIN_2X_BOUND = 2.1   # harness.hpp:55
+
+
+def standard_bloom_fpp(bits_per_key: float, k: int) -> float:
+    """model.cpp:130-140."""
+    if not math.isfinite(bits_per_key) or bits_per_key <= 0.0:
+        raise ValueError("bits_per_key must be positive")
+    if k < 1:
+        raise ValueError("k must be at least 1")
+    return math.pow(1.0 - math.exp(-float(k) / bits_per_key), float(k))
+
+
+def optimal_bloom_k(bits_per_key: float) -> int:
+    """model.cpp:142-158: best integer k over 1..max(16, ceil(bpk*ln2)+2)."""
+    if not math.isfinite(bits_per_key) or bits_per_key <= 0.0:
+        raise ValueError("bits_per_key must be positive")
+    k_max = max(16, int(math.ceil(bits_per_key * math.log(2))) + 2)
+    best_k, best = 1, standard_bloom_fpp(bits_per_key, 1)
+    for k in range(2, k_max + 1):
+        f = standard_bloom_fpp(bits_per_key, k)
+        if f < best:
+            best, best_k = f, k
+    return best_k
+
+
+def run_model(a_min: float = 20.0, a_max: float = 52.0, steps: int = 65) -> dict:
+    """run_model + within_2x_report (harness.cpp:110-129, model.cpp:214-236):
+    the sbbf fpp against a same-space standard Bloom filter (optimal k)."""
+    if not (a_min >= 0.0) or a_min > a_max:
+        raise ValueError("--a-min must satisfy 0 <= a-min <= a-max")
+    if steps < 1:
+        raise ValueError("--steps must be at least 1")
+    if steps == 1 and a_min != a_max:
+        raise ValueError("--steps 1 needs --a-min equal to --a-max")
+    rows, max_ratio = [], 0.0
+    for i in range(steps):
+        t = 0.0 if steps == 1 else i / (steps - 1)
+        a = a_min + t * (a_max - a_min)
+        row = {"a": a, "bits_per_key": 0.0, "sbbf_fpp": 0.0, "standard_fpp": 0.0, "ratio": 0.0}
+        if a > 0.0:
+            bpk = 256.0 / a
+            sb = sbbf_fpp(a)
+            st = standard_bloom_fpp(bpk, optimal_bloom_k(bpk))
+            row.update(bits_per_key=bpk, sbbf_fpp=sb, standard_fpp=st, ratio=sb / st)
+            max_ratio = max(max_ratio, row["ratio"])
+        rows.append(row)
+    return {"rows": rows, "max_ratio": max_ratio}
 
 
 def run_bench(ndv: int, filter_bytes: int, seed: int = 1, reps: int = 5, huge_ok: bool = False,
@@ -234,6 +284,13 @@ def main(argv=None) -> int:
     fs.add_argument("--key-mode", default="random64")
     fs.add_argument("--huge", action="store_true")
     fs.add_argument("--json", action="store_true")
+    md = sub.add_parser("model", help="tabulate sbbf fpp against a same-space standard Bloom filter")
+    md.add_argument("--a-min", type=float, default=20.0)
+    md.add_argument("--a-max", type=float, default=52.0)
+    md.add_argument("--steps", type=int, default=65)
+    md.add_argument("--csv")
+    md.add_argument("--json", action="store_true")
+    md.add_argument("--assert-2x", action="store_true")
     sz = sub.add_parser("size", help="smallest filter meeting a target fpp")
     sz.add_argument("--ndv", type=int, required=True)
     sz.add_argument("--fpp", type=float, required=True)
@@ -266,6 +323,26 @@ def main(argv=None) -> int:
                 _print_report(r)
                 ratio = r["measured_fpp"] / r["model_fpp"] if r["model_fpp"] > 0 else 0.0
                 print(f"measured/model fpp ratio: {ratio:.3f}")
+        elif args.cmd == "model":
+            r = run_model(args.a_min, args.a_max, args.steps)
+            if args.json:
+                print(json.dumps(r, indent=2))
+            else:
+                print(f"{'a':>10} {'bits_per_key':>14} {'sbbf_fpp':>14} {'standard_fpp':>14} {'ratio':>10}")
+                for row in r["rows"]:
+                    print(f"{row['a']:10.3f} {row['bits_per_key']:14.4f} {row['sbbf_fpp']:14.6g} "
+                          f"{row['standard_fpp']:14.6g} {row['ratio']:10.4f}")
+                print(f"max ratio: {r['max_ratio']:.4f}")
+            if args.csv:
+                with open(args.csv, "w") as fh:
+                    fh.write("a,bits_per_key,sbbf_fpp,standard_fpp,ratio\n")
+                    for row in r["rows"]:
+                        fh.write(",".join(f"{row[k]:.10g}" for k in
+                                          ("a", "bits_per_key", "sbbf_fpp", "standard_fpp", "ratio")) + "\n")
+            if args.assert_2x and r["max_ratio"] > WITHIN_2X_BOUND:
+                print(f"FAIL: max sbbf/standard fpp ratio {r['max_ratio']:.4f} exceeds {WITHIN_2X_BOUND:.2f}",
+                      file=sys.stderr)
+                return 3
         elif args.cmd == "size":
             r = sizing(args.ndv, args.fpp)
             if args.json:

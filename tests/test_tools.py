@@ -83,3 +83,24 @@ def test_size_cli(reference, capsys):
     assert tools.main(["size", "--ndv", "1000", "--fpp", "1.5"]) == 1
     r = tools.sizing(123_457, 0.02)
     assert r["num_buckets"] == reference.lib.ref_size_for(123_457, 0.02)
+
+
+def test_model_cli_matches_reference(reference, capsys, tmp_path):
+    """`sbbf model` (run_model / within_2x_report): every row bit-exact with
+    the reference's standard_bloom_fpp / optimal_bloom_k / sbbf_fpp."""
+    from paper_2101_01719_b200 import tools
+    r = tools.run_model()
+    assert len(r["rows"]) == 65
+    for row in r["rows"]:
+        bpk = 256.0 / row["a"]
+        k = reference.lib.ref_optimal_bloom_k(bpk)
+        assert tools.optimal_bloom_k(bpk) == k
+        assert row["standard_fpp"] == reference.lib.ref_standard_bloom_fpp(bpk, k)
+        assert row["sbbf_fpp"] == reference.lib.ref_sbbf_fpp(row["a"])
+    assert r["max_ratio"] <= tools.WITHIN_2X_BOUND
+    csv = tmp_path / "m.csv"
+    assert tools.main(["model", "--assert-2x", "--csv", str(csv)]) == 0
+    assert csv.read_text().splitlines()[0] == "a,bits_per_key,sbbf_fpp,standard_fpp,ratio"
+    assert capsys.readouterr().out.splitlines()[-1] == f"max ratio: {r['max_ratio']:.4f}"
+    assert tools.main(["model", "--a-min", "5", "--a-max", "1"]) == 1
+    assert tools.main(["model", "--a-min", "60", "--a-max", "200", "--steps", "9", "--assert-2x"]) in (0, 3)
