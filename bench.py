@@ -449,6 +449,15 @@ def roofline(res: dict, l2_sector_gs: float | None, hbm_peak: float, peak_note: 
           "traffic": None, "bytes_per_key": per_key, "bytes_note": note, "peak_note": peak_note}
     if l2_sector_gs:
         rate = L / t / 1e9
+        # the resource that actually binds this kernel, for a reader of `frac`
+        rf["binding"] = ({"resource": "L2 random-sector request rate (filter L2-resident)",
+                          "frac": rate / l2_sector_gs} if resident and not blocked else
+                         {"resource": "DRAM random-sector rate (direct probes beyond L2)",
+                          "frac": rate / l2_sector_gs} if not blocked else
+                         {"resource": "blocked passes: partition issue rate + L2-served probes "
+                                      "(profiles/r1_blocked_partition.md)",
+                          "vs_direct_ceiling": rate / l2_sector_gs,
+                          "note": "lookups/s over the DRAM random-sector ceiling that bounds direct probes"})
         rf["random_sector"] = {"lookup_gkeys_s": rate, "ceiling_gsectors_s": l2_sector_gs,
                                "frac": rate / l2_sector_gs,
                                "note": "one 32-B sector per key vs the measured random-sector "

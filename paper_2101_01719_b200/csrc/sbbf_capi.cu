@@ -90,7 +90,6 @@ namespace {
 
 constexpr uint64_t kSliceBytes = 16ull << 20;  // blocked path: one slice + chunk bitmap stay in L2
 
-bool beyond_l2(const sbbf_gpu* f) { return f->nb * 32 > f->di.l2_bytes / 2; }
 // Blocking pays once random probes mostly miss L2: a ~L2-sized filter (config
 // 3) already hits L2 often enough that the partition passes cost more than
 // they save (profiles/r1_blocked_partition.md).
@@ -100,12 +99,14 @@ bool blocked_pays(const sbbf_gpu* f, uint64_t n) {
 
 int resolve_insert(const sbbf_gpu* f, uint64_t n) {
   if (f->insert_variant != SBBF_INSERT_AUTO) return f->insert_variant;
-  // L2-resident filters are bound by the L2 atomic unit (op count): plain
-  // 64-bit reds. Beyond L2, a batch of at least half a key per block is
-  // grouped by filter slice first (blocked path, sbbf_blocked.cu); smaller
-  // batches load the lane pair first (a load fills L2 faster than a missing
-  // atomic, and duplicates/hot keys skip the atomic entirely).
-  if (!beyond_l2(f)) return SBBF_INSERT_WIDE;
+  // Up to ~2x L2 (config 3's 128 MiB: much of it stays L2-resident) the
+  // inserts are bound by the L2 atomic unit (op count): plain 64-bit reds
+  // (51.5 vs 45.4 G/s with test-before-set, scripts/variant_ab.py). Beyond,
+  // a batch of at least half a key per block is grouped by filter slice
+  // first (blocked path, sbbf_blocked.cu); smaller batches load the lane pair
+  // first (a load fills L2 faster than a missing atomic, and duplicates /
+  // hot keys skip the atomic entirely: 22 vs 8 G/s on config 4).
+  if (f->nb * 32 <= 2 * static_cast<uint64_t>(f->di.l2_bytes)) return SBBF_INSERT_WIDE;
   return blocked_pays(f, n) ? SBBF_INSERT_BLOCKED : SBBF_INSERT_WIDE_TEST;
 }
 
