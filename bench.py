@@ -195,6 +195,7 @@ def run_config_device(cid: int, steps: int, warmup: int, device, collect_parity=
         "ms_per_step": statistics.mean(t_step), "ms_insert": statistics.mean(t_ins),
         "ms_lookup": statistics.mean(t_find), "ms_step_min": min(t_step),
         "ms_step_split": statistics.mean(a + b for a, b in zip(t_ins, t_find)),
+        "ms_steps": [round(t, 4) for t in t_step],
         "launches_per_step": launches / steps,
         "insert_variant": f.resolved_variants(chunk)[0], "find_variant": f.resolved_variants(L)[1],
     }

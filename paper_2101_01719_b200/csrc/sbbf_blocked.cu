@@ -7,7 +7,7 @@
 // profiles/r1_microbench_*.log). The blocked path trades that for streaming:
 //
 //   1. chunk_scatter: every 4096-key chunk of the batch is rewritten
-//      bucket-major (bucket = filter slice of ~16 MiB) inside its own region,
+//      bucket-major (bucket = filter slice of ~32 MiB) inside its own region,
 //      with 16-bit bucket offsets per chunk (and, for lookups, each slot's
 //      16-bit source position): one read, coalesced writes, no count pass;
 //   2. segment_kernel: bucket by bucket over every chunk's run of that
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
 
 // Probe (lookup) or OR (insert) bucket by bucket: CTA blockIdx handles bucket
 // b = blockIdx / groups over chunks [grp*G, grp*G + G); CTAs run in blockIdx
-// order, so the keys in flight all fall in one or two ~16 MiB filter slices
+// order, so the keys in flight all fall in one or two ~32 MiB filter slices
 // and their sectors / atomics are served by L2. Each warp works on 4 chunk
 // segments at a time (independent loads in flight); a segment is the
 // chunk's contiguous run of bucket b. Lookups store one answer byte per
@@ -836,7 +836,7 @@ cudaError_t find_chunk(const DeviceInfo& di, const uint32_t* blocks, const Geom&
 // Filters beyond kMaxBuckets slices (> ~1 GiB): a first partition groups the
 // batch chunk by "super-slice" (exact block ranges, global bucket-major
 // layout with source positions), then each super-slice runs the single-level
-// path on its sub-filter, so every slice the probes touch stays ~16 MiB.
+// path on its sub-filter, so every slice the probes touch stays ~32 MiB.
 struct TwoLevel {
   uint64_t* keys = nullptr;       // [m] grouped by super-slice
   uint32_t* pos = nullptr;        // [m] source index (lookups)

@@ -88,7 +88,11 @@ struct sbbf_gpu {
 
 namespace {
 
-constexpr uint64_t kSliceBytes = 16ull << 20;  // blocked path: one slice + chunk bitmap stay in L2
+// Blocked path slice size: the slice being probed stays L2-resident while its
+// keys stream by. On config 4 (1 GiB): 32 MiB slices 84.4 / 48.3 Gkeys/s
+// (lookup / insert), 16 MiB 81.6 / 47.8, 64 MiB 68.7 / 38.0, 8 MiB 46.4 / 35.0
+// (scripts/variant_ab.py; bucket counts round up to powers of two).
+constexpr uint64_t kSliceBytes = 32ull << 20;
 
 // Blocking pays once random probes mostly miss L2: a ~L2-sized filter (config
 // 3) already hits L2 often enough that the partition passes cost more than

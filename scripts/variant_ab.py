@@ -25,6 +25,12 @@ bits = torch.empty((L + 31) // 32, dtype=torch.int32, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 chunk = cfg.insert_chunk or N
 f = SplitBlockFilter(cfg.num_buckets)
+for _ in range(3):  # untimed warm-up: clocks, pool growth, plan
+    f.clear()
+    for s in range(0, N, chunk):
+        f.add_hashes(ins[s:s + chunk])
+    f.find_hashes_bits(look, bits)
+torch.cuda.synchronize()
 for iv, fv, name in [(0, 0, "auto"), (_lib.INSERT_WIDE_TEST, _lib.FIND_GLOBAL, "direct"),
                      (_lib.INSERT_BLOCKED, _lib.FIND_BLOCKED, "blocked"), (_lib.INSERT_WIDE, _lib.FIND_GLOBAL, "wide")]:
     f.set_insert_variant(iv)

@@ -225,9 +225,9 @@ def test_blocked_path_skew(cuda, oracle, nb, shape):
     assert np.array_equal(bits_to_bytes(bits, probes.size), want_res)
 
 
-@pytest.mark.parametrize("nb", [2**26, 2**26 + 12345])
+@pytest.mark.parametrize("nb", [2**27, 2**27 + 12345])
 def test_blocked_two_level(cuda, oracle, nb):
-    """Filters beyond 64 slices of 16 MiB (> 1 GiB) take the two-level
+    """Filters beyond 64 slices of 32 MiB (> 2 GiB) take the two-level
     blocked path: super-slices by exact block range, then slices."""
     rng = np.random.default_rng(nb)
     hs = rng.integers(0, 2**64, size=3_000_017, dtype=np.uint64)
