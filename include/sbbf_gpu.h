@@ -107,7 +107,7 @@ int sbbf_gpu_find_batch_bits(const sbbf_gpu_t* f, const uint64_t* d_hashes, uint
 
 /* --- host-buffer drop-ins: add_hashes(span) / find_hashes(span, uint8_t*)
  *     with the caller's host memory, filter.hpp:81-83. Chunked, with the
- *     host<->device copies overlapped with the kernels on two streams.
+ *     host<->device copies overlapped with the kernels on three streams.
  *     Synchronous on return. ------------------------------------------ */
 int sbbf_gpu_add_hashes_host(sbbf_gpu_t* f, const uint64_t* h_hashes, uint64_t n);
 int sbbf_gpu_find_hashes_host(const sbbf_gpu_t* f, const uint64_t* h_hashes, uint64_t n,

@@ -217,8 +217,8 @@ int ensure_host_path(sbbf_gpu* f) {
 }
 
 // The host-buffer pipeline: chunk c goes H2D -> kernel -> (D2H) on stream
-// c % 2, so chunk c+1's upload overlaps chunk c's kernel and download (the
-// copy engines are full duplex).
+// c % kHostStreams, so chunk c+1's upload overlaps chunk c's kernel and
+// download (the copy engines are full duplex).
 enum class HostOp { kInsert, kFindBytes, kFindBits };
 
 int host_pipeline(sbbf_gpu* f, HostOp op, const uint64_t* h_hashes, uint64_t n, void* h_out) {
