@@ -256,6 +256,32 @@ int sbbf_route_find_window(sbbf_route_t* rt, const sbbf_gpu_t* shard, void* stre
 /* d_results[i] = answer for key i of the last lookup dispatch (0/1 bytes). */
 int sbbf_route_combine(sbbf_route_t* rt, uint8_t* d_results, void* stream);
 
+/* --- multi-GPU sharded filter (SURVEY.md §8(b) "sharded layer") ----------
+ * One rank per GPU of an NCCL communicator (ncclComm_t passed as void*).
+ * Rank r owns blocks [floor(rB/P), floor((r+1)B/P)) and routes keys through
+ * the fused peer-memory dispatch above; the phases are ordered by 1-element
+ * NCCL all-reduces on the caller's stream (no host sync). insert / find /
+ * find_bits are collective (every rank calls them, batches <= max_batch
+ * keys per rank); any rank may pass any keys. NCCL is loaded at run time
+ * (libnccl.so.2): without it these return SBBF_ENODEV. */
+typedef struct sbbf_dist sbbf_dist_t;
+/* 128-byte ncclUniqueId from rank 0, to broadcast out of band, and a
+ * communicator built from it (for callers without one). */
+int sbbf_dist_unique_id(void* id);
+int sbbf_dist_comm_init(const void* id, int world, int rank, int device, void** comm);
+int sbbf_dist_comm_destroy(void* comm);
+int sbbf_dist_create(void* comm, uint64_t total_buckets, uint64_t max_batch, int device, sbbf_dist_t** out);
+int sbbf_dist_destroy(sbbf_dist_t* d);
+int sbbf_dist_rank(const sbbf_dist_t* d);
+int sbbf_dist_world(const sbbf_dist_t* d);
+/* This rank's shard (a filter handle: blocks, image CRC, ...). */
+sbbf_gpu_t* sbbf_dist_shard(sbbf_dist_t* d);
+int sbbf_dist_insert(sbbf_dist_t* d, const uint64_t* d_hashes, uint64_t n, void* stream);
+int sbbf_dist_find(sbbf_dist_t* d, const uint64_t* d_hashes, uint64_t n, uint8_t* d_results, void* stream);
+int sbbf_dist_find_bits(sbbf_dist_t* d, const uint64_t* d_hashes, uint64_t n, uint32_t* d_bits, void* stream);
+/* Whole filter into h_dst (total_buckets*32 bytes) on rank `root`. */
+int sbbf_dist_gather(sbbf_dist_t* d, void* h_dst, int root);
+
 /* L2 fetch-granularity hint for `device` (cudaLimitMaxL2FetchGranularity,
  * 0..128 bytes; process-wide for that device). 32 makes a random 32-byte
  * block miss fetch one sector from HBM instead of a wider line. *old (if

@@ -79,6 +79,18 @@ PROTOTYPES = {
     "sbbf_pack_bits": (_i, [_vp, _u64, _vp, _vp]),
     "sbbf_gpu_hash_counter_strings": (_i, [_u64, _u64, _u64, _vp, _vp]),
     "sbbf_gpu_fpp_mc": (_i, [C.c_double, _u64, _u64, _u64, _i, C.POINTER(C.c_double)]),
+    "sbbf_dist_unique_id": (_i, [_vp]),
+    "sbbf_dist_comm_init": (_i, [_vp, _i, _i, _i, C.POINTER(_vp)]),
+    "sbbf_dist_comm_destroy": (_i, [_vp]),
+    "sbbf_dist_create": (_i, [_vp, _u64, _u64, _i, C.POINTER(_vp)]),
+    "sbbf_dist_destroy": (_i, [_vp]),
+    "sbbf_dist_rank": (_i, [_vp]),
+    "sbbf_dist_world": (_i, [_vp]),
+    "sbbf_dist_shard": (_vp, [_vp]),
+    "sbbf_dist_insert": (_i, [_vp, _vp, _u64, _vp]),
+    "sbbf_dist_find": (_i, [_vp, _vp, _u64, _vp, _vp]),
+    "sbbf_dist_find_bits": (_i, [_vp, _vp, _u64, _vp, _vp]),
+    "sbbf_dist_gather": (_i, [_vp, _vp, _i]),
     "sbbf_route_window_bytes": (_u64, [_u32, _u64]),
     "sbbf_route_create": (_i, [_u32, _u32, _u64, _i, C.POINTER(_vp)]),
     "sbbf_route_destroy": (None, [_vp]),

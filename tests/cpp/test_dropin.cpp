@@ -7,6 +7,8 @@
 #include <stdexcept>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "sbbf_gpu.hpp"
 
 extern "C" {
@@ -94,6 +96,34 @@ int main() {
     io = e.code() == sbbf::gpu::PersistErrc::kIo;
   }
   REQUIRE(io);
+  // the C++ sharded layer over a 1-rank NCCL communicator (skipped when the
+  // machine has no NCCL: sbbf_dist_* report SBBF_ENODEV then)
+  unsigned char uid[128];
+  if (sbbf_dist_unique_id(uid) == SBBF_OK) {
+    void* comm = nullptr;
+    REQUIRE(sbbf_dist_comm_init(uid, 1, 0, 0, &comm) == SBBF_OK);
+    sbbf_dist_t* dist = nullptr;
+    REQUIRE(sbbf_dist_create(comm, nb, 1u << 20, 0, &dist) == SBBF_OK);
+    uint64_t* d_keys = nullptr;
+    uint8_t* d_res = nullptr;
+    REQUIRE(cudaMalloc(&d_keys, non.size() * 8) == cudaSuccess);
+    REQUIRE(cudaMalloc(&d_res, non.size()) == cudaSuccess);
+    REQUIRE(cudaMemcpy(d_keys, ins.data(), ins.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess);
+    REQUIRE(sbbf_dist_insert(dist, d_keys, ins.size(), nullptr) == SBBF_OK);
+    REQUIRE(cudaMemcpy(d_keys, non.data(), non.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess);
+    REQUIRE(sbbf_dist_find(dist, d_keys, non.size(), d_res, nullptr) == SBBF_OK);
+    std::vector<uint8_t> dres(non.size());
+    REQUIRE(cudaMemcpy(dres.data(), d_res, non.size(), cudaMemcpyDeviceToHost) == cudaSuccess);
+    REQUIRE(dres == ref);
+    std::vector<uint32_t> whole(nb * 8);
+    REQUIRE(sbbf_dist_gather(dist, whole.data(), 0) == SBBF_OK);
+    REQUIRE(whole == want);
+    cudaFree(d_keys);
+    cudaFree(d_res);
+    REQUIRE(sbbf_dist_destroy(dist) == SBBF_OK);
+    REQUIRE(sbbf_dist_comm_destroy(comm) == SBBF_OK);
+    std::printf("cpp sharded layer (world 1) ok\n");
+  }
   std::printf("cpp drop-in ok: crc 0xe34f8bef, %llu false positives\n", (unsigned long long)fp);
   return 0;
 }

@@ -443,3 +443,50 @@ def test_fused_route_big_shards(cuda, oracle):
         assert np.array_equal(out.cpu().numpy(), oracle.find_hashes(want, looks[r])), r
     for rt in routes:
         rt.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("total", [32768, 7919 * 5])
+def test_dist_c_abi_world1(cuda, oracle, total):
+    """The C++ sharded layer (sbbf_dist_*, csrc/sbbf_dist.cu) over a 1-rank
+    NCCL communicator it builds itself: insert / find / find_bits / gather
+    against the oracle."""
+    import ctypes as C
+
+    from oracle import bits_to_bytes
+    from paper_2101_01719_b200 import _lib
+    L = _lib.lib()
+    uid = (C.c_uint8 * 128)()
+    _lib.check(L.sbbf_dist_unique_id(uid), "unique_id")
+    comm = C.c_void_p()
+    _lib.check(L.sbbf_dist_comm_init(uid, 1, 0, 0, C.byref(comm)), "comm_init")
+    d = C.c_void_p()
+    _lib.check(L.sbbf_dist_create(comm, total, 1 << 20, 0, C.byref(d)), "dist_create")
+    try:
+        assert L.sbbf_dist_rank(d) == 0 and L.sbbf_dist_world(d) == 1
+        rng = np.random.default_rng(total)
+        h = rng.integers(0, 2**64, size=600_000, dtype=np.uint64)
+        look = np.concatenate([h[:3000], rng.integers(0, 2**64, size=200_001, dtype=np.uint64)])
+        dh = torch.from_numpy(h.view(np.int64)).to(cuda)
+        dl = torch.from_numpy(look.view(np.int64)).to(cuda)
+        s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(L.sbbf_dist_insert(d, C.c_void_p(dh.data_ptr()), h.size, s), "dist_insert")
+        out = torch.empty(look.size, dtype=torch.uint8, device=cuda)
+        _lib.check(L.sbbf_dist_find(d, C.c_void_p(dl.data_ptr()), look.size, C.c_void_p(out.data_ptr()), s),
+                   "dist_find")
+        bits = torch.empty((look.size + 31) // 32, dtype=torch.int32, device=cuda)
+        _lib.check(L.sbbf_dist_find_bits(d, C.c_void_p(dl.data_ptr()), look.size, C.c_void_p(bits.data_ptr()), s),
+                   "dist_find_bits")
+        torch.cuda.synchronize()
+        want = oracle.build(total, h)
+        full = np.zeros((total, 8), np.uint32)
+        _lib.check(L.sbbf_dist_gather(d, full.ctypes.data_as(C.c_void_p), 0), "dist_gather")
+        assert np.array_equal(full, want)
+        want_res = oracle.find_hashes(want, look)
+        assert np.array_equal(out.cpu().numpy(), want_res)
+        assert np.array_equal(bits_to_bytes(bits.cpu().numpy().view(np.uint32), look.size), want_res)
+        with pytest.raises(_lib.SbbfError):     # over max_batch
+            _lib.check(L.sbbf_dist_insert(d, C.c_void_p(dh.data_ptr()), 2 << 20, s), "dist_insert")
+    finally:
+        L.sbbf_dist_destroy(d)
+        L.sbbf_dist_comm_destroy(comm)
