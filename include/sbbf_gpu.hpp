@@ -144,6 +144,45 @@ class SplitBlockFilter {
   sbbf_gpu_t* h_ = nullptr;
 };
 
+// --- multi-GPU: one rank's view of a block-range sharded filter -------------
+// (sbbf_dist_*; the reference has no distributed mode). Collective calls:
+// every rank of the NCCL communicator calls them in the same order.
+class ShardedFilter {
+ public:
+  ShardedFilter(void* nccl_comm, std::uint64_t total_buckets, std::uint64_t max_batch, int device = 0) {
+    if (total_buckets == 0) throw std::invalid_argument("SplitBlockFilter needs at least one bucket");
+    check(sbbf_dist_create(nccl_comm, total_buckets, max_batch, device, &d_), "ShardedFilter");
+    total_ = total_buckets;
+  }
+  ShardedFilter(const ShardedFilter&) = delete;
+  ShardedFilter& operator=(const ShardedFilter&) = delete;
+  ~ShardedFilter() { sbbf_dist_destroy(d_); }
+
+  int rank() const noexcept { return sbbf_dist_rank(d_); }
+  int world() const noexcept { return sbbf_dist_world(d_); }
+  void add_hashes_device(const std::uint64_t* d_hashes, std::uint64_t n, void* stream = nullptr) {
+    check(sbbf_dist_insert(d_, d_hashes, n, stream), "sbbf_dist_insert");
+  }
+  void find_hashes_device(const std::uint64_t* d_hashes, std::uint64_t n, std::uint8_t* d_results,
+                          void* stream = nullptr) {
+    check(sbbf_dist_find(d_, d_hashes, n, d_results, stream), "sbbf_dist_find");
+  }
+  void find_bits_device(const std::uint64_t* d_hashes, std::uint64_t n, std::uint32_t* d_bits,
+                        void* stream = nullptr) {
+    check(sbbf_dist_find_bits(d_, d_hashes, n, d_bits, stream), "sbbf_dist_find_bits");
+  }
+  // The whole filter (the shards in rank order) on `root`; empty elsewhere.
+  std::vector<Block> blocks(int root = 0) {
+    std::vector<Block> out(rank() == root ? total_ : 0);
+    check(sbbf_dist_gather(d_, out.data(), root), "sbbf_dist_gather");
+    return out;
+  }
+
+ private:
+  sbbf_dist_t* d_ = nullptr;
+  std::uint64_t total_ = 0;
+};
+
 // --- persist.hpp:33-66 mirror (FilterImage v1; CRC computed on the GPU) ----
 enum class PersistErrc { kTruncated, kBadMagic, kBadVersion, kBadBucketCount, kBadChecksum, kIo };
 

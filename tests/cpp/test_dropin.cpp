@@ -121,6 +121,16 @@ int main() {
     cudaFree(d_keys);
     cudaFree(d_res);
     REQUIRE(sbbf_dist_destroy(dist) == SBBF_OK);
+    {  // the RAII wrapper
+      sbbf::gpu::ShardedFilter sf(comm, nb, 1u << 20);
+      REQUIRE(sf.rank() == 0 && sf.world() == 1);
+      REQUIRE(cudaMalloc(&d_keys, ins.size() * 8) == cudaSuccess);
+      REQUIRE(cudaMemcpy(d_keys, ins.data(), ins.size() * 8, cudaMemcpyHostToDevice) == cudaSuccess);
+      sf.add_hashes_device(d_keys, ins.size());
+      const auto whole_blocks = sf.blocks();
+      REQUIRE(std::memcmp(whole_blocks.data(), want.data(), nb * 32) == 0);
+      cudaFree(d_keys);
+    }
     REQUIRE(sbbf_dist_comm_destroy(comm) == SBBF_OK);
     std::printf("cpp sharded layer (world 1) ok\n");
   }
