@@ -166,10 +166,10 @@ def run_config_device(cid: int, steps: int, warmup: int, device, collect_parity=
         f.find_hashes_bits(look, bits)
         ev[-1].record(stream)
 
-    for _ in range(warmup):
+    for _ in range(warmup):  # the same event pattern as the timed steps
         f.clear()
         flush_l2()
-        one_step([torch.cuda.Event(enable_timing=True) for _ in range(3)])
+        one_step([torch.cuda.Event(enable_timing=True) for _ in range(2)])
     torch.cuda.synchronize(device)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
     l0 = launch_count()
