@@ -485,7 +485,7 @@ cudaError_t bucket_partition(const DeviceInfo& di, const Geom& g, uint32_t S, co
 // lookups, each slot's 16-bit source position inside the chunk.
 struct ChunkSmem {
   uint64_t key[kPartChunk];
-  uint16_t pos[kPartChunk];
+  alignas(16) uint16_t pos[kPartChunk];
   uint32_t wcnt[kPartWarps][kMaxBuckets];
   uint32_t boff[kMaxBuckets + 1];
 };
@@ -567,9 +567,21 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
       }
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < cnt; i += kPartThreads) {
-      out[base + i] = sm.key[i];
-      if (pos16) pos16[base + i] = sm.pos[i];
+    if (cnt == kPartChunk) {
+      // 16-byte copies: two keys / eight positions per thread per step
+      const uint4* ks = reinterpret_cast<const uint4*>(sm.key);
+      uint4* ko = reinterpret_cast<uint4*>(out + base);
+      for (uint32_t v = threadIdx.x; v < kPartChunk / 2; v += kPartThreads) ko[v] = ks[v];
+      if (pos16) {
+        const uint4* ps = reinterpret_cast<const uint4*>(sm.pos);
+        uint4* po = reinterpret_cast<uint4*>(pos16 + base);
+        for (uint32_t v = threadIdx.x; v < kPartChunk / 8; v += kPartThreads) po[v] = ps[v];
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < cnt; i += kPartThreads) {
+        out[base + i] = sm.key[i];
+        if (pos16) pos16[base + i] = sm.pos[i];
+      }
     }
     __syncthreads();
   }
