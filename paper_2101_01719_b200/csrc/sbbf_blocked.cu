@@ -630,10 +630,14 @@ __global__ void __launch_bounds__(kSegThreads, kMinB)
       // test-before-set: grouped duplicates (config 4's hot keys) skip the atomic
       const uint32_t pair = lane & 3;
       const uint32_t seed_lo = dev::lane_seed_rt(2 * pair), seed_hi = dev::lane_seed_rt(2 * pair + 1);
+      uint64_t hn[kSegQ];
+#pragma unroll
+      for (int q = 0; q < kSegQ; ++q)
+        hn[q] = (lane >> 2) < len[q] ? dev::ld_stream_u64(keys + seg[q] + (lane >> 2), pol) : 0;
       for (uint32_t j = lane >> 2; j < maxlen; j += 8) {
         uint64_t h[kSegQ];
 #pragma unroll
-        for (int q = 0; q < kSegQ; ++q) h[q] = j < len[q] ? dev::ld_stream_u64(keys + seg[q] + j, pol) : 0;
+        for (int q = 0; q < kSegQ; ++q) h[q] = hn[q];
         uint64_t* ptr[kSegQ];
         uint64_t mask[kSegQ], cur[kSegQ];
 #pragma unroll
@@ -646,14 +650,20 @@ __global__ void __launch_bounds__(kSegThreads, kMinB)
           cur[q] = mask[q] ? dev::ld_pair(ptr[q], keep) : ~0ull;
         }
 #pragma unroll
+        for (int q = 0; q < kSegQ; ++q) hn[q] = j + 8 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 8, pol) : 0;
+#pragma unroll
         for (int q = 0; q < kSegQ; ++q)
           if (mask[q] & ~cur[q]) dev::red_or64(ptr[q], mask[q], keep);
       }
     } else {
+      // the next step's keys load while this step's sectors are in flight
+      uint64_t hn[kSegQ];
+#pragma unroll
+      for (int q = 0; q < kSegQ; ++q) hn[q] = lane < len[q] ? dev::ld_stream_u64(keys + seg[q] + lane, pol) : 0;
       for (uint32_t j = lane; j < maxlen; j += 32) {
         uint64_t h[kSegQ];
 #pragma unroll
-        for (int q = 0; q < kSegQ; ++q) h[q] = j < len[q] ? dev::ld_stream_u64(keys + seg[q] + j, pol) : 0;
+        for (int q = 0; q < kSegQ; ++q) h[q] = hn[q];
         dev::Block8 bl[kSegQ];
         uint32_t owned = 0;
 #pragma unroll
@@ -663,6 +673,9 @@ __global__ void __launch_bounds__(kSegThreads, kMinB)
           owned |= static_cast<uint32_t>(ok) << q;
           dev::ld_block_nc_normal(blocks + (ok ? blk : 0) * 8, bl[q]);
         }
+#pragma unroll
+        for (int q = 0; q < kSegQ; ++q)
+          hn[q] = j + 32 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 32, pol) : 0;
 #pragma unroll
         for (int q = 0; q < kSegQ; ++q)
           if (j < len[q]) ans[seg[q] + j] = (((owned >> q) & 1u) && dev::block_contains(bl[q], h[q])) ? 1 : 0;
