@@ -226,6 +226,40 @@ def run_config_device(cid: int, steps: int, warmup: int, device, collect_parity=
     return out
 
 
+def run_keys_frontend(steps: int, device) -> dict:
+    """The XXH64 key frontend (kHasherXxh64, hash.cpp:108-114) on config 2's
+    shapes: the same splitmix64 streams used as u64 KEYS, hashed inside the
+    insert / lookup kernels (sbbf_gpu_insert_keys_u64 / find_keys_u64_bits).
+    Device-timed like the headline step; reported, not the headline."""
+    import torch
+
+    from paper_2101_01719_b200 import SplitBlockFilter
+    from paper_2101_01719_b200 import workload as W
+    cfg = W.CONFIGS[2]
+    N, L = cfg.inserts.n, cfg.lookups.n
+    st = W.StreamHandle(cfg.inserts, device.index or 0)
+    keys = W.gen_inserts(st, 0, N, device=device.index or 0)
+    probes = W.gen_lookups(st, cfg.lookups, N, 0, L, device=device.index or 0)
+    bits = torch.empty((L + 31) // 32, dtype=torch.int32, device=device)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
+    f = SplitBlockFilter(cfg.num_buckets, hasher_id=1, device=device.index or 0)
+    ts = []
+    for k in range(steps + 3):
+        f.clear()
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        f.add_keys(keys)
+        f.find_keys_bits(probes, out=bits)
+        e1.record()
+        torch.cuda.synchronize(device)
+        if k >= 3:
+            ts.append(e0.elapsed_time(e1))
+    ms = statistics.mean(ts)
+    return {"workload": "config 2 shapes, u64 keys hashed in-kernel (XXH64 seed 0)", "ms_per_step": ms,
+            "value": (N + L) / (ms * 1e-3) / 1e9, "unit": "Gkeys/s"}
+
+
 def sector_ceiling(device, filter_bytes: int, red: bool = False, n: int = 1 << 28) -> float:
     """Random 32-B sector rate (G sectors/s) on a buffer of filter_bytes."""
     import ctypes as C
@@ -558,6 +592,8 @@ def main() -> None:
         "configs": {k: {kk: v for kk, v in r.items() if kk not in ("name",)}
                     for k, r in extras.items()},
     }
+    if args.config == 2:
+        line["keys_frontend"] = run_keys_frontend(max(3, min(args.steps, 10)), device)
     if not args.no_e2e:
         line["e2e"] = run_e2e(args.config, max(3, min(args.steps, 10)), device)
     if not args.no_cpu_baseline:

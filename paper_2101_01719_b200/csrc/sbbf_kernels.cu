@@ -13,9 +13,12 @@
 //   * insert_*_test   — load first, red only lanes whose bits are missing (bits
 //     are monotone): a miss is filled by the faster read path and
 //     duplicate/hot keys (config 4's Zipf) skip the atomic.
-//   * find_global     — one thread per key, U keys in flight per thread, one
-//     256-bit LDG per key (LDG.E.256), hashes streamed evict-first, results
-//     either 0/1 bytes (drop-in) or a __ballot_sync-packed bitmap.
+//   * find_pipe       — one thread per key, U = 4 keys in flight per thread plus
+//     the next tile's hashes (software pipelined), one 256-bit LDG per key
+//     (LDG.E.256), hashes streamed evict-first, results either 0/1 bytes
+//     (drop-in) or a __ballot_sync-packed bitmap; launched as a programmatic
+//     dependent of a preceding insert; kKeys hashes u64 keys (XXH64) as they
+//     stream in.
 //   * find_smem       — small filters (<= ~200 KiB, e.g. config 1) are staged
 //     into shared memory per CTA with cp.async.bulk (TMA bulk copy, mbarrier
 //     completion) and probed with two 128-bit LDS per key.
@@ -187,73 +190,13 @@ __global__ void __launch_bounds__(kThreads) insert_thread_kernel(uint32_t* __res
 // Warp tile = 32*U consecutive keys; lane l owns keys base + u*32 + l. All U
 // hash loads, then all U block loads are issued before any is consumed, so
 // each thread keeps U independent 32-byte sector reads in flight.
-template <int U, bool kBits>
-constexpr int find_min_blocks() { return U >= 8 ? (kBits ? 2 : 4) : 5; }
-
-template <int U, bool kBits, bool kKeys = false>
-__global__ void __launch_bounds__(kThreads, find_min_blocks<U, kBits>())
-    find_global_kernel(const uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ hashes,
-                       uint64_t n, void* __restrict__ out, uint64_t seed = 0) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t pol = dev::policy_evict_first();
-  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
-  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
-  constexpr uint64_t kTile = 32 * U;
-  const uint64_t ntiles = (n + kTile - 1) / kTile;
-  // Launched as a programmatic dependent of a preceding insert: warm the
-  // first tile's hashes into L2 (they do not depend on the insert), then wait
-  // for the insert grid to complete before touching the filter.
-  if (warp < ntiles) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t idx = warp * kTile + u * 32 + lane;
-      if (idx < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(hashes + idx));
-    }
-  }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  for (uint64_t t = warp; t < ntiles; t += nwarps) {
-    const uint64_t base = t * kTile;
-    uint64_t h[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t idx = base + u * 32 + lane;
-      h[u] = idx < n ? dev::to_hash<kKeys>(dev::ld_stream_u64(hashes + idx, pol), seed) : 0;
-    }
-    Block8 b[U];
-    uint32_t owned = 0;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      bool ok;
-      dev::ld_block_nc(blocks + local_block(h[u], g, ok) * 8, b[u]);
-      owned |= static_cast<uint32_t>(ok) << u;
-    }
-    uint32_t mine = 0;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t idx = base + u * 32 + lane;
-      const bool hit = dev::block_contains(b[u], h[u]) && ((owned >> u) & 1u) && idx < n;
-      if constexpr (kBits) {
-        const uint32_t word = __ballot_sync(0xffffffffu, hit);
-        if (lane == u) mine = word;
-      } else {
-        if (idx < n) dev::st_stream_u8(static_cast<uint8_t*>(out) + idx, hit ? 1u : 0u);
-      }
-    }
-    if constexpr (kBits) {
-      const uint64_t nwords = (n + 31) >> 5;
-      const uint64_t widx = (base >> 5) + lane;
-      if (lane < U && widx < nwords) dev::st_stream_u32(static_cast<uint32_t*>(out) + widx, mine);
-    }
-  }
-}
-
 // Software-pipelined variant: the next tile's hashes are loaded while this
 // tile's block loads are in flight, so the HBM latency of the hash stream is
 // off the per-warp critical path.
-template <int U, bool kBits, int kMinBlocks = 2>
+template <int U, bool kBits, int kMinBlocks = 2, bool kKeys = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     find_pipe_kernel(const uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ hashes,
-                     uint64_t n, void* __restrict__ out) {
+                     uint64_t n, void* __restrict__ out, uint64_t seed = 0) {
   const int lane = threadIdx.x & 31;
   const uint64_t pol = dev::policy_evict_first();
   const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
@@ -264,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint64_t idx = warp * kTile + u * 32 + lane;
-    hn[u] = (warp < ntiles && idx < n) ? dev::ld_stream_u64(hashes + idx, pol) : 0;
+    hn[u] = (warp < ntiles && idx < n) ? dev::to_hash<kKeys>(dev::ld_stream_u64(hashes + idx, pol), seed) : 0;
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // filter reads only after the insert grid
   for (uint64_t t = warp; t < ntiles; t += nwarps) {
@@ -284,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t idx = tn * kTile + u * 32 + lane;
-      hn[u] = (tn < ntiles && idx < n) ? dev::ld_stream_u64(hashes + idx, pol) : 0;
+      hn[u] = (tn < ntiles && idx < n) ? dev::to_hash<kKeys>(dev::ld_stream_u64(hashes + idx, pol), seed) : 0;
     }
     uint32_t mine = 0;
 #pragma unroll
@@ -535,7 +478,6 @@ cudaError_t launch_insert_ordered(const DeviceInfo& di, uint32_t* blocks, const 
   return cudaGetLastError();
 }
 
-constexpr int kFindU = 8;
 
 // Fused XXH64 frontends: u64 keys hashed inside the insert / lookup kernel.
 cudaError_t launch_insert_keys(const DeviceInfo& di, bool test, uint32_t* blocks, const Geom& g,
@@ -558,18 +500,22 @@ cudaError_t launch_find_keys(const DeviceInfo& di, const uint32_t* blocks, const
                              uint64_t n, uint64_t seed, void* out, bool bits, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   note_launch();
-  static const int occ_b = resident_blocks(find_global_kernel<kFindU, true, true>, kThreads, 0);
-  static const int occ_y = resident_blocks(find_global_kernel<kFindU, false, true>, kThreads, 0);
-  const uint64_t grid = grid_for(n, kThreads * kFindU, di.sms, bits ? occ_b : occ_y);
-  if (bits)
-    find_global_kernel<kFindU, true, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, keys, n,
-                                                                                           out, seed);
-  else
-    find_global_kernel<kFindU, false, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, keys, n,
-                                                                                            out, seed);
-  return cudaGetLastError();
+  // the pipelined lookup with XXH64 applied to each key as it streams in,
+  // launched like the raw-hash lookup (programmatic dependent of an insert)
+  constexpr int kU = 4, kMinB = 3;
+  static const int occ = resident_blocks(find_pipe_kernel<kU, true, kMinB, true>, kThreads, 0);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kU, di.sms, occ)));
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return bits ? cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, true, kMinB, true>, blocks, g, keys, n, out, seed)
+              : cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, false, kMinB, true>, blocks, g, keys, n, out, seed);
 }
-
 cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* blocks, const Geom& g,
                         const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
@@ -599,8 +545,8 @@ cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* block
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return bits ? cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, true, kMinB>, blocks, g, hashes, n, out)
-                : cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, false, kMinB>, blocks, g, hashes, n, out);
+    return bits ? cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, true, kMinB>, blocks, g, hashes, n, out, uint64_t{0})
+                : cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, false, kMinB>, blocks, g, hashes, n, out, uint64_t{0});
   }
   return cudaGetLastError();
 }
