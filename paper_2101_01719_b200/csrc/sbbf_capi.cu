@@ -126,7 +126,10 @@ int resolve_find(const sbbf_gpu* f, uint64_t n) {
   // Staging the filter costs one filter-size copy per CTA; it pays once each
   // SM probes enough keys to amortise it.
   if (smem_fits(f) && n >= 64 * f->nb) return SBBF_FIND_SMEM;
-  if (blocked_pays(f, n)) return SBBF_FIND_BLOCKED;
+  // Lookups gain from blocking as soon as the filter outgrows L2: config 3's
+  // 128 MiB filter, 108.2 vs 102.1 Gkeys/s direct (scripts/variant_ab.py);
+  // inserts only beyond 2 x L2 (resolve_insert).
+  if (f->nb * 32 > static_cast<uint64_t>(f->di.l2_bytes) && n >= f->nb / 2) return SBBF_FIND_BLOCKED;
   return SBBF_FIND_GLOBAL;
 }
 
