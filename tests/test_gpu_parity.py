@@ -184,6 +184,46 @@ def test_idempotence_and_order_independence(cuda, oracle):
     assert np.array_equal(a.blocks(), oracle.build(4096, hs))
 
 
+def test_concurrent_threads_all_paths(cuda, oracle):
+    """Four host threads, each with its own stream, insert into and look up
+    one filter concurrently, through every insert path including the blocked
+    one (shared plan, per-call pool scratch): bytes equal the oracle's; each
+    thread's lookups of keys inserted before its barrier are all hits."""
+    import threading
+    nb = 1 << 23   # 256 MiB: beyond 2 x L2, so AUTO inserts take the blocked path
+    rng = np.random.default_rng(11)
+    parts = [rng.integers(0, 2**64, size=1_500_000 + 1000 * t, dtype=np.uint64) for t in range(4)]
+    f = SplitBlockFilter(nb)
+    variants = [_lib.INSERT_AUTO, _lib.INSERT_BLOCKED, _lib.INSERT_WIDE_TEST, _lib.INSERT_LANE8]
+    barrier = threading.Barrier(4)
+    errors = []
+
+    def work(t):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                d = dev(parts[t], cuda)
+                g = SplitBlockFilter(nb)           # per-thread filter: the variant is per handle
+                g.set_insert_variant(variants[t])
+                g.add_hashes(d)
+                f.add_hashes(d)                    # the shared filter, concurrently
+                s.synchronize()
+                barrier.wait()
+                got = f.find_hashes(d).cpu().numpy()
+                assert got.all(), t
+                assert np.array_equal(g.blocks(), oracle.build(nb, parts[t])), t
+        except Exception as exc:  # noqa: BLE001
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    assert np.array_equal(f.blocks(), oracle.build(nb, np.concatenate(parts)))
+
+
 def test_no_false_negatives_acceptance(cuda):
     # acceptance.cpp:63-82: 10^6 hashes, {1, 7, 4096} buckets
     rng = np.random.default_rng(0xACC0001)
