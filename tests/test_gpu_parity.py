@@ -190,10 +190,12 @@ def test_concurrent_threads_all_paths(cuda, oracle):
     one (shared plan, per-call pool scratch): bytes equal the oracle's; each
     thread's lookups of keys inserted before its barrier are all hits."""
     import threading
-    nb = 1 << 23   # 256 MiB: beyond 2 x L2, so AUTO inserts take the blocked path
+    nb = 1 << 23   # 256 MiB
     rng = np.random.default_rng(11)
     parts = [rng.integers(0, 2**64, size=1_500_000 + 1000 * t, dtype=np.uint64) for t in range(4)]
     f = SplitBlockFilter(nb)
+    f.set_insert_variant(_lib.INSERT_BLOCKED)      # concurrent blocked calls on one handle
+    f.set_find_variant(_lib.FIND_BLOCKED)
     variants = [_lib.INSERT_AUTO, _lib.INSERT_BLOCKED, _lib.INSERT_WIDE_TEST, _lib.INSERT_LANE8]
     barrier = threading.Barrier(4)
     errors = []
