@@ -376,6 +376,8 @@ def cpu_reference_run(cid: int, reps: int, threads: int, device=None, sample: in
         ref = O.Reference()
         kind = "reference"
         ti, tl, res, blocks = ref.time_build_probe(cfg.num_buckets, ins, look, threads, reps)
+        # lookups on one core as well as on all of them
+        tl1 = ref.time_build_probe(cfg.num_buckets, ins, look, 1, 3)[1] if threads > 1 and not sample else tl
     except (FileNotFoundError, OSError):
         kind = "port"
         ti, tl = [], []
@@ -388,6 +390,7 @@ def cpu_reference_run(cid: int, reps: int, threads: int, device=None, sample: in
             res = orc.find_hashes(b, look, threads)
             tl.append(time.perf_counter() - t0)
         blocks = b
+        tl1 = tl
     mi, ml = statistics.median(ti), statistics.median(tl)
     # (an 8 GiB config-5 image is not checksummed here: the tests pin parity)
     crc = None if sample else image_crc(np.ascontiguousarray(blocks).tobytes(), cfg.num_buckets)
@@ -397,6 +400,7 @@ def cpu_reference_run(cid: int, reps: int, threads: int, device=None, sample: in
                       f"insert 1 thread (the reference's only writer mode), lookup {threads} "
                       f"jthreads (harness.cpp:173-200); -O3 -DNDEBUG, AVX2 backend",
             "insert_gkeys_s": N / mi / 1e9, "lookup_gkeys_s": L / ml / 1e9,
+            "lookup_gkeys_s_1thread": L / statistics.median(tl1) / 1e9,
             "image_crc": f"{crc:#010x}" if crc is not None else None, "hits": int(res.sum())}
 
 
@@ -422,6 +426,7 @@ def run_reference_arm(args) -> None:
         "e2e": {"value": r["value"], "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "insert_gkeys_s": r["insert_gkeys_s"], "lookup_gkeys_s": r["lookup_gkeys_s"],
+        "lookup_gkeys_s_1thread": r["lookup_gkeys_s_1thread"],
         "image_crc": r["image_crc"],
     }
     print(json.dumps(line), flush=True)
@@ -599,7 +604,8 @@ def main() -> None:
     if not args.no_cpu_baseline:
         try:
             cb = cpu_reference_run(args.config, 5, os.cpu_count() or 1)
-            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "insert_gkeys_s",
+                                                       "lookup_gkeys_s", "lookup_gkeys_s_1thread")}
             line["cpu_baseline"]["image_crc"] = cb["image_crc"]
         except Exception as exc:  # the baseline never blocks the GPU line
             line["cpu_baseline"] = {"value": None, "error": repr(exc)}
