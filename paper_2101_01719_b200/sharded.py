@@ -442,11 +442,18 @@ def bench_main(args) -> dict | None:
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    # SBBF_BENCH_DEVICE / SBBF_BENCH_BACKEND: exercise this N>1 code path with
+    # every rank on one GPU and a host backend (tests only; no timing claim)
+    local = int(os.environ.get("SBBF_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29531")
-    dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+    backend = os.environ.get("SBBF_BENCH_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+    else:
+        dist.init_process_group(backend, rank=rank, world_size=world)
     cfg = W.CONFIGS[args.config]
     if args.config == 5:
         N = L = int(getattr(args, "sample_keys", 1 << 27))

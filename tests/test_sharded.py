@@ -490,3 +490,26 @@ def test_dist_c_abi_world1(cuda, oracle, total):
     finally:
         L.sbbf_dist_destroy(d)
         L.sbbf_dist_comm_destroy(comm)
+
+
+@pytest.mark.gpu
+def test_bench_world2_code_path(cuda):
+    """bench.py's torchrun (N > 1) path end to end — both ranks on this one
+    GPU, a host backend for the collectives, fused IPC routing — so the
+    multi-GPU line assembles; no timing claim is made from it."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SBBF_BENCH_DEVICE="0", SBBF_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+                          os.path.join(root, "bench.py"), "--gpus", "2", "--route", "fused",
+                          "--sample-keys", str(1 << 20), "--steps", "2", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1                         # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["config_id"] == 5 and d["value"] > 0
+    assert "peer-memory windows" in d["config"]["workload"]
