@@ -410,7 +410,10 @@ def run_reference_arm(args) -> None:
         return
     threads = os.cpu_count() or 1
     world = env_int("WORLD_SIZE", 1)
-    sample = args.sample_keys * world if args.config == 5 else None
+    # config 5: the sharded arm's whole-job per-step sample, capped at 2^28
+    # keys each way so that the CPU run (8 GiB filter, one insert thread)
+    # stays within minutes; the metric is a rate
+    sample = min(args.sample_keys * world, 1 << 28) if args.config == 5 else None
     reps = max(args.steps, 3) if sample is None else 3  # config 5: each rep builds an 8 GiB filter
     r = cpu_reference_run(args.config, reps, threads, sample=sample)
     from paper_2101_01719_b200 import workload as W
