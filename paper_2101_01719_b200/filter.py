@@ -103,6 +103,18 @@ class SplitBlockFilter:
         except Exception:
             pass
 
+    def __enter__(self) -> "SplitBlockFilter":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
+
+    def __repr__(self) -> str:
+        if not (getattr(self, "_h", None) and self._h.value):
+            return "SplitBlockFilter(<closed>)"
+        return (f"SplitBlockFilter(num_buckets={self.num_buckets()}, bytes={self.size_bytes()}, "
+                f"hasher_id={self.hasher_id()}, device={self._device})")
+
     @classmethod
     def from_blocks(cls, blocks, hasher_id: int = 0, device: int = 0) -> "SplitBlockFilter":
         """filter.hpp:74-75 — adopt existing block contents ((B, 8) uint32 or B*32 bytes)."""
