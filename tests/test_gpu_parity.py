@@ -386,3 +386,39 @@ def test_config_full(cuda, oracle, golden_configs, cid, iv, fv):
     assert r["member_hits"] == g["members"]
     assert r["false_positives"] == g["false_positives"]
     assert r["crcs"] == g["lookup_bitmap_chunk_crcs"]
+
+
+@pytest.mark.parametrize("nb,variant", [(32768, None), (1 << 23, "blocked")])
+def test_cuda_graph_capture(cuda, oracle, nb, variant):
+    """The device-pointer ABI is stream-ordered with no host sync, so an
+    insert + lookup step captures into a CUDA graph and replays bit-exactly
+    (direct path, and the single-level blocked path with its stream-ordered
+    pool scratch)."""
+    rng = np.random.default_rng(nb)
+    hs = rng.integers(0, 2**64, size=1 << 20, dtype=np.uint64)
+    look = np.concatenate([hs[: 1 << 18], rng.integers(0, 2**64, size=(1 << 20) - (1 << 18), dtype=np.uint64)])
+    d, dl = dev(hs, cuda), dev(look, cuda)
+    bits = torch.empty(look.size // 32, dtype=torch.int32, device=cuda)
+    f = SplitBlockFilter(nb)
+    if variant == "blocked":
+        f.set_insert_variant(_lib.INSERT_BLOCKED)
+        f.set_find_variant(_lib.FIND_BLOCKED)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):            # warm up (plans, pool) outside the capture
+        f.add_hashes(d)
+        f.find_hashes_bits(dl, bits)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        f.add_hashes(d)
+        f.find_hashes_bits(dl, bits)
+    want = oracle.build(nb, hs)
+    for _ in range(2):
+        f.clear()
+        bits.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(f.blocks(), want)
+        assert np.array_equal(bits_to_bytes(u32(bits), look.size), oracle.find_hashes(want, look))
