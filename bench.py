@@ -477,7 +477,7 @@ def roofline(res: dict, l2_sector_gs: float | None, hbm_peak: float, peak_note: 
         # bitmap once and the filter once per batch (each slice is L2-resident
         # while its bucket is probed)
         per_key = 8.0 + 0.125 + res["filter_bytes"] / L
-        kernel = "blocked find: bucket_count/scan/scatter + probe_grouped + expand (sbbf_blocked.cu)"
+        kernel = "blocked find: chunk_scatter + segment_kernel + unpermute (sbbf_blocked.cu)"
         note = ("blocked: 8 B hash + 1/8 B bitmap + filter streamed once (filter_bytes/lookups); "
                 "the partition's extra passes are overhead, not algorithmic bytes")
     elif resident:

@@ -37,7 +37,7 @@
 namespace sbbf {
 namespace {
 
-constexpr uint64_t kBlockedChunk = uint64_t{1} << 28;  // keys per partition round (3.1 GB scratch)
+constexpr uint64_t kBlockedChunk = uint64_t{1} << 28;  // keys per blocked round (~3 GB of scratch for lookups)
 
 // ---------------------------------------------------------------------------
 // bucket partition

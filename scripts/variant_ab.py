@@ -31,7 +31,7 @@ for _ in range(3):  # untimed warm-up: clocks, pool growth, plan
         f.add_hashes(ins[s:s + chunk])
     f.find_hashes_bits(look, bits)
 torch.cuda.synchronize()
-for iv, fv, name in [(0, 0, "auto"), (_lib.INSERT_WIDE_TEST, _lib.FIND_GLOBAL, "direct"),
+for iv, fv, name in [(0, 0, "auto"), (0, _lib.FIND_SMEM, "smem"), (_lib.INSERT_WIDE_TEST, _lib.FIND_GLOBAL, "direct"),
                      (_lib.INSERT_BLOCKED, _lib.FIND_BLOCKED, "blocked"), (_lib.INSERT_WIDE, _lib.FIND_GLOBAL, "wide")]:
     f.set_insert_variant(iv)
     f.set_find_variant(fv)
