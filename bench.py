@@ -571,6 +571,7 @@ def main() -> None:
     l2_read = sector_ceiling(device, max(main_res["filter_bytes"], 1 << 20))
     hbm_read = sector_ceiling(device, 4 << 30)
     hbm_red = sector_ceiling(device, 4 << 30, red=True)
+    l2_red = sector_ceiling(device, max(main_res["filter_bytes"], 1 << 20), red=True)
     for r in [main_res] + list(extras.values()):
         # the denominator is the random-sector rate on a buffer of the filter's
         # own size (a 128 MiB filter is partly L2-served, a 1 GiB one is not)
@@ -592,8 +593,14 @@ def main() -> None:
                         "programmatic dependent of the insert grid); ms_insert/ms_lookup: separate steps "
                         f"with a mid-step event (their sum {main_res['ms_step_split']:.4f} ms)"),
         "roofline": main_res["roofline"],
+        # the insert phase's own bound: one 32-B sector red request per key
+        # (L1 merges a key's lane reds) against random sector reds on a
+        # buffer of the filter's size (sbbf_bench_sector_red)
+        "insert_roofline": {"bound": "L2 atomic sector-request rate",
+                            "achieved_gkeys_s": main_res["insert_gkeys_s"], "ceiling_gsectors_s": l2_red,
+                            "frac": main_res["insert_gkeys_s"] / l2_red},
         "random_sector_ceilings_gs": {"l2_read_1MiB": l2_read, "hbm_read_4GiB": hbm_read,
-                                      "hbm_red_4GiB": hbm_red},
+                                      "hbm_red_4GiB": hbm_red, "l2_red_filter": l2_red},
         "gpu_launches": int(main_res["launches_per_step"] * args.steps),
         "clocks": clk, "parity": main_res.get("parity"),
         "variants": {"insert": main_res["insert_variant"], "find": main_res["find_variant"]},
