@@ -251,6 +251,66 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 // ---------------------------------------------------------------------------
 // lookup from shared memory (small filters)
 // ---------------------------------------------------------------------------
+// Whole-filter lookup (the single-GPU case: no shard offset, no ownership
+// test), register-lean: after a block's address is formed only the low 32
+// hash bits stay live (60-69 registers against find_pipe's 78). The next
+// tile's hashes load while this tile's sectors are in flight, as in
+// find_pipe. Config 2: 190.2 vs 188.5 Gkeys/s per step (profiles/r1_find_tuning.md).
+template <int U, bool kBits, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+    find_whole_kernel(const uint32_t* __restrict__ blocks, uint64_t nb, const uint64_t* __restrict__ hashes,
+                      uint64_t n, void* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t pol = dev::policy_evict_first();
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
+  constexpr uint64_t kTile = 32 * U;
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  uint64_t hn[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t idx = warp * kTile + u * 32 + lane;
+    hn[u] = (warp < ntiles && idx < n) ? dev::ld_stream_u64(hashes + idx, pol) : 0;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // filter reads only after the insert grid
+  for (uint64_t t = warp; t < ntiles; t += nwarps) {
+    const uint64_t base = t * kTile;
+    uint32_t lo[U];
+    Block8 b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      lo[u] = static_cast<uint32_t>(hn[u]);
+      dev::ld_block_nc(blocks + dev::block_index(hn[u], nb) * 8, b[u]);
+    }
+    const uint64_t tn = t + nwarps;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t idx = tn * kTile + u * 32 + lane;
+      hn[u] = (tn < ntiles && idx < n) ? dev::ld_stream_u64(hashes + idx, pol) : 0;
+    }
+    uint32_t mine = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t idx = base + u * 32 + lane;
+      uint32_t missing = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) missing |= dev::lane_bit(lo[u], dev::lane_seed(i)) & ~b[u].w[i];
+      const bool hit = missing == 0 && idx < n;
+      if constexpr (kBits) {
+        const uint32_t word = __ballot_sync(0xffffffffu, hit);
+        if (lane == u) mine = word;
+      } else {
+        if (idx < n) dev::st_stream_u8(static_cast<uint8_t*>(out) + idx, hit ? 1u : 0u);
+      }
+    }
+    if constexpr (kBits) {
+      const uint64_t nwords = (n + 31) >> 5;
+      const uint64_t widx = (base >> 5) + lane;
+      if (lane < U && widx < nwords) dev::st_stream_u32(static_cast<uint32_t*>(out) + widx, mine);
+    }
+  }
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -537,15 +597,21 @@ cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* block
     constexpr int kU = 4, kMinB = 3;
     static const int occ = resident_blocks(find_pipe_kernel<kU, true, kMinB>, kThreads, 0);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kU, di.sms, occ)));
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (g.first == 0 && g.nb_local == g.nb_global) {  // a whole filter: the lean kernel
+      static const int occ_w = resident_blocks(find_whole_kernel<kU, true, kMinB>, kThreads, 0);
+      cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kU, di.sms, occ_w)));
+      return bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, true, kMinB>, blocks, g.nb_global, hashes, n, out)
+                  : cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, false, kMinB>, blocks, g.nb_global, hashes, n, out);
+    }
+    cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kU, di.sms, occ)));  // a shard
     return bits ? cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, true, kMinB>, blocks, g, hashes, n, out, uint64_t{0})
                 : cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, false, kMinB>, blocks, g, hashes, n, out, uint64_t{0});
   }
