@@ -94,9 +94,11 @@ namespace {
 // (scripts/variant_ab.py; bucket counts round up to powers of two).
 constexpr uint64_t kSliceBytes = 32ull << 20;
 
-// Blocking pays once random probes mostly miss L2: a ~L2-sized filter (config
-// 3) already hits L2 often enough that the partition passes cost more than
-// they save (profiles/r1_blocked_partition.md).
+// Blocked inserts pay once random atomics mostly miss L2: into a ~L2-sized
+// filter (config 3) plain reds hit L2 often enough that the partition passes
+// cost more than they save (39.1 vs 55.8 Gkeys/s). Lookups switch earlier
+// (resolve_find). Both need at least half a key per block, or the slices'
+// lines are fetched for too few keys.
 bool blocked_pays(const sbbf_gpu* f, uint64_t n) {
   return f->nb * 32 > 2 * static_cast<uint64_t>(f->di.l2_bytes) && n >= f->nb / 2;
 }
