@@ -12,7 +12,9 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsbbf_gpu.so")
+# SBBF_LIB=debug selects libsbbf_gpu_debug.so (device-side bounds checks)
+LIB_PATH = os.path.join(HERE, "libsbbf_gpu_debug.so" if os.environ.get("SBBF_LIB") == "debug"
+                        else "libsbbf_gpu.so")
 
 SBBF_OK = 0
 SBBF_EINVAL = -1

@@ -368,6 +368,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) bucket_scatter_k
     for (uint32_t i = threadIdx.x; i < cnt; i += kPartThreads) {
       const uint32_t b = sm.bk[i];
       const uint64_t slot = sm.gbase[b] + (i - sm.boff[b]);
+      SBBF_DCHECK(b < bm.S && i >= sm.boff[b] && (routed || slot < n));
       if (routed)
         sm.dst[b][slot - sm.bstart[b]] = sm.key[i];  // consecutive threads -> consecutive peer slots
       else
@@ -562,6 +563,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
     for (int j = 0; j < kPartPerThread; ++j) {
       if (bk[j] != 0xffffffffu) {
         const uint32_t loc = sm.boff[bk[j]] + sm.wcnt[warp][bk[j]] + off[j];
+        SBBF_DCHECK(loc < cnt && bk[j] < bm.S);
         sm.key[loc] = h[j];
         sm.pos[loc] = static_cast<uint16_t>(j * kPartThreads + threadIdx.x);
       }
@@ -620,6 +622,7 @@ __global__ void __launch_bounds__(kSegThreads, kMinB)
       if (ch < c_end) {
         st = boffs[ch * kBoffStride + b];
         en = boffs[ch * kBoffStride + b + 1];
+        SBBF_DCHECK(st <= en && en <= boffs[ch * kBoffStride + kMaxBuckets] && ch * kPartChunk + en <= m);
       }
       seg[q] = ch * kPartChunk + st;
       len[q] = en - st;
@@ -713,11 +716,16 @@ __global__ void __launch_bounds__(kUnpermThreads, 4) unpermute_kernel(const uint
       const uint32_t pw[4] = {pv[k].x, pv[k].y, pv[k].z, pv[k].w};
       const uint32_t aw[2] = {av[k].x, av[k].y};
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
+      for (int e = 0; e < 8; ++e) {
+        SBBF_DCHECK(((pw[e >> 1] >> ((e & 1) * 16)) & 0xffffu) < kPartChunk);
         a[(pw[e >> 1] >> ((e & 1) * 16)) & 0xffffu] = static_cast<uint8_t>(aw[e >> 2] >> ((e & 3) * 8));
+      }
     }
   } else {
-    for (uint32_t i = threadIdx.x; i < cnt; i += kUnpermThreads) a[pos16[base + i]] = ans[base + i];
+    for (uint32_t i = threadIdx.x; i < cnt; i += kUnpermThreads) {
+      SBBF_DCHECK(pos16[base + i] < cnt);
+      a[pos16[base + i]] = ans[base + i];
+    }
   }
   __syncthreads();
   if (bits) {

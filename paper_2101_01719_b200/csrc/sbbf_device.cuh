@@ -9,6 +9,23 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
+
+// Device-side bounds checks for the debug build (`make debug`:
+// libsbbf_gpu_debug.so, -DSBBF_DEBUG). compute-sanitizer is unavailable on
+// the GPU pool, so the test suite runs once against this build instead; a
+// failed check prints its location and traps. Compiled out otherwise.
+#ifdef SBBF_DEBUG
+#define SBBF_DCHECK(c)                                                               \
+  do {                                                                               \
+    if (!(c)) {                                                                      \
+      printf("SBBF_DCHECK failed: %s at %s:%d\n", #c, __FILE__, __LINE__);           \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+#else
+#define SBBF_DCHECK(c) ((void)0)
+#endif
 
 namespace sbbf {
 namespace dev {

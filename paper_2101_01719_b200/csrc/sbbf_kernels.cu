@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       lo[u] = static_cast<uint32_t>(hn[u]);
+      SBBF_DCHECK(dev::block_index(hn[u], nb) < nb);
       dev::ld_block_nc(blocks + dev::block_index(hn[u], nb) * 8, b[u]);
     }
     const uint64_t tn = t + nwarps;

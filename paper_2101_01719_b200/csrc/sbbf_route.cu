@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kWinThreads, 4) window_insert_kernel(uint32_t*
     uint64_t h = 0;
     if (idx < n) {
       const uint32_t r = region_of(prefix, P, idx);
+      SBBF_DCHECK(r < P && idx - prefix[r] < R);
       h = dev::ld_stream_u64(keys + r * R + (idx - prefix[r]), pol);
     }
     const uint32_t valid = __ballot_sync(0xffffffffu, idx < n);
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(kWinThreads, 3) window_find_kernel(const uint3
       h[u] = 0;
       if (idx < n) {
         const uint32_t r = region_of(prefix, P, idx);
+        SBBF_DCHECK(r < P && idx - prefix[r] < R);
         slot[u] = r * R + (idx - prefix[r]);
         h[u] = dev::ld_stream_u64(keys + slot[u], pol);
       }
@@ -163,6 +165,7 @@ __global__ void __launch_bounds__(kWinThreads) combine_kernel(const unsigned lon
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWinThreads;
   for (uint64_t s = static_cast<uint64_t>(blockIdx.x) * kWinThreads + threadIdx.x; s < n; s += stride) {
     const uint32_t r = region_of(prefix, P, s);
+    SBBF_DCHECK(r < P && pos[s] < n);
     out[pos[s]] = src[r][s - prefix[r]];
   }
 }

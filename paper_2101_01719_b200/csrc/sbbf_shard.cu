@@ -114,8 +114,10 @@ __global__ void __launch_bounds__(kShardThreads) shard_scatter_kernel(
 __global__ void scatter_u8_kernel(const uint8_t* __restrict__ src, const uint32_t* __restrict__ pos,
                                   uint64_t n, uint8_t* __restrict__ dst) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    SBBF_DCHECK(pos[i] < n);
     dst[pos[i]] = src[i];
+  }
 }
 
 __global__ void pack_bits_kernel(const uint8_t* __restrict__ src, uint64_t n, uint32_t* __restrict__ bits) {
