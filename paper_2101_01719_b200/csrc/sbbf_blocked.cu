@@ -694,12 +694,16 @@ constexpr int kUnpermThreads = 256;
 
 __global__ void __launch_bounds__(kUnpermThreads, 4) unpermute_kernel(const uint8_t* __restrict__ ans,
                                                                    const uint16_t* __restrict__ pos16, uint64_t m,
-                                                                   void* __restrict__ out, bool bits) {
+                                                                   void* __restrict__ out, bool bits,
+                                                                   const uint16_t* __restrict__ boffs = nullptr) {
   static_assert(kPartChunk <= 65536, "positions are 16-bit");
   __shared__ __align__(16) uint8_t a[kPartChunk];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kPartChunk;
-  const uint32_t cnt = static_cast<uint32_t>(m - base < kPartChunk ? m - base : kPartChunk);
+  // chunks laid out region by region (blocked_find_regions) carry their own
+  // key count; otherwise every chunk but the last is full
+  const uint32_t cnt = boffs ? boffs[static_cast<uint64_t>(blockIdx.x) * kBoffStride + kMaxBuckets]
+                             : static_cast<uint32_t>(m - base < kPartChunk ? m - base : kPartChunk);
   if (cnt == kPartChunk) {
     // full chunk: 8 positions (16 B) + 8 answers (8 B) per vector load
     constexpr int kVec = kPartChunk / (kUnpermThreads * 8);
@@ -965,6 +969,68 @@ cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geo
   if (tl.ans) cudaFreeAsync(tl.ans, s);
   if (tl.bytes) cudaFreeAsync(tl.bytes, s);
   if (tl.counts) cudaFreeAsync(tl.counts, s);
+  return e;
+}
+
+// Keys given as several arrays (a rank's receive-window regions): each
+// region's chunks take consecutive chunk slots of one scratch, so a single
+// segment pass — one sweep of the filter through L2 — covers them all, with
+// no staging copy. Single-level plans and batches up to kBlockedChunk keys;
+// anything else returns cudaErrorNotSupported (the caller gathers instead).
+namespace {
+uint64_t region_chunks(const uint64_t* counts, uint32_t nr, std::vector<uint64_t>& off) {
+  off.assign(nr + 1, 0);
+  for (uint32_t r = 0; r < nr; ++r) off[r + 1] = off[r] + (counts[r] + kPartChunk - 1) / kPartChunk;
+  return off[nr];
+}
+}  // namespace
+
+cudaError_t blocked_insert_regions(const DeviceInfo& di, uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
+                                   const uint64_t* const* keys, const uint64_t* counts, uint32_t nr, cudaStream_t s) {
+  std::vector<uint64_t> off;
+  const uint64_t C = region_chunks(counts, nr, off);
+  if (plan.super_parts > 1 || C * kPartChunk > kBlockedChunk) return cudaErrorNotSupported;
+  if (C == 0) return cudaSuccess;
+  Scratch sc;
+  cudaError_t e = alloc_scratch(sc, C * kPartChunk, false, s);
+  for (uint32_t r = 0; e == cudaSuccess && r < nr; ++r)
+    if (counts[r])
+      e = chunk_partition(di, g, plan.parts, keys[r], counts[r], sc.keys + off[r] * kPartChunk, nullptr,
+                          sc.boffs + off[r] * kBoffStride, s);
+  if (e == cudaSuccess) e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, plan.parts, C * kPartChunk, nullptr, s);
+  free_scratch(sc, s);
+  return e;
+}
+
+cudaError_t blocked_find_regions(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
+                                 const uint64_t* const* keys, const uint64_t* counts, uint32_t nr, uint8_t* const* outs,
+                                 cudaStream_t s) {
+  std::vector<uint64_t> off;
+  const uint64_t C = region_chunks(counts, nr, off);
+  if (plan.super_parts > 1 || C * kPartChunk > kBlockedChunk) return cudaErrorNotSupported;
+  if (C == 0) return cudaSuccess;
+  Scratch sc;
+  uint8_t* bytes = nullptr;  // answers in the chunk layout: region r's at off[r] * kPartChunk
+  cudaError_t e = alloc_scratch(sc, C * kPartChunk, true, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&bytes), C * kPartChunk, s);
+  for (uint32_t r = 0; e == cudaSuccess && r < nr; ++r)
+    if (counts[r])
+      e = chunk_partition(di, g, plan.parts, keys[r], counts[r], sc.keys + off[r] * kPartChunk,
+                          sc.pos16 + off[r] * kPartChunk, sc.boffs + off[r] * kBoffStride, s);
+  if (e == cudaSuccess)
+    e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, plan.parts, C * kPartChunk,
+                               sc.ans, s);
+  if (e == cudaSuccess) {
+    note_launch();
+    unpermute_kernel<<<static_cast<unsigned>(C), kUnpermThreads, 0, s>>>(sc.ans, sc.pos16, C * kPartChunk, bytes,
+                                                                         false, sc.boffs);
+    e = cudaGetLastError();
+  }
+  for (uint32_t r = 0; e == cudaSuccess && r < nr; ++r)
+    if (counts[r])
+      e = cudaMemcpyAsync(outs[r], bytes + off[r] * kPartChunk, counts[r], cudaMemcpyDeviceToDevice, s);
+  if (bytes) cudaFreeAsync(bytes, s);
+  free_scratch(sc, s);
   return e;
 }
 

@@ -264,6 +264,54 @@ int host_pipeline(sbbf_gpu* f, HostOp op, const uint64_t* h_hashes, uint64_t n, 
 
 }  // namespace
 
+namespace sbbf {
+
+int gpu_insert_regions(sbbf_gpu_t* f, const uint64_t* const* keys, const uint64_t* counts, uint32_t nr,
+                       cudaStream_t s, bool* handled) {
+  *handled = false;
+  uint64_t total = 0;
+  for (uint32_t r = 0; r < nr; ++r) total += counts[r];
+  if (total == 0) {
+    *handled = true;
+    return SBBF_OK;
+  }
+  if (resolve_insert(f, total) != SBBF_INSERT_BLOCKED) return SBBF_OK;
+  DeviceGuard g(f->di.device);
+  if (ensure_plan(f) != SBBF_OK) return SBBF_ENOMEM;
+  const cudaError_t e = blocked_insert_regions(f->di, f->d_blocks, f->geom, f->plan, keys, counts, nr, s);
+  if (e == cudaErrorNotSupported) {
+    cudaGetLastError();
+    return SBBF_OK;
+  }
+  *handled = true;
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "blocked_insert_regions");
+}
+
+int gpu_find_regions(const sbbf_gpu_t* fc, const uint64_t* const* keys, const uint64_t* counts, uint32_t nr,
+                     uint8_t* const* outs, cudaStream_t s, bool* handled) {
+  auto* f = const_cast<sbbf_gpu*>(fc);
+  *handled = false;
+  uint64_t total = 0;
+  for (uint32_t r = 0; r < nr; ++r) total += counts[r];
+  if (total == 0) {
+    *handled = true;
+    return SBBF_OK;
+  }
+  if (resolve_find(f, total) != SBBF_FIND_BLOCKED) return SBBF_OK;
+  DeviceGuard g(f->di.device);
+  if (ensure_plan(f) != SBBF_OK) return SBBF_ENOMEM;
+  const cudaError_t e = blocked_find_regions(f->di, f->d_blocks, f->geom, f->plan, keys, counts, nr, outs, s);
+  if (e == cudaErrorNotSupported) {
+    cudaGetLastError();
+    return SBBF_OK;
+  }
+  *handled = true;
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "blocked_find_regions");
+}
+
+}  // namespace sbbf
+
+
 extern "C" {
 
 int sbbf_gpu_abi_version(void) { return SBBF_GPU_ABI_VERSION; }

@@ -91,6 +91,23 @@ cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g
 cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
                          const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s);
 
+// The same over several key arrays at once (a rank's receive-window
+// regions): one filter sweep, no staging copy. cudaErrorNotSupported when
+// the plan is two-level or the regions exceed one blocked round.
+cudaError_t blocked_insert_regions(const DeviceInfo& di, uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
+                                   const uint64_t* const* keys, const uint64_t* counts, uint32_t nr, cudaStream_t s);
+cudaError_t blocked_find_regions(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
+                                 const uint64_t* const* keys, const uint64_t* counts, uint32_t nr, uint8_t* const* outs,
+                                 cudaStream_t s);
+
+// Filter-handle entry points for the route layer (sbbf_capi.cu): the blocked
+// region path when AUTO would block the gathered batch; *handled = false
+// otherwise (the caller gathers and uses the public ABI).
+int gpu_insert_regions(sbbf_gpu_t* f, const uint64_t* const* keys, const uint64_t* counts, uint32_t nr,
+                       cudaStream_t s, bool* handled);
+int gpu_find_regions(const sbbf_gpu_t* f, const uint64_t* const* keys, const uint64_t* counts, uint32_t nr,
+                     uint8_t* const* outs, cudaStream_t s, bool* handled);
+
 // XXH64 key frontend (kHasherXxh64): hashing kernels and fused insert/find.
 cudaError_t launch_hash_u64(const uint64_t* keys, uint64_t n, uint64_t seed, uint64_t* out, cudaStream_t s);
 cudaError_t launch_hash_bytes(const uint8_t* data, const uint64_t* offsets, uint64_t n, uint64_t seed,

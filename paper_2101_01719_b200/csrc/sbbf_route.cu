@@ -436,10 +436,17 @@ int sbbf_route_insert_window(sbbf_route_t* rt, sbbf_gpu_t* shard, void* stream) 
     std::vector<uint64_t> cnt(rt->parts);
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     int rc = window_counts(rt, p, s, cnt.data());
+    // the regions go straight into one blocked pass (one sweep of the shard
+    // through L2, no staging copy) ...
+    std::vector<const uint64_t*> ptrs(rt->parts);
+    for (uint32_t r = 0; r < rt->parts; ++r)
+      ptrs[r] = reinterpret_cast<const uint64_t*>(rt->window + keys_off(rt, p, r));
+    bool handled = false;
+    if (rc == SBBF_OK) rc = sbbf::gpu_insert_regions(shard, ptrs.data(), cnt.data(), rt->parts, s, &handled);
+    if (rc != SBBF_OK || handled) return rc;
+    // ... or, when the shard's plan cannot take regions, into one gathered batch
     uint64_t* keys = nullptr;
     uint64_t total = 0;
-    // one contiguous batch, so the blocked pass streams the shard through L2
-    // once per call rather than once per source region
     if (rc == SBBF_OK) rc = gather_regions(rt, p, cnt, s, &keys, &total);
     if (rc == SBBF_OK && total) rc = sbbf_gpu_insert_batch(shard, keys, total, stream);
     if (keys) cudaFreeAsync(keys, s);
@@ -464,6 +471,15 @@ int sbbf_route_find_window(sbbf_route_t* rt, const sbbf_gpu_t* shard, void* stre
     std::vector<uint64_t> cnt(rt->parts);
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     int rc = window_counts(rt, p, s, cnt.data());
+    std::vector<const uint64_t*> ptrs(rt->parts);
+    std::vector<uint8_t*> outs(rt->parts);
+    for (uint32_t r = 0; r < rt->parts; ++r) {
+      ptrs[r] = reinterpret_cast<const uint64_t*>(rt->window + keys_off(rt, p, r));
+      outs[r] = rt->window + res_off(rt, p, r);
+    }
+    bool handled = false;
+    if (rc == SBBF_OK) rc = sbbf::gpu_find_regions(shard, ptrs.data(), cnt.data(), rt->parts, outs.data(), s, &handled);
+    if (rc != SBBF_OK || handled) return rc;
     uint64_t* keys = nullptr;
     uint64_t total = 0;
     uint8_t* ans = nullptr;

@@ -412,18 +412,21 @@ def test_fused_ipc_processes(cuda, oracle, world, total):
 
 
 @pytest.mark.gpu
-def test_fused_route_big_shards(cuda, oracle):
-    """Shards beyond 2 x L2 (the config-5 regime): the owner's window ops go
-    through the L2-blocked path region by region; still bit-exact."""
+@pytest.mark.parametrize("per_source", [1_500_000, 5_300_000])
+def test_fused_route_big_shards(cuda, oracle, per_source):
+    """Shards beyond 2 x L2 (the config-5 regime). With few keys per owner
+    the window goes through the direct path (gathered); with at least half a
+    key per block, the blocked path takes the source regions as they are (one
+    filter sweep, no staging copy). Bit-exact either way."""
     parts, total = 2, 2 * (300 << 20) // 32 + 3
     ops = S.CudaShardOps(0)
     bounds = S.shard_bounds(total, parts)
     db = ops._dev_bounds(bounds)
     shards = [ops.create(total, bounds[r], bounds[r + 1] - bounds[r]) for r in range(parts)]
     assert all(s.size_bytes() > 2 * (126 << 20) for s in shards)
-    routes = _linked_routes(parts, 1 << 21)
+    routes = _linked_routes(parts, 1 << 23)
     rng = np.random.default_rng(4242)
-    batch = [rng.integers(0, 2**64, size=1_500_000 + 77 * r, dtype=np.uint64) for r in range(parts)]
+    batch = [rng.integers(0, 2**64, size=per_source + 77 * r, dtype=np.uint64) for r in range(parts)]
     for r in range(parts):
         routes[r].dispatch(torch.from_numpy(batch[r].view(np.int64)).to(cuda), total, db, keep_positions=False)
     for r in range(parts):
@@ -431,7 +434,7 @@ def test_fused_route_big_shards(cuda, oracle):
     want = oracle.build(total, np.concatenate(batch))
     for r in range(parts):
         assert np.array_equal(shards[r].blocks(), want[bounds[r]:bounds[r + 1]]), r
-    looks = [np.concatenate([batch[1 - r][:400_000], rng.integers(0, 2**64, size=900_000, dtype=np.uint64)])
+    looks = [np.concatenate([batch[1 - r][:per_source // 4], rng.integers(0, 2**64, size=per_source, dtype=np.uint64)])
              for r in range(parts)]
     for r in range(parts):
         routes[r].dispatch(torch.from_numpy(looks[r].view(np.int64)).to(cuda), total, db, keep_positions=True)
