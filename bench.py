@@ -260,6 +260,54 @@ def run_keys_frontend(steps: int, device) -> dict:
             "value": (N + L) / (ms * 1e-3) / 1e9, "unit": "Gkeys/s"}
 
 
+def run_widened(device) -> dict:
+    """SURVEY.md §8(f) rows measured beside the reference's CPU path
+    (oracle/_ref, this host): the FilterImage CRC / serialize of a 1 GiB
+    filter and the fpp-sim experiment. Reported, not the headline."""
+    import numpy as np
+    import torch
+
+    import oracle as O
+    from paper_2101_01719_b200 import SplitBlockFilter
+    from paper_2101_01719_b200.fppsim import fpp_sim
+
+    out = {}
+    nb = 1 << 25  # config 4's 1 GiB
+    f = SplitBlockFilter(nb, device=device.index or 0)
+    f.add_keys(torch.arange(1 << 24, dtype=torch.int64, device=device))
+    f.image_crc()
+    torch.cuda.synchronize(device)
+    t0 = time.perf_counter()
+    for _ in range(5):
+        f.image_crc()                      # device CRC-32 of the 1 GiB block array
+    t_crc = (time.perf_counter() - t0) / 5
+    t0 = time.perf_counter()
+    img = f.serialize()                    # D2H of the image + device CRC
+    t_ser = time.perf_counter() - t0
+    del f
+    sample = np.frombuffer(img, np.uint8)[: 64 << 20]
+    ref = O.Reference()
+    t0 = time.perf_counter()
+    ref.crc32(sample.tobytes())
+    t_ref = time.perf_counter() - t0
+    out["image"] = {"filter_bytes": nb * 32, "gpu_crc_gbs": nb * 32 / t_crc / 1e9,
+                    "gpu_serialize_gbs": len(img) / t_ser / 1e9,
+                    "reference_crc_gbs": sample.size / t_ref / 1e9,
+                    "reference_sample": "crc32_ieee over the first 64 MiB of the same image, 1 thread"}
+    r = fpp_sim(100_000_000, 128 << 20, 10_000_000, 20160216, huge_ok=True, device=device.index or 0)
+    r.pop("filter", None)
+    t0 = time.perf_counter()
+    fp_ref, _ = ref.fpp_sim(1_000_000, 1 << 20, 1_000_000, 20160216)
+    t_ref = time.perf_counter() - t0
+    out["fpp_sim"] = {"gpu": {"ndv": r["ndv"], "filter_bytes": r["filter_bytes"], "queries": r["negative_queries"],
+                              "wall_s": r["wall_time_s"], "insert_mops": r["million_ops_per_sec"],
+                              "measured_fpp": r["measured_fpp"], "model_fpp": r["model_fpp"]},
+                      "reference": {"ndv": 1_000_000, "filter_bytes": 1 << 20, "queries": 1_000_000,
+                                    "wall_s": t_ref, "ops_per_s_m": 2e6 / t_ref / 1e6,
+                                    "note": "run_fpp_sim's loop on one thread (add_hash / find_hash per key)"}}
+    return out
+
+
 def sector_ceiling(device, filter_bytes: int, red: bool = False, n: int = 1 << 28) -> float:
     """Random 32-B sector rate (G sectors/s) on a buffer of filter_bytes."""
     import ctypes as C
@@ -609,6 +657,11 @@ def main() -> None:
     }
     if args.config == 2:
         line["keys_frontend"] = run_keys_frontend(max(3, min(args.steps, 10)), device)
+        if not args.no_cpu_baseline:
+            try:
+                line["widened"] = run_widened(device)
+            except Exception as exc:  # the extra rows never block the headline line
+                line["widened"] = {"error": repr(exc)}
     if not args.no_e2e:
         line["e2e"] = run_e2e(args.config, max(3, min(args.steps, 10)), device)
     if not args.no_cpu_baseline:
