@@ -17,7 +17,7 @@ def dev(a, cuda):
     return torch.from_numpy(np.ascontiguousarray(a, np.uint64).view(np.int64)).to(cuda)
 
 
-@pytest.mark.parametrize("nb", [1, 2, 3, 7, 255, 256, 2048, 2049, 4096, 65537, 1 << 20])
+@pytest.mark.parametrize("nb", [1, 2, 3, 7, 255, 256, 2048, 2049, 4096, 65537, 1 << 20, 9_470_000 + 2049])
 @pytest.mark.parametrize("hasher_id", [0, 1])
 def test_image_matches_oracle(cuda, oracle, nb, hasher_id):
     rng = np.random.default_rng(nb)
