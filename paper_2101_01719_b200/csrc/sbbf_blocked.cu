@@ -29,6 +29,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 #include "sbbf_device.cuh"
@@ -845,6 +846,15 @@ cudaError_t route_partition(const DeviceInfo& di, uint64_t total, uint32_t parts
 
 namespace {
 
+// SBBF_BLOCKED_PIPELINE=0 disables the overlapped multi-round lookup (A/B only).
+bool pipeline_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("SBBF_BLOCKED_PIPELINE");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 // One batch chunk (m <= kBlockedChunk keys) through the single-level path.
 cudaError_t insert_chunk(const DeviceInfo& di, uint32_t* blocks, const Geom& g, uint32_t parts, const uint64_t* keys,
                          uint64_t m, Scratch& sc, cudaStream_t s) {
@@ -929,9 +939,75 @@ cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g
   return e;
 }
 
+namespace {
+
+// Batches of several rounds (single-level plans): round c+1's chunk_scatter
+// runs on a high-priority side stream while round c is probed and
+// un-permuted on the caller's stream, with double-buffered scratch. The
+// scatter is issue/barrier bound and the probe L1/L2-sector bound, so the
+// two overlap on the SMs. Events fork from and join back into `s` (CUDA
+// graph capture safe).
+cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks, const Geom& g,
+                                   const BlockedPlan& plan, const uint64_t* hashes, uint64_t n, void* out,
+                                   bool bits, cudaStream_t s) {
+  const uint64_t cap = kBlockedChunk;
+  Scratch sc[2];
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_in = nullptr, ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+  int least = 0, greatest = 0;
+  cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, greatest);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    e = cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = alloc_scratch(sc[k], cap, true, s);
+  }
+  // the side stream starts behind everything already queued on s (the
+  // caller's hashes and the scratch allocations)
+  if (e == cudaSuccess) e = cudaEventRecord(ev_in, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_in, 0);
+  uint64_t c = 0;
+  for (uint64_t off = 0; e == cudaSuccess && off < n; off += cap, ++c) {
+    const uint64_t m = n - off < cap ? n - off : cap;
+    const int k = static_cast<int>(c & 1);
+    void* dst = bits ? static_cast<void*>(static_cast<uint32_t*>(out) + off / 32)
+                     : static_cast<void*>(static_cast<uint8_t*>(out) + off);
+    if (c >= 2) e = cudaStreamWaitEvent(side, freed[k], 0);  // round c-2 done with this scratch
+    if (e == cudaSuccess) e = chunk_partition(di, g, plan.parts, hashes + off, m, sc[k].keys, sc[k].pos16,
+                                              sc[k].boffs, side);
+    if (e == cudaSuccess) e = cudaEventRecord(ready[k], side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ready[k], 0);
+    if (e == cudaSuccess)
+      e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc[k].keys, sc[k].boffs, plan.parts, m,
+                                 sc[k].ans, s);
+    if (e == cudaSuccess) {
+      note_launch();
+      unpermute_kernel<<<static_cast<unsigned>((m + kPartChunk - 1) / kPartChunk), kUnpermThreads, 0, s>>>(
+          sc[k].ans, sc[k].pos16, m, dst, bits);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(freed[k], s);
+  }
+  // every side-stream launch was joined into s through ready[]; the scratch
+  // frees are ordered on s behind the last un-permute
+  for (int k = 0; k < 2; ++k) free_scratch(sc[k], s);
+  if (side) cudaStreamDestroy(side);
+  if (ev_in) cudaEventDestroy(ev_in);
+  for (int k = 0; k < 2; ++k) {
+    if (ready[k]) cudaEventDestroy(ready[k]);
+    if (freed[k]) cudaEventDestroy(freed[k]);
+  }
+  return e;
+}
+
+}  // namespace
+
 cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
                          const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
+  if (plan.super_parts == 1 && n > kBlockedChunk && pipeline_enabled())
+    return blocked_find_pipelined(di, blocks, g, plan, hashes, n, out, bits, s);
   const uint64_t cap = n < kBlockedChunk ? n : kBlockedChunk;  // a multiple of 32 unless n is the whole batch
   Scratch sc;
   TwoLevel tl;

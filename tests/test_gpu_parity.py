@@ -422,3 +422,40 @@ def test_cuda_graph_capture(cuda, oracle, nb, variant):
         torch.cuda.synchronize()
         assert np.array_equal(f.blocks(), want)
         assert np.array_equal(bits_to_bytes(u32(bits), look.size), oracle.find_hashes(want, look))
+
+
+def test_blocked_pipelined_rounds(cuda, oracle):
+    """Lookups beyond one blocked round (2^28 keys) overlap round c+1's
+    partition with round c's probe on a side stream, double-buffered. Bytes
+    and bits must equal the direct lookup's (itself oracle-checked), also
+    when the call is captured into a CUDA graph (fork/join on events)."""
+    nb = (1 << 23) + 777                       # 256 MiB: blocked lookups
+    rng = np.random.default_rng(1234)
+    hs = rng.integers(0, 2**64, size=2_000_003, dtype=np.uint64)
+    f = SplitBlockFilter(nb)
+    f.add_hashes(dev(hs, cuda))
+    want_blocks = oracle.build(nb, hs)
+    assert np.array_equal(f.blocks(), want_blocks)
+    n = (1 << 28) + 4096 * 3 + 17              # two rounds, the second ragged
+    look = torch.randint(-2**63, 2**63 - 1, (n,), dtype=torch.int64, device=cuda)
+    look[: hs.size] = dev(hs, cuda)            # members in the first round
+    look[n - 1000:] = dev(hs[:1000], cuda)     # and at the very end
+    f.set_find_variant(_lib.FIND_GLOBAL)
+    want = f.find_hashes(look)
+    want_bits = f.find_hashes_bits(look)
+    f.set_find_variant(_lib.FIND_BLOCKED)
+    assert torch.equal(f.find_hashes(look), want)
+    bits = f.find_hashes_bits(look)
+    assert torch.equal(bits, want_bits)
+    sample = look[-300_000:].cpu().numpy().view(np.uint64)
+    assert np.array_equal(want[-300_000:].cpu().numpy(), oracle.find_hashes(want_blocks, sample))
+    assert int(want[: hs.size].sum()) == hs.size and int(want[n - 1000:].sum()) == 1000
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        f.find_hashes_bits(look, bits)
+    bits.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(bits, want_bits)
