@@ -399,9 +399,11 @@ def run_e2e(cid: int, steps: int, device) -> dict:
 # --------------------------------------------------------------------------------
 # CPU baseline: the reference itself (oracle/_ref), run_bench's method
 # --------------------------------------------------------------------------------
-def cpu_reference_run(cid: int, reps: int, threads: int, device=None, sample: int | None = None) -> dict:
+def cpu_reference_run(cid: int, reps: int, threads: int, device=None, sample: int | None = None,
+                      warmup: int = 0) -> dict:
     """sample (config 5): the step is `sample` inserts + `sample` lookups of
-    config 5's streams (the sharded arm's whole-job sample), not 8e9 + 8e9."""
+    config 5's streams (the sharded arm's whole-job sample), not 8e9 + 8e9.
+    The first `warmup` reps run untimed (dropped)."""
     import dataclasses
 
     import numpy as np
@@ -423,13 +425,14 @@ def cpu_reference_run(cid: int, reps: int, threads: int, device=None, sample: in
     try:
         ref = O.Reference()
         kind = "reference"
-        ti, tl, res, blocks = ref.time_build_probe(cfg.num_buckets, ins, look, threads, reps)
+        ti, tl, res, blocks = ref.time_build_probe(cfg.num_buckets, ins, look, threads, warmup + reps)
+        ti, tl = ti[warmup:], tl[warmup:]
         # lookups on one core as well as on all of them
         tl1 = ref.time_build_probe(cfg.num_buckets, ins, look, 1, 3)[1] if threads > 1 and not sample else tl
     except (FileNotFoundError, OSError):
         kind = "port"
         ti, tl = [], []
-        for _ in range(reps):
+        for r in range(warmup + reps):
             b = orc.new_blocks(cfg.num_buckets)
             t0 = time.perf_counter()
             orc.add_hashes(b, ins)
@@ -437,6 +440,9 @@ def cpu_reference_run(cid: int, reps: int, threads: int, device=None, sample: in
             t0 = time.perf_counter()
             res = orc.find_hashes(b, look, threads)
             tl.append(time.perf_counter() - t0)
+            if r < warmup:
+                ti.pop()
+                tl.pop()
         blocks = b
         tl1 = tl
     mi, ml = statistics.median(ti), statistics.median(tl)
@@ -463,12 +469,12 @@ def run_reference_arm(args) -> None:
     # stays within minutes; the metric is a rate
     sample = min(args.sample_keys * world, 1 << 28) if args.config == 5 else None
     reps = max(args.steps, 3) if sample is None else 3  # config 5: each rep builds an 8 GiB filter
-    r = cpu_reference_run(args.config, reps, threads, sample=sample)
+    r = cpu_reference_run(args.config, reps, threads, sample=sample, warmup=args.warmup)
     from paper_2101_01719_b200 import workload as W
     cfg = W.CONFIGS[args.config]
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "Gkeys/s",
-        "n_gpus": args.gpus, "steps": reps, "warmup": 0,
+        "n_gpus": args.gpus, "steps": reps, "warmup": args.warmup,
         "ms_per_step": ((2 * sample) if sample else (cfg.inserts.n + cfg.lookups.n)) / r["value"] / 1e6,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (seeded splitmix64 hash streams, BASELINE.json)",
