@@ -30,6 +30,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "sbbf_device.cuh"
@@ -941,6 +942,31 @@ cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g
 
 namespace {
 
+struct PipeCtx {
+  std::mutex mu;
+  bool ready_ok = false;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_in = nullptr, ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+  cudaError_t init() {  // under mu
+    if (ready_ok) return cudaSuccess;
+    int least = 0, greatest = 0;
+    cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (e == cudaSuccess && !side) e = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, greatest);
+    if (e == cudaSuccess && !ev_in) e = cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming);
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+      if (!ready[k]) e = cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming);
+      if (e == cudaSuccess && !freed[k]) e = cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming);
+    }
+    ready_ok = e == cudaSuccess;
+    return e;
+  }
+};
+
+PipeCtx& pipe_ctx(int device) {  // per device ordinal, never destroyed (process lifetime)
+  static PipeCtx ctx[64];
+  return ctx[device & 63];
+}
+
 // Batches of several rounds (single-level plans): round c+1's chunk_scatter
 // runs on a high-priority side stream while round c is probed and
 // un-permuted on the caller's stream, with double-buffered scratch. The
@@ -952,17 +978,15 @@ cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks,
                                    bool bits, cudaStream_t s) {
   const uint64_t cap = kBlockedChunk;
   Scratch sc[2];
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_in = nullptr, ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
-  int least = 0, greatest = 0;
-  cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
-  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, greatest);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming);
-  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
-    e = cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = alloc_scratch(sc[k], cap, true, s);
-  }
+  // one side stream and event set per device, created once (creating them per
+  // call put 7-13 ms outliers into config-4 steps); the lock serialises the
+  // enqueue of concurrent callers, the device work stays stream-ordered
+  PipeCtx& ctx = pipe_ctx(di.device);
+  std::lock_guard<std::mutex> lock(ctx.mu);
+  cudaError_t e = ctx.init();
+  cudaStream_t side = ctx.side;
+  cudaEvent_t ev_in = ctx.ev_in, *ready = ctx.ready, *freed = ctx.freed;
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = alloc_scratch(sc[k], cap, true, s);
   // the side stream starts behind everything already queued on s (the
   // caller's hashes and the scratch allocations)
   if (e == cudaSuccess) e = cudaEventRecord(ev_in, s);
@@ -992,12 +1016,6 @@ cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks,
   // every side-stream launch was joined into s through ready[]; the scratch
   // frees are ordered on s behind the last un-permute
   for (int k = 0; k < 2; ++k) free_scratch(sc[k], s);
-  if (side) cudaStreamDestroy(side);
-  if (ev_in) cudaEventDestroy(ev_in);
-  for (int k = 0; k < 2; ++k) {
-    if (ready[k]) cudaEventDestroy(ready[k]);
-    if (freed[k]) cudaEventDestroy(freed[k]);
-  }
   return e;
 }
 

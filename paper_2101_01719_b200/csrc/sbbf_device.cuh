@@ -232,6 +232,10 @@ __device__ __forceinline__ void red_or64(uint64_t* p, uint64_t v, uint64_t polic
                : "memory");
 }
 
+__device__ __forceinline__ void red_or64_nohint(uint64_t* p, uint64_t v) {
+  asm volatile("red.relaxed.gpu.global.or.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ uint64_t ld_pair(const uint64_t* p, uint64_t policy) {
   uint64_t v;
   asm volatile("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(policy));

@@ -32,6 +32,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 
 #include "sbbf_device.cuh"
 #include "sbbf_internal.h"
@@ -105,7 +106,10 @@ __global__ void __launch_bounds__(kThreads, 4) insert_lane8_kernel(uint32_t* __r
 // (little-endian lanes, filter.hpp:23-24).
 // kKeys: the input is u64 keys, hashed on the fly with XXH64(seed) (the
 // reference's kHasherXxh64 frontend fused into the insert).
-template <bool kTest, bool kKeys = false, int kT = 4>
+// kHint: reds carry an L2 evict-last policy (filters near or beyond L2 size);
+// without it an L2-resident filter's 1M-key insert is 1.2 us faster
+// (scripts/microbench_red.cu: 15.2 vs 16.4 us).
+template <bool kTest, bool kKeys = false, int kT = 4, bool kHint = true>
 __global__ void __launch_bounds__(kThreads, 4) insert_wide_kernel(uint32_t* __restrict__ blocks, Geom g,
                                                                   const uint64_t* __restrict__ hashes,
                                                                   uint64_t n, uint64_t seed = 0) {
@@ -158,8 +162,11 @@ __global__ void __launch_bounds__(kThreads, 4) insert_wide_kernel(uint32_t* __re
           if (mask[r] & ~cur[r]) dev::red_or64(ptr[r], mask[r], keep);
       } else {
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (mask[r]) dev::red_or64(ptr[r], mask[r], keep);
+        for (int r = 0; r < 4; ++r) {
+          if (!mask[r]) continue;
+          if constexpr (kHint) dev::red_or64(ptr[r], mask[r], keep);
+          else dev::red_or64_nohint(ptr[r], mask[r]);
+        }
       }
     }
   }
@@ -497,6 +504,17 @@ uint64_t grid_for(uint64_t work_items, uint64_t items_per_block, int sms, int pe
   return g < 1 ? 1 : g;
 }
 
+// Evict-last hints on the insert reds only pay where the filter competes for
+// L2 (> L2 / 2); SBBF_RED_HINT=0/1 forces either (A/B only).
+bool red_hint(const DeviceInfo& di, const Geom& g) {
+  static const int force = [] {
+    const char* v = getenv("SBBF_RED_HINT");
+    return v ? atoi(v) : -1;
+  }();
+  if (force >= 0) return force != 0;
+  return g.nb_local * 32 * 2 > static_cast<uint64_t>(di.l2_bytes);
+}
+
 cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, const Geom& g,
                           const uint64_t* hashes, uint64_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
@@ -523,7 +541,11 @@ cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, c
     // step 187.4 -> 188.6, config 3 inserts 51.9 -> 55.7 Gkeys/s vs a
     // persistent grid of 4 CTAs/SM)
     const uint64_t grid = (n + kThreads * 4 - 1) / (kThreads * 4);
-    insert_wide_kernel<false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n);
+    if (red_hint(di, g))
+      insert_wide_kernel<false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n);
+    else
+      insert_wide_kernel<false, false, 4, false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g,
+                                                                                                 hashes, n);
   }
   return cudaGetLastError();
 }

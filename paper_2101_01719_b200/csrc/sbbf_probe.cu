@@ -4,8 +4,10 @@
 // Both kernels draw block indices from splitmix64 in registers (no hash
 // stream), so they measure only the random-sector path the SBBF kernels
 // share: one 256-bit LDG per key (sector_read) or one 32-byte atomic-OR
-// sector op per key via 8 lane reds (sector_red). Run on a buffer larger than
-// L2 they give the HBM random-sector ceiling; on a 1 MiB buffer, the L2 one.
+// sector op per key via the inserts' own pattern, 4 lanes x red.b64 (L1
+// merges them into one sector request; sector_red). Run on a buffer larger
+// than L2 they give the HBM random-sector ceiling; on a 1 MiB buffer, the L2
+// one.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -51,18 +53,20 @@ __global__ void __launch_bounds__(256, 4) sector_read_kernel(const uint32_t* __r
 
 __global__ void __launch_bounds__(256, 4) sector_red_kernel(uint32_t* __restrict__ buf, uint64_t nb,
                                                             uint64_t n, uint64_t seed) {
+  // insert_wide_kernel's pattern: 4 threads per key, one red.b64 per lane
+  // pair (no cache hint, as its L2-resident launch)
   const int lane = threadIdx.x & 31;
-  const int word = lane & 7;
-  const uint64_t keep = dev::policy_evict_last();
+  const int pair = lane & 3;
   const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t t = warp; t * 32 < n; t += nwarps) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const uint64_t k = t * 32 + r * 4 + (lane >> 3);
+    for (int r = 0; r < 4; ++r) {
+      const uint64_t k = t * 32 + r * 8 + (lane >> 2);
       if (k < n) {
         const uint64_t h = mix(seed + (k + 1) * 0x9e3779b97f4a7c15ull);
-        dev::red_or(buf + dev::block_index(h, nb) * 8 + word, 1u << (h & 31), keep);
+        const uint64_t m = (uint64_t{1} << (h & 31)) | (uint64_t{1} << (32 + ((h >> 5) & 31)));
+        dev::red_or64_nohint(reinterpret_cast<uint64_t*>(buf + dev::block_index(h, nb) * 8) + pair, m);
       }
     }
   }
