@@ -535,7 +535,9 @@ def roofline(res: dict, l2_sector_gs: float | None, hbm_peak: float, peak_note: 
         note = ("blocked: 8 B hash + 1/8 B bitmap + filter streamed once (filter_bytes/lookups); "
                 "the partition's extra passes are overhead, not algorithmic bytes")
     elif resident:
-        per_key, kernel = 8.125, "find_pipe_kernel/find_smem_kernel (bitmap)"
+        per_key = 8.125
+        kernel = ("find_smem_kernel (bitmap)" if res.get("find_variant") == 2 else
+                  "find_whole_kernel<4, bits, 3> (bitmap)")
         note = "filter L2-resident: hash stream 8 B + bitmap 1/8 B per key from HBM"
     else:
         per_key, kernel = 40.125, "find_pipe_kernel (bitmap)"
@@ -547,7 +549,8 @@ def roofline(res: dict, l2_sector_gs: float | None, hbm_peak: float, peak_note: 
     if l2_sector_gs:
         rate = L / t / 1e9
         # the resource that actually binds this kernel, for a reader of `frac`
-        rf["binding"] = ({"resource": "L2 random-sector request rate (filter L2-resident)",
+        rf["binding"] = ({"resource": "random-sector request rate, filter L2-resident (about one 32-B sector "
+                                      "per SM-clock; ncu: L1TEX 90 % busy, profiles/r1h_ncu_summary.md)",
                           "frac": rate / l2_sector_gs} if resident and not blocked else
                          {"resource": "DRAM random-sector rate (direct probes beyond L2)",
                           "frac": rate / l2_sector_gs} if not blocked else
@@ -648,11 +651,15 @@ def main() -> None:
                         f"with a mid-step event (their sum {main_res['ms_step_split']:.4f} ms)"),
         "roofline": main_res["roofline"],
         # the insert phase's own bound: one 32-B sector red request per key
-        # (L1 merges a key's lane reds) against random sector reds on a
-        # buffer of the filter's size (sbbf_bench_sector_red)
+        # (L1 merges a key's four lane-pair reds) against the same red pattern
+        # on a buffer of the filter's size (sbbf_bench_sector_red)
         "insert_roofline": {"bound": "L2 atomic sector-request rate",
                             "achieved_gkeys_s": main_res["insert_gkeys_s"], "ceiling_gsectors_s": l2_red,
-                            "frac": main_res["insert_gkeys_s"] / l2_red},
+                            "frac": main_res["insert_gkeys_s"] / l2_red,
+                            "note": ("ceiling = the insert's own pattern (4 lanes x red.b64, one sector "
+                                     "request per key) in steady state on a filter-sized buffer; a 1M-key "
+                                     "launch also pays ~6 us of fixed launch/drain time "
+                                     "(scripts/microbench_red.cu, profiles/r1h_ncu_summary.md)")},
         "random_sector_ceilings_gs": {"l2_read_1MiB": l2_read, "hbm_read_4GiB": hbm_read,
                                       "hbm_red_4GiB": hbm_red, "l2_red_filter": l2_red},
         "gpu_launches": int(main_res["launches_per_step"] * args.steps),
