@@ -170,6 +170,32 @@ int main() {
   for (uint64_t i = 0; i < nmax; ++i) h[i] = mix(3 + (i + 1) * 0x9e3779b97f4a7c15ull);
   CK(cudaMemcpy(b.keys, h.data(), nmax * 8, cudaMemcpyHostToDevice));
   run("empty kernel (launch + event overhead)", b, nb, 0, sms, [] { empty_kernel<<<1, 32>>>(); });
+  run("2 empty kernels", b, nb, 0, sms, [] { empty_kernel<<<1, 32>>>(); empty_kernel<<<1, 32>>>(); });
+  run("empty kernel, 1184 CTAs", b, nb, 0, sms, [=] { empty_kernel<<<sms * 8, 256>>>(); });
+  run("empty kernel, GPU idle before (no flush)", b, nb, 0, sms, [] { empty_kernel<<<1, 32>>>(); }, false);
+  {
+    cudaGraph_t gr;
+    cudaGraphExec_t ge;
+    cudaStream_t cs;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    const uint64_t n = 1000000;
+    const unsigned grid = unsigned((n + 1023) / 1024);
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeGlobal));
+    ins_kernel<1, 0, 4><<<grid, 256, 0, cs>>>(b.filter, nb, b.keys, n);
+    CK(cudaStreamEndCapture(cs, &gr));
+    CK(cudaGraphInstantiate(&ge, gr, 0));
+    run("stream hint=none once T=4, CUDA graph", b, nb, n, sms, [=] { CK(cudaGraphLaunch(ge, 0)); });
+  }
+  for (int per_sm : {2, 3, 4, 6, 8, 12, 16}) {
+    const uint64_t n = 1000000;
+    char name[64];
+    snprintf(name, sizeof name, "stream hint=none persist %d/SM T=2", per_sm);
+    run(name, b, nb, n, sms, [=] { ins_kernel<1, 0, 2><<<sms * per_sm, 256>>>(b.filter, nb, b.keys, n); });
+    snprintf(name, sizeof name, "stream hint=none persist %d/SM T=1", per_sm);
+    run(name, b, nb, n, sms, [=] { ins_kernel<1, 0, 1><<<sms * per_sm, 256>>>(b.filter, nb, b.keys, n); });
+  }
+  run("stream hint=none once T=1", b, nb, 1000000, sms,
+      [=] { ins_kernel<1, 0, 1><<<unsigned((1000000 + 255) / 256), 256>>>(b.filter, nb, b.keys, 1000000); });
   for (uint64_t n : {uint64_t{1000000}, uint64_t{2000000}, uint64_t{4000000}}) {
     const unsigned grid = unsigned((n + 1023) / 1024);
     run("regs   hint=none  once T=4 WARM filter", b, nb, n, sms,
