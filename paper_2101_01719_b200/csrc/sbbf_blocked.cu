@@ -89,24 +89,19 @@ __device__ __forceinline__ uint32_t bucket_of(uint64_t h, const BucketMap& bm) {
   return static_cast<uint32_t>(q);
 }
 
-// Lanes whose bucket equals `v`, given the per-bit ballots of the warp:
-// AND over bits k of (bal[k] if bit k of v is set, else ~bal[k]), written as
-// bal[k] ^ flip_k(v) so each bit costs one LOP3.
-__device__ __forceinline__ uint32_t flip(uint32_t v, int k) { return ((v >> k) & 1u) - 1u; }
-
-template <int BITS>
-__device__ __forceinline__ uint32_t lanes_with(uint32_t v, const uint32_t (&bal)[kMaxBits], uint32_t active) {
-  uint32_t m = active;
-#pragma unroll
-  for (int k = 0; k < BITS; ++k) m &= bal[k] ^ flip(v, k);
-  return m;
-}
-
+// One ballot per bucket-id bit. Written in PTX so that each bit is a single
+// predicate-producing LOP3 feeding the VOTE (the C++ form compiled to a
+// shift, a mask and a 64-bit compare per bit).
 template <int BITS>
 __device__ __forceinline__ void bit_ballots(uint32_t bk, uint32_t (&bal)[kMaxBits]) {
 #pragma unroll
-  for (int k = 0; k < BITS; ++k) bal[k] = __ballot_sync(0xffffffffu, (bk >> k) & 1u);
+  for (int k = 0; k < BITS; ++k)
+    asm("{ .reg .pred p; .reg .b32 t; and.b32 t, %1, %2; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 %0, p, 0xffffffff; }"
+        : "=r"(bal[k])
+        : "r"(bk), "r"(1u << k));
 }
+
+__device__ __forceinline__ uint32_t flip(uint32_t v, int k) { return ((v >> k) & 1u) - 1u; }
 
 // Per-lane flip masks of the buckets lane l owns (l and l + 32), hoisted
 // out of the key loops: bits 0..4 are shared by both buckets.
@@ -136,21 +131,38 @@ __device__ __forceinline__ void owner_counts(const OwnerMasks& om, const uint32_
 
 // One warp step over 32 keys: rank of each lane inside its bucket group and
 // the per-bucket counts added to the lane-owned counters c0 (bucket = lane)
-// and c1 (bucket = lane + 32).
+// and c1 (bucket = lane + 32). Each lane first forms the mask of lanes holding
+// the buckets it owns (BITS LOP3s against its precomputed flip masks); a key's
+// peer mask and prior count then come from its bucket's owner lane by
+// shuffle, instead of every lane rebuilding its own bucket's mask bit by bit.
 template <int BITS>
 __device__ __forceinline__ uint32_t warp_rank(uint32_t bk, bool valid, uint32_t lane, const OwnerMasks& om,
                                               uint32_t& c0, uint32_t& c1) {
   const uint32_t active = __ballot_sync(0xffffffffu, valid);
   uint32_t bal[kMaxBits];
   bit_ballots<BITS>(bk, bal);
-  const uint32_t peers = lanes_with<BITS>(bk, bal, active);
-  // prior count of my bucket in this warp, from the lane that owns it
-  uint32_t prior = __shfl_sync(0xffffffffu, c0, bk & 31);
+  constexpr int kLow = BITS < 5 ? BITS : 5;
+  uint32_t m0 = active;
+#pragma unroll
+  for (int k = 0; k < kLow; ++k) m0 &= bal[k] ^ om.f[k];
+  uint32_t m1 = 0;
   if constexpr (BITS > 5) {
-    const uint32_t p1 = __shfl_sync(0xffffffffu, c1, bk & 31);
-    prior = (bk & 32) ? p1 : prior;
+    m1 = m0 & bal[5];
+    m0 &= ~bal[5];
   }
-  owner_counts<BITS>(om, bal, active, c0, c1);
+  const uint32_t src = bk & 31;
+  uint32_t peers = __shfl_sync(0xffffffffu, m0, src);
+  uint32_t prior = __shfl_sync(0xffffffffu, c0, src);
+  if constexpr (BITS > 5) {
+    const uint32_t p1 = __shfl_sync(0xffffffffu, m1, src);
+    const uint32_t q1 = __shfl_sync(0xffffffffu, c1, src);
+    if (bk & 32) {
+      peers = p1;
+      prior = q1;
+    }
+    c1 += __popc(m1);
+  }
+  c0 += __popc(m0);
   return prior + __popc(peers & ((1u << lane) - 1u));
 }
 
