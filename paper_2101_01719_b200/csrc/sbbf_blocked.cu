@@ -1043,8 +1043,10 @@ cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks,
     }
     if (e == cudaSuccess) e = cudaEventRecord(freed[k], s);
   }
-  // every side-stream launch was joined into s through ready[]; the scratch
-  // frees are ordered on s behind the last un-permute
+  // join the side stream into s once more (it covers an error exit between a
+  // side launch and its ready[] wait), so the scratch frees on s are ordered
+  // behind every partition that writes it
+  if (side && ev_in && cudaEventRecord(ev_in, side) == cudaSuccess) cudaStreamWaitEvent(s, ev_in, 0);
   for (int k = 0; k < 2; ++k) free_scratch(sc[k], s);
   return e;
 }
