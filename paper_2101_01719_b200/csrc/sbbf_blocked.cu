@@ -47,7 +47,7 @@ constexpr uint64_t kBlockedChunk = uint64_t{1} << 28;  // keys per blocked round
 // Bucket of a key = its local block scaled to [0, S) by a 32.32 fixed-point
 // multiply: monotone in the block, so bucket k is a contiguous block range of
 // ~nb/S blocks (neighbouring buckets may share a boundary block — harmless,
-// each key is still handled on its own). S <= 64.
+// each key is still handled on its own). S <= 64 for the whole-batch partition, <= 128 for the chunk-local one.
 //
 // Ranking inside a warp is a ballot "multisplit": for a BITS-bit bucket id,
 // BITS ballots give every lane the mask of lanes holding its bucket (AND of
@@ -60,8 +60,13 @@ constexpr int kPartMinBlocks = 2;
 constexpr int kPartWarps = kPartThreads / 32;
 constexpr int kPartPerThread = 8;
 constexpr uint64_t kPartChunk = kPartThreads * kPartPerThread;
-constexpr int kMaxBuckets = 64;
+constexpr int kMaxBuckets = 64;     // whole-batch partition (shard routing, super-slices)
 constexpr int kMaxBits = 6;
+constexpr int kChunkBuckets = 128;  // chunk-local partition (blocked path): up to 128 slices
+constexpr int kChunkBits = 7;
+// buckets each lane owns (lane + 32 i) for BITS-bit bucket ids
+template <int BITS>
+constexpr int owned() { return BITS > 5 ? 1 << (BITS - 5) : 1; }
 
 struct BucketMap {
   uint64_t nb_global, first, nb_local, mult;  // mult = floor(S * 2^32 / nb_local)
@@ -93,7 +98,7 @@ __device__ __forceinline__ uint32_t bucket_of(uint64_t h, const BucketMap& bm) {
 // predicate-producing LOP3 feeding the VOTE (the C++ form compiled to a
 // shift, a mask and a 64-bit compare per bit).
 template <int BITS>
-__device__ __forceinline__ void bit_ballots(uint32_t bk, uint32_t (&bal)[kMaxBits]) {
+__device__ __forceinline__ void bit_ballots(uint32_t bk, uint32_t (&bal)[kChunkBits]) {
 #pragma unroll
   for (int k = 0; k < BITS; ++k)
     asm("{ .reg .pred p; .reg .b32 t; and.b32 t, %1, %2; setp.ne.u32 p, t, 0; vote.sync.ballot.b32 %0, p, 0xffffffff; }"
@@ -103,8 +108,8 @@ __device__ __forceinline__ void bit_ballots(uint32_t bk, uint32_t (&bal)[kMaxBit
 
 __device__ __forceinline__ uint32_t flip(uint32_t v, int k) { return ((v >> k) & 1u) - 1u; }
 
-// Per-lane flip masks of the buckets lane l owns (l and l + 32), hoisted
-// out of the key loops: bits 0..4 are shared by both buckets.
+// Per-lane flip masks of the buckets lane l owns (l + 32 i), hoisted out of
+// the key loops: bits 0..4 are shared by all of them.
 struct OwnerMasks {
   uint32_t f[5];
   __device__ __forceinline__ explicit OwnerMasks(uint32_t lane) {
@@ -113,71 +118,76 @@ struct OwnerMasks {
   }
 };
 
-// Add this warp step's counts of buckets lane and lane + 32 to c0 / c1.
+// m[i] = the lanes of this warp step whose key is in bucket lane + 32 i.
 template <int BITS>
-__device__ __forceinline__ void owner_counts(const OwnerMasks& om, const uint32_t (&bal)[kMaxBits], uint32_t active,
-                                             uint32_t& c0, uint32_t& c1) {
+__device__ __forceinline__ void owner_masks(const OwnerMasks& om, const uint32_t (&bal)[kChunkBits], uint32_t active,
+                                            uint32_t (&m)[owned<BITS>()]) {
   constexpr int kLow = BITS < 5 ? BITS : 5;
-  uint32_t m = active;
+  uint32_t base = active;
 #pragma unroll
-  for (int k = 0; k < kLow; ++k) m &= bal[k] ^ om.f[k];
-  if constexpr (BITS > 5) {
-    c0 += __popc(m & ~bal[5]);
-    c1 += __popc(m & bal[5]);
-  } else {
-    c0 += __popc(m);
+  for (int k = 0; k < kLow; ++k) base &= bal[k] ^ om.f[k];
+#pragma unroll
+  for (int i = 0; i < owned<BITS>(); ++i) {
+    uint32_t x = base;
+    if constexpr (BITS > 5) x &= (i & 1) ? bal[5] : ~bal[5];
+    if constexpr (BITS > 6) x &= (i & 2) ? bal[6] : ~bal[6];
+    m[i] = x;
   }
 }
 
+// Add this warp step's counts of the lane's owned buckets to c[].
+template <int BITS>
+__device__ __forceinline__ void owner_counts(const OwnerMasks& om, const uint32_t (&bal)[kChunkBits], uint32_t active,
+                                             uint32_t (&c)[owned<BITS>()]) {
+  uint32_t m[owned<BITS>()];
+  owner_masks<BITS>(om, bal, active, m);
+#pragma unroll
+  for (int i = 0; i < owned<BITS>(); ++i) c[i] += __popc(m[i]);
+}
+
 // One warp step over 32 keys: rank of each lane inside its bucket group and
-// the per-bucket counts added to the lane-owned counters c0 (bucket = lane)
-// and c1 (bucket = lane + 32). Each lane first forms the mask of lanes holding
-// the buckets it owns (BITS LOP3s against its precomputed flip masks); a key's
-// peer mask and prior count then come from its bucket's owner lane by
-// shuffle, instead of every lane rebuilding its own bucket's mask bit by bit.
+// the per-bucket counts added to the lane-owned counters c[i] (bucket =
+// lane + 32 i). Each lane first forms the masks of lanes holding the buckets
+// it owns (BITS LOP3s against its precomputed flip masks); a key's peer mask
+// and prior count then come from its bucket's owner lane by shuffle, instead
+// of every lane rebuilding its own bucket's mask bit by bit.
 template <int BITS>
 __device__ __forceinline__ uint32_t warp_rank(uint32_t bk, bool valid, uint32_t lane, const OwnerMasks& om,
-                                              uint32_t& c0, uint32_t& c1) {
+                                              uint32_t (&c)[owned<BITS>()]) {
   const uint32_t active = __ballot_sync(0xffffffffu, valid);
-  uint32_t bal[kMaxBits];
+  uint32_t bal[kChunkBits];
   bit_ballots<BITS>(bk, bal);
-  constexpr int kLow = BITS < 5 ? BITS : 5;
-  uint32_t m0 = active;
+  uint32_t m[owned<BITS>()];
+  owner_masks<BITS>(om, bal, active, m);
+  const uint32_t src = bk & 31, hi = bk >> 5;
+  uint32_t peers = 0, prior = 0;
 #pragma unroll
-  for (int k = 0; k < kLow; ++k) m0 &= bal[k] ^ om.f[k];
-  uint32_t m1 = 0;
-  if constexpr (BITS > 5) {
-    m1 = m0 & bal[5];
-    m0 &= ~bal[5];
-  }
-  const uint32_t src = bk & 31;
-  uint32_t peers = __shfl_sync(0xffffffffu, m0, src);
-  uint32_t prior = __shfl_sync(0xffffffffu, c0, src);
-  if constexpr (BITS > 5) {
-    const uint32_t p1 = __shfl_sync(0xffffffffu, m1, src);
-    const uint32_t q1 = __shfl_sync(0xffffffffu, c1, src);
-    if (bk & 32) {
-      peers = p1;
-      prior = q1;
+  for (int i = 0; i < owned<BITS>(); ++i) {
+    const uint32_t p = __shfl_sync(0xffffffffu, m[i], src);
+    const uint32_t q = __shfl_sync(0xffffffffu, c[i], src);
+    if (owned<BITS>() == 1 || hi == static_cast<uint32_t>(i)) {
+      peers = p;
+      prior = q;
     }
-    c1 += __popc(m1);
   }
-  c0 += __popc(m0);
+#pragma unroll
+  for (int i = 0; i < owned<BITS>(); ++i) c[i] += __popc(m[i]);
   return prior + __popc(peers & ((1u << lane) - 1u));
 }
 
 // Slot of each key in the chunk's bucket-major smem staging: lane l fetches
-// its warp's base of buckets l and l + 32 once (bucket offset + this warp's
+// its warp's base of its owned buckets once (bucket offset + this warp's
 // prefix), and each key takes its bucket's base by shuffle — no dependent
 // per-key shared-memory loads (they were ~30 % of chunk_scatter's stalls).
 template <int BITS>
-__device__ __forceinline__ uint32_t slot_base(uint32_t bk, uint32_t base0, uint32_t base1) {
-  const uint32_t b0 = __shfl_sync(0xffffffffu, base0, bk & 31);
-  if constexpr (BITS > 5) {
-    const uint32_t b1 = __shfl_sync(0xffffffffu, base1, bk & 31);
-    return (bk & 32) ? b1 : b0;
+__device__ __forceinline__ uint32_t slot_base(uint32_t bk, const uint32_t (&base)[owned<BITS>()]) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int i = 0; i < owned<BITS>(); ++i) {
+    const uint32_t b = __shfl_sync(0xffffffffu, base[i], bk & 31);
+    if (owned<BITS>() == 1 || (bk >> 5) == static_cast<uint32_t>(i)) r = b;
   }
-  return b0;
+  return r;
 }
 
 // Both passes give CTA c the same contiguous run of chunks, so the count
@@ -216,7 +226,7 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) bucket_count_ker
   const OwnerMasks om(lane);
   const uint64_t pol = dev::policy_evict_first();
   if (threadIdx.x < kMaxBuckets) cta[threadIdx.x] = 0;
-  uint32_t c0 = 0, c1 = 0;
+  uint32_t c[owned<BITS>()] = {};
   uint64_t ch0, ch1;
   cta_chunk_range(n, ch0, ch1);
   // Software pipeline: the next chunk's loads are in flight while this
@@ -232,9 +242,9 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) bucket_count_ker
     if (base + kPartChunk <= n) {
 #pragma unroll
       for (int j = 0; j < kPartPerThread; ++j) {
-        uint32_t bal[kMaxBits];
+        uint32_t bal[kChunkBits];
         bit_ballots<BITS>(bucket_of<kTop>(h[j], bm), bal);
-        owner_counts<BITS>(om, bal, 0xffffffffu, c0, c1);
+        owner_counts<BITS>(om, bal, 0xffffffffu, c);
       }
     } else {
 #pragma unroll
@@ -242,15 +252,16 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) bucket_count_ker
         const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
         const uint32_t bk = i < n ? bucket_of<kTop>(h[j], bm) : 0u;
         const uint32_t active = __ballot_sync(0xffffffffu, i < n);
-        uint32_t bal[kMaxBits];
+        uint32_t bal[kChunkBits];
         bit_ballots<BITS>(bk, bal);
-        owner_counts<BITS>(om, bal, active, c0, c1);
+        owner_counts<BITS>(om, bal, active, c);
       }
     }
   }
   __syncthreads();
-  if (lane < bm.S && c0) atomicAdd(&cta[lane], c0);
-  if (lane + 32 < bm.S && c1) atomicAdd(&cta[lane + 32], c1);
+#pragma unroll
+  for (int i = 0; i < owned<BITS>(); ++i)
+    if (lane + 32 * i < bm.S && c[i]) atomicAdd(&cta[lane + 32 * i], c[i]);
   __syncthreads();
   if (threadIdx.x < kMaxBuckets) cta_hist[static_cast<uint64_t>(blockIdx.x) * kMaxBuckets + threadIdx.x] = cta[threadIdx.x];
 }
@@ -332,12 +343,12 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) bucket_scatter_k
     uint64_t h[kPartPerThread];
     uint32_t bk[kPartPerThread], off[kPartPerThread];
     load_chunk(hashes, n, ch, pol, h);
-    uint32_t c0 = 0, c1 = 0;
+    uint32_t c[owned<BITS>()] = {};
     if (cnt == kPartChunk) {
 #pragma unroll
       for (int j = 0; j < kPartPerThread; ++j) {
         bk[j] = bucket_of<kTop>(h[j], bm);
-        off[j] = warp_rank<BITS>(bk[j], true, lane, om, c0, c1);
+        off[j] = warp_rank<BITS>(bk[j], true, lane, om, c);
       }
     } else {
 #pragma unroll
@@ -345,12 +356,12 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) bucket_scatter_k
         const uint64_t i = base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x;
         const bool valid = i < n;
         bk[j] = valid ? bucket_of<kTop>(h[j], bm) : 0u;
-        off[j] = warp_rank<BITS>(bk[j], valid, lane, om, c0, c1);
+        off[j] = warp_rank<BITS>(bk[j], valid, lane, om, c);
         if (!valid) bk[j] = 0xffffffffu;
       }
     }
-    sm.wcnt[warp][lane] = c0;
-    sm.wcnt[warp][lane + 32] = c1;
+#pragma unroll
+    for (int i = 0; i < kMaxBuckets / 32; ++i) sm.wcnt[warp][lane + 32 * i] = i < owned<BITS>() ? c[i] : 0u;
     __syncthreads();
     if (warp == 0) {
       // bucket totals (lane owns buckets lane, lane+32), warp prefixes, a
@@ -383,11 +394,12 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks) bucket_scatter_k
       sm.cursor[lane + 32] += t1;
     }
     __syncthreads();
-    const uint32_t base0 = sm.boff[lane] + sm.wcnt[warp][lane];
-    const uint32_t base1 = sm.boff[lane + 32] + sm.wcnt[warp][lane + 32];
+    uint32_t sbase[owned<BITS>()];
+#pragma unroll
+    for (int i = 0; i < owned<BITS>(); ++i) sbase[i] = sm.boff[lane + 32 * i] + sm.wcnt[warp][lane + 32 * i];
 #pragma unroll
     for (int j = 0; j < kPartPerThread; ++j) {
-      const uint32_t loc = slot_base<BITS>(bk[j], base0, base1) + off[j];
+      const uint32_t loc = slot_base<BITS>(bk[j], sbase) + off[j];
       if (bk[j] != 0xffffffffu) {
         sm.key[loc] = h[j];
         sm.pos[loc] = static_cast<uint32_t>(base + static_cast<uint64_t>(j) * kPartThreads + threadIdx.x);
@@ -517,10 +529,10 @@ cudaError_t bucket_partition(const DeviceInfo& di, const Geom& g, uint32_t S, co
 struct ChunkSmem {
   uint64_t key[kPartChunk];
   alignas(16) uint16_t pos[kPartChunk];
-  uint32_t wcnt[kPartWarps][kMaxBuckets];
-  uint32_t boff[kMaxBuckets + 1];
+  uint32_t wcnt[kPartWarps][kChunkBuckets];
+  uint32_t boff[kChunkBuckets + 1];
 };
-constexpr int kBoffStride = kMaxBuckets + 1;
+constexpr int kBoffStride = kChunkBuckets + 1;
 
 template <int BITS, bool kTop>
 __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
@@ -538,62 +550,74 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
     uint64_t h[kPartPerThread];
     uint32_t bk[kPartPerThread], off[kPartPerThread];
     load_chunk(hashes, n, ch, pol, h);
-    uint32_t c0 = 0, c1 = 0;
+    uint32_t c[owned<BITS>()] = {};
     if (cnt == kPartChunk) {
 #pragma unroll
       for (int j = 0; j < kPartPerThread; ++j) {
         bk[j] = bucket_of<kTop>(h[j], bm);
-        off[j] = warp_rank<BITS>(bk[j], true, lane, om, c0, c1);
+        off[j] = warp_rank<BITS>(bk[j], true, lane, om, c);
       }
     } else {
 #pragma unroll
       for (int j = 0; j < kPartPerThread; ++j) {
         const bool valid = j * kPartThreads + threadIdx.x < cnt;
         bk[j] = valid ? bucket_of<kTop>(h[j], bm) : 0u;
-        off[j] = warp_rank<BITS>(bk[j], valid, lane, om, c0, c1);
+        off[j] = warp_rank<BITS>(bk[j], valid, lane, om, c);
         if (!valid) bk[j] = 0xffffffffu;
       }
     }
-    sm.wcnt[warp][lane] = c0;
-    sm.wcnt[warp][lane + 32] = c1;
+#pragma unroll
+    for (int i = 0; i < kChunkBuckets / 32; ++i) sm.wcnt[warp][lane + 32 * i] = i < owned<BITS>() ? c[i] : 0u;
     __syncthreads();
     if (warp == 0) {
-      // per-bucket totals over the warps (lane owns buckets lane, lane + 32),
+      // per-bucket totals over the warps (lane owns buckets lane + 32 i),
       // exclusive prefixes over warps and over buckets
-      uint32_t t0 = 0, t1 = 0;
+      constexpr int kO = owned<BITS>();
+      uint32_t t[kO] = {};
 #pragma unroll
       for (int w = 0; w < kPartWarps; ++w) {
-        const uint32_t a = sm.wcnt[w][lane], b = sm.wcnt[w][lane + 32];
-        sm.wcnt[w][lane] = t0;
-        sm.wcnt[w][lane + 32] = t1;
-        t0 += a;
-        t1 += b;
-      }
-      uint32_t s0 = t0, s1 = t1;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y0 = __shfl_up_sync(0xffffffffu, s0, d), y1 = __shfl_up_sync(0xffffffffu, s1, d);
-        if (lane >= static_cast<uint32_t>(d)) {
-          s0 += y0;
-          s1 += y1;
+        for (int i = 0; i < kO; ++i) {
+          const uint32_t a = sm.wcnt[w][lane + 32 * i];
+          sm.wcnt[w][lane + 32 * i] = t[i];
+          t[i] += a;
         }
       }
-      const uint32_t sum0 = __shfl_sync(0xffffffffu, s0, 31);
-      sm.boff[lane] = s0 - t0;
-      sm.boff[lane + 32] = sum0 + s1 - t1;
+      uint32_t sc[kO];
+#pragma unroll
+      for (int i = 0; i < kO; ++i) sc[i] = t[i];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+        for (int i = 0; i < kO; ++i) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, sc[i], d);
+          if (lane >= static_cast<uint32_t>(d)) sc[i] += y;
+        }
+      }
       uint16_t* bo = boffs + ch * kBoffStride;
       // buckets >= S are empty: their offsets equal cnt (lanes >= S may hold
       // counts of aliased ids, which no key uses)
-      bo[lane] = static_cast<uint16_t>(lane < bm.S ? s0 - t0 : cnt);
-      bo[lane + 32] = static_cast<uint16_t>(lane + 32 < bm.S ? sum0 + s1 - t1 : cnt);
-      if (lane == 0) bo[kMaxBuckets] = static_cast<uint16_t>(cnt);
+      uint32_t carry = 0;
+#pragma unroll
+      for (int i = 0; i < kChunkBuckets / 32; ++i) {
+        const uint32_t b = lane + 32 * i;
+        uint32_t o = cnt;
+        if (i < kO) {
+          o = carry + sc[i] - t[i];
+          carry += __shfl_sync(0xffffffffu, sc[i], 31);
+          sm.boff[b] = o;
+        }
+        bo[b] = static_cast<uint16_t>(b < bm.S ? o : cnt);
+      }
+      if (lane == 0) bo[kChunkBuckets] = static_cast<uint16_t>(cnt);
     }
     __syncthreads();
-    const uint32_t base0 = sm.boff[lane] + sm.wcnt[warp][lane];
-    const uint32_t base1 = sm.boff[lane + 32] + sm.wcnt[warp][lane + 32];
+    uint32_t sbase[owned<BITS>()];
+#pragma unroll
+    for (int i = 0; i < owned<BITS>(); ++i) sbase[i] = sm.boff[lane + 32 * i] + sm.wcnt[warp][lane + 32 * i];
 #pragma unroll
     for (int j = 0; j < kPartPerThread; ++j) {
-      const uint32_t loc = slot_base<BITS>(bk[j], base0, base1) + off[j];
+      const uint32_t loc = slot_base<BITS>(bk[j], sbase) + off[j];
       if (bk[j] != 0xffffffffu) {
         SBBF_DCHECK(loc < cnt && bk[j] < bm.S && loc == sm.boff[bk[j]] + sm.wcnt[warp][bk[j]] + off[j]);
         sm.key[loc] = h[j];
@@ -654,7 +678,7 @@ __global__ void __launch_bounds__(kSegThreads, kMinB)
       if (ch < c_end) {
         st = boffs[ch * kBoffStride + b];
         en = boffs[ch * kBoffStride + b + 1];
-        SBBF_DCHECK(st <= en && en <= boffs[ch * kBoffStride + kMaxBuckets] && ch * kPartChunk + en <= m);
+        SBBF_DCHECK(st <= en && en <= boffs[ch * kBoffStride + kChunkBuckets] && ch * kPartChunk + en <= m);
       }
       seg[q] = ch * kPartChunk + st;
       len[q] = en - st;
@@ -734,7 +758,7 @@ __global__ void __launch_bounds__(kUnpermThreads, 4) unpermute_kernel(const uint
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kPartChunk;
   // chunks laid out region by region (blocked_find_regions) carry their own
   // key count; otherwise every chunk but the last is full
-  const uint32_t cnt = boffs ? boffs[static_cast<uint64_t>(blockIdx.x) * kBoffStride + kMaxBuckets]
+  const uint32_t cnt = boffs ? boffs[static_cast<uint64_t>(blockIdx.x) * kBoffStride + kChunkBuckets]
                              : static_cast<uint32_t>(m - base < kPartChunk ? m - base : kPartChunk);
   if (cnt == kPartChunk) {
     // full chunk: 8 positions (16 B) + 8 answers (8 B) per vector load
@@ -807,6 +831,7 @@ cudaError_t chunk_partition(const DeviceInfo& di, const Geom& g, uint32_t S, con
     SBBF_CHUNK_CASE(4)
     SBBF_CHUNK_CASE(5)
     SBBF_CHUNK_CASE(6)
+    SBBF_CHUNK_CASE(7)
 #undef SBBF_CHUNK_CASE
     default: return cudaErrorInvalidValue;
   }
@@ -911,7 +936,7 @@ cudaError_t find_chunk(const DeviceInfo& di, const uint32_t* blocks, const Geom&
   return e;
 }
 
-// Filters beyond kMaxBuckets slices (> ~1 GiB): a first partition groups the
+// Filters beyond kChunkBuckets slices (> 4 GiB): a first partition groups the
 // batch chunk by "super-slice" (exact block ranges, global bucket-major
 // layout with source positions), then each super-slice runs the single-level
 // path on its sub-filter, so every slice the probes touch stays ~32 MiB.

@@ -142,11 +142,12 @@ int ensure_plan(sbbf_gpu* f) {
   std::lock_guard<std::mutex> lock(f->plan_mu);
   if (f->d_plan_bounds) return SBBF_OK;
   uint64_t parts = (f->nb * 32 + kSliceBytes - 1) / kSliceBytes;
-  // beyond 64 slices (bucket ids are <= 6 bits): super-slices of <= 64 slices
-  uint64_t super = (parts + 63) / 64;
+  // beyond 128 slices (chunk-local bucket ids are <= 7 bits, filters beyond
+  // 4 GiB): super-slices of <= 128 slices (the super partition takes <= 64)
+  uint64_t super = (parts + 127) / 128;
   super = super > 64 ? 64 : super;
   if (super > 1) parts = (parts + super - 1) / super;
-  parts = parts < 2 ? 2 : (parts > 64 ? 64 : parts);
+  parts = parts < 2 ? 2 : (parts > 128 ? 128 : parts);
   uint64_t pow2 = 1;
   while (pow2 < parts) pow2 <<= 1;  // a power of two lets the partition use the hash's top bits
   parts = pow2;

@@ -267,10 +267,12 @@ def test_blocked_path_skew(cuda, oracle, nb, shape):
     assert np.array_equal(bits_to_bytes(bits, probes.size), want_res)
 
 
-@pytest.mark.parametrize("nb", [2**27, 2**27 + 12345])
+@pytest.mark.parametrize("nb", [2**27, 3 * 2**25 + 5, 2**27 + 12345])
 def test_blocked_two_level(cuda, oracle, nb):
-    """Filters beyond 64 slices of 32 MiB (> 2 GiB) take the two-level
-    blocked path: super-slices by exact block range, then slices."""
+    """Filters up to 128 slices of 32 MiB (4 GiB) take the single-level
+    blocked path with 7-bit slice ids (2^27 blocks: top hash bits; 3 GiB + 5
+    blocks: the fixed-point map); beyond, the two-level path: super-slices by
+    exact block range, then slices (2^27 + 12345 blocks)."""
     rng = np.random.default_rng(nb)
     hs = rng.integers(0, 2**64, size=3_000_017, dtype=np.uint64)
     probes = np.concatenate([hs[:500_000], rng.integers(0, 2**64, size=1_500_003, dtype=np.uint64)])
