@@ -209,18 +209,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
   constexpr uint64_t kTile = 32 * U;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
+  // hn holds the next tile's raw inputs; with kKeys the XXH64 is applied when
+  // the tile is consumed, so the prefetch never waits on its own loads
   uint64_t hn[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint64_t idx = warp * kTile + u * 32 + lane;
-    hn[u] = (warp < ntiles && idx < n) ? dev::to_hash<kKeys>(dev::ld_stream_u64(hashes + idx, pol), seed) : 0;
+    hn[u] = (warp < ntiles && idx < n) ? dev::ld_stream_u64(hashes + idx, pol) : 0;
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // filter reads only after the insert grid
   for (uint64_t t = warp; t < ntiles; t += nwarps) {
     const uint64_t base = t * kTile;
     uint64_t h[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) h[u] = hn[u];
+    for (int u = 0; u < U; ++u) h[u] = dev::to_hash<kKeys>(hn[u], seed);
     Block8 b[U];
     uint32_t owned = 0;
 #pragma unroll
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t idx = tn * kTile + u * 32 + lane;
-      hn[u] = (tn < ntiles && idx < n) ? dev::to_hash<kKeys>(dev::ld_stream_u64(hashes + idx, pol), seed) : 0;
+      hn[u] = (tn < ntiles && idx < n) ? dev::ld_stream_u64(hashes + idx, pol) : 0;
     }
     uint32_t mine = 0;
 #pragma unroll
@@ -263,10 +265,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 // hash bits stay live (60-69 registers against find_pipe's 78). The next
 // tile's hashes load while this tile's sectors are in flight, as in
 // find_pipe. Config 2: 190.2 vs 188.5 Gkeys/s per step (profiles/r1_find_tuning.md).
-template <int U, bool kBits, int kMinBlocks>
+template <int U, bool kBits, int kMinBlocks, bool kKeys = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     find_whole_kernel(const uint32_t* __restrict__ blocks, uint64_t nb, const uint64_t* __restrict__ hashes,
-                      uint64_t n, void* __restrict__ out) {
+                      uint64_t n, void* __restrict__ out, uint64_t seed = 0) {
   const int lane = threadIdx.x & 31;
   const uint64_t pol = dev::policy_evict_first();
   const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
@@ -286,9 +288,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     Block8 b[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      lo[u] = static_cast<uint32_t>(hn[u]);
-      SBBF_DCHECK(dev::block_index(hn[u], nb) < nb);
-      dev::ld_block_nc(blocks + dev::block_index(hn[u], nb) * 8, b[u]);
+      const uint64_t h = dev::to_hash<kKeys>(hn[u], seed);  // XXH64 at consumption (kKeys)
+      lo[u] = static_cast<uint32_t>(h);
+      SBBF_DCHECK(dev::block_index(h, nb) < nb);
+      dev::ld_block_nc(blocks + dev::block_index(h, nb) * 8, b[u]);
     }
     const uint64_t tn = t + nwarps;
 #pragma unroll
@@ -597,6 +600,14 @@ cudaError_t launch_find_keys(const DeviceInfo& di, const uint32_t* blocks, const
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (g.first == 0 && g.nb_local == g.nb_global) {  // a whole filter: the lean kernel, as for raw hashes
+    static const int occ_w = resident_blocks(find_whole_kernel<kU, true, kMinB, true>, kThreads, 0);
+    cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kU, di.sms, occ_w)));
+    return bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, true, kMinB, true>, blocks, g.nb_global, keys, n, out,
+                                     seed)
+                : cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, false, kMinB, true>, blocks, g.nb_global, keys, n,
+                                     out, seed);
+  }
   return bits ? cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, true, kMinB, true>, blocks, g, keys, n, out, seed)
               : cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, false, kMinB, true>, blocks, g, keys, n, out, seed);
 }
@@ -631,8 +642,10 @@ cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* block
     if (g.first == 0 && g.nb_local == g.nb_global) {  // a whole filter: the lean kernel
       static const int occ_w = resident_blocks(find_whole_kernel<kU, true, kMinB>, kThreads, 0);
       cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kU, di.sms, occ_w)));
-      return bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, true, kMinB>, blocks, g.nb_global, hashes, n, out)
-                  : cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, false, kMinB>, blocks, g.nb_global, hashes, n, out);
+      return bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, true, kMinB>, blocks, g.nb_global, hashes, n, out,
+                                       uint64_t{0})
+                  : cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, false, kMinB>, blocks, g.nb_global, hashes, n, out,
+                                       uint64_t{0});
     }
     cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kU, di.sms, occ)));  // a shard
     return bits ? cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, true, kMinB>, blocks, g, hashes, n, out, uint64_t{0})
