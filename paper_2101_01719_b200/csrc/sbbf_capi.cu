@@ -128,9 +128,11 @@ int resolve_find(const sbbf_gpu* f, uint64_t n) {
   // Staging the filter costs one filter-size copy per CTA; it pays once each
   // SM probes enough keys to amortise it.
   if (smem_fits(f) && n >= 64 * f->nb) return SBBF_FIND_SMEM;
-  // Lookups gain from blocking as soon as the filter outgrows L2: config 3's
-  // 128 MiB filter, 108.2 vs 102.1 Gkeys/s direct (scripts/variant_ab.py);
-  // inserts only beyond 2 x L2 (resolve_insert).
+  // A whole filter up to ~1.2 x L2 is probed directly in two range-split
+  // passes (config 3: 137.6 vs 112.8 Gkeys/s blocked, sbbf_kernels.cu
+  // split_log2). Beyond, lookups gain from blocking as soon as the batch
+  // has half a key per block; inserts only beyond 2 x L2 (resolve_insert).
+  if (sbbf::split_log2(f->di, f->geom, true) > 0) return SBBF_FIND_GLOBAL;
   if (f->nb * 32 > static_cast<uint64_t>(f->di.l2_bytes) && n >= f->nb / 2) return SBBF_FIND_BLOCKED;
   return SBBF_FIND_GLOBAL;
 }

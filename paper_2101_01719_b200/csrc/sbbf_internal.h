@@ -42,6 +42,10 @@ void set_last_error(const std::string& msg);  // what sbbf_gpu_last_error() retu
 void note_launch();
 uint64_t grid_for(uint64_t work_items, uint64_t items_per_block, int sms, int per_sm);
 
+// 0, or k for 2^k range-split passes of the direct insert / lookup over a whole
+// filter somewhat larger than L2 (sbbf_kernels.cu).
+int split_log2(const DeviceInfo& di, const Geom& g, bool lookup);
+
 cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, const Geom& g,
                           const uint64_t* hashes, uint64_t n, cudaStream_t s);
 cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* blocks, const Geom& g,

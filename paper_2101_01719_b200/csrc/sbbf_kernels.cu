@@ -109,10 +109,15 @@ __global__ void __launch_bounds__(kThreads, 4) insert_lane8_kernel(uint32_t* __r
 // kHint: reds carry an L2 evict-last policy (filters near or beyond L2 size);
 // without it an L2-resident filter's 1M-key insert is 1.2 us faster
 // (scripts/microbench_red.cu: 15.2 vs 16.4 us).
-template <bool kTest, bool kKeys = false, int kT = 4, bool kHint = true>
+// kSplit: this pass inserts only the keys whose top hash bits (h >> psh)
+// equal pid — one contiguous block range of a whole filter (block_index is
+// monotone in the hash) — so a filter somewhat larger than L2 is inserted
+// range by range, each range L2-resident while its reds land.
+template <bool kTest, bool kKeys = false, int kT = 4, bool kHint = true, bool kSplit = false>
 __global__ void __launch_bounds__(kThreads, 4) insert_wide_kernel(uint32_t* __restrict__ blocks, Geom g,
                                                                   const uint64_t* __restrict__ hashes,
-                                                                  uint64_t n, uint64_t seed = 0) {
+                                                                  uint64_t n, uint64_t seed = 0, uint32_t psh = 63,
+                                                                  uint64_t pid = 0) {
   const int lane = threadIdx.x & 31;
   const int sub = lane >> 2;   // which of the 8 keys of a round
   const int pair = lane & 3;   // which 64-bit lane pair of the block this thread owns
@@ -128,6 +133,46 @@ __global__ void __launch_bounds__(kThreads, 4) insert_wide_kernel(uint32_t* __re
   // now (it waits in griddepcontrol.wait for this grid to finish before it
   // reads the filter) so its launch latency hides behind this kernel's tail.
   asm volatile("griddepcontrol.launch_dependents;");
+  if constexpr (kSplit) {
+    // compact this pass's keys per warp in shared memory, then run the
+    // 4-lanes-per-key red rounds over them only
+    __shared__ uint64_t cbuf[kThreads / 32][32 * kT];
+    uint64_t* cb = cbuf[threadIdx.x >> 5];
+    for (uint64_t t = warp; t < nsteps; t += nwarps) {
+      const uint64_t base = t * (32 * kT);
+      uint64_t h[kT];
+#pragma unroll
+      for (int j = 0; j < kT; ++j) {
+        const uint64_t idx = base + j * 32 + lane;
+        h[j] = idx < n ? dev::to_hash<kKeys>(dev::ld_stream_u64(hashes + idx, pol), seed) : 0;
+      }
+      uint32_t total = 0;
+#pragma unroll
+      for (int j = 0; j < kT; ++j) {
+        const bool in = base + j * 32 + lane < n && (h[j] >> psh) == pid;
+        const uint32_t bal = __ballot_sync(0xffffffffu, in);
+        if (in) cb[total + __popc(bal & ((1u << lane) - 1u))] = h[j];
+        total += __popc(bal);
+      }
+      __syncwarp();
+      for (uint32_t k0 = 0; k0 < total; k0 += 8) {
+        const uint32_t k = k0 + sub;
+        if (k < total) {
+          const uint64_t hk = cb[k];
+          const uint32_t low = static_cast<uint32_t>(hk);
+          bool ok;
+          uint64_t* ptr = reinterpret_cast<uint64_t*>(blocks + local_block(hk, g, ok) * 8) + pair;
+          const uint64_t mask = (static_cast<uint64_t>(dev::lane_bit(low, seed_hi)) << 32) | dev::lane_bit(low, seed_lo);
+          if (ok) {
+            if constexpr (kHint) dev::red_or64(ptr, mask, keep);
+            else dev::red_or64_nohint(ptr, mask);
+          }
+        }
+      }
+      __syncwarp();
+    }
+    return;
+  }
   for (uint64_t t = warp; t < nsteps; t += nwarps) {
     const uint64_t base = t * (32 * kT);
     uint64_t h[kT];
@@ -265,10 +310,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 // hash bits stay live (60-69 registers against find_pipe's 78). The next
 // tile's hashes load while this tile's sectors are in flight, as in
 // find_pipe. Config 2: 190.2 vs 188.5 Gkeys/s per step (profiles/r1_find_tuning.md).
-template <int U, bool kBits, int kMinBlocks, bool kKeys = false>
+// kSplit: one pass of a range-split lookup over a filter somewhat larger than
+// L2 — only keys whose top hash bits (h >> psh) equal pid are probed, so this
+// pass's probes stay in one L2-resident block range; the first pass stores
+// the bitmap words, later passes OR theirs in (bytes: each pass stores its
+// own keys' bytes).
+template <int U, bool kBits, int kMinBlocks, bool kKeys = false, bool kSplit = false>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
     find_whole_kernel(const uint32_t* __restrict__ blocks, uint64_t nb, const uint64_t* __restrict__ hashes,
-                      uint64_t n, void* __restrict__ out, uint64_t seed = 0) {
+                      uint64_t n, void* __restrict__ out, uint64_t seed = 0, uint32_t psh = 63, uint64_t pid = 0,
+                      bool first = true) {
   const int lane = threadIdx.x & 31;
   const uint64_t pol = dev::policy_evict_first();
   const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
@@ -286,12 +337,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
     const uint64_t base = t * kTile;
     uint32_t lo[U];
     Block8 b[U];
+    uint32_t mine_part = 0;  // kSplit: bit u = key u of this lane is in this pass's range
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t h = dev::to_hash<kKeys>(hn[u], seed);  // XXH64 at consumption (kKeys)
       lo[u] = static_cast<uint32_t>(h);
       SBBF_DCHECK(dev::block_index(h, nb) < nb);
-      dev::ld_block_nc(blocks + dev::block_index(h, nb) * 8, b[u]);
+      if constexpr (kSplit) {
+        const bool in = (h >> psh) == pid;
+        mine_part |= static_cast<uint32_t>(in) << u;
+        if (in) dev::ld_block_nc(blocks + dev::block_index(h, nb) * 8, b[u]);
+      } else {
+        dev::ld_block_nc(blocks + dev::block_index(h, nb) * 8, b[u]);
+      }
     }
     const uint64_t tn = t + nwarps;
 #pragma unroll
@@ -306,18 +364,22 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       uint32_t missing = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) missing |= dev::lane_bit(lo[u], dev::lane_seed(i)) & ~b[u].w[i];
-      const bool hit = missing == 0 && idx < n;
+      const bool in = !kSplit || ((mine_part >> u) & 1u);
+      const bool hit = missing == 0 && idx < n && in;
       if constexpr (kBits) {
         const uint32_t word = __ballot_sync(0xffffffffu, hit);
         if (lane == u) mine = word;
       } else {
-        if (idx < n) dev::st_stream_u8(static_cast<uint8_t*>(out) + idx, hit ? 1u : 0u);
+        if (idx < n && in) dev::st_stream_u8(static_cast<uint8_t*>(out) + idx, hit ? 1u : 0u);
       }
     }
     if constexpr (kBits) {
       const uint64_t nwords = (n + 31) >> 5;
       const uint64_t widx = (base >> 5) + lane;
-      if (lane < U && widx < nwords) dev::st_stream_u32(static_cast<uint32_t*>(out) + widx, mine);
+      if (lane < U && widx < nwords) {
+        if (!kSplit || first) dev::st_stream_u32(static_cast<uint32_t*>(out) + widx, mine);
+        else if (mine) atomicOr(static_cast<uint32_t*>(out) + widx, mine);
+      }
     }
   }
 }
@@ -518,6 +580,21 @@ bool red_hint(const DeviceInfo& di, const Geom& g) {
   return g.nb_local * 32 * 2 > static_cast<uint64_t>(di.l2_bytes);
 }
 
+// Range-split passes for a whole filter somewhat larger than L2: 2^k passes,
+// each over every key but touching only one contiguous 1/2^k of the filter,
+// which stays L2-resident while its keys land (config 3's 128 MiB filter:
+// inserts 55.4 -> 113.6 Gkeys/s with 2 passes, 85.6 with 4; lookups 112.8
+// (blocked) -> 137.6 with 2 passes, 69.2 with 4, whose extra hash-stream
+// passes cost more than they save). Each range must fit in ~0.6 x L2.
+int split_log2(const DeviceInfo& di, const Geom& g, bool lookup) {
+  if (g.first != 0 || g.nb_local != g.nb_global) return 0;  // top hash bits = block ranges of a whole filter only
+  const double part = 0.6 * static_cast<double>(di.l2_bytes);
+  const double bytes = static_cast<double>(g.nb_local) * 32.0;
+  if (bytes <= part) return 0;
+  if (bytes <= 2 * part) return 1;
+  return lookup || bytes > 4 * part ? 0 : 2;
+}
+
 cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, const Geom& g,
                           const uint64_t* hashes, uint64_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
@@ -544,7 +621,12 @@ cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, c
     // step 187.4 -> 188.6, config 3 inserts 51.9 -> 55.7 Gkeys/s vs a
     // persistent grid of 4 CTAs/SM)
     const uint64_t grid = (n + kThreads * 4 - 1) / (kThreads * 4);
-    if (red_hint(di, g))
+    const int split_log = split_log2(di, g, false);
+    if (split_log > 0) {
+      for (uint64_t p = 0; p < (uint64_t{1} << split_log); ++p)
+        insert_wide_kernel<false, false, 4, true, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
+            blocks, g, hashes, n, 0, static_cast<uint32_t>(64 - split_log), p);
+    } else if (red_hint(di, g))
       insert_wide_kernel<false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n);
     else
       insert_wide_kernel<false, false, 4, false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g,
@@ -604,9 +686,9 @@ cudaError_t launch_find_keys(const DeviceInfo& di, const uint32_t* blocks, const
     static const int occ_w = resident_blocks(find_whole_kernel<kU, true, kMinB, true>, kThreads, 0);
     cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kU, di.sms, occ_w)));
     return bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, true, kMinB, true>, blocks, g.nb_global, keys, n, out,
-                                     seed)
+                                     seed, 63u, uint64_t{0}, true)
                 : cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, false, kMinB, true>, blocks, g.nb_global, keys, n,
-                                     out, seed);
+                                     out, seed, 63u, uint64_t{0}, true);
   }
   return bits ? cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, true, kMinB, true>, blocks, g, keys, n, out, seed)
               : cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, false, kMinB, true>, blocks, g, keys, n, out, seed);
@@ -642,10 +724,26 @@ cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* block
     if (g.first == 0 && g.nb_local == g.nb_global) {  // a whole filter: the lean kernel
       static const int occ_w = resident_blocks(find_whole_kernel<kU, true, kMinB>, kThreads, 0);
       cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kU, di.sms, occ_w)));
+      const int split_log = split_log2(di, g, true);
+      if (split_log > 0) {
+        constexpr int kUS = kU, kMinS = kMinB;  // U = 8 at 2 CTAs/SM measured the same (136.5 vs 137.6)
+        static const int occ_s = resident_blocks(find_whole_kernel<kUS, true, kMinS, false, true>, kThreads, 0);
+        cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kUS, di.sms, occ_s)));
+        cudaError_t e = cudaSuccess;
+        for (uint64_t p = 0; p < (uint64_t{1} << split_log) && e == cudaSuccess; ++p) {
+          const uint32_t psh = static_cast<uint32_t>(64 - split_log);
+          const bool first = p == 0;
+          e = bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kUS, true, kMinS, false, true>, blocks, g.nb_global,
+                                        hashes, n, out, uint64_t{0}, psh, p, first)
+                   : cudaLaunchKernelEx(&cfg, find_whole_kernel<kUS, false, kMinS, false, true>, blocks, g.nb_global,
+                                        hashes, n, out, uint64_t{0}, psh, p, first);
+        }
+        return e;
+      }
       return bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, true, kMinB>, blocks, g.nb_global, hashes, n, out,
-                                       uint64_t{0})
+                                       uint64_t{0}, 63u, uint64_t{0}, true)
                   : cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, false, kMinB>, blocks, g.nb_global, hashes, n, out,
-                                       uint64_t{0});
+                                       uint64_t{0}, 63u, uint64_t{0}, true);
     }
     cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kU, di.sms, occ)));  // a shard
     return bits ? cudaLaunchKernelEx(&cfg, find_pipe_kernel<kU, true, kMinB>, blocks, g, hashes, n, out, uint64_t{0})

@@ -461,3 +461,24 @@ def test_blocked_pipelined_rounds(cuda, oracle):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(bits, want_bits)
+
+
+@pytest.mark.parametrize("nb", [1 << 22, 4_400_007, (1 << 23) + 5])
+def test_range_split_passes(cuda, oracle, nb):
+    """Whole filters somewhat larger than L2 insert (2 or 4 passes) and look
+    up (2 passes, up to ~1.2 x L2) in range-split passes over the top hash
+    bits: every pass touches one L2-resident block range; bitmap words are
+    stored by the first pass and ORed by the next. Bit-exact against the
+    oracle for bytes and bits, with ragged batch sizes."""
+    rng = np.random.default_rng(nb)
+    hs = rng.integers(0, 2**64, size=3_000_017, dtype=np.uint64)
+    probes = np.concatenate([hs[:700_001], rng.integers(0, 2**64, size=1_300_003, dtype=np.uint64)])
+    f = SplitBlockFilter(nb)
+    f.add_hashes(dev(hs, cuda))
+    want = oracle.build(nb, hs)
+    assert np.array_equal(f.blocks(), want)
+    want_res = oracle.find_hashes(want, probes)
+    f.set_find_variant(_lib.FIND_GLOBAL)
+    assert np.array_equal(f.find_hashes(dev(probes, cuda)).cpu().numpy(), want_res)
+    bits = u32(f.find_hashes_bits(dev(probes, cuda)))
+    assert np.array_equal(bits_to_bytes(bits, probes.size), want_res)
