@@ -518,6 +518,12 @@ def ncu_traffic(res: dict):
     return per_key * res["lookups"]
 
 
+def lookup_split(filter_bytes: int, l2_bytes: int) -> bool:
+    """sbbf_kernels.cu split_log2 for lookups: whole filters in (0.6, 1.2] x L2
+    are probed in two range-split passes."""
+    return 0.6 * l2_bytes < filter_bytes <= 1.2 * l2_bytes
+
+
 def roofline(res: dict, l2_sector_gs: float | None, hbm_peak: float, peak_note: str,
              l2_bytes: int) -> dict:
     """Dominant kernel = lookup. Algorithmic HBM bytes/key: 8 (hash in) + 1/8
@@ -525,8 +531,16 @@ def roofline(res: dict, l2_sector_gs: float | None, hbm_peak: float, peak_note: 
     L = res["lookups"]
     resident = res["filter_bytes"] <= l2_bytes // 2
     blocked = res.get("find_variant") == 3
+    split = lookup_split(res["filter_bytes"], l2_bytes) and res.get("find_variant") == 1
     t = res["ms_lookup"] * 1e-3
-    if blocked:
+    if split:
+        # two range-split passes (sbbf_kernels.cu split_log2): every pass
+        # streams all hashes and probes the keys of one L2-resident half
+        per_key = 2 * 8.0 + 0.125 + res["filter_bytes"] / L
+        kernel = "find_whole_kernel<4, bits, 3, 0, split> x 2 range passes (bitmap)"
+        note = ("range-split: 8 B hash per pass (2 passes) + 1/8 B bitmap + each filter half read "
+                "once into L2 (filter_bytes/lookups)")
+    elif blocked:
         # L2-blocked lookup: the algorithmic minimum streams the hash and the
         # bitmap once and the filter once per batch (each slice is L2-resident
         # while its bucket is probed)
@@ -552,6 +566,9 @@ def roofline(res: dict, l2_sector_gs: float | None, hbm_peak: float, peak_note: 
         rf["binding"] = ({"resource": "random-sector request rate, filter L2-resident (about one 32-B sector "
                                       "per SM-clock; ncu: L1TEX 90 % busy, profiles/r1h_ncu_summary.md)",
                           "frac": rate / l2_sector_gs} if resident and not blocked else
+                         {"resource": "range-split passes: L2 random-sector rate on each half "
+                                      "(bench.py measures it on a half-filter buffer)",
+                          "frac": rate / l2_sector_gs} if split else
                          {"resource": "DRAM random-sector rate (direct probes beyond L2)",
                           "frac": rate / l2_sector_gs} if not blocked else
                          {"resource": "blocked passes: partition issue rate + L2-served probes "
@@ -632,7 +649,10 @@ def main() -> None:
     for r in [main_res] + list(extras.values()):
         # the denominator is the random-sector rate on a buffer of the filter's
         # own size (a 128 MiB filter is partly L2-served, a 1 GiB one is not)
-        ceil = l2_read if r is main_res else sector_ceiling(device, r["filter_bytes"])
+        # (range-split lookups: a half-filter buffer, the range each pass probes)
+        half = lookup_split(r["filter_bytes"], l2_bytes) and r.get("find_variant") == 1
+        ceil = (l2_read if r is main_res else
+                sector_ceiling(device, r["filter_bytes"] // 2 if half else r["filter_bytes"]))
         r["random_sector_frac_lookup"] = r["lookup_gkeys_s"] / ceil
         r["random_sector_ceiling_gs"] = ceil
         r["roofline"] = roofline(r, ceil, hbm_peak, peak_note, l2_bytes)
