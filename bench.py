@@ -537,7 +537,7 @@ def roofline(res: dict, l2_sector_gs: float | None, hbm_peak: float, peak_note: 
         # two range-split passes (sbbf_kernels.cu split_log2): every pass
         # streams all hashes and probes the keys of one L2-resident half
         per_key = 2 * 8.0 + 0.125 + res["filter_bytes"] / L
-        kernel = "find_whole_kernel<4, bits, 3, 0, split> x 2 range passes (bitmap)"
+        kernel = "find_split_kernel x 2 range passes (warp-compacted, bitmap)"
         note = ("range-split: 8 B hash per pass (2 passes) + 1/8 B bitmap + each filter half read "
                 "once into L2 (filter_bytes/lookups)")
     elif blocked:

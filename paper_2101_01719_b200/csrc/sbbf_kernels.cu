@@ -384,6 +384,82 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   }
 }
 
+// One range-split lookup pass, compacted (bitmap output): each warp takes
+// 256 consecutive keys, moves this pass's keys (top hash bits == pid) to
+// the front of a per-warp shared buffer with their in-tile index, probes
+// only those (full warps, up to 4 sector loads in flight per lane), and
+// assembles the 8 bitmap words of the 256 keys in shared memory. The first
+// pass stores the words, later passes OR theirs in.
+constexpr int kSplitTile = 256;
+__global__ void __launch_bounds__(kThreads, 3)
+    find_split_kernel(const uint32_t* __restrict__ blocks, uint64_t nb, const uint64_t* __restrict__ hashes,
+                      uint64_t n, uint32_t* __restrict__ out, uint32_t psh, uint64_t pid, bool first) {
+  __shared__ uint64_t ckey[kThreads / 32][kSplitTile];
+  __shared__ uint8_t cidx[kThreads / 32][kSplitTile];
+  __shared__ uint32_t cbits[kThreads / 32][kSplitTile / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t pol = dev::policy_evict_first();
+  const uint64_t warp = (static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
+  const uint64_t ntiles = (n + kSplitTile - 1) / kSplitTile;
+  const uint64_t nwords = (n + 31) >> 5;
+  if (lane < kSplitTile / 32) cbits[w][lane] = 0;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // filter / bitmap only after the previous grid
+  // (a register prefetch of the next tile's hashes measured slower: 107
+  // registers, 2 CTAs/SM, 131.1 vs 148.2 Gkeys/s on config 3)
+  for (uint64_t t = warp; t < ntiles; t += nwarps) {
+    const uint64_t base = t * kSplitTile;
+    uint64_t h[kSplitTile / 32];
+#pragma unroll
+    for (int k = 0; k < kSplitTile / 32; ++k) {
+      const uint64_t idx = base + k * 32 + lane;
+      h[k] = idx < n ? dev::ld_stream_u64(hashes + idx, pol) : 0;
+    }
+    uint32_t total = 0;
+#pragma unroll
+    for (int k = 0; k < kSplitTile / 32; ++k) {
+      const bool in = base + k * 32 + lane < n && (h[k] >> psh) == pid;
+      const uint32_t bal = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        const uint32_t pos = total + __popc(bal & ((1u << lane) - 1u));
+        ckey[w][pos] = h[k];
+        cidx[w][pos] = static_cast<uint8_t>(k * 32 + lane);
+      }
+      total += __popc(bal);
+    }
+    __syncwarp();
+    for (uint32_t r0 = 0; r0 < total; r0 += 128) {
+      Block8 b[4];
+      uint64_t hk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t j = r0 + u * 32 + lane;
+        hk[u] = j < total ? ckey[w][j] : 0;
+        if (j < total) dev::ld_block_nc(blocks + dev::block_index(hk[u], nb) * 8, b[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t j = r0 + u * 32 + lane;
+        if (j < total && dev::block_contains(b[u], hk[u])) {
+          const uint32_t ci = cidx[w][j];
+          atomicOr(&cbits[w][ci >> 5], 1u << (ci & 31));
+        }
+      }
+    }
+    __syncwarp();
+    if (lane < kSplitTile / 32) {
+      const uint64_t widx = (base >> 5) + lane;
+      const uint32_t word = cbits[w][lane];
+      cbits[w][lane] = 0;
+      if (widx < nwords) {
+        if (first) dev::st_stream_u32(out + widx, word);
+        else if (word) atomicOr(out + widx, word);
+      }
+    }
+    __syncwarp();
+  }
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -586,6 +662,14 @@ bool red_hint(const DeviceInfo& di, const Geom& g) {
 // inserts 55.4 -> 113.6 Gkeys/s with 2 passes, 85.6 with 4; lookups 112.8
 // (blocked) -> 137.6 with 2 passes, 69.2 with 4, whose extra hash-stream
 // passes cost more than they save). Each range must fit in ~0.6 x L2.
+bool split_compact() {  // SBBF_SPLIT_COMPACT=0 selects the uncompacted pass kernel (A/B only)
+  static const bool on = [] {
+    const char* v = getenv("SBBF_SPLIT_COMPACT");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 int split_log2(const DeviceInfo& di, const Geom& g, bool lookup) {
   if (g.first != 0 || g.nb_local != g.nb_global) return 0;  // top hash bits = block ranges of a whole filter only
   const double part = 0.6 * static_cast<double>(di.l2_bytes);
@@ -730,13 +814,21 @@ cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* block
         static const int occ_s = resident_blocks(find_whole_kernel<kUS, true, kMinS, false, true>, kThreads, 0);
         cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kUS, di.sms, occ_s)));
         cudaError_t e = cudaSuccess;
+        static const int occ_c = resident_blocks(find_split_kernel, kThreads, 0);
         for (uint64_t p = 0; p < (uint64_t{1} << split_log) && e == cudaSuccess; ++p) {
           const uint32_t psh = static_cast<uint32_t>(64 - split_log);
           const bool first = p == 0;
-          e = bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kUS, true, kMinS, false, true>, blocks, g.nb_global,
-                                        hashes, n, out, uint64_t{0}, psh, p, first)
-                   : cudaLaunchKernelEx(&cfg, find_whole_kernel<kUS, false, kMinS, false, true>, blocks, g.nb_global,
-                                        hashes, n, out, uint64_t{0}, psh, p, first);
+          if (bits && split_compact()) {
+            cudaLaunchConfig_t cc = cfg;
+            cc.gridDim = dim3(static_cast<unsigned>(grid_for(n, kSplitTile * (kThreads / 32), di.sms, occ_c)));
+            e = cudaLaunchKernelEx(&cc, find_split_kernel, blocks, g.nb_global, hashes, n,
+                                   static_cast<uint32_t*>(out), psh, p, first);
+          } else {
+            e = bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kUS, true, kMinS, false, true>, blocks, g.nb_global,
+                                          hashes, n, out, uint64_t{0}, psh, p, first)
+                     : cudaLaunchKernelEx(&cfg, find_whole_kernel<kUS, false, kMinS, false, true>, blocks,
+                                          g.nb_global, hashes, n, out, uint64_t{0}, psh, p, first);
+          }
         }
         return e;
       }
