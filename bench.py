@@ -200,6 +200,9 @@ def run_config_device(cid: int, steps: int, warmup: int, device, collect_parity=
         "insert_variant": f.resolved_variants(chunk)[0], "find_variant": f.resolved_variants(L)[1],
     }
     out["value"] = (N + L) / (out["ms_per_step"] * 1e-3) / 1e9
+    # the reference's run_bench reports the median of its reps
+    # (harness.cpp:233-242); the extra configs' lines carry it beside the mean
+    out["value_median_step"] = (N + L) / (statistics.median(t_step) * 1e-3) / 1e9
     out["insert_gkeys_s"] = N / (out["ms_insert"] * 1e-3) / 1e9
     out["lookup_gkeys_s"] = L / (out["ms_lookup"] * 1e-3) / 1e9
     if collect_parity:
