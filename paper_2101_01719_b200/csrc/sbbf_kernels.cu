@@ -744,7 +744,14 @@ cudaError_t launch_insert_keys(const DeviceInfo& di, bool test, uint32_t* blocks
     insert_wide_kernel<true, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, keys, n, seed);
   } else {
     const uint64_t grid = (n + kThreads * 4 - 1) / (kThreads * 4);  // as launch_insert's WIDE path
-    insert_wide_kernel<false, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, keys, n, seed);
+    const int split_log = split_log2(di, g, false);
+    if (split_log > 0) {  // range-split passes, as launch_insert
+      for (uint64_t p = 0; p < (uint64_t{1} << split_log); ++p)
+        insert_wide_kernel<false, true, 4, true, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
+            blocks, g, keys, n, seed, static_cast<uint32_t>(64 - split_log), p);
+    } else {
+      insert_wide_kernel<false, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, keys, n, seed);
+    }
   }
   return cudaGetLastError();
 }
@@ -769,6 +776,18 @@ cudaError_t launch_find_keys(const DeviceInfo& di, const uint32_t* blocks, const
   if (g.first == 0 && g.nb_local == g.nb_global) {  // a whole filter: the lean kernel, as for raw hashes
     static const int occ_w = resident_blocks(find_whole_kernel<kU, true, kMinB, true>, kThreads, 0);
     cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kU, di.sms, occ_w)));
+    const int split_log = split_log2(di, g, true);
+    if (split_log > 0) {  // range-split passes (XXH64 applied in each pass)
+      cudaError_t e = cudaSuccess;
+      for (uint64_t p = 0; p < (uint64_t{1} << split_log) && e == cudaSuccess; ++p) {
+        const uint32_t psh = static_cast<uint32_t>(64 - split_log);
+        e = bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, true, kMinB, true, true>, blocks, g.nb_global, keys,
+                                      n, out, seed, psh, p, p == 0)
+                 : cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, false, kMinB, true, true>, blocks, g.nb_global,
+                                      keys, n, out, seed, psh, p, p == 0);
+      }
+      return e;
+    }
     return bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, true, kMinB, true>, blocks, g.nb_global, keys, n, out,
                                      seed, 63u, uint64_t{0}, true)
                 : cudaLaunchKernelEx(&cfg, find_whole_kernel<kU, false, kMinB, true>, blocks, g.nb_global, keys, n,
