@@ -7,13 +7,17 @@ every key of its lookup stream (packed lookup bitmap out). Inputs are
 resident in HBM before timing; L2 is flushed (256 MiB memset + 256 MiB read, untimed)
 between timed steps. `value` = (inserts + lookups) / device time per step.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--extra 3,4]
+N = 1 (default): BASELINE config 4 — the largest single-GPU config (1e9
+inserts with Zipf duplicates in 2^26-key chunks into a 1 GiB filter, then
+2e9 lookups). Configs 2 and 3 are reported under `configs`.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--extra 2,3]
     python bench.py --impl reference ...   # the reference's CPU path (oracle/_ref)
 
 N > 1 (torchrun, one rank per GPU): config 5's sharded mode — the filter is
 partitioned by contiguous block range and keys are routed to their owner
-rank with an NCCL all-to-all (paper_2101_01719_b200.sharded); per-rank keys
-are fixed, so scaling is weak. Rank 0 prints one JSON line.
+rank (paper_2101_01719_b200.sharded); per-rank keys are fixed, so scaling is
+weak. Rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -192,8 +196,11 @@ def run_config_device(cid: int, steps: int, warmup: int, device, collect_parity=
     out = {
         "config": cid, "name": cfg.name, "num_buckets": cfg.num_buckets,
         "filter_bytes": cfg.filter_bytes, "inserts": N, "lookups": L,
+        "insert_chunk": chunk,
         "ms_per_step": statistics.mean(t_step), "ms_insert": statistics.mean(t_ins),
-        "ms_lookup": statistics.mean(t_find), "ms_step_min": min(t_step),
+        "ms_lookup": statistics.mean(t_find), "ms_step_min": min(t_step), "ms_step_max": max(t_step),
+        "ms_step_median": statistics.median(t_step),
+        "step_max_over_min": max(t_step) / min(t_step),
         "ms_step_split": statistics.mean(a + b for a, b in zip(t_ins, t_find)),
         "ms_steps": [round(t, 4) for t in t_step],
         "launches_per_step": launches / steps,
@@ -201,7 +208,7 @@ def run_config_device(cid: int, steps: int, warmup: int, device, collect_parity=
     }
     out["value"] = (N + L) / (out["ms_per_step"] * 1e-3) / 1e9
     # the reference's run_bench reports the median of its reps
-    # (harness.cpp:233-242); the extra configs' lines carry it beside the mean
+    # (harness.cpp:233-242): printed beside the mean
     out["value_median_step"] = (N + L) / (statistics.median(t_step) * 1e-3) / 1e9
     out["insert_gkeys_s"] = N / (out["ms_insert"] * 1e-3) / 1e9
     out["lookup_gkeys_s"] = L / (out["ms_lookup"] * 1e-3) / 1e9
@@ -346,8 +353,13 @@ def sector_ceiling(device, filter_bytes: int, red: bool = False, n: int = 1 << 2
 
 
 def run_e2e(cid: int, steps: int, device) -> dict:
-    """Same metric through the public API with pinned HOST buffers: every step
-    uploads the step's hashes and downloads the 0/1 result bytes."""
+    """Same metric through the public API with HOST buffers: every step the
+    library uploads the step's hashes (pinned host memory; chunked and
+    overlapped with the kernels on three streams inside
+    sbbf_gpu_add_hashes_host / sbbf_gpu_find_hashes_host) and downloads the
+    0/1 result bytes, the reference's find_hashes output (filter.cpp:91).
+    Inserts go in the config's chunks (config 4: 2^26 keys per add_hashes
+    call, as the reference's batched build)."""
     import numpy as np
     import torch
 
@@ -356,12 +368,27 @@ def run_e2e(cid: int, steps: int, device) -> dict:
 
     cfg = W.CONFIGS[cid]
     N, L = cfg.inserts.n, cfg.lookups.n
+    chunk = cfg.insert_chunk or N
     st = W.StreamHandle(cfg.inserts, device.index or 0)
-    ins_h = torch.empty(N, dtype=torch.int64, pin_memory=True)
-    look_h = torch.empty(L, dtype=torch.int64, pin_memory=True)
-    res_h = torch.empty(L, dtype=torch.uint8, pin_memory=True)
-    ins_h.copy_(W.gen_inserts(st, 0, N, device=device.index or 0))
-    look_h.copy_(W.gen_lookups(st, cfg.lookups, N, 0, L, device=device.index or 0))
+    pinned, note = True, "pinned host arrays (torch pin_memory)"
+    try:
+        ins_h = torch.empty(N, dtype=torch.int64, pin_memory=True)
+        look_h = torch.empty(L, dtype=torch.int64, pin_memory=True)
+        res_h = torch.empty(L, dtype=torch.uint8, pin_memory=True)
+    except RuntimeError as exc:  # page-locked limits: pageable arrays, the driver stages the copies
+        pinned, note = False, f"pageable host arrays (pinning failed: {exc!r:.80})"
+        ins_h = torch.empty(N, dtype=torch.int64)
+        look_h = torch.empty(L, dtype=torch.int64)
+        res_h = torch.empty(L, dtype=torch.uint8)
+    # inputs generated on the device in 2^27-key pieces, copied to the host untimed
+    piece = 1 << 27
+    for s0 in range(0, N, piece):
+        m = min(piece, N - s0)
+        ins_h[s0:s0 + m].copy_(W.gen_inserts(st, s0, m, device=device.index or 0))
+    for s0 in range(0, L, piece):
+        m = min(piece, L - s0)
+        look_h[s0:s0 + m].copy_(W.gen_lookups(st, cfg.lookups, N, s0, m, device=device.index or 0))
+    torch.cuda.synchronize(device)
     ins_np = ins_h.numpy().view(np.uint64)
     look_np = look_h.numpy().view(np.uint64)
     res_np = res_h.numpy()
@@ -371,12 +398,13 @@ def run_e2e(cid: int, steps: int, device) -> dict:
         f.clear()
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()
-        f.add_hashes(ins_np)                 # H2D + insert kernels
-        f.find_hashes(look_np, res_np)       # H2D + lookup kernels + D2H of results
+        for s0 in range(0, N, chunk):
+            f.add_hashes(ins_np[s0:s0 + chunk])   # H2D + insert kernels (synchronous)
+        f.find_hashes(look_np, res_np)           # H2D + lookup kernels + D2H of the results
         t1 = time.perf_counter()
         if k >= 2:
             times.append(t1 - t0)
-    ok = int(res_np.sum())
+    hits = int(res_np.sum(dtype=np.uint64))
     del f
     # the bound e2e runs into: pinned H2D copy bandwidth (one 256 MiB copy, best of 3)
     big = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
@@ -390,23 +418,48 @@ def run_e2e(cid: int, steps: int, device) -> dict:
         best = min(best, time.perf_counter() - t0)
     h2d_gbs = (256 << 20) / best / 1e9
     med = statistics.median(times)
-    return {"value": (N + L) / med / 1e9, "unit": "Gkeys/s",
-            "h2d_bytes_per_step": 8 * (N + L), "d2h_bytes_per_step": L,
-            "ms_per_step": med * 1e3, "hits": ok,
-            "h2d_gbs_achieved": 8 * (N + L) / med / 1e9, "h2d_gbs_peak_measured": h2d_gbs,
-            "bound": "PCIe host-to-device copy of the hashes (8 B/key)",
-            "api": "SplitBlockFilter.add_hashes/find_hashes on pinned host arrays "
-                   "(sbbf_gpu_add_hashes_host / sbbf_gpu_find_hashes_host)"}
+    g = golden().get(str(cid))
+    out = {"value": (N + L) / med / 1e9, "unit": "Gkeys/s",
+           "h2d_bytes_per_step": 8 * (N + L), "d2h_bytes_per_step": L,
+           "ms_per_step": med * 1e3, "steps": len(times), "hits": hits,
+           "h2d_gbs_achieved": 8 * (N + L) / med / 1e9, "h2d_gbs_peak_measured": h2d_gbs,
+           "bound": "PCIe host-to-device copy of the hashes (8 B/key)", "host_memory": note,
+           "api": f"SplitBlockFilter.add_hashes (chunks of {chunk} keys) / find_hashes on host arrays "
+                  "(sbbf_gpu_add_hashes_host / sbbf_gpu_find_hashes_host)"}
+    if g:
+        out["hits_match_reference"] = hits == g["member_hits"] + g["false_positives"]
+    del ins_h, look_h, res_h, big, dbig
+    return out
 
 
 # --------------------------------------------------------------------------------
 # CPU baseline: the reference itself (oracle/_ref), run_bench's method
 # --------------------------------------------------------------------------------
-def cpu_reference_run(cid: int, reps: int, threads: int, device=None, sample: int | None = None,
+def cpu_sample(cid: int, world: int = 1, sample_keys: int = 1 << 27):
+    """(inserts, lookups, description) of the bounded CPU sample for a config.
+    Configs 1-3 run in full. Config 4 (1e9 + 2e9 keys would take minutes per
+    rep on one insert thread): one 2^26-key insert chunk — the first of the
+    config's batched-insert chunks — into a fresh 1 GiB filter, then the
+    first 2^27 lookups, the config's 1:2 insert:lookup mix. Config 5: the
+    sharded arm's whole-job per-step sample (world x sample_keys each way,
+    capped at 2^28), into the 8 GiB filter."""
+    from paper_2101_01719_b200 import workload as W
+    cfg = W.CONFIGS[cid]
+    if cid == 4:
+        return (1 << 26, 1 << 27,
+                "config-4 sample: insert positions [0, 2^26) (the first 2^26-key chunk) into a fresh "
+                "1 GiB filter, then lookup positions [0, 2^27) of the config's lookup stream")
+    if cid == 5:
+        n = min(sample_keys * world, 1 << 28)
+        return n, n, f"a config-5 sample ({n} inserts + {n} lookups) into the 8 GiB filter"
+    return cfg.inserts.n, cfg.lookups.n, f"config {cid} in full"
+
+
+def cpu_reference_run(cid: int, reps: int, threads: int, world: int = 1, sample_keys: int = 1 << 27,
                       warmup: int = 0) -> dict:
-    """sample (config 5): the step is `sample` inserts + `sample` lookups of
-    config 5's streams (the sharded arm's whole-job sample), not 8e9 + 8e9.
-    The first `warmup` reps run untimed (dropped)."""
+    """The reference core itself (oracle/_ref, run_bench's method,
+    harness.cpp:132-245) on the bounded sample of `cpu_sample`. The first
+    `warmup` reps run untimed (dropped)."""
     import dataclasses
 
     import numpy as np
@@ -415,23 +468,24 @@ def cpu_reference_run(cid: int, reps: int, threads: int, device=None, sample: in
     from paper_2101_01719_b200 import workload as W
 
     cfg = W.CONFIGS[cid]
-    N, L = cfg.inserts.n, cfg.lookups.n
+    N, L, what = cpu_sample(cid, world, sample_keys)
     ins_spec = cfg.inserts
-    if sample:
-        N = L = sample
-        ins_spec = dataclasses.replace(cfg.inserts, n=sample)
+    num_inserts = cfg.inserts.n
+    if cid == 5:
+        ins_spec = dataclasses.replace(cfg.inserts, n=N)
+        num_inserts = N
     orc = O.Oracle()
     table = W.zipf_cdf_table(cfg.inserts.zipf_s, cfg.inserts.zipf_n) if cfg.inserts.dup_num else None
     ost = orc.stream(ins_spec, table)
     ins = orc.gen_inserts(ost, 0, N)
-    look = orc.gen_lookups(ost, cfg.lookups, N, 0, L)
+    look = orc.gen_lookups(ost, cfg.lookups, num_inserts, 0, L)
     try:
         ref = O.Reference()
         kind = "reference"
         ti, tl, res, blocks = ref.time_build_probe(cfg.num_buckets, ins, look, threads, warmup + reps)
         ti, tl = ti[warmup:], tl[warmup:]
         # lookups on one core as well as on all of them
-        tl1 = ref.time_build_probe(cfg.num_buckets, ins, look, 1, 3)[1] if threads > 1 and not sample else tl
+        tl1 = ref.time_build_probe(cfg.num_buckets, ins, look, 1, 1)[1] if threads > 1 and cid < 5 else tl
     except (FileNotFoundError, OSError):
         kind = "port"
         ti, tl = [], []
@@ -449,16 +503,17 @@ def cpu_reference_run(cid: int, reps: int, threads: int, device=None, sample: in
         blocks = b
         tl1 = tl
     mi, ml = statistics.median(ti), statistics.median(tl)
-    # (an 8 GiB config-5 image is not checksummed here: the tests pin parity)
-    crc = None if sample else image_crc(np.ascontiguousarray(blocks).tobytes(), cfg.num_buckets)
-    what = f"a config-5 sample ({N} inserts + {L} lookups)" if sample else f"config {cid} in full ({N} inserts + {L} lookups)"
+    # image CRC only for the configs run in full (their goldens exist)
+    full = cid in (1, 2, 3)
+    crc = image_crc(np.ascontiguousarray(blocks).tobytes(), cfg.num_buckets) if full else None
     return {"value": (N + L) / (mi + ml) / 1e9, "unit": "Gkeys/s", "cores": threads, "kind": kind,
             "sample": f"{what}, median of {reps} reps; "
                       f"insert 1 thread (the reference's only writer mode), lookup {threads} "
                       f"jthreads (harness.cpp:173-200); -O3 -DNDEBUG, AVX2 backend",
+            "inserts": N, "lookups": L,
             "insert_gkeys_s": N / mi / 1e9, "lookup_gkeys_s": L / ml / 1e9,
             "lookup_gkeys_s_1thread": L / statistics.median(tl1) / 1e9,
-            "image_crc": f"{crc:#010x}" if crc is not None else None, "hits": int(res.sum())}
+            "image_crc": f"{crc:#010x}" if crc is not None else None, "hits": int(res.sum(dtype=np.uint64))}
 
 
 def run_reference_arm(args) -> None:
@@ -467,21 +522,16 @@ def run_reference_arm(args) -> None:
         return
     threads = os.cpu_count() or 1
     world = env_int("WORLD_SIZE", 1)
-    # config 5: the sharded arm's whole-job per-step sample, capped at 2^28
-    # keys each way so that the CPU run (8 GiB filter, one insert thread)
-    # stays within minutes; the metric is a rate
-    sample = min(args.sample_keys * world, 1 << 28) if args.config == 5 else None
-    reps = max(args.steps, 3) if sample is None else 3  # config 5: each rep builds an 8 GiB filter
-    r = cpu_reference_run(args.config, reps, threads, sample=sample, warmup=args.warmup)
-    from paper_2101_01719_b200 import workload as W
-    cfg = W.CONFIGS[args.config]
+    reps = max(args.steps, 1)
+    r = cpu_reference_run(args.config, reps, threads, world=world, sample_keys=args.sample_keys,
+                          warmup=args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "Gkeys/s",
         "n_gpus": args.gpus, "steps": reps, "warmup": args.warmup,
-        "ms_per_step": ((2 * sample) if sample else (cfg.inserts.n + cfg.lookups.n)) / r["value"] / 1e6,
+        "ms_per_step": (r["inserts"] + r["lookups"]) / r["value"] / 1e6,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (seeded splitmix64 hash streams, BASELINE.json)",
-        "config": workload_config(args.config, sample),
+        "config": workload_config(args.config, world, args.sample_keys),
         "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": r["value"], "unit": "Gkeys/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -492,33 +542,39 @@ def run_reference_arm(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def workload_config(cid: int, sample: int | None = None) -> dict:
+def workload_config(cid: int, world: int = 1, sample_keys: int = 1 << 27) -> dict:
+    """The `config` object of both arms (identical for the same command)."""
     from paper_2101_01719_b200 import workload as W
     cfg = W.CONFIGS[cid]
-    if sample:
-        return {"workload": f"BASELINE config 5 sample: {sample:,} inserts + {sample:,} lookups (25% members) "
-                            f"into the 8 GiB filter ({cfg.num_buckets} blocks)", "config_id": cid,
-                "inserts": sample, "lookups": sample, "num_buckets": cfg.num_buckets,
-                "parallelism": "reference CPU path (rank 0)"}
-    return {"workload": f"BASELINE config {cid}: {cfg.inserts.n:,} inserts into "
-                        f"{cfg.filter_bytes:,} B ({cfg.num_buckets} blocks), then "
-                        f"{cfg.lookups.n:,} lookups", "config_id": cid,
-            "inserts": cfg.inserts.n, "lookups": cfg.lookups.n, "num_buckets": cfg.num_buckets,
-            "l2": "flushed between timed steps (256 MiB memset then 256 MiB read, untimed)",
-            "lookup_output": "packed bitmap (1 bit/key)", "parallelism": "single GPU"}
+    if cid == 5:
+        return {"workload": f"BASELINE config 5 sample: 8 GiB filter ({cfg.num_buckets} blocks) sharded over "
+                            f"{world} rank(s) by block range; per rank per step {sample_keys:,} inserts "
+                            f"+ {sample_keys:,} lookups (25% members)", "config_id": cid,
+                "inserts_per_rank": sample_keys, "lookups_per_rank": sample_keys,
+                "num_buckets": cfg.num_buckets, "parallelism": f"shard{world}",
+                "l2": "flushed between timed steps (untimed)"}
+    c = {"workload": f"BASELINE config {cid}: {cfg.inserts.n:,} inserts into "
+                     f"{cfg.filter_bytes:,} B ({cfg.num_buckets} blocks), then "
+                     f"{cfg.lookups.n:,} lookups", "config_id": cid,
+         "inserts": cfg.inserts.n, "lookups": cfg.lookups.n, "num_buckets": cfg.num_buckets,
+         "l2": "flushed between timed steps (256 MiB memset then 256 MiB read, untimed)",
+         "lookup_output": "packed bitmap (1 bit/key)", "parallelism": "single GPU"}
+    if cfg.insert_chunk:
+        c["insert_chunk"] = cfg.insert_chunk
+    return c
 
 
-def ncu_traffic(res: dict):
-    """DRAM bytes per lookup launch from the committed ncu capture
-    (profiles/traffic.json), scaled to this run's keys per launch; None when
-    no capture exists for this config's lookup kernel."""
+def ncu_traffic(cid: int, phase: str, keys: int):
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of one
+    phase (`lookup` / `insert`: every kernel the phase launches) from the
+    committed ncu launch lists (profiles/traffic.json), per key, scaled to
+    this run's keys; None when no capture exists."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            t = json.load(fh)[str(res["config"])]
+            t = json.load(fh)[str(cid)][phase]
     except Exception:
-        return None
-    per_key = (t["dram_read_bytes"] + t["dram_write_bytes"]) / t["keys_per_launch"]
-    return per_key * res["lookups"]
+        return None, None
+    return t["dram_bytes_per_key"] * keys, t
 
 
 def lookup_split(filter_bytes: int, l2_bytes: int) -> bool:
@@ -527,65 +583,53 @@ def lookup_split(filter_bytes: int, l2_bytes: int) -> bool:
     return 0.6 * l2_bytes < filter_bytes <= 1.2 * l2_bytes
 
 
-def roofline(res: dict, l2_sector_gs: float | None, hbm_peak: float, peak_note: str,
-             l2_bytes: int) -> dict:
-    """Dominant kernel = lookup. Algorithmic HBM bytes/key: 8 (hash in) + 1/8
-    (bitmap out) + 32 (random sector) when the filter exceeds L2."""
-    L = res["lookups"]
+def roofline(res: dict, hbm_peak: float, peak_note: str, l2_bytes: int, l2_read_gs: float,
+             l2_red_gs: float) -> tuple[dict, dict]:
+    """The north star's roofline: one random 32-byte sector per key (read
+    for a lookup, read-modify-write = 64 B for an insert) at HBM bandwidth —
+    or, for a filter that fits in L2, at the L2 random-sector rate measured
+    on a filter-sized buffer (sbbf_bench_sector_read / _red: MEASURED_PEAKS
+    has no L2 figure). achieved = keys x 32 (64) B / phase time; frac =
+    achieved / peak. The streamed bytes the kernels actually move (hashes,
+    partition passes, bitmap) are reported under `stream` and, measured by
+    ncu, as `traffic`."""
+    L, N = res["lookups"], res["inserts"]
+    t_l, t_i = res["ms_lookup"] * 1e-3, res["ms_insert"] * 1e-3
     resident = res["filter_bytes"] <= l2_bytes // 2
-    blocked = res.get("find_variant") == 3
-    split = lookup_split(res["filter_bytes"], l2_bytes) and res.get("find_variant") == 1
-    t = res["ms_lookup"] * 1e-3
-    if split:
-        # two range-split passes (sbbf_kernels.cu split_log2): every pass
-        # streams all hashes and probes the keys of one L2-resident half
-        per_key = 2 * 8.0 + 0.125 + res["filter_bytes"] / L
-        kernel = "find_split_kernel x 2 range passes (warp-compacted, bitmap)"
-        note = ("range-split: 8 B hash per pass (2 passes) + 1/8 B bitmap + each filter half read "
-                "once into L2 (filter_bytes/lookups)")
-    elif blocked:
-        # L2-blocked lookup: the algorithmic minimum streams the hash and the
-        # bitmap once and the filter once per batch (each slice is L2-resident
-        # while its bucket is probed)
-        per_key = 8.0 + 0.125 + res["filter_bytes"] / L
-        kernel = "blocked find: chunk_scatter + segment_kernel + unpermute (sbbf_blocked.cu)"
-        note = ("blocked: 8 B hash + 1/8 B bitmap + filter streamed once (filter_bytes/lookups); "
-                "the partition's extra passes are overhead, not algorithmic bytes")
-    elif resident:
-        per_key = 8.125
-        kernel = ("find_smem_kernel (bitmap)" if res.get("find_variant") == 2 else
-                  "find_whole_kernel<4, bits, 3> (bitmap)")
-        note = "filter L2-resident: hash stream 8 B + bitmap 1/8 B per key from HBM"
+    if resident:
+        peak_l = l2_read_gs * 32.0
+        peak_i = l2_red_gs * 64.0
+        pnote = ("L2: random 32-B sector rate measured in this run on a filter-sized buffer "
+                 f"({l2_read_gs:.1f} G sectors/s read, {l2_red_gs:.1f} G/s red; sbbf_bench_sector_*), "
+                 "x 32 B (lookup) / x 64 B (insert)")
+        bound = "l2"
     else:
-        per_key, kernel = 40.125, "find_pipe_kernel (bitmap)"
-        note = "32 B random sector + 8 B hash + 1/8 B bitmap per key"
-    achieved = L * per_key / t / 1e9
-    rf = {"bound": "hbm", "kernel": kernel,
-          "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-          "traffic": None, "bytes_per_key": per_key, "bytes_note": note, "peak_note": peak_note}
-    if l2_sector_gs:
-        rate = L / t / 1e9
-        # the resource that actually binds this kernel, for a reader of `frac`
-        rf["binding"] = ({"resource": "random-sector request rate, filter L2-resident (about one 32-B sector "
-                                      "per SM-clock; ncu: L1TEX 90 % busy, profiles/r1h_ncu_summary.md)",
-                          "frac": rate / l2_sector_gs} if resident and not blocked else
-                         {"resource": "range-split passes: L2 random-sector rate on each half "
-                                      "(bench.py measures it on a half-filter buffer)",
-                          "frac": rate / l2_sector_gs} if split else
-                         {"resource": "DRAM random-sector rate (direct probes beyond L2)",
-                          "frac": rate / l2_sector_gs} if not blocked else
-                         {"resource": "blocked passes: partition issue rate + L2-served probes "
-                                      "(profiles/r1_blocked_partition.md)",
-                          "vs_direct_ceiling": rate / l2_sector_gs,
-                          "note": "lookups/s over the DRAM random-sector ceiling that bounds direct probes"})
-        rf["random_sector"] = {"lookup_gkeys_s": rate, "ceiling_gsectors_s": l2_sector_gs,
-                               "frac": rate / l2_sector_gs,
-                               "note": "one 32-B sector per key vs the measured random-sector "
-                                       "read rate on a buffer of the filter's size "
-                                       "(sbbf_bench_sector_read)"
-                                       + ("; the blocked path turns random HBM sectors into "
-                                          "L2 hits, so frac > 1 is expected" if blocked else "")}
-    return rf
+        peak_l = peak_i = hbm_peak
+        pnote = peak_note
+        bound = "hbm"
+    kernels = {1: "find_whole_kernel / find_split_kernel (direct, bitmap)", 2: "find_smem_kernel",
+               3: "blocked: partition + slice sweep (sbbf_blocked.cu)"}
+    ach_l = L * 32.0 / t_l / 1e9
+    traffic, tl = ncu_traffic(res["config"], "lookup", L)
+    rl = {"bound": bound, "kernel": kernels.get(res.get("find_variant"), "lookup"),
+          "achieved": ach_l, "peak": peak_l, "unit": "GB/s", "frac": ach_l / peak_l,
+          "traffic": traffic, "bytes_per_key": 32.0,
+          "ceiling_gkeys_s": peak_l / 32.0, "lookup_gkeys_s": L / t_l / 1e9,
+          "peak_note": pnote,
+          "bytes_note": "north-star roofline: one random 32-B sector read per lookup",
+          "traffic_note": ("ncu dram__bytes_read.sum + dram__bytes_write.sum of every kernel of the lookup "
+                           f"phase ({tl['source']}), {tl['dram_bytes_per_key']:.2f} B/key x {L} lookups"
+                           if tl else "no ncu capture committed for this config")}
+    ach_i = N * 64.0 / t_i / 1e9
+    traffic_i, ti = ncu_traffic(res["config"], "insert", N)
+    ri = {"bound": bound, "achieved": ach_i, "peak": peak_i, "unit": "GB/s", "frac": ach_i / peak_i,
+          "traffic": traffic_i, "bytes_per_key": 64.0, "ceiling_gkeys_s": peak_i / 64.0,
+          "insert_gkeys_s": N / t_i / 1e9, "peak_note": pnote,
+          "bytes_note": "north-star roofline: read-modify-write of one random 32-B sector per insert",
+          "traffic_note": ("ncu DRAM bytes of every kernel of the insert phase "
+                           f"({ti['source']}), {ti['dram_bytes_per_key']:.2f} B/key" if ti else
+                           "no ncu capture committed for this config")}
+    return rl, ri
 
 
 def main() -> None:
@@ -595,12 +639,13 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=None,
-                    help="2 (default, single GPU) / 3 / 4; under torchrun the default is 5 (sharded)")
+                    help="4 (default, single GPU) / 2 / 3; under torchrun the default is 5 (sharded)")
     ap.add_argument("--sample-keys", type=int, default=1 << 27,
                     help="config 5: inserts and lookups per rank per step (bounded sample)")
-    ap.add_argument("--extra", default="3,4", help="extra configs reported under 'configs'")
+    ap.add_argument("--extra", default="2,3", help="extra configs reported under 'configs'")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-widened", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="run the multi-GPU sharded path even at world size 1")
     ap.add_argument("--route", default="auto", choices=["auto", "fused", "nccl"],
@@ -609,7 +654,7 @@ def main() -> None:
     args.warmup = max(args.warmup, 3)
 
     if args.config is None:
-        args.config = 5 if env_int("WORLD_SIZE", 1) > 1 else 2
+        args.config = 5 if env_int("WORLD_SIZE", 1) > 1 else 4
     if args.impl == "reference":
         run_reference_arm(args)
         return
@@ -624,6 +669,16 @@ def main() -> None:
         line = sharded.bench_main(args)
         if rank == 0:
             line["clocks"] = clocks.stop()
+            if args.config == 5:
+                line["config"] = dict(workload_config(5, world, args.sample_keys),
+                                      routing=line["config"].get("workload", ""))
+                if not args.no_cpu_baseline and world == 1:
+                    try:
+                        cb = cpu_reference_run(5, 1, os.cpu_count() or 1, world=1, sample_keys=args.sample_keys)
+                        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                                                   "insert_gkeys_s", "lookup_gkeys_s")}
+                    except Exception as exc:  # the baseline never blocks the GPU line
+                        line["cpu_baseline"] = {"value": None, "error": repr(exc)}
             print(json.dumps(line), flush=True)
         return
 
@@ -637,29 +692,22 @@ def main() -> None:
     clocks = ClockSampler(device.index or 0)
     clocks.start()
     main_res = run_config_device(args.config, args.steps, args.warmup, device)
+    clk = clocks.stop()
     extras = {}
     for c in [int(x) for x in args.extra.split(",") if x.strip()]:
         if c == args.config or c not in (1, 2, 3, 4):
             continue
         extras[str(c)] = run_config_device(c, max(3, min(args.steps, 5)), 3, device)
-    clk = clocks.stop()
 
-    # random-sector ceilings (roofline denominators)
-    l2_read = sector_ceiling(device, max(main_res["filter_bytes"], 1 << 20))
-    hbm_read = sector_ceiling(device, 4 << 30)
-    hbm_red = sector_ceiling(device, 4 << 30, red=True)
-    l2_red = sector_ceiling(device, max(main_res["filter_bytes"], 1 << 20), red=True)
+    # L2 random-sector ceilings (the roofline denominators of L2-resident filters)
+    ceil = {}
     for r in [main_res] + list(extras.values()):
-        # the denominator is the random-sector rate on a buffer of the filter's
-        # own size (a 128 MiB filter is partly L2-served, a 1 GiB one is not)
-        # (range-split lookups: a half-filter buffer, the range each pass probes)
-        half = lookup_split(r["filter_bytes"], l2_bytes) and r.get("find_variant") == 1
-        ceil = (l2_read if r is main_res else
-                sector_ceiling(device, r["filter_bytes"] // 2 if half else r["filter_bytes"]))
-        r["random_sector_frac_lookup"] = r["lookup_gkeys_s"] / ceil
-        r["random_sector_ceiling_gs"] = ceil
-        r["roofline"] = roofline(r, ceil, hbm_peak, peak_note, l2_bytes)
-        r["roofline"]["traffic"] = ncu_traffic(r)
+        fb = max(r["filter_bytes"], 1 << 20)
+        if fb <= l2_bytes // 2 and fb not in ceil:
+            ceil[fb] = (sector_ceiling(device, fb), sector_ceiling(device, fb, red=True))
+    for r in [main_res] + list(extras.values()):
+        l2r, l2w = ceil.get(max(r["filter_bytes"], 1 << 20), (None, None))
+        r["roofline"], r["insert_roofline"] = roofline(r, hbm_peak, peak_note, l2_bytes, l2r or 0.0, l2w or 0.0)
 
     line = {
         "metric": METRIC, "value": main_res["value"], "unit": "Gkeys/s", "n_gpus": 1,
@@ -667,42 +715,36 @@ def main() -> None:
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (seeded splitmix64 hash streams of BASELINE.json, generated in HBM)",
         "config": workload_config(args.config),
+        "value_median_step": main_res["value_median_step"],
+        "ms_step_median": main_res["ms_step_median"], "ms_step_min": main_res["ms_step_min"],
+        "ms_step_max": main_res["ms_step_max"], "step_max_over_min": main_res["step_max_over_min"],
         "insert_gkeys_s": main_res["insert_gkeys_s"], "lookup_gkeys_s": main_res["lookup_gkeys_s"],
         "ms_insert": main_res["ms_insert"], "ms_lookup": main_res["ms_lookup"],
-        "step_timing": ("value/ms_per_step: CUDA events at step start and end only (the lookup grid is a "
-                        "programmatic dependent of the insert grid); ms_insert/ms_lookup: separate steps "
-                        f"with a mid-step event (their sum {main_res['ms_step_split']:.4f} ms)"),
-        "roofline": main_res["roofline"],
-        # the insert phase's own bound: one 32-B sector red request per key
-        # (L1 merges a key's four lane-pair reds) against the same red pattern
-        # on a buffer of the filter's size (sbbf_bench_sector_red)
-        "insert_roofline": {"bound": "L2 atomic sector-request rate",
-                            "achieved_gkeys_s": main_res["insert_gkeys_s"], "ceiling_gsectors_s": l2_red,
-                            "frac": main_res["insert_gkeys_s"] / l2_red,
-                            "note": ("ceiling = the insert's own pattern (4 lanes x red.b64, one sector "
-                                     "request per key) in steady state on a filter-sized buffer; a 1M-key "
-                                     "launch also pays ~6 us of fixed launch/drain time "
-                                     "(scripts/microbench_red.cu, profiles/r1h_ncu_summary.md)")},
-        "random_sector_ceilings_gs": {"l2_read_1MiB": l2_read, "hbm_read_4GiB": hbm_read,
-                                      "hbm_red_4GiB": hbm_red, "l2_red_filter": l2_red},
-        "gpu_launches": int(main_res["launches_per_step"] * args.steps),
+        "step_timing": ("value/ms_per_step: mean of the K timed steps, CUDA events at step start and end "
+                        "only; ms_insert/ms_lookup: separate steps with a mid-step event "
+                        f"(their sum {main_res['ms_step_split']:.4f} ms)"),
+        "roofline": main_res["roofline"], "insert_roofline": main_res["insert_roofline"],
+        "gpu_launches": int(round(main_res["launches_per_step"] * args.steps)),
+        "launches_per_step": main_res["launches_per_step"],
         "clocks": clk, "parity": main_res.get("parity"),
         "variants": {"insert": main_res["insert_variant"], "find": main_res["find_variant"]},
         "configs": {k: {kk: v for kk, v in r.items() if kk not in ("name",)}
                     for k, r in extras.items()},
     }
-    if args.config == 2:
-        line["keys_frontend"] = run_keys_frontend(max(3, min(args.steps, 10)), device)
-        if not args.no_cpu_baseline:
-            try:
-                line["widened"] = run_widened(device)
-            except Exception as exc:  # the extra rows never block the headline line
-                line["widened"] = {"error": repr(exc)}
+    if not args.no_widened:
+        try:
+            line["keys_frontend"] = run_keys_frontend(max(3, min(args.steps, 10)), device)
+            line["widened"] = run_widened(device)
+        except Exception as exc:  # the extra rows never block the headline line
+            line["widened"] = {"error": repr(exc)}
     if not args.no_e2e:
-        line["e2e"] = run_e2e(args.config, max(3, min(args.steps, 10)), device)
+        try:
+            line["e2e"] = run_e2e(args.config, 3, device)
+        except Exception as exc:  # reported, never blocks the line
+            line["e2e"] = {"value": None, "error": repr(exc)}
     if not args.no_cpu_baseline:
         try:
-            cb = cpu_reference_run(args.config, 5, os.cpu_count() or 1)
+            cb = cpu_reference_run(args.config, 3, os.cpu_count() or 1)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample", "insert_gkeys_s",
                                                        "lookup_gkeys_s", "lookup_gkeys_s_1thread")}
             line["cpu_baseline"]["image_crc"] = cb["image_crc"]

@@ -20,7 +20,8 @@ extern "C" {
  * splitmix64(seed) in registers; d_sink receives up to 1024 words. */
 int sbbf_bench_sector_read(const uint32_t* d_buf, uint64_t num_blocks, uint64_t n, uint64_t seed,
                            uint32_t* d_sink, void* stream);
-/* n random 32-byte atomic-OR sector updates (8 lane reds per key). */
+/* n random 32-byte atomic-OR sector updates (4 threads per key, one red.global.or.b64
+ * per lane pair: the insert kernels' pattern). */
 int sbbf_bench_sector_red(uint32_t* d_buf, uint64_t num_blocks, uint64_t n, uint64_t seed,
                           void* stream);
 

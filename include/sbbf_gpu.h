@@ -21,7 +21,14 @@
  *    caller. "h_" pointers are host pointers (pinned or pageable).
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
  *    stream). Device-pointer operations are asynchronous and stream-ordered.
- *    Host-pointer operations (*_host) and to_host/from_host are synchronous.
+ *    Host-pointer operations (*_host, add_hash/find_hash) and
+ *    to_host/from_host are synchronous and start behind ALL work already
+ *    queued on the filter's device (cudaDeviceSynchronize first), so device
+ *    inserts queued on any stream are visible to a following host lookup.
+ *  - Lookups are launched as programmatic dependents of the previous grid on
+ *    the stream (PDL). They read nothing — neither the filter nor the
+ *    caller's hashes — before griddepcontrol.wait, so the hashes may come
+ *    from the kernel launched just before (e.g. a hashing kernel).
  *  - Inserts use atomic OR (red.global.or), so concurrent insert_batch calls
  *    on one handle are safe — the "atomic OR writes" option SPEC.md:131
  *    permits. A find concurrent with an insert may see either answer for

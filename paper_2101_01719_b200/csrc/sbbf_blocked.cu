@@ -801,6 +801,300 @@ __global__ void __launch_bounds__(kUnpermThreads, 4) unpermute_kernel(const uint
   }
 }
 
+// ---------------------------------------------------------------------------
+// persistent slice sweep (replaces segment_kernel + unpermute_kernel)
+// ---------------------------------------------------------------------------
+// One cooperative launch of every resident CTA. CTA c owns a contiguous run
+// of partition chunks and walks the buckets (filter slices) in order; for
+// bucket b it processes the concatenation of its chunks' runs of bucket b as
+// one flat list, split evenly over its warps (no ragged per-run tails, no
+// dependent offset loads: each bucket's run table is built once in shared
+// memory by a block scan). All CTAs sweep the slices in lockstep: before
+// bucket b a CTA waits until every CTA has finished bucket b - kSweepSlack,
+// so at most kSweepSlack + 1 slices (~32 MiB each) are live in L2 at any
+// time whatever the batch size (a grid of independent CTAs keeps ~4 slices
+// in flight on a 2^26-key round and thrashes L2: scripts/microbench_l2res.cu).
+// The wait is only a locality device: results never depend on it.
+// Lookups store one answer byte per routed slot and finish with an epilogue
+// that returns the CTA's own chunks to source order (bitmap or bytes) —
+// the separate unpermute launch is gone.
+constexpr int kSweepThreads = 256;
+constexpr int kSweepWarps = kSweepThreads / 32;
+constexpr int kSweepMaxChunks = 512;  // chunks per CTA (shared-memory run tables)
+constexpr int kSweepSlack = 1;
+
+struct SweepArgs {
+  uint32_t* blocks;
+  Geom g;
+  const uint64_t* keys;   // bucket-major chunk regions (chunk_scatter)
+  const uint16_t* boffs;  // [nchunks][kBoffStride] run offsets; entry kChunkBuckets = chunk key count
+  uint64_t nchunks;
+  uint32_t S;
+  uint8_t* ans;           // lookups: one answer byte per slot
+  const uint16_t* pos16;  // lookups: source position of each slot in its chunk
+  void* out;              // lookups: bitmap words / bytes, chunk ch at bit / byte ch * kPartChunk
+  bool bits;
+  unsigned* done;         // [S] CTAs finished per bucket (zeroed before the launch); null = no lockstep
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Exclusive scan of len[0..nk) (nk <= kSweepMaxChunks) into P[0..nk], by
+// the whole block (each thread sums a contiguous pair, then a warp scan of
+// the warp totals).
+__device__ __forceinline__ void block_scan_runs(uint32_t* P, uint32_t nk, uint32_t* wsum) {
+  constexpr int kPer = kSweepMaxChunks / kSweepThreads;
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  uint32_t v[kPer], tot = 0;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const uint32_t k = t * kPer + i;
+    v[i] = k < nk ? P[k] : 0u;
+    tot += v[i];
+  }
+  uint32_t inc = tot;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= static_cast<uint32_t>(d)) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < kSweepWarps ? wsum[lane] : 0u, wi = w;
+#pragma unroll
+    for (int d = 1; d < kSweepWarps; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, wi, d);
+      if (lane >= static_cast<uint32_t>(d)) wi += y;
+    }
+    if (lane < kSweepWarps) wsum[lane] = wi - w;  // exclusive warp bases
+    if (lane == kSweepWarps - 1) wsum[kSweepWarps] = wi;  // total
+  }
+  __syncthreads();
+  uint32_t run = wsum[warp] + inc - tot;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const uint32_t k = t * kPer + i;
+    if (k < nk) P[k] = run;
+    run += v[i];
+  }
+  if (t == 0) P[nk] = wsum[kSweepWarps];
+  __syncthreads();
+}
+
+// Run k of the flat list holding position t: advance from the previous k
+// (positions only grow within a warp's range).
+__device__ __forceinline__ uint32_t run_of(const uint32_t* P, uint32_t k, uint32_t t) {
+  while (P[k + 1] <= t) ++k;
+  return k;
+}
+
+template <bool kInsert, int kU>
+__global__ void __launch_bounds__(kSweepThreads, kInsert ? 4 : 6) sweep_kernel(SweepArgs a) {
+  __shared__ uint32_t P[kSweepMaxChunks + 1];
+  __shared__ uint16_t st16[kSweepMaxChunks];
+  __shared__ uint32_t wsum[kSweepWarps + 1];
+  __shared__ __align__(16) uint8_t stage[kInsert ? 16 : kPartChunk];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t c0 = a.nchunks * blockIdx.x / gridDim.x, c1 = a.nchunks * (blockIdx.x + 1) / gridDim.x;
+  const uint32_t nk = static_cast<uint32_t>(c1 - c0);
+  const uint64_t pol = dev::policy_evict_first();
+  const uint64_t keep = dev::policy_evict_last();
+  const Geom g = a.g;
+  for (uint32_t b = 0; b < a.S; ++b) {
+    // run table of bucket b over this CTA's chunks
+    for (uint32_t k = threadIdx.x; k < nk; k += kSweepThreads) {
+      const uint16_t* row = a.boffs + (c0 + k) * kBoffStride;
+      const uint16_t st = row[b], en = row[b + 1];
+      SBBF_DCHECK(st <= en && en <= row[kChunkBuckets]);
+      st16[k] = st;
+      P[k] = static_cast<uint32_t>(en - st);
+    }
+    if (a.done && b >= kSweepSlack && threadIdx.x == 0) {
+      const unsigned* d = a.done + (b - kSweepSlack);
+      while (ld_acquire_u32(d) < gridDim.x) __nanosleep(64);
+    }
+    __syncthreads();
+    block_scan_runs(P, nk, wsum);
+    const uint32_t T = P[nk];
+    // this warp's share of the flat list
+    const uint32_t r0 = static_cast<uint32_t>(static_cast<uint64_t>(T) * warp / kSweepWarps);
+    const uint32_t r1 = static_cast<uint32_t>(static_cast<uint64_t>(T) * (warp + 1) / kSweepWarps);
+    if constexpr (kInsert) {
+      // 4 lanes per key (one 64-bit lane pair each), 8 keys per warp row, kU
+      // rows in flight; test-before-set: hot keys (config 4's Zipf
+      // duplicates) skip the atomic
+      const uint32_t pair = lane & 3, sub = lane >> 2;
+      const uint32_t seed_lo = dev::lane_seed_rt(2 * pair), seed_hi = dev::lane_seed_rt(2 * pair + 1);
+      uint32_t k = 0;
+      if (r0 < r1) {  // first run of this warp (binary search once)
+        uint32_t lo = 0, hi = nk;
+        while (lo + 1 < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (P[mid] <= r0) lo = mid; else hi = mid;
+        }
+        k = lo;
+      }
+      for (uint32_t t0 = r0; t0 < r1; t0 += 8 * kU) {
+        uint64_t* ptr[kU];
+        uint64_t mask[kU], cur[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint32_t t = t0 + u * 8 + sub;
+          mask[u] = 0;
+          ptr[u] = reinterpret_cast<uint64_t*>(a.blocks) + pair;
+          if (t < r1) {
+            k = run_of(P, k, t);
+            const uint64_t slot = (c0 + k) * kPartChunk + st16[k] + (t - P[k]);
+            const uint64_t h = dev::ld_stream_u64(a.keys + slot, pol);
+            const uint64_t blk = dev::block_index(h, g.nb_global) - g.first;
+            if (blk < g.nb_local) {
+              const uint32_t low = static_cast<uint32_t>(h);
+              ptr[u] = reinterpret_cast<uint64_t*>(a.blocks + blk * 8) + pair;
+              mask[u] = (static_cast<uint64_t>(dev::lane_bit(low, seed_hi)) << 32) | dev::lane_bit(low, seed_lo);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) cur[u] = mask[u] ? dev::ld_pair(ptr[u], keep) : ~0ull;
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (mask[u] & ~cur[u]) dev::red_or64(ptr[u], mask[u], keep);
+      }
+    } else {
+      uint32_t k = 0;
+      if (r0 < r1) {
+        uint32_t lo = 0, hi = nk;
+        while (lo + 1 < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (P[mid] <= r0) lo = mid; else hi = mid;
+        }
+        k = lo;
+      }
+      // kU keys per lane per step, the next step's keys load while this
+      // step's sectors are in flight
+      uint64_t hn[kU], sn[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t t = r0 + u * 32 + lane;
+        sn[u] = ~0ull;
+        hn[u] = 0;
+        if (t < r1) {
+          k = run_of(P, k, t);
+          sn[u] = (c0 + k) * kPartChunk + st16[k] + (t - P[k]);
+          hn[u] = dev::ld_stream_u64(a.keys + sn[u], pol);
+        }
+      }
+      for (uint32_t t0 = r0; t0 < r1; t0 += 32 * kU) {
+        uint64_t h[kU], slot[kU];
+        dev::Block8 bl[kU];
+        uint32_t owned = 0;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          h[u] = hn[u];
+          slot[u] = sn[u];
+          const uint64_t blk = dev::block_index(h[u], g.nb_global) - g.first;
+          const bool ok = blk < g.nb_local && slot[u] != ~0ull;
+          owned |= static_cast<uint32_t>(ok) << u;
+          dev::ld_block_nc_normal(a.blocks + (ok ? blk : 0) * 8, bl[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint32_t t = t0 + 32 * kU + u * 32 + lane;
+          sn[u] = ~0ull;
+          hn[u] = 0;
+          if (t < r1) {
+            k = run_of(P, k, t);
+            sn[u] = (c0 + k) * kPartChunk + st16[k] + (t - P[k]);
+            hn[u] = dev::ld_stream_u64(a.keys + sn[u], pol);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (slot[u] != ~0ull)
+            dev::st_stream_u8(a.ans + slot[u], (((owned >> u) & 1u) && dev::block_contains(bl[u], h[u])) ? 1u : 0u);
+      }
+    }
+    __syncthreads();  // bucket b done by this CTA (and its run table free)
+    if (a.done && threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(a.done + b, 1u);
+    }
+  }
+  if constexpr (!kInsert) {
+    // epilogue: this CTA's chunks back to source order (as unpermute_kernel
+    // did in its own launch). The answer bytes were stored by this CTA's
+    // threads before the barrier above, so coherent L2 loads (.cg) see
+    // them. The next chunk's positions and answers load while this chunk is
+    // scattered through shared memory.
+    constexpr int kVec = kPartChunk / (kSweepThreads * 8);
+    uint4 pv[kVec];
+    uint2 av[kVec];
+    auto load_full = [&](uint64_t ch) {
+#pragma unroll
+      for (int v = 0; v < kVec; ++v) {
+        const uint64_t i = ch * kPartChunk + (v * kSweepThreads + threadIdx.x) * 8;
+        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(pv[v].x), "=r"(pv[v].y), "=r"(pv[v].z), "=r"(pv[v].w) : "l"(a.pos16 + i));
+        asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(av[v].x), "=r"(av[v].y) : "l"(a.ans + i));
+      }
+    };
+    uint32_t cnt_next = c0 < c1 ? a.boffs[c0 * kBoffStride + kChunkBuckets] : 0;
+    if (c0 < c1 && cnt_next == kPartChunk) load_full(c0);
+    for (uint64_t ch = c0; ch < c1; ++ch) {
+      const uint32_t cnt = cnt_next;
+      const uint64_t base = ch * kPartChunk;
+      if (cnt == kPartChunk) {
+#pragma unroll
+        for (int v = 0; v < kVec; ++v) {
+          const uint32_t pw[4] = {pv[v].x, pv[v].y, pv[v].z, pv[v].w};
+          const uint32_t aw[2] = {av[v].x, av[v].y};
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const uint32_t q = (pw[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
+            SBBF_DCHECK(q < kPartChunk);
+            stage[q] = static_cast<uint8_t>(aw[e >> 2] >> ((e & 3) * 8));
+          }
+        }
+      } else {
+        for (uint32_t i = threadIdx.x; i < cnt; i += kSweepThreads) {
+          uint16_t q;
+          uint16_t v;
+          asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(q) : "l"(a.pos16 + base + i));
+          asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(a.ans + base + i));
+          SBBF_DCHECK(q < cnt);
+          stage[q] = static_cast<uint8_t>(v);
+        }
+      }
+      cnt_next = ch + 1 < c1 ? a.boffs[(ch + 1) * kBoffStride + kChunkBuckets] : 0;
+      if (cnt_next == kPartChunk) load_full(ch + 1);
+      __syncthreads();
+      if (a.bits) {
+        uint32_t* ob = static_cast<uint32_t*>(a.out) + (base >> 5);
+        for (uint32_t wd = warp; wd * 32 < cnt; wd += kSweepWarps) {
+          const uint32_t i = wd * 32 + lane;
+          const uint32_t word = __ballot_sync(0xffffffffu, i < cnt && stage[i]);
+          if (lane == 0) dev::st_stream_u32(ob + wd, word);
+        }
+      } else {
+        uint8_t* o = static_cast<uint8_t*>(a.out) + base;
+        if (cnt == kPartChunk && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
+          const uint4* src = reinterpret_cast<const uint4*>(stage);
+          uint4* dst = reinterpret_cast<uint4*>(o);
+          for (uint32_t v = threadIdx.x; v < kPartChunk / 16; v += kSweepThreads) dst[v] = src[v];
+        } else {
+          for (uint32_t i = threadIdx.x; i < cnt; i += kSweepThreads) o[i] = stage[i];
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 template <int BITS, bool kTop>
 cudaError_t chunk_partition_bits(const DeviceInfo& di, const BucketMap& bm, const uint64_t* hashes, uint64_t m,
                                  uint64_t* out, uint16_t* pos16, uint16_t* boffs, cudaStream_t s) {
@@ -837,6 +1131,59 @@ cudaError_t chunk_partition(const DeviceInfo& di, const Geom& g, uint32_t S, con
   }
 }
 
+// SBBF_SWEEP=0 selects the previous segment_kernel + unpermute pair (A/B only).
+bool sweep_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("SBBF_SWEEP");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+// One cooperative launch of the persistent sweep over chunks [0, nchunks).
+// `done` is S counters of scratch (zeroed here). If the cooperative launch
+// is refused (another client holds SMs, MPS limits), the same kernel runs
+// as an ordinary launch without the lockstep wait.
+template <bool kInsert>
+cudaError_t launch_sweep(const DeviceInfo& di, SweepArgs a, cudaStream_t s) {
+  constexpr int kU = kInsert ? 4 : 2;
+  auto kern = sweep_kernel<kInsert, kU>;
+  static const int occ = [&] {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kSweepThreads, 0) != cudaSuccess || b < 1) b = 1;
+    return b;
+  }();
+  uint64_t grid = static_cast<uint64_t>(di.sms) * occ;
+  if (grid > a.nchunks) grid = a.nchunks;
+  const uint64_t min_grid = (a.nchunks + kSweepMaxChunks - 1) / kSweepMaxChunks;
+  if (grid < min_grid) grid = min_grid;
+  if (grid == 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kSweepThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cudaError_t e = cudaSuccess;
+  const bool lockstep = a.done != nullptr && grid <= static_cast<uint64_t>(di.sms) * occ;
+  if (lockstep) {
+    e = cudaMemsetAsync(a.done, 0, a.S * sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    note_launch();
+    e = cudaLaunchKernelEx(&cfg, kern, a);
+    if (e == cudaSuccess) return e;
+    cudaGetLastError();  // cooperative launch refused: run without the lockstep
+  }
+  a.done = nullptr;
+  cfg.attrs = nullptr;
+  cfg.numAttrs = 0;
+  note_launch();
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
 template <bool kInsert>
 cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* keys, const uint16_t* boffs, uint32_t S,
                             uint64_t m, uint8_t* ans, cudaStream_t s) {
@@ -859,6 +1206,7 @@ struct Scratch {
   uint16_t* boffs = nullptr;
   uint16_t* pos16 = nullptr;
   uint8_t* ans = nullptr;
+  unsigned* done = nullptr;  // sweep lockstep counters, one per bucket
 };
 
 cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, bool lookup, cudaStream_t s) {
@@ -869,6 +1217,7 @@ cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, bool lookup, cudaStream_t s
     e = cudaMallocAsync(reinterpret_cast<void**>(&sc.boffs), nchunks * kBoffStride * sizeof(uint16_t), s);
   if (lookup && e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.pos16), cap * sizeof(uint16_t), s);
   if (lookup && e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.ans), cap, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.done), kChunkBuckets * sizeof(unsigned), s);
   return e;
 }
 
@@ -877,6 +1226,7 @@ void free_scratch(Scratch& sc, cudaStream_t s) {
   if (sc.boffs) cudaFreeAsync(sc.boffs, s);
   if (sc.pos16) cudaFreeAsync(sc.pos16, s);
   if (sc.ans) cudaFreeAsync(sc.ans, s);
+  if (sc.done) cudaFreeAsync(sc.done, s);
   sc = Scratch{};
 }
 
@@ -915,6 +1265,11 @@ bool pipeline_enabled() {
 cudaError_t insert_chunk(const DeviceInfo& di, uint32_t* blocks, const Geom& g, uint32_t parts, const uint64_t* keys,
                          uint64_t m, Scratch& sc, cudaStream_t s) {
   cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, nullptr, sc.boffs, s);
+  if (e == cudaSuccess && sweep_enabled()) {
+    const SweepArgs a{blocks, g, sc.keys, sc.boffs, (m + kPartChunk - 1) / kPartChunk, parts,
+                      nullptr, nullptr, nullptr, false, sc.done};
+    return launch_sweep<true>(di, a, s);
+  }
   if (e == cudaSuccess) e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, parts, m, nullptr, s);
   return e;
 }
@@ -923,7 +1278,13 @@ cudaError_t find_chunk(const DeviceInfo& di, const uint32_t* blocks, const Geom&
                        const uint64_t* keys, uint64_t m, Scratch& sc, void* dst, bool bits, cudaStream_t s) {
   // 1. every chunk bucket-major in its own region (+ positions, offsets)
   cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, sc.pos16, sc.boffs, s);
-  // 2. probe slice by slice (L2-resident), one answer byte per routed slot
+  // 2. probe slice by slice (L2-resident), one answer byte per routed slot,
+  // 3. each CTA returns its chunks to source order (persistent sweep)
+  if (e == cudaSuccess && sweep_enabled()) {
+    const SweepArgs a{const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, (m + kPartChunk - 1) / kPartChunk,
+                      parts, sc.ans, sc.pos16, dst, bits, sc.done};
+    return launch_sweep<false>(di, a, s);
+  }
   if (e == cudaSuccess)
     e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, parts, m, sc.ans, s);
   // 3. back to source order, straight into the caller's bitmap / bytes
@@ -1081,7 +1442,7 @@ cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks,
 cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
                          const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  if (plan.super_parts == 1 && n > kBlockedChunk && pipeline_enabled())
+  if (plan.super_parts == 1 && n > kBlockedChunk && pipeline_enabled() && !sweep_enabled())
     return blocked_find_pipelined(di, blocks, g, plan, hashes, n, out, bits, s);
   const uint64_t cap = n < kBlockedChunk ? n : kBlockedChunk;  // a multiple of 32 unless n is the whole batch
   Scratch sc;
@@ -1148,7 +1509,12 @@ cudaError_t blocked_insert_regions(const DeviceInfo& di, uint32_t* blocks, const
     if (counts[r])
       e = chunk_partition(di, g, plan.parts, keys[r], counts[r], sc.keys + off[r] * kPartChunk, nullptr,
                           sc.boffs + off[r] * kBoffStride, s);
-  if (e == cudaSuccess) e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, plan.parts, C * kPartChunk, nullptr, s);
+  if (e == cudaSuccess && sweep_enabled()) {
+    const SweepArgs a{blocks, g, sc.keys, sc.boffs, C, plan.parts, nullptr, nullptr, nullptr, false, sc.done};
+    e = launch_sweep<true>(di, a, s);
+  } else if (e == cudaSuccess) {
+    e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, plan.parts, C * kPartChunk, nullptr, s);
+  }
   free_scratch(sc, s);
   return e;
 }
@@ -1168,14 +1534,20 @@ cudaError_t blocked_find_regions(const DeviceInfo& di, const uint32_t* blocks, c
     if (counts[r])
       e = chunk_partition(di, g, plan.parts, keys[r], counts[r], sc.keys + off[r] * kPartChunk,
                           sc.pos16 + off[r] * kPartChunk, sc.boffs + off[r] * kBoffStride, s);
-  if (e == cudaSuccess)
-    e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, plan.parts, C * kPartChunk,
-                               sc.ans, s);
-  if (e == cudaSuccess) {
-    note_launch();
-    unpermute_kernel<<<static_cast<unsigned>(C), kUnpermThreads, 0, s>>>(sc.ans, sc.pos16, C * kPartChunk, bytes,
-                                                                         false, sc.boffs);
-    e = cudaGetLastError();
+  if (e == cudaSuccess && sweep_enabled()) {
+    const SweepArgs a{const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, C, plan.parts, sc.ans, sc.pos16, bytes,
+                      false, sc.done};
+    e = launch_sweep<false>(di, a, s);
+  } else {
+    if (e == cudaSuccess)
+      e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, plan.parts, C * kPartChunk,
+                                 sc.ans, s);
+    if (e == cudaSuccess) {
+      note_launch();
+      unpermute_kernel<<<static_cast<unsigned>(C), kUnpermThreads, 0, s>>>(sc.ans, sc.pos16, C * kPartChunk, bytes,
+                                                                           false, sc.boffs);
+      e = cudaGetLastError();
+    }
   }
   for (uint32_t r = 0; e == cudaSuccess && r < nr; ++r)
     if (counts[r])

@@ -256,13 +256,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   // hn holds the next tile's raw inputs; with kKeys the XXH64 is applied when
   // the tile is consumed, so the prefetch never waits on its own loads
+  // Every global read, the caller's hashes included, comes after
+  // griddepcontrol.wait: the previous grid on the stream may be the one that
+  // produced the hashes (a key-hashing or generator kernel), and its writes
+  // are only guaranteed visible past the wait. The early launch still hides
+  // this grid's launch and CTA rasterisation behind the previous grid's tail.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   uint64_t hn[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint64_t idx = warp * kTile + u * 32 + lane;
     hn[u] = (warp < ntiles && idx < n) ? dev::ld_stream_u64(hashes + idx, pol) : 0;
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // filter reads only after the insert grid
   for (uint64_t t = warp; t < ntiles; t += nwarps) {
     const uint64_t base = t * kTile;
     uint64_t h[U];
@@ -326,13 +331,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * kThreads) >> 5;
   constexpr uint64_t kTile = 32 * U;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
+  // Every global read, the caller's hashes included, comes after
+  // griddepcontrol.wait: the previous grid on the stream may be the one that
+  // produced the hashes (a key-hashing or generator kernel), and its writes
+  // are only guaranteed visible past the wait. The early launch still hides
+  // this grid's launch and CTA rasterisation behind the previous grid's tail.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   uint64_t hn[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint64_t idx = warp * kTile + u * 32 + lane;
     hn[u] = (warp < ntiles && idx < n) ? dev::ld_stream_u64(hashes + idx, pol) : 0;
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // filter reads only after the insert grid
   for (uint64_t t = warp; t < ntiles; t += nwarps) {
     const uint64_t base = t * kTile;
     uint32_t lo[U];

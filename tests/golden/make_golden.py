@@ -7,6 +7,8 @@ the committed fixtures travel to the GPU box, the reference does not.
 
     python tests/golden/make_golden.py            # configs 1-3 + unit cases
     python tests/golden/make_golden.py --cfg4     # also config 4 (~minutes)
+    python tests/golden/make_golden.py --cfg5     # config 5 (8 GiB, 8e9 + 8e9; ~10 min)
+                                                  # and the sharded bench's per-world samples
 
 Inputs: the reference tests' own std::mt19937_64 draws (seeds from
 filter_test.cpp / persist_test.cpp / acceptance.cpp) and the BASELINE.json
@@ -144,6 +146,85 @@ def config_golden(ref: Reference, orc: Oracle, cid: int, threads: int) -> dict:
     return out
 
 
+def image_crc_of_blocks(blocks: np.ndarray, num_buckets: int, hasher_id: int = 0) -> int:
+    """FilterImage v1 trailer CRC (persist.cpp:72-88) without materialising
+    the image: zlib's IEEE CRC-32 over the 17-byte header, then the blocks
+    (checked against the reference's own serialize() on the smaller cases)."""
+    import zlib
+    hdr = b"SBBF" + bytes([1]) + hasher_id.to_bytes(4, "little") + num_buckets.to_bytes(8, "little")
+    return zlib.crc32(memoryview(np.ascontiguousarray(blocks)).cast("B"), zlib.crc32(hdr)) & 0xFFFFFFFF
+
+
+def stream_golden(ref: Reference, orc: Oracle, num_buckets: int, ins_spec, lk, n_ins: int, n_look: int,
+                  threads: int, chunk: int = 1 << 26, serialize_check: bool = False) -> dict:
+    """Insert positions [0, n_ins) of ins_spec into a reference filter of
+    num_buckets in chunks (add_hashes, filter.cpp:184-190), then look up
+    positions [0, n_look) of lk's mixed stream (members drawn from the n_ins
+    inserts) with find_hashes over `threads` jthreads (harness.cpp:173-200).
+    Large configs stream both sides in chunks (no 64 GB arrays)."""
+    t0 = time.time()
+    st = orc.stream(ins_spec)
+    f = ref.filter(num_buckets)
+    first_ins = None
+    for s in range(0, n_ins, chunk):
+        a = orc.gen_inserts(st, s, min(chunk, n_ins - s))
+        if first_ins is None:
+            first_ins = [int(x) for x in a[:4]]
+        f.add_hashes(a)
+    t_ins = time.time() - t0
+    blocks = f.blocks()
+    crc = image_crc_of_blocks(blocks, num_buckets)
+    if serialize_check:
+        assert crc == image_crc(f.serialize()), "zlib image CRC != reference serialize()"
+    pop = orc.popcount(blocks)
+    del blocks
+    member_hits = nonmember_hits = 0
+    res_crcs = []
+    first_look = None
+    for s in range(0, n_look, chunk):
+        m = min(chunk, n_look - s)
+        q = orc.gen_lookups(st, lk, n_ins, s, m)
+        if first_look is None:
+            first_look = [int(x) for x in q[:4]]
+        r = f.find_hashes(q, threads)
+        j = np.arange(s, s + m, dtype=np.uint64)
+        mem = ((j + 1) * lk.p // lk.q) > (j * lk.p // lk.q)
+        member_hits += int(r[mem].sum())
+        nonmember_hits += int(r[~mem].sum())
+        res_crcs.append(orc.crc32(np.packbits(r, bitorder="little").tobytes()))
+    n_members = W.member_count(lk, n_ins, 0, n_look)
+    out = {"num_buckets": num_buckets, "inserts": n_ins, "lookups": n_look,
+           "first_inserts": first_ins, "first_lookups": first_look,
+           "image_crc": crc, "popcount": pop, "members": n_members, "member_hits": member_hits,
+           "nonmembers": n_look - n_members, "false_positives": nonmember_hits,
+           "lookup_bitmap_chunk_crcs": res_crcs, "chunk_keys": chunk,
+           "seconds": round(time.time() - t0, 1), "insert_seconds": round(t_ins, 1)}
+    print(f"nb={num_buckets} ins={n_ins} look={n_look}: crc={crc:#x} fp={nonmember_hits}/{n_look - n_members} "
+          f"members={member_hits}/{n_members} ({out['seconds']} s)", flush=True)
+    return out
+
+
+def config5_golden(ref: Reference, orc: Oracle, threads: int) -> tuple[dict, dict]:
+    """Config 5 in full (8 GiB filter, 8e9 inserts of splitmix64(9), 8e9
+    lookups, 25 % members, non-members splitmix64(10)) and the sharded
+    bench's per-step samples: at world P every rank r originates insert
+    positions [r*S, (r+1)*S) and lookup positions [r*S, (r+1)*S) of the
+    config-5 streams with P*S inserts (paper_2101_01719_b200/sharded.py
+    bench_main), so the union over ranks is the prefix P*S of each stream."""
+    cfg = W.CONFIGS[5]
+    full = stream_golden(ref, orc, cfg.num_buckets, cfg.inserts, cfg.lookups, cfg.inserts.n, cfg.lookups.n,
+                         threads)
+    full["config"] = 5
+    samples = {}
+    S = 1 << 27
+    for P in (1, 2, 4, 8):
+        g = stream_golden(ref, orc, cfg.num_buckets, cfg.inserts, cfg.lookups, P * S, P * S, threads,
+                          serialize_check=(P == 1))
+        g.update({"world": P, "per_rank_keys": S})
+        samples[str(P)] = g
+    return full, samples
+
+
 def frontend_cases(ref: Reference) -> dict:
     """XXH64 frontend (hash.cpp) and run_fpp_sim (harness.cpp:67-109) goldens."""
     g: dict = {}
@@ -194,9 +275,15 @@ def build_query_inputs():
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg4", action="store_true")
+    ap.add_argument("--cfg5", action="store_true")
     ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
     args = ap.parse_args()
     ref, orc = Reference(), Oracle()
+    if args.cfg5:
+        full, samples = config5_golden(ref, orc, args.threads)
+        with open(os.path.join(OUT, "config5.json"), "w") as fh:
+            json.dump({"5": full, "samples": samples}, fh, indent=1)
+        return
     with open(os.path.join(OUT, "unit_cases.json"), "w") as fh:
         json.dump(unit_cases(ref, orc), fh)
     with open(os.path.join(OUT, "frontend.json"), "w") as fh:
