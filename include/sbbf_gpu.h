@@ -148,6 +148,12 @@ int sbbf_gpu_block_index_batch(const uint64_t* d_hashes, uint64_t n, uint64_t nu
 int sbbf_gpu_make_mask_batch(const uint64_t* d_hashes, uint64_t n, uint32_t* d_lanes,
                              void* stream);
 
+/* The same on host arrays (computed by the device kernels on `device`,
+ * synchronous): what a caller of the reference's free functions links. */
+int sbbf_gpu_block_index_host(const uint64_t* h_hashes, uint64_t n, uint64_t num_buckets, uint64_t* h_out,
+                              int device);
+int sbbf_gpu_make_mask_host(const uint64_t* h_hashes, uint64_t n, uint32_t* h_lanes, int device);
+
 /* --- tuning ----------------------------------------------------------- */
 int sbbf_gpu_set_insert_variant(sbbf_gpu_t* f, int variant);
 int sbbf_gpu_set_find_variant(sbbf_gpu_t* f, int variant);
@@ -165,6 +171,15 @@ int sbbf_gpu_resolved_find_variant(const sbbf_gpu_t* f, uint64_t n);
 uint64_t sbbf_gpu_image_size(uint64_t num_buckets);
 int sbbf_gpu_image_crc(const sbbf_gpu_t* f, uint32_t* crc);
 int sbbf_gpu_serialize(const sbbf_gpu_t* f, void* h_dst, uint64_t cap, uint64_t* written);
+/* CRC-32 (IEEE, crc32_ieee persist.cpp:15-40) of the block array bytes alone,
+ * computed on the GPU: a shard's contribution to the gathered image CRC. */
+int sbbf_gpu_blocks_crc(const sbbf_gpu_t* f, uint32_t* crc);
+/* Host CRC-32 helpers: continue `crc` over len bytes, and the CRC of A||B
+ * from crc(A), crc(B) and len(B) (zlib's crc32_combine). Shards' block CRCs
+ * combine in rank order into the gathered filter's image CRC without moving
+ * the blocks. */
+uint32_t sbbf_crc32_update(uint32_t crc, const void* data, uint64_t len);
+uint32_t sbbf_crc32_combine(uint32_t crc1, uint32_t crc2, uint64_t len2);
 int sbbf_gpu_deserialize(const void* h_img, uint64_t len, int device, sbbf_gpu_t** out, int* errc);
 int sbbf_gpu_save(const sbbf_gpu_t* f, const char* path, int* errc);
 int sbbf_gpu_load(const char* path, int device, sbbf_gpu_t** out, int* errc);

@@ -12,9 +12,10 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# SBBF_LIB=debug selects libsbbf_gpu_debug.so (device-side bounds checks)
-LIB_PATH = os.path.join(HERE, "libsbbf_gpu_debug.so" if os.environ.get("SBBF_LIB") == "debug"
-                        else "libsbbf_gpu.so")
+# SBBF_LIB=<tag> selects libsbbf_gpu_<tag>.so: `debug` (device-side bounds
+# checks, `make debug`) or an A/B build (`make exp EXP_FLAGS=...`)
+_TAG = os.environ.get("SBBF_LIB", "")
+LIB_PATH = os.path.join(HERE, f"libsbbf_gpu_{_TAG}.so" if _TAG else "libsbbf_gpu.so")
 
 SBBF_OK = 0
 SBBF_EINVAL = -1
@@ -54,6 +55,8 @@ PROTOTYPES = {
     "sbbf_gpu_blocks_to_host": (_i, [_vp, _u64, _u64, _vp]),
     "sbbf_gpu_block_index_batch": (_i, [_vp, _u64, _u64, _vp, _vp]),
     "sbbf_gpu_make_mask_batch": (_i, [_vp, _u64, _vp, _vp]),
+    "sbbf_gpu_block_index_host": (_i, [_vp, _u64, _u64, _vp, _i]),
+    "sbbf_gpu_make_mask_host": (_i, [_vp, _u64, _vp, _i]),
     "sbbf_gpu_set_insert_variant": (_i, [_vp, _i]),
     "sbbf_gpu_set_find_variant": (_i, [_vp, _i]),
     "sbbf_gpu_resolved_insert_variant": (_i, [_vp, _u64]),
@@ -61,6 +64,9 @@ PROTOTYPES = {
     "sbbf_gpu_set_l2_fetch_granularity": (_i, [_i, _i, C.POINTER(_i)]),
     "sbbf_gpu_image_size": (_u64, [_u64]),
     "sbbf_gpu_image_crc": (_i, [_vp, C.POINTER(_u32)]),
+    "sbbf_gpu_blocks_crc": (_i, [_vp, C.POINTER(_u32)]),
+    "sbbf_crc32_update": (_u32, [_u32, _vp, _u64]),
+    "sbbf_crc32_combine": (_u32, [_u32, _u32, _u64]),
     "sbbf_gpu_serialize": (_i, [_vp, _vp, _u64, C.POINTER(_u64)]),
     "sbbf_gpu_deserialize": (_i, [_vp, _u64, _i, C.POINTER(_vp), C.POINTER(_i)]),
     "sbbf_gpu_save": (_i, [_vp, C.c_char_p, C.POINTER(_i)]),

@@ -29,6 +29,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -835,6 +836,8 @@ struct SweepArgs {
   void* out;              // lookups: bitmap words / bytes, chunk ch at bit / byte ch * kPartChunk
   bool bits;
   unsigned* done;         // [S] CTAs finished per bucket (zeroed before the launch); null = no lockstep
+  int prefetch;           // 1: each CTA bulk-prefetches its share of slice b+1 into L2 while sweeping b
+  int slack;              // before bucket b wait for bucket b - slack everywhere (0: never wait)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned* p) {
@@ -894,7 +897,7 @@ __device__ __forceinline__ uint32_t run_of(const uint32_t* P, uint32_t k, uint32
 }
 
 template <bool kInsert, int kU>
-__global__ void __launch_bounds__(kSweepThreads, kInsert ? 4 : 6) sweep_kernel(SweepArgs a) {
+__global__ void __launch_bounds__(kSweepThreads, kInsert ? 4 : 5) sweep_kernel(SweepArgs a) {
   __shared__ uint32_t P[kSweepMaxChunks + 1];
   __shared__ uint16_t st16[kSweepMaxChunks];
   __shared__ uint32_t wsum[kSweepWarps + 1];
@@ -905,7 +908,23 @@ __global__ void __launch_bounds__(kSweepThreads, kInsert ? 4 : 6) sweep_kernel(S
   const uint64_t pol = dev::policy_evict_first();
   const uint64_t keep = dev::policy_evict_last();
   const Geom g = a.g;
+  // slice b of the (local) filter: blocks [b * nb / S, (b + 1) * nb / S]
+  auto prefetch_slice = [&](uint32_t b) {
+    const uint64_t lo = g.nb_local * b / a.S, hi0 = (g.nb_local * (b + 1) + a.S - 1) / a.S;
+    const uint64_t hi = hi0 < g.nb_local ? hi0 : g.nb_local;
+    const uint64_t n = hi > lo ? hi - lo : 0;
+    const uint64_t p0 = lo + n * blockIdx.x / gridDim.x, p1 = lo + n * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t bytes = (p1 - p0) * 32;
+    const char* base = reinterpret_cast<const char*>(a.blocks + p0 * 8);
+    for (uint64_t o = 0; o < bytes; o += (1u << 20)) {
+      const uint64_t len = bytes - o < (1u << 20) ? bytes - o : (1u << 20);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"(static_cast<uint32_t>(len))
+                   : "memory");
+    }
+  };
+  if (a.prefetch && threadIdx.x == 0) prefetch_slice(0);
   for (uint32_t b = 0; b < a.S; ++b) {
+    if (a.prefetch && threadIdx.x == 32 && b + 1 < a.S) prefetch_slice(b + 1);
     // run table of bucket b over this CTA's chunks
     for (uint32_t k = threadIdx.x; k < nk; k += kSweepThreads) {
       const uint16_t* row = a.boffs + (c0 + k) * kBoffStride;
@@ -914,8 +933,8 @@ __global__ void __launch_bounds__(kSweepThreads, kInsert ? 4 : 6) sweep_kernel(S
       st16[k] = st;
       P[k] = static_cast<uint32_t>(en - st);
     }
-    if (a.done && b >= kSweepSlack && threadIdx.x == 0) {
-      const unsigned* d = a.done + (b - kSweepSlack);
+    if (a.done && a.slack > 0 && b >= static_cast<uint32_t>(a.slack) && threadIdx.x == 0) {
+      const unsigned* d = a.done + (b - a.slack);
       while (ld_acquire_u32(d) < gridDim.x) __nanosleep(64);
     }
     __syncthreads();
@@ -939,28 +958,46 @@ __global__ void __launch_bounds__(kSweepThreads, kInsert ? 4 : 6) sweep_kernel(S
         }
         k = lo;
       }
+      // the next row group's keys load while this group's pairs / reds are in flight
+      uint64_t hn[kU];
+      bool vn[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint32_t t = r0 + u * 8 + sub;
+        vn[u] = t < r1;
+        hn[u] = 0;
+        if (vn[u]) {
+          k = run_of(P, k, t);
+          hn[u] = dev::ld_stream_u64(a.keys + (c0 + k) * kPartChunk + st16[k] + (t - P[k]), pol);
+        }
+      }
       for (uint32_t t0 = r0; t0 < r1; t0 += 8 * kU) {
         uint64_t* ptr[kU];
         uint64_t mask[kU], cur[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-          const uint32_t t = t0 + u * 8 + sub;
           mask[u] = 0;
           ptr[u] = reinterpret_cast<uint64_t*>(a.blocks) + pair;
-          if (t < r1) {
-            k = run_of(P, k, t);
-            const uint64_t slot = (c0 + k) * kPartChunk + st16[k] + (t - P[k]);
-            const uint64_t h = dev::ld_stream_u64(a.keys + slot, pol);
-            const uint64_t blk = dev::block_index(h, g.nb_global) - g.first;
-            if (blk < g.nb_local) {
-              const uint32_t low = static_cast<uint32_t>(h);
-              ptr[u] = reinterpret_cast<uint64_t*>(a.blocks + blk * 8) + pair;
-              mask[u] = (static_cast<uint64_t>(dev::lane_bit(low, seed_hi)) << 32) | dev::lane_bit(low, seed_lo);
-            }
+          const uint64_t h = hn[u];
+          const uint64_t blk = dev::block_index(h, g.nb_global) - g.first;
+          if (vn[u] && blk < g.nb_local) {
+            const uint32_t low = static_cast<uint32_t>(h);
+            ptr[u] = reinterpret_cast<uint64_t*>(a.blocks + blk * 8) + pair;
+            mask[u] = (static_cast<uint64_t>(dev::lane_bit(low, seed_hi)) << 32) | dev::lane_bit(low, seed_lo);
           }
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) cur[u] = mask[u] ? dev::ld_pair(ptr[u], keep) : ~0ull;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint32_t t = t0 + 8 * kU + u * 8 + sub;
+          vn[u] = t < r1;
+          hn[u] = 0;
+          if (vn[u]) {
+            k = run_of(P, k, t);
+            hn[u] = dev::ld_stream_u64(a.keys + (c0 + k) * kPartChunk + st16[k] + (t - P[k]), pol);
+          }
+        }
 #pragma unroll
         for (int u = 0; u < kU; ++u)
           if (mask[u] & ~cur[u]) dev::red_or64(ptr[u], mask[u], keep);
@@ -1140,6 +1177,23 @@ bool sweep_enabled() {
   return on;
 }
 
+// SBBF_SWEEP_PREFETCH=0 disables the next-slice L2 prefetch (A/B only).
+int sweep_prefetch() {
+  static const int on = [] {
+    const char* v = getenv("SBBF_SWEEP_PREFETCH");
+    return (v && v[0] == '0') ? 0 : 1;
+  }();
+  return on;
+}
+
+int sweep_slack() {
+  static const int v = [] {
+    const char* e = getenv("SBBF_SWEEP_SLACK");
+    return e ? atoi(e) : kSweepSlack;
+  }();
+  return v;
+}
+
 // One cooperative launch of the persistent sweep over chunks [0, nchunks).
 // `done` is S counters of scratch (zeroed here). If the cooperative launch
 // is refused (another client holds SMs, MPS limits), the same kernel runs
@@ -1175,6 +1229,9 @@ cudaError_t launch_sweep(const DeviceInfo& di, SweepArgs a, cudaStream_t s) {
     note_launch();
     e = cudaLaunchKernelEx(&cfg, kern, a);
     if (e == cudaSuccess) return e;
+    if (getenv("SBBF_SWEEP_DEBUG"))
+      fprintf(stderr, "sbbf sweep: cooperative launch of %llu CTAs refused: %s\n",
+              static_cast<unsigned long long>(grid), cudaGetErrorString(e));
     cudaGetLastError();  // cooperative launch refused: run without the lockstep
   }
   a.done = nullptr;
@@ -1267,7 +1324,7 @@ cudaError_t insert_chunk(const DeviceInfo& di, uint32_t* blocks, const Geom& g, 
   cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, nullptr, sc.boffs, s);
   if (e == cudaSuccess && sweep_enabled()) {
     const SweepArgs a{blocks, g, sc.keys, sc.boffs, (m + kPartChunk - 1) / kPartChunk, parts,
-                      nullptr, nullptr, nullptr, false, sc.done};
+                      nullptr, nullptr, nullptr, false, sc.done, sweep_prefetch(), sweep_slack()};
     return launch_sweep<true>(di, a, s);
   }
   if (e == cudaSuccess) e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, parts, m, nullptr, s);
@@ -1282,7 +1339,7 @@ cudaError_t find_chunk(const DeviceInfo& di, const uint32_t* blocks, const Geom&
   // 3. each CTA returns its chunks to source order (persistent sweep)
   if (e == cudaSuccess && sweep_enabled()) {
     const SweepArgs a{const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, (m + kPartChunk - 1) / kPartChunk,
-                      parts, sc.ans, sc.pos16, dst, bits, sc.done};
+                      parts, sc.ans, sc.pos16, dst, bits, sc.done, sweep_prefetch(), sweep_slack()};
     return launch_sweep<false>(di, a, s);
   }
   if (e == cudaSuccess)
@@ -1510,7 +1567,7 @@ cudaError_t blocked_insert_regions(const DeviceInfo& di, uint32_t* blocks, const
       e = chunk_partition(di, g, plan.parts, keys[r], counts[r], sc.keys + off[r] * kPartChunk, nullptr,
                           sc.boffs + off[r] * kBoffStride, s);
   if (e == cudaSuccess && sweep_enabled()) {
-    const SweepArgs a{blocks, g, sc.keys, sc.boffs, C, plan.parts, nullptr, nullptr, nullptr, false, sc.done};
+    const SweepArgs a{blocks, g, sc.keys, sc.boffs, C, plan.parts, nullptr, nullptr, nullptr, false, sc.done, sweep_prefetch(), sweep_slack()};
     e = launch_sweep<true>(di, a, s);
   } else if (e == cudaSuccess) {
     e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, plan.parts, C * kPartChunk, nullptr, s);
@@ -1536,7 +1593,7 @@ cudaError_t blocked_find_regions(const DeviceInfo& di, const uint32_t* blocks, c
                           sc.pos16 + off[r] * kPartChunk, sc.boffs + off[r] * kBoffStride, s);
   if (e == cudaSuccess && sweep_enabled()) {
     const SweepArgs a{const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, C, plan.parts, sc.ans, sc.pos16, bytes,
-                      false, sc.done};
+                      false, sc.done, sweep_prefetch(), sweep_slack()};
     e = launch_sweep<false>(di, a, s);
   } else {
     if (e == cudaSuccess)

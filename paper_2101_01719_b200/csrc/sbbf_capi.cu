@@ -78,7 +78,8 @@ struct sbbf_gpu {
   cudaStream_t hs[kHostStreams] = {};
   uint64_t* d_stage[kHostStreams] = {};
   void* d_res[kHostStreams] = {};
-  uint64_t* d_one = nullptr;  // single-key scratch: [hash, result]
+  uint64_t* h_one = nullptr;  // single-key slot [hash, result]: pinned host memory, mapped
+  uint64_t* d_one = nullptr;  // ... and its device alias
   // L2-blocked path: filter slice bounds (global block ids), created lazily.
   std::mutex plan_mu;
   sbbf::BlockedPlan plan;
@@ -237,6 +238,12 @@ int host_pipeline(sbbf_gpu* f, HostOp op, const uint64_t* h_hashes, uint64_t n, 
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   int rc = ensure_host_path(f);
   if (rc != SBBF_OK) return rc;
+  // The host calls are synchronous, like to_host: they start behind every
+  // piece of work already queued on the device (the library's own streams
+  // are non-blocking, so an insert the caller queued on its stream would not
+  // otherwise be ordered before these lookups).
+  cudaError_t e0 = cudaDeviceSynchronize();
+  if (e0 != cudaSuccess) return cuda_fail(e0, "cudaDeviceSynchronize");
   for (uint64_t off = 0, c = 0; off < n; off += kHostChunk, ++c) {
     const uint64_t m = (n - off < kHostChunk) ? n - off : kHostChunk;
     const int s = static_cast<int>(c % kHostStreams);
@@ -355,7 +362,8 @@ int sbbf_gpu_create_shard(uint64_t total_buckets, uint64_t first_block, uint64_t
     f->di.l2_bytes = static_cast<size_t>(v);
   e = cudaMalloc(&f->d_blocks, num_buckets * 32);
   if (e == cudaSuccess) e = cudaMemset(f->d_blocks, 0, num_buckets * 32);
-  if (e == cudaSuccess) e = cudaMalloc(&f->d_one, 2 * sizeof(uint64_t));
+  if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&f->h_one), 2 * sizeof(uint64_t), cudaHostAllocMapped);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&f->d_one), f->h_one, 0);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     const int rc = cuda_fail(e, "allocating the block array");
@@ -372,7 +380,7 @@ int sbbf_gpu_destroy(sbbf_gpu_t* f) {
     DeviceGuard g(f->di.device);
     if (f->d_blocks) cudaDeviceSynchronize();
     cudaFree(f->d_blocks);
-    cudaFree(f->d_one);
+    if (f->h_one) cudaFreeHost(f->h_one);
     cudaFree(f->d_plan_bounds);
     cudaFree(f->d_super_bounds);
     for (int i = 0; i < kHostStreams; ++i) {
@@ -457,9 +465,13 @@ int sbbf_gpu_add_hash(sbbf_gpu_t* f, uint64_t hash) {
   if (!f) return fail(SBBF_EINVAL, "null filter");
   std::lock_guard<std::mutex> lock(f->host_mu);
   DeviceGuard g(f->di.device);
-  cudaError_t e = cudaMemcpy(f->d_one, &hash, sizeof(hash), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess)
+  // behind all queued work (as the host calls); the hash goes through the
+  // pinned, device-mapped slot (no separate copy)
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) {
+    f->h_one[0] = hash;
     e = sbbf::launch_insert(f->di, SBBF_INSERT_WIDE, f->d_blocks, f->geom, f->d_one, 1, nullptr);
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
   return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "add_hash");
 }
@@ -469,13 +481,15 @@ int sbbf_gpu_find_hash(const sbbf_gpu_t* f, uint64_t hash, int* found) {
   sbbf_gpu* m = const_cast<sbbf_gpu*>(f);
   std::lock_guard<std::mutex> lock(m->host_mu);
   DeviceGuard g(f->di.device);
-  uint8_t r = 0;
-  cudaError_t e = cudaMemcpy(m->d_one, &hash, sizeof(hash), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess)
+  cudaError_t e = cudaDeviceSynchronize();  // behind all queued work, as the host calls
+  if (e == cudaSuccess) {
+    m->h_one[0] = hash;
     e = sbbf::launch_find(f->di, SBBF_FIND_GLOBAL, f->d_blocks, f->geom, m->d_one, 1, m->d_one + 1,
                           false, nullptr);
-  if (e == cudaSuccess) e = cudaMemcpy(&r, m->d_one + 1, 1, cudaMemcpyDeviceToHost);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
   if (e != cudaSuccess) return cuda_fail(e, "find_hash");
+  const uint8_t r = static_cast<uint8_t>(m->h_one[1] & 0xff);
   *found = r ? 1 : 0;
   return SBBF_OK;
 }
@@ -526,6 +540,54 @@ int sbbf_gpu_make_mask_batch(const uint64_t* d_hashes, uint64_t n, uint32_t* d_l
   if (!d_hashes || !d_lanes) return fail(SBBF_EINVAL, "null buffer");
   cudaError_t e = sbbf::launch_make_mask(d_hashes, n, d_lanes, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? SBBF_OK : cuda_fail(e, "make_mask kernel");
+}
+
+// Host-array forms of the two free functions (block_index filter.hpp:42,
+// make_mask filter.hpp:47): the values are computed by the device kernels
+// above on `device`, through a small device staging copy. For drop-in
+// callers of the reference's free functions (tests/cpp/dropin/sbbf/filter.hpp).
+namespace {
+int host_free_fn(const uint64_t* h_hashes, uint64_t n, uint64_t num_buckets, void* h_out, size_t out_per_key,
+                 bool mask, int device) {
+  if (n == 0) return SBBF_OK;
+  if (!h_hashes || !h_out) return fail(SBBF_EINVAL, "null buffer");
+  if (device < 0 || device >= 64) return fail(SBBF_ENODEV, "bad device ordinal");
+  DeviceGuard g(device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  // per-device staging, grown on demand and kept (these are called per value
+  // by reference-style callers)
+  static std::mutex mu;
+  static uint64_t* d_buf[64] = {};
+  static uint64_t cap[64] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  const uint64_t need = n * (sizeof(uint64_t) + out_per_key);
+  cudaError_t e = cudaSuccess;
+  if (cap[device] < need) {
+    if (d_buf[device]) cudaFree(d_buf[device]);
+    d_buf[device] = nullptr;
+    cap[device] = 0;
+    e = cudaMalloc(&d_buf[device], need);
+    if (e == cudaSuccess) cap[device] = need;
+  }
+  uint64_t* d_in = d_buf[device];
+  void* d_out = d_in + n;
+  if (e == cudaSuccess) e = cudaMemcpy(d_in, h_hashes, n * sizeof(uint64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = mask ? sbbf::launch_make_mask(d_in, n, static_cast<uint32_t*>(d_out), nullptr)
+             : sbbf::launch_block_index(d_in, n, num_buckets, static_cast<uint64_t*>(d_out), nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(h_out, d_out, n * out_per_key, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? SBBF_OK : cuda_fail(e, mask ? "make_mask" : "block_index");
+}
+}  // namespace
+
+int sbbf_gpu_block_index_host(const uint64_t* h_hashes, uint64_t n, uint64_t num_buckets, uint64_t* h_out,
+                              int device) {
+  if (num_buckets == 0) return fail(SBBF_EINVAL, "num_buckets must be >= 1");
+  return host_free_fn(h_hashes, n, num_buckets, h_out, sizeof(uint64_t), false, device);
+}
+
+int sbbf_gpu_make_mask_host(const uint64_t* h_hashes, uint64_t n, uint32_t* h_lanes, int device) {
+  return host_free_fn(h_hashes, n, 0, h_lanes, 8 * sizeof(uint32_t), true, device);
 }
 
 int sbbf_gpu_set_l2_fetch_granularity(int device, int bytes, int* old) {
@@ -590,6 +652,25 @@ int sbbf_gpu_image_crc(const sbbf_gpu_t* f, uint32_t* crc) {
   if (e != cudaSuccess) return cuda_fail(e, "image crc");
   *crc = sbbf::crc32_combine(sbbf::crc32_host_update(0, hdr, 17), body, f->nb * 32);
   return SBBF_OK;
+}
+
+int sbbf_gpu_blocks_crc(const sbbf_gpu_t* f, uint32_t* crc) {
+  if (!f || !crc) return fail(SBBF_EINVAL, "null argument");
+  DeviceGuard g(f->di.device);
+  cudaError_t e = cudaDeviceSynchronize();
+  uint32_t body = 0;
+  if (e == cudaSuccess) e = sbbf::device_crc32(f->d_blocks, f->nb * 32, &body, nullptr);
+  if (e != cudaSuccess) return cuda_fail(e, "blocks crc");
+  *crc = body;
+  return SBBF_OK;
+}
+
+uint32_t sbbf_crc32_update(uint32_t crc, const void* data, uint64_t len) {
+  return data ? sbbf::crc32_host_update(crc, static_cast<const uint8_t*>(data), len) : crc;
+}
+
+uint32_t sbbf_crc32_combine(uint32_t crc1, uint32_t crc2, uint64_t len2) {
+  return sbbf::crc32_combine(crc1, crc2, len2);
 }
 
 int sbbf_gpu_serialize(const sbbf_gpu_t* f, void* h_dst, uint64_t cap, uint64_t* written) {

@@ -252,6 +252,13 @@ class SplitBlockFilter:
         check(_lib.lib().sbbf_gpu_image_crc(self._h, C.byref(crc)), "sbbf_gpu_image_crc")
         return int(crc.value)
 
+    def blocks_crc(self) -> int:
+        """CRC-32 of the block array bytes alone (GPU): a shard's part of the
+        gathered image CRC (ShardedFilter.image_crc combines them)."""
+        crc = C.c_uint32(0)
+        check(_lib.lib().sbbf_gpu_blocks_crc(self._h, C.byref(crc)), "sbbf_gpu_blocks_crc")
+        return int(crc.value)
+
     def serialize(self) -> bytes:
         """serialize() (persist.cpp:72-88): the canonical v1 image."""
         L = _lib.lib()

@@ -398,6 +398,30 @@ class ShardedFilter:
     def local_blocks(self) -> np.ndarray:
         return self.ops.blocks(self.shard)
 
+    def image_crc(self, hasher_id: int = 0) -> int:
+        """FilterImage CRC (persist.cpp:72-88) of the gathered filter — the
+        shards concatenated in rank order — without moving the blocks: every
+        rank CRCs its shard on its GPU, the CRCs are all-gathered and combined
+        in rank order behind the 17-byte header (collective; every rank
+        returns the same value)."""
+        L = _lib.lib()
+        mine = self.shard.blocks_crc() if hasattr(self.shard, "blocks_crc") else None
+        if mine is None:  # host shard ops (tests): CRC the local blocks on the host
+            b = np.ascontiguousarray(self.local_blocks())
+            mine = int(L.sbbf_crc32_update(0, b.ctypes.data_as(C.c_void_p), b.nbytes))
+        crcs = [mine]
+        if self.world > 1:
+            crcs = [None] * self.world
+            dist.all_gather_object(crcs, mine, group=self.group)
+        hdr = (b"SBBF" + bytes([1]) + int(hasher_id).to_bytes(4, "little") +
+               int(self.total).to_bytes(8, "little"))
+        buf = (C.c_uint8 * len(hdr)).from_buffer_copy(hdr)
+        crc = int(L.sbbf_crc32_update(0, C.cast(buf, C.c_void_p), len(hdr)))
+        for r in range(self.world):
+            n = (self.bounds[r + 1] - self.bounds[r]) * 32
+            crc = int(L.sbbf_crc32_combine(crc, int(crcs[r]), n))
+        return crc
+
     def gather_blocks(self, dst: int = 0):
         """Whole filter (num_buckets, 8) on rank `dst` (None elsewhere): the shards
         in rank order, which must equal the single-filter bytes."""
@@ -499,7 +523,7 @@ def bench_main(args) -> dict | None:
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        step(ins, look)
+        last_bits = step(ins, look)
         e1.record()
         torch.cuda.synchronize(dev)
         t = torch.tensor([e0.elapsed_time(e1)], device=dev)
@@ -508,6 +532,40 @@ def bench_main(args) -> dict | None:
     launches = launch_count() - l0
     ms = statistics.mean(times)
     sent = f.last_exchange.get("sent", [])
+    # parity of the last timed step (config 5): the gathered filter's image
+    # CRC (shard CRCs combined in rank order, no block movement) and the
+    # false-positive / member-hit counts of the lookup bitmaps, against the
+    # reference's golden for the same world-wide sample
+    # (tests/golden/config5.json "samples", make_golden.py --cfg5)
+    parity = None
+    if args.config == 5:
+        crc = f.image_crc()
+        j = np.arange(rank * L, (rank + 1) * L, dtype=np.uint64)
+        mem = ((j + 1) * cfg.lookups.p // cfg.lookups.q) > (j * cfg.lookups.p // cfg.lookups.q)
+        mwords = torch.from_numpy(np.packbits(mem, bitorder="little").view(np.int32).copy()).to(dev)
+        lut = torch.tensor([bin(i).count("1") for i in range(256)], dtype=torch.int64, device=dev)
+        nwords = (L + 31) // 32
+        hits = last_bits[:nwords]
+        cnt = torch.stack([lut[(hits & mwords).view(torch.uint8).long()].sum(),
+                           lut[(hits & ~mwords).view(torch.uint8).long()].sum()])
+        dist.all_reduce(cnt)
+        mh, fp = (int(x) for x in cnt.tolist())
+        parity = {"image_crc": f"{crc:#010x}", "member_hits": mh, "false_positives": fp,
+                  "members": world * int(mem.sum()), "nonmembers": world * L - world * int(mem.sum()),
+                  "how": "last timed step: gathered-filter image CRC (shard CRCs combined in rank order) "
+                         "and lookup-bitmap counts, vs the reference on the same world-wide sample"}
+        try:
+            import json as _json
+            with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests",
+                                   "golden", "config5.json")) as fh:
+                gs = _json.load(fh)["samples"].get(str(world))
+        except Exception:
+            gs = None
+        if gs and gs["per_rank_keys"] == N and N == L:
+            parity["reference"] = {"image_crc": f"{gs['image_crc']:#010x}", "member_hits": gs["member_hits"],
+                                   "false_positives": gs["false_positives"]}
+            parity["matches_reference"] = (crc == gs["image_crc"] and mh == gs["member_hits"]
+                                           and fp == gs["false_positives"])
 
     # e2e: hashes from pinned host memory, bitmap back to the host, every step
     e2e, e2e_err = [], ""
@@ -555,15 +613,23 @@ def bench_main(args) -> dict | None:
                     "h2d_bytes_per_step": 8 * (N + L), "d2h_bytes_per_step": 4 * ((L + 31) // 32),
                     "ms_per_step": e2e_s * 1e3, "note": "per rank; max over ranks of wall time",
                     **({"error": e2e_err} if e2e_err else {})},
-            "roofline": {"bound": "hbm", "kernel": "whole sharded step (partition + exchange + probe)", "routing": how,
-                         "achieved": (N + L) * 40.0 / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                         "frac": (N + L) * 40.0 / (ms * 1e-3) / 1e9 / peak, "traffic": None,
-                         "bytes_per_key": 40.0, "peak_note": peak_note,
-                         "bytes_note": "per rank: 8 B hash + one random 32-B sector per key (shard beyond L2)",
-                         "nvlink": {"bytes_per_key_forward": fwd,
-                                    "achieved_gbs": (N + L) * fwd / (ms * 1e-3) / 1e9,
-                                    "peer_peak_gbs": 770.0}},
+            "roofline": {"bound": "hbm", "kernel": "whole sharded step (partition + exchange + insert + probe)",
+                         "routing": how,
+                         "achieved": (64.0 * N + 32.0 * L) / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": (64.0 * N + 32.0 * L) / (ms * 1e-3) / 1e9 / peak, "traffic": None,
+                         "bytes_per_key": (64.0 * N + 32.0 * L) / (N + L), "peak_note": peak_note,
+                         "bytes_note": ("north-star roofline per rank: one random 32-B sector per lookup, a "
+                                        "32-B read-modify-write (64 B) per insert, against one GPU's HBM"),
+                         "nvlink": {"bytes_per_step_per_rank": (N + L) * fwd + L * (world - 1) / world,
+                                    "bytes_note": "computed, not measured: keys whose owner is another rank "
+                                                  "(8 B each way out) plus their 1-B answers back",
+                                    "achieved_gbs": ((N + L) * fwd + L * (world - 1) / world) / (ms * 1e-3) / 1e9,
+                                    "peer_peak_gbs": 900.0}},
+            "collective": {"backend": dist.get_backend(), "world": dist.get_world_size(),
+                           "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version())
+                           if backend == "nccl" else None},
             "gpu_launches": launches, "time": "max over ranks of CUDA-event step time",
+            "parity": parity,
             "last_exchange_sent_keys": sent,
         }
     dist.destroy_process_group()

@@ -54,7 +54,17 @@ enum : int {
   kDiscard = 4,       // discard.global.L2 the key lines after they are consumed
   kKeysNormal = 8,    // keys loaded without the evict_first hint
   kOutNone = 16,      // no answer stores (reduced to a per-thread xor)
+  kChunked = 32,      // keys in the blocked path's chunk-local layout: region r's keys are 128-key
+                      // runs at chunk*4096 + r*128 (32 KB stride)
+  kChunkedPad = 64,   // the same with a 4128-key (33 KB) chunk stride
 };
+
+template <int F>
+__device__ __forceinline__ uint64_t key_addr(uint64_t i, uint64_t r, uint64_t per_region) {
+  if (!(F & (kChunked | kChunkedPad))) return i;
+  const uint64_t li = i - r * per_region, ch = li >> 7, off = li & 127;
+  return ch * ((F & kChunkedPad) ? 4128 : 4096) + r * 128 + off;
+}
 
 template <int F, int U>
 __global__ void __launch_bounds__(256, 8) sweep(const uint32_t* __restrict__ filt, uint64_t region_blocks,
@@ -74,10 +84,11 @@ __global__ void __launch_bounds__(256, 8) sweep(const uint32_t* __restrict__ fil
     for (int u = 0; u < U; ++u) {
       const uint64_t i = i0 + u * 256;
       if (i < k1) {
+        const uint64_t ka = key_addr<F>(i, r, per_region);
         if (F & kKeysNormal)
-          asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(h[u]) : "l"(keys + i));
+          asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(h[u]) : "l"(keys + ka));
         else
-          asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(h[u]) : "l"(keys + i), "l"(pf));
+          asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(h[u]) : "l"(keys + ka), "l"(pf));
       } else {
         h[u] = 0;
       }
@@ -122,7 +133,7 @@ __global__ void __launch_bounds__(256, 8) sweep(const uint32_t* __restrict__ fil
           asm volatile("st.global.L1::no_allocate.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(out + i), "r"(miss == 0 ? 1u : 0u), "l"(pf)
                        : "memory");
         else
-          asm volatile("st.global.L1::no_allocate.u8 [%0], %1;" ::"l"(out + i), "r"(miss == 0 ? 1u : 0u) : "memory");
+          asm volatile("st.global.L1::no_allocate.u8 [%0], %1;" ::"l"(out + key_addr<F>(i, r, per_region)), "r"(miss == 0 ? 1u : 0u) : "memory");
       }
     }
   }
@@ -376,10 +387,10 @@ int main(int argc, char** argv) {
   uint32_t* sink;
   CK(cudaMalloc(&filt, filter_blocks * 32));
   CK(cudaMemset(filt, 0x5a, filter_blocks * 32));
-  CK(cudaMalloc(&keys, n * 8));
-  CK(cudaMalloc(&out, n));
+  CK(cudaMalloc(&keys, n * 8 + (n / 4096) * 32 * 8));
+  CK(cudaMalloc(&out, n + (n / 4096) * 32));
   CK(cudaMalloc(&sink, 64));
-  gen_keys<<<1184, 256>>>(keys, n);
+  gen_keys<<<1184, 256>>>(keys, n + (n / 4096) * 32);
   CK(cudaDeviceSynchronize());
   const uint64_t r32 = (32ull << 20) / 32, r16 = (16ull << 20) / 32, r64 = (64ull << 20) / 32, r8 = (8ull << 20) / 32;
   if (mask & 1) run<0, 1>(filt, filter_blocks, r32, keys, n, out, sink, "baseline (keys ef, probe normal)");
@@ -398,6 +409,13 @@ int main(int argc, char** argv) {
   if (mask & 8192) run<kProbeLast | kOutFirst | kDiscard, 1>(filt, filter_blocks, r16, keys, n, out, sink, "all three");
   if (mask & 16384) run<kProbeLast | kOutFirst | kDiscard, 1>(filt, filter_blocks, r64, keys, n, out, sink, "all three");
   if (mask & 32768) run<kOutNone, 4>(filt, filter_blocks, r32, keys, n, out, sink, "no answer stores");
+  if (mask & (1u << 31)) {
+    run<0, 1>(filt, filter_blocks, r32, keys, n, out, sink, "flat keys");
+    run<kChunked, 1>(filt, filter_blocks, r32, keys, n, out, sink, "chunk-local keys, 32 KB stride");
+    run<kChunkedPad, 1>(filt, filter_blocks, r32, keys, n, out, sink, "chunk-local keys, 33 KB stride");
+    run<kChunked | kOutNone, 1>(filt, filter_blocks, r32, keys, n, out, sink, "chunk-local, no answers");
+    run<kChunked, 1>(filt, filter_blocks, r16, keys, n, out, sink, "chunk-local keys, 32 KB stride");
+  }
   const uint64_t ni = 1ull << 26;  // one config-4 insert chunk
   if (mask & (1u << 16)) irun<0>(filt, filter_blocks, r32, keys, ni, "4 thr/key red.b64");
   if (mask & (1u << 17)) irun<1>(filt, filter_blocks, r32, keys, ni, "4 thr/key test+red.b64");

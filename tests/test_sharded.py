@@ -108,7 +108,8 @@ def _worker(rank, world, port, total, n_ins, n_look, q):
                                                                   dtype=np.uint64)])
         ans = f.find_hashes(torch.from_numpy(look.view(np.int64))).numpy()
         full = f.gather_blocks(0)
-        q.put((rank, ins, look, ans, full, f.first, f.count, f.last_exchange))
+        crc = f.image_crc()   # collective: shard CRCs combined in rank order
+        q.put((rank, ins, look, ans, full, f.first, f.count, f.last_exchange, crc))
     finally:
         dist.destroy_process_group()
 
@@ -133,6 +134,8 @@ def test_gloo_sharded_matches_oracle(oracle, world, total):
     assert full.shape == (total, 8)
     assert np.array_equal(full, want)                     # shards concatenate to the reference filter
     assert oracle.image_crc(full) == oracle.image_crc(want)
+    # the gathered image CRC without moving blocks, identical on every rank
+    assert all(g[8] == oracle.image_crc(want) for g in got)
     for rank, ins, look, ans, *_ in got:
         assert np.array_equal(ans, oracle.find_hashes(want, look)), rank
         assert ans[: len(look) // 2].all()               # no false negatives across ranks
