@@ -303,6 +303,30 @@ int sbbf_dist_find(sbbf_dist_t* d, const uint64_t* d_hashes, uint64_t n, uint8_t
 int sbbf_dist_find_bits(sbbf_dist_t* d, const uint64_t* d_hashes, uint64_t n, uint32_t* d_bits, void* stream);
 /* Whole filter into h_dst (total_buckets*32 bytes) on rank `root`. */
 int sbbf_dist_gather(sbbf_dist_t* d, void* h_dst, int root);
+/* FilterImage CRC of the gathered filter (shard CRCs on each GPU, combined in
+ * rank order; no block movement). Collective; every rank gets it. */
+int sbbf_dist_image_crc(sbbf_dist_t* d, uint32_t* crc);
+/* Failure detection: wait for `stream` on the host while polling
+ * ncclCommGetAsyncError. On an asynchronous NCCL error (a dead peer, a
+ * network fault) or after timeout_ms (<= 0: no deadline) the communicator is
+ * aborted (ncclCommAbort, which also frees it: the caller must not destroy
+ * that communicator afterwards), the call returns SBBF_ECUDA and every later
+ * call on the handle fails fast instead of hanging in a barrier. */
+int sbbf_dist_sync(sbbf_dist_t* d, void* stream, int64_t timeout_ms);
+/* The same layer over caller-provided collectives instead of NCCL (e.g. a
+ * host process group, or one GPU shared by several processes, which NCCL
+ * refuses). allgather: rank-order gather of `bytes` host bytes from every
+ * rank into recv (world*bytes). barrier: every rank's work queued on its
+ * stream before the call completes before any rank's work queued after it
+ * (may synchronize the stream on the host). Both return 0 on success. */
+typedef struct sbbf_dist_hooks {
+  int rank, world;
+  void* ctx;
+  int (*allgather)(void* ctx, const void* send, void* recv, uint64_t bytes);
+  int (*barrier)(void* ctx, void* stream);
+} sbbf_dist_hooks;
+int sbbf_dist_create_hooks(const sbbf_dist_hooks* hooks, uint64_t total_buckets, uint64_t max_batch, int device,
+                           sbbf_dist_t** out);
 
 /* L2 fetch-granularity hint for `device` (cudaLimitMaxL2FetchGranularity,
  * 0..128 bytes; process-wide for that device). 32 makes a random 32-byte

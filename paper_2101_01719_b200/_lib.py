@@ -99,6 +99,9 @@ PROTOTYPES = {
     "sbbf_dist_find": (_i, [_vp, _vp, _u64, _vp, _vp]),
     "sbbf_dist_find_bits": (_i, [_vp, _vp, _u64, _vp, _vp]),
     "sbbf_dist_gather": (_i, [_vp, _vp, _i]),
+    "sbbf_dist_image_crc": (_i, [_vp, C.POINTER(_u32)]),
+    "sbbf_dist_sync": (_i, [_vp, _vp, C.c_int64]),
+    "sbbf_dist_create_hooks": (_i, [_vp, _u64, _u64, _i, C.POINTER(_vp)]),
     "sbbf_route_window_bytes": (_u64, [_u32, _u64]),
     "sbbf_route_create": (_i, [_u32, _u32, _u64, _i, C.POINTER(_vp)]),
     "sbbf_route_destroy": (None, [_vp]),

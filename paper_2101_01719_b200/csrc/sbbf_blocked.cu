@@ -656,16 +656,26 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
 constexpr int kSegThreads = 256;
 constexpr int kSegWarps = kSegThreads / 32;
 constexpr uint32_t kSegChunksPerCta = 64;
+// SBBF_SEG_CHUNKS overrides the chunks per segment CTA (A/B only)
+uint32_t seg_chunks_per_cta() {
+  static const uint32_t v = [] {
+    const char* e = getenv("SBBF_SEG_CHUNKS");
+    const int x = e ? atoi(e) : 0;
+    return x > 0 ? static_cast<uint32_t>(x) : kSegChunksPerCta;
+  }();
+  return v;
+}
 
 template <bool kInsert, int kSegQ, int kMinB = (kSegQ > 4 ? 2 : 3)>
 __global__ void __launch_bounds__(kSegThreads, kMinB)
     segment_kernel(uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
-                   const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint8_t* __restrict__ ans) {
+                   const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint8_t* __restrict__ ans,
+                   uint32_t per_cta) {
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t b = blockIdx.x / groups, grp = blockIdx.x % groups;
   const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
-  const uint64_t c_begin = static_cast<uint64_t>(grp) * kSegChunksPerCta;
-  const uint64_t c_end = c_begin + kSegChunksPerCta < nchunks ? c_begin + kSegChunksPerCta : nchunks;
+  const uint64_t c_begin = static_cast<uint64_t>(grp) * per_cta;
+  const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
   const uint64_t pol = dev::policy_evict_first();
   const uint64_t keep = dev::policy_evict_last();
   for (uint64_t c = c_begin + warp * kSegQ; c < c_end; c += kSegWarps * kSegQ) {
@@ -1245,16 +1255,17 @@ template <bool kInsert>
 cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* keys, const uint16_t* boffs, uint32_t S,
                             uint64_t m, uint8_t* ans, cudaStream_t s) {
   const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
-  const uint32_t groups = static_cast<uint32_t>((nchunks + kSegChunksPerCta - 1) / kSegChunksPerCta);
+  const uint32_t per_cta = seg_chunks_per_cta();
+  const uint32_t groups = static_cast<uint32_t>((nchunks + per_cta - 1) / per_cta);
   note_launch();
   // Segments per warp step / min CTAs per SM, measured on config 4
   // (profiles/r1_blocked_partition.md): inserts 4 / 3 (4 lanes per key;
   // 1 or 2 segments: same or slower); lookups 1 / 8 — 1.54 ms per 2^28 keys,
   // vs 1.82 (2 segments), 1.89 (4), 2.37 (8): occupancy beats per-lane MLP.
   if constexpr (kInsert)
-    segment_kernel<true, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans);
+    segment_kernel<true, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta);
   else
-    segment_kernel<false, 1, 8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans);
+    segment_kernel<false, 1, 8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta);
   return cudaGetLastError();
 }
 

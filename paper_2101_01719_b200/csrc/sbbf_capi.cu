@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -94,6 +95,15 @@ namespace {
 // (lookup / insert), 16 MiB 81.6 / 47.8, 64 MiB 68.7 / 38.0, 8 MiB 46.4 / 35.0
 // (scripts/variant_ab.py; bucket counts round up to powers of two).
 constexpr uint64_t kSliceBytes = 32ull << 20;
+// SBBF_SLICE_MB overrides the slice size (A/B measurements only).
+uint64_t slice_bytes() {
+  static const uint64_t v = [] {
+    const char* e = getenv("SBBF_SLICE_MB");
+    const long mb = e ? atol(e) : 0;
+    return mb > 0 ? static_cast<uint64_t>(mb) << 20 : kSliceBytes;
+  }();
+  return v;
+}
 
 // Blocked inserts pay once random atomics mostly miss L2: into a ~L2-sized
 // filter (config 3) plain reds hit L2 often enough that the partition passes
@@ -144,7 +154,7 @@ int resolve_find(const sbbf_gpu* f, uint64_t n) {
 int ensure_plan(sbbf_gpu* f) {
   std::lock_guard<std::mutex> lock(f->plan_mu);
   if (f->d_plan_bounds) return SBBF_OK;
-  uint64_t parts = (f->nb * 32 + kSliceBytes - 1) / kSliceBytes;
+  uint64_t parts = (f->nb * 32 + slice_bytes() - 1) / slice_bytes();
   // beyond 128 slices (chunk-local bucket ids are <= 7 bits, filters beyond
   // 4 GiB): super-slices of <= 128 slices (the super partition takes <= 64)
   uint64_t super = (parts + 127) / 128;

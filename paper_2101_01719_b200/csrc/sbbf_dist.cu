@@ -21,9 +21,14 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -44,6 +49,8 @@ struct Nccl {
   decltype(&ncclGroupStart) group_start = nullptr;
   decltype(&ncclGroupEnd) group_end = nullptr;
   decltype(&ncclGetErrorString) error_string = nullptr;
+  decltype(&ncclCommGetAsyncError) get_async_error = nullptr;
+  decltype(&ncclCommAbort) comm_abort = nullptr;
   bool ok = false;
   std::string why;
 };
@@ -72,9 +79,12 @@ const Nccl& nccl() {
     SBBF_SYM(group_start, ncclGroupStart);
     SBBF_SYM(group_end, ncclGroupEnd);
     SBBF_SYM(error_string, ncclGetErrorString);
+    SBBF_SYM(get_async_error, ncclCommGetAsyncError);
+    SBBF_SYM(comm_abort, ncclCommAbort);
 #undef SBBF_SYM
     n.ok = n.get_unique_id && n.comm_init_rank && n.comm_destroy && n.comm_count && n.comm_user_rank &&
-           n.all_gather && n.all_reduce && n.send && n.recv && n.group_start && n.group_end && n.error_string;
+           n.all_gather && n.all_reduce && n.send && n.recv && n.group_start && n.group_end && n.error_string &&
+           n.get_async_error && n.comm_abort;
     if (!n.ok) n.why = "libnccl.so.2 lacks an expected symbol";
   });
   return n;
@@ -100,7 +110,10 @@ int cuda_check(cudaError_t e, const char* what) {
 }  // namespace
 
 struct sbbf_dist {
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm = nullptr;      // NCCL mode (null in hooks mode)
+  sbbf_dist_hooks hooks{};        // hooks mode: the caller's collectives
+  bool use_hooks = false;
+  bool aborted = false;           // a watchdog aborted the communicator: every call fails
   int rank = 0, world = 1, device = 0;
   uint64_t total = 0;
   std::vector<uint64_t> bounds;   // world + 1 entries
@@ -113,8 +126,50 @@ struct sbbf_dist {
 namespace {
 
 int barrier(sbbf_dist* d, cudaStream_t s) {
+  if (d->aborted) return dist_fail(SBBF_ECUDA, "sharded filter: communicator aborted");
   if (d->world == 1) return SBBF_OK;
+  if (d->use_hooks) {
+    const int rc = d->hooks.barrier(d->hooks.ctx, s);
+    return rc == 0 ? SBBF_OK : dist_fail(SBBF_ECUDA, "sharded filter: barrier hook failed");
+  }
   return nccl_check(nccl().all_reduce(d->d_flag, d->d_flag, 1, ncclInt32, ncclSum, d->comm, s), "barrier");
+}
+
+// Host-side wait for `s` with NCCL failure detection: poll the stream and
+// ncclCommGetAsyncError; on an asynchronous NCCL error (a peer died, a
+// network fault) or after timeout_ms, abort the communicator
+// (ncclCommAbort: the stuck kernels are torn down instead of spinning on a
+// peer forever) and fail. timeout_ms <= 0 waits without a deadline.
+int wait_stream(sbbf_dist* d, cudaStream_t s, long long timeout_ms, const char* what) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return SBBF_OK;
+    if (q != cudaErrorNotReady) return cuda_check(q, what);
+    if (!d->use_hooks && d->comm && d->world > 1) {
+      ncclResult_t ae = ncclSuccess;
+      nccl().get_async_error(d->comm, &ae);
+      if (ae != ncclSuccess && ae != ncclInProgress) {
+        nccl().comm_abort(d->comm);
+        d->comm = nullptr;
+        d->aborted = true;
+        return dist_fail(SBBF_ECUDA, std::string(what) + ": NCCL asynchronous error (" + nccl().error_string(ae) +
+                                         "); communicator aborted");
+      }
+    }
+    const long long ms =
+        std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_ms > 0 && ms > timeout_ms) {
+      if (!d->use_hooks && d->comm) {
+        nccl().comm_abort(d->comm);
+        d->comm = nullptr;
+      }
+      d->aborted = true;
+      return dist_fail(SBBF_ECUDA, std::string(what) + ": timed out after " + std::to_string(ms) +
+                                       " ms (a peer rank is not progressing); communicator aborted");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
 }
 
 struct Guard {
@@ -173,6 +228,76 @@ int sbbf_dist_destroy(sbbf_dist_t* d) {
   return SBBF_OK;
 }
 
+namespace {
+
+// SBBF_DIST_DEBUG=1 traces the collective steps on stderr (hang diagnosis).
+void trace(const sbbf_dist* d, const char* what) {
+  static const bool on = getenv("SBBF_DIST_DEBUG") != nullptr;
+  if (on) fprintf(stderr, "sbbf_dist rank %d/%d: %s\n", d->rank, d->world, what);
+}
+
+// Rank-order gather of `bytes` host bytes from every rank: ncclAllGather
+// through a device buffer, or the caller's hook.
+int allgather_host(sbbf_dist* d, const void* send, void* recv, uint64_t bytes) {
+  if (d->world == 1) {
+    std::memcpy(recv, send, bytes);
+    return SBBF_OK;
+  }
+  if (d->use_hooks)
+    return d->hooks.allgather(d->hooks.ctx, send, recv, bytes) == 0 ? SBBF_OK
+                                                                      : dist_fail(SBBF_ECUDA, "allgather hook failed");
+  uint8_t* dv = nullptr;
+  int rc = cuda_check(cudaMalloc(&dv, bytes * d->world), "allgather");
+  if (rc == SBBF_OK) rc = cuda_check(cudaMemcpy(dv + bytes * d->rank, send, bytes, cudaMemcpyHostToDevice), "allgather");
+  if (rc == SBBF_OK)
+    rc = nccl_check(nccl().all_gather(dv + bytes * d->rank, dv, bytes, ncclUint8, d->comm, nullptr), "ncclAllGather");
+  if (rc == SBBF_OK) rc = wait_stream(d, nullptr, 600000, "allgather");
+  if (rc == SBBF_OK) rc = cuda_check(cudaMemcpy(recv, dv, bytes * d->world, cudaMemcpyDeviceToHost), "allgather");
+  cudaFree(dv);
+  return rc;
+}
+
+// Shard, bounds, barrier flag and receive window; window handles exchanged
+// with one rank-order gather; every rank maps every window before anyone
+// dispatches.
+int create_common(sbbf_dist* d, uint64_t total_buckets, uint64_t max_batch) {
+  int rc = SBBF_OK;
+  if (total_buckets < static_cast<uint64_t>(d->world))
+    rc = dist_fail(SBBF_EINVAL, "sbbf_dist_create: fewer buckets than ranks");
+  if (rc == SBBF_OK) {
+    d->bounds.resize(d->world + 1);
+    rc = sbbf_shard_bounds(total_buckets, static_cast<uint32_t>(d->world), d->bounds.data());
+  }
+  if (rc == SBBF_OK)
+    rc = sbbf_gpu_create_shard(total_buckets, d->bounds[d->rank], d->bounds[d->rank + 1] - d->bounds[d->rank],
+                               d->device, &d->shard);
+  if (rc == SBBF_OK) rc = cuda_check(cudaMalloc(&d->d_bounds, d->world * sizeof(uint64_t)), "bounds");
+  if (rc == SBBF_OK)
+    rc = cuda_check(cudaMemcpy(d->d_bounds, d->bounds.data(), d->world * sizeof(uint64_t), cudaMemcpyHostToDevice),
+                    "bounds");
+  if (rc == SBBF_OK) rc = cuda_check(cudaMalloc(&d->d_flag, sizeof(int)), "barrier flag");
+  if (rc == SBBF_OK) rc = cuda_check(cudaMemset(d->d_flag, 0, sizeof(int)), "barrier flag");
+  if (rc == SBBF_OK)
+    rc = sbbf_route_create(static_cast<uint32_t>(d->world), static_cast<uint32_t>(d->rank), max_batch, d->device,
+                           &d->route);
+  trace(d, rc == SBBF_OK ? "create: shard and window ready" : "create: shard/window failed");
+  if (rc == SBBF_OK && d->world > 1) {
+    std::vector<uint8_t> mine(64), all(static_cast<size_t>(64) * d->world);
+    rc = sbbf_route_ipc_handle(d->route, mine.data());
+    if (rc == SBBF_OK) rc = allgather_host(d, mine.data(), all.data(), 64);
+    trace(d, "create: handles exchanged");
+    for (int p = 0; rc == SBBF_OK && p < d->world; ++p)
+      if (p != d->rank) rc = sbbf_route_open_peer(d->route, static_cast<uint32_t>(p), all.data() + 64 * p);
+    trace(d, "create: peers mapped");
+    if (rc == SBBF_OK) rc = barrier(d, nullptr);
+    if (rc == SBBF_OK) rc = wait_stream(d, nullptr, 600000, "create");
+    trace(d, "create: done");
+  }
+  return rc;
+}
+
+}  // namespace
+
 int sbbf_dist_create(void* comm, uint64_t total_buckets, uint64_t max_batch, int device, sbbf_dist_t** out) {
   if (!comm || !out || total_buckets == 0 || max_batch == 0)
     return dist_fail(SBBF_EINVAL, "sbbf_dist_create: bad argument");
@@ -185,48 +310,60 @@ int sbbf_dist_create(void* comm, uint64_t total_buckets, uint64_t max_batch, int
   d->total = total_buckets;
   int rc = nccl_check(nccl().comm_count(d->comm, &d->world), "ncclCommCount");
   if (rc == SBBF_OK) rc = nccl_check(nccl().comm_user_rank(d->comm, &d->rank), "ncclCommUserRank");
-  if (rc == SBBF_OK && total_buckets < static_cast<uint64_t>(d->world))
-    rc = dist_fail(SBBF_EINVAL, "sbbf_dist_create: fewer buckets than ranks");
-  if (rc == SBBF_OK) {
-    d->bounds.resize(d->world + 1);
-    rc = sbbf_shard_bounds(total_buckets, static_cast<uint32_t>(d->world), d->bounds.data());
+  if (rc == SBBF_OK) rc = create_common(d, total_buckets, max_batch);
+  if (rc != SBBF_OK) {
+    d->comm = d->aborted ? nullptr : d->comm;
+    sbbf_dist_destroy(d);
+    return rc;
   }
-  if (rc == SBBF_OK)
-    rc = sbbf_gpu_create_shard(total_buckets, d->bounds[d->rank], d->bounds[d->rank + 1] - d->bounds[d->rank],
-                               device, &d->shard);
-  if (rc == SBBF_OK) rc = cuda_check(cudaMalloc(&d->d_bounds, d->world * sizeof(uint64_t)), "bounds");
-  if (rc == SBBF_OK)
-    rc = cuda_check(cudaMemcpy(d->d_bounds, d->bounds.data(), d->world * sizeof(uint64_t), cudaMemcpyHostToDevice),
-                    "bounds");
-  if (rc == SBBF_OK) rc = cuda_check(cudaMalloc(&d->d_flag, sizeof(int)), "barrier flag");
-  if (rc == SBBF_OK) rc = cuda_check(cudaMemset(d->d_flag, 0, sizeof(int)), "barrier flag");
-  if (rc == SBBF_OK)
-    rc = sbbf_route_create(static_cast<uint32_t>(d->world), static_cast<uint32_t>(d->rank), max_batch, device,
-                           &d->route);
-  if (rc == SBBF_OK && d->world > 1) {
-    // exchange the window handles (one ncclAllGather of 64-byte records)
-    uint8_t* d_handles = nullptr;
-    std::vector<uint8_t> h(static_cast<size_t>(64) * d->world);
-    rc = sbbf_route_ipc_handle(d->route, h.data() + 64 * d->rank);
-    if (rc == SBBF_OK) rc = cuda_check(cudaMalloc(&d_handles, h.size()), "handles");
-    if (rc == SBBF_OK) rc = cuda_check(cudaMemcpy(d_handles + 64 * d->rank, h.data() + 64 * d->rank, 64,
-                                                  cudaMemcpyHostToDevice), "handles");
-    if (rc == SBBF_OK)
-      rc = nccl_check(nccl().all_gather(d_handles + 64 * d->rank, d_handles, 64, ncclUint8, d->comm, nullptr),
-                      "ncclAllGather(handles)");
-    if (rc == SBBF_OK) rc = cuda_check(cudaMemcpy(h.data(), d_handles, h.size(), cudaMemcpyDeviceToHost), "handles");
-    cudaFree(d_handles);
-    for (int p = 0; rc == SBBF_OK && p < d->world; ++p)
-      if (p != d->rank) rc = sbbf_route_open_peer(d->route, static_cast<uint32_t>(p), h.data() + 64 * p);
-    // every rank has mapped every window before anyone dispatches
-    if (rc == SBBF_OK) rc = barrier(d, nullptr);
-    if (rc == SBBF_OK) rc = cuda_check(cudaDeviceSynchronize(), "create");
-  }
+  *out = d;
+  return SBBF_OK;
+}
+
+int sbbf_dist_create_hooks(const sbbf_dist_hooks* hooks, uint64_t total_buckets, uint64_t max_batch, int device,
+                           sbbf_dist_t** out) {
+  if (!hooks || !out || total_buckets == 0 || max_batch == 0 || hooks->world < 1 || hooks->rank < 0 ||
+      hooks->rank >= hooks->world || !hooks->allgather || !hooks->barrier)
+    return dist_fail(SBBF_EINVAL, "sbbf_dist_create_hooks: bad argument");
+  *out = nullptr;
+  Guard g(device);
+  auto* d = new sbbf_dist;
+  d->hooks = *hooks;
+  d->use_hooks = true;
+  d->rank = hooks->rank;
+  d->world = hooks->world;
+  d->device = device;
+  d->total = total_buckets;
+  const int rc = create_common(d, total_buckets, max_batch);
   if (rc != SBBF_OK) {
     sbbf_dist_destroy(d);
     return rc;
   }
   *out = d;
+  return SBBF_OK;
+}
+
+int sbbf_dist_sync(sbbf_dist_t* d, void* stream, int64_t timeout_ms) {
+  if (!d) return dist_fail(SBBF_EINVAL, "sbbf_dist_sync: null handle");
+  if (d->aborted) return dist_fail(SBBF_ECUDA, "sharded filter: communicator aborted");
+  Guard g(d->device);
+  return wait_stream(d, static_cast<cudaStream_t>(stream), timeout_ms, "sbbf_dist_sync");
+}
+
+int sbbf_dist_image_crc(sbbf_dist_t* d, uint32_t* crc) {
+  if (!d || !crc) return dist_fail(SBBF_EINVAL, "sbbf_dist_image_crc: bad argument");
+  if (d->aborted) return dist_fail(SBBF_ECUDA, "sharded filter: communicator aborted");
+  Guard g(d->device);
+  uint32_t mine = 0;
+  int rc = sbbf_gpu_blocks_crc(d->shard, &mine);
+  std::vector<uint32_t> all(d->world);
+  if (rc == SBBF_OK) rc = allgather_host(d, &mine, all.data(), sizeof(uint32_t));
+  if (rc != SBBF_OK) return rc;
+  uint8_t hdr[17] = {'S', 'B', 'B', 'F', 1, 0, 0, 0, 0};
+  for (int i = 0; i < 8; ++i) hdr[9 + i] = static_cast<uint8_t>(d->total >> (8 * i));
+  uint32_t c = sbbf_crc32_update(0, hdr, sizeof(hdr));
+  for (int p = 0; p < d->world; ++p) c = sbbf_crc32_combine(c, all[p], (d->bounds[p + 1] - d->bounds[p]) * 32);
+  *crc = c;
   return SBBF_OK;
 }
 
@@ -239,8 +376,11 @@ int sbbf_dist_insert(sbbf_dist_t* d, const uint64_t* d_hashes, uint64_t n, void*
   Guard g(d->device);
   const auto s = static_cast<cudaStream_t>(stream);
   int rc = sbbf_route_dispatch(d->route, d_hashes, n, d->total, d->d_bounds, 0, stream);
+  trace(d, "insert: dispatched");
   if (rc == SBBF_OK) rc = barrier(d, s);
+  trace(d, "insert: barrier passed");
   if (rc == SBBF_OK) rc = sbbf_route_insert_window(d->route, d->shard, stream);
+  trace(d, "insert: window inserted");
   return rc;
 }
 
@@ -249,10 +389,15 @@ int sbbf_dist_find(sbbf_dist_t* d, const uint64_t* d_hashes, uint64_t n, uint8_t
   Guard g(d->device);
   const auto s = static_cast<cudaStream_t>(stream);
   int rc = sbbf_route_dispatch(d->route, d_hashes, n, d->total, d->d_bounds, 1, stream);
+  trace(d, "find: dispatched");
   if (rc == SBBF_OK) rc = barrier(d, s);
+  trace(d, "find: barrier 1 passed");
   if (rc == SBBF_OK) rc = sbbf_route_find_window(d->route, d->shard, stream);
+  trace(d, "find: window probed");
   if (rc == SBBF_OK) rc = barrier(d, s);
+  trace(d, "find: barrier 2 passed");
   if (rc == SBBF_OK) rc = sbbf_route_combine(d->route, d_results, stream);
+  trace(d, "find: combined");
   return rc;
 }
 
@@ -275,14 +420,28 @@ int sbbf_dist_find_bits(sbbf_dist_t* d, const uint64_t* d_hashes, uint64_t n, ui
 int sbbf_dist_gather(sbbf_dist_t* d, void* h_dst, int root) {
   if (!d || root < 0 || root >= d->world || (d->rank == root && !h_dst))
     return dist_fail(SBBF_EINVAL, "sbbf_dist_gather: bad argument");
+  if (d->aborted) return dist_fail(SBBF_ECUDA, "sharded filter: communicator aborted");
   Guard g(d->device);
   int rc = cuda_check(cudaDeviceSynchronize(), "gather");
   if (rc != SBBF_OK) return rc;
   const uint64_t mine = d->bounds[d->rank + 1] - d->bounds[d->rank];
+  if (d->use_hooks || d->world == 1) {
+    // every shard padded to the largest, gathered on the host in rank order
+    uint64_t most = 0;
+    for (int p = 0; p < d->world; ++p) most = std::max<uint64_t>(most, d->bounds[p + 1] - d->bounds[p]);
+    std::vector<uint8_t> send(most * 32), all(most * 32 * d->world);
+    rc = sbbf_gpu_to_host(d->shard, send.data(), mine * 32);
+    if (rc == SBBF_OK) rc = allgather_host(d, send.data(), all.data(), most * 32);
+    if (rc == SBBF_OK && d->rank == root)
+      for (int p = 0; p < d->world; ++p)
+        std::memcpy(static_cast<uint8_t*>(h_dst) + d->bounds[p] * 32, all.data() + most * 32 * p,
+                    (d->bounds[p + 1] - d->bounds[p]) * 32);
+    return rc;
+  }
   if (d->rank != root) {
     rc = nccl_check(nccl().send(sbbf_gpu_device_blocks(d->shard), mine * 32, ncclUint8, root, d->comm, nullptr),
                     "ncclSend(shard)");
-    if (rc == SBBF_OK) rc = cuda_check(cudaDeviceSynchronize(), "gather");
+    if (rc == SBBF_OK) rc = wait_stream(d, nullptr, 600000, "gather");
     return rc;
   }
   auto* out = static_cast<uint8_t*>(h_dst);
@@ -293,6 +452,7 @@ int sbbf_dist_gather(sbbf_dist_t* d, void* h_dst, int root) {
     uint8_t* stage = nullptr;
     rc = cuda_check(cudaMalloc(&stage, cnt * 32), "gather stage");
     if (rc == SBBF_OK) rc = nccl_check(nccl().recv(stage, cnt * 32, ncclUint8, p, d->comm, nullptr), "ncclRecv(shard)");
+    if (rc == SBBF_OK) rc = wait_stream(d, nullptr, 600000, "gather");
     if (rc == SBBF_OK)
       rc = cuda_check(cudaMemcpy(out + d->bounds[p] * 32, stage, cnt * 32, cudaMemcpyDeviceToHost), "gather");
     cudaFree(stage);

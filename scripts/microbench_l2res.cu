@@ -57,7 +57,18 @@ enum : int {
   kChunked = 32,      // keys in the blocked path's chunk-local layout: region r's keys are 128-key
                       // runs at chunk*4096 + r*128 (32 KB stride)
   kChunkedPad = 64,   // the same with a 4128-key (33 KB) chunk stride
+  kAhead1 = 128,      // each CTA bulk-prefetches its share of region r+1 into L2 first
+  kAhead2 = 256,      // ... of region r+2
 };
+
+// CTA g of `groups` prefetches its share of region rr (if it exists)
+__device__ __forceinline__ void prefetch_share(const uint32_t* filt, uint64_t region_blocks, uint64_t regions,
+                                               uint64_t rr, uint32_t g, uint32_t groups) {
+  if (rr >= regions || threadIdx.x != 0) return;
+  const uint64_t bytes = region_blocks * 32, share = (bytes / groups) & ~15ull;
+  const char* p = reinterpret_cast<const char*>(filt + rr * region_blocks * 8) + g * share;
+  if (share) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((uint32_t)share) : "memory");
+}
 
 template <int F>
 __device__ __forceinline__ uint64_t key_addr(uint64_t i, uint64_t r, uint64_t per_region) {
@@ -78,6 +89,8 @@ __global__ void __launch_bounds__(256, 8) sweep(const uint32_t* __restrict__ fil
   const uint32_t* base = filt + r * region_blocks * 8;
   const uint64_t pf = pol_first(), pl = pol_last();
   uint32_t acc = 0;
+  if (F & kAhead1) prefetch_share(filt, region_blocks, (1ull << 30) / (region_blocks * 32), r + 1, g, groups);
+  if (F & kAhead2) prefetch_share(filt, region_blocks, (1ull << 30) / (region_blocks * 32), r + 2, g, groups);
   for (uint64_t i0 = k0 + threadIdx.x; i0 < k1; i0 += 256 * U) {
     uint64_t h[U];
 #pragma unroll
@@ -158,6 +171,8 @@ __global__ void __launch_bounds__(256, 8) isweep(uint32_t* __restrict__ filt, ui
   const uint64_t pf = pol_first(), pl = pol_last();
   constexpr int TPK = M == 2 ? 8 : (M == 3 ? 1 : 4);
   const uint32_t sub = threadIdx.x % TPK;
+  if (M == 8) prefetch_share(filt, region_blocks, (1ull << 30) / (region_blocks * 32), r + 1, g, groups);
+  if (M == 9) prefetch_share(filt, region_blocks, (1ull << 30) / (region_blocks * 32), r + 2, g, groups);
   if (M == 6 || M == 7) {
     // prefetch this CTA's share of the region into L2 first (128-B lines)
     const uint64_t bytes = region_blocks * 32, share = (bytes + groups - 1) / groups;
@@ -201,7 +216,7 @@ __global__ void __launch_bounds__(256, 8) isweep(uint32_t* __restrict__ filt, ui
         asm volatile("ld.global.u64 %0, [%1];" : "=l"(cur) : "l"(p));
         need = (m & ~cur) != 0;
       }
-      if (M == 5) {
+      if (M == 5 || M == 8 || M == 9) {
         uint64_t cur;
         asm volatile("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(cur) : "l"(p), "l"(pl));
         need = (m & ~cur) != 0;
@@ -409,6 +424,19 @@ int main(int argc, char** argv) {
   if (mask & 8192) run<kProbeLast | kOutFirst | kDiscard, 1>(filt, filter_blocks, r16, keys, n, out, sink, "all three");
   if (mask & 16384) run<kProbeLast | kOutFirst | kDiscard, 1>(filt, filter_blocks, r64, keys, n, out, sink, "all three");
   if (mask & 32768) run<kOutNone, 4>(filt, filter_blocks, r32, keys, n, out, sink, "no answer stores");
+  if (mask & (1u << 14)) {  // prefetch-ahead of the next region(s)
+    run<0, 1>(filt, filter_blocks, r16, keys, n, out, sink, "16 MiB, no prefetch");
+    run<kAhead1, 1>(filt, filter_blocks, r16, keys, n, out, sink, "16 MiB, prefetch r+1");
+    run<kAhead2, 1>(filt, filter_blocks, r16, keys, n, out, sink, "16 MiB, prefetch r+2");
+    run<kAhead1, 1>(filt, filter_blocks, r8, keys, n, out, sink, "8 MiB, prefetch r+1");
+    run<kAhead1, 1>(filt, filter_blocks, r32, keys, n, out, sink, "32 MiB, prefetch r+1");
+    const uint64_t ni = 1ull << 26;
+    irun<5>(filt, filter_blocks, r16, keys, ni, "test+red el 16 MiB");
+    irun<8>(filt, filter_blocks, r16, keys, ni, "test+red el 16 MiB, pf r+1");
+    irun<9>(filt, filter_blocks, r16, keys, ni, "test+red el 16 MiB, pf r+2");
+    irun<8>(filt, filter_blocks, r8, keys, ni, "test+red el 8 MiB, pf r+1");
+    irun<8>(filt, filter_blocks, r32, keys, ni, "test+red el 32 MiB, pf r+1");
+  }
   if (mask & (1u << 31)) {
     run<0, 1>(filt, filter_blocks, r32, keys, n, out, sink, "flat keys");
     run<kChunked, 1>(filt, filter_blocks, r32, keys, n, out, sink, "chunk-local keys, 32 KB stride");

@@ -35,3 +35,40 @@ def test_cpp_dropin_runs(cuda):
     assert out.returncode == 0, out.stderr + out.stdout
     assert "cpp drop-in ok" in out.stdout
     assert "cpp sharded layer (world 1) ok" in out.stdout
+
+
+ACC = os.path.join(ROOT, "tests", "cpp", "acceptance_gpu")
+
+
+def test_reference_acceptance_builds_against_gpu_library():
+    """The reference's own acceptance suite and its callers (harness.cpp,
+    model.cpp, persist.cpp), compiled unmodified with the filter.hpp
+    stand-in, link libsbbf_gpu.so and none of the reference's filter.cpp."""
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True, capture_output=True)
+    if not os.path.exists(ACC):
+        pytest.skip("reference sources absent and no prebuilt tests/cpp/acceptance_gpu")
+    syms = subprocess.run(["nm", "-C", ACC], capture_output=True, text=True).stdout
+    assert "find_many_avx2" not in syms and "add_avx2" not in syms      # the CPU core is not linked
+    ldd = subprocess.run(["ldd", ACC], capture_output=True, text=True).stdout
+    assert "libsbbf_gpu.so" in ldd
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_reference_acceptance_on_gpu(cuda):
+    """proj/tests/acceptance/acceptance.cpp (criteria 1-9; 4c needs --huge)
+    running on the GPU library: every filter it builds, probes, serializes,
+    reloads and benchmarks (run_bench, run_fpp_sim, sbbf_fpp_mc) is an HBM
+    filter behind the C ABI. Criteria 1, 2 and 9 are the drop-in contract
+    (no false negatives, bit-exact vectors and path identity, one block and
+    eight lane hashes per op)."""
+    if not os.path.exists(ACC):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=False, capture_output=True)
+    if not os.path.exists(ACC):
+        pytest.skip("tests/cpp/acceptance_gpu was not built (needs /root/reference at build time)")
+    out = subprocess.run([ACC], capture_output=True, text=True, timeout=1500)
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("[")]
+    for crit in ("criterion 1:", "criterion 2:", "criterion 9:", "criterion 4d:", "criterion 8:"):
+        assert any(ln.startswith("[PASS]") and crit in ln for ln in lines), out.stdout + out.stderr
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "all criteria passed" in out.stdout

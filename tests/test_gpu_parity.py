@@ -482,3 +482,32 @@ def test_range_split_passes(cuda, oracle, nb):
     assert np.array_equal(f.find_hashes(dev(probes, cuda)).cpu().numpy(), want_res)
     bits = u32(f.find_hashes_bits(dev(probes, cuda)))
     assert np.array_equal(bits_to_bytes(bits, probes.size), want_res)
+
+
+@pytest.mark.parametrize("nb", [1 << 22, 4_400_007, (1 << 23) + 5])
+def test_range_split_passes_keys_frontend(cuda, oracle, nb):
+    """The fused XXH64 key frontend (hash_u64_key, hash.cpp:108-114) takes
+    the same range-split passes: add_keys / find_keys / find_keys_bits over
+    u64 keys must equal hashing on the device first and then inserting /
+    probing the hashes (itself oracle-checked above), including the bitmap
+    path where the first pass stores each word and later passes OR into it."""
+    rng = np.random.default_rng(nb ^ 0xF00D)
+    keys = rng.integers(0, 2**64, size=2_000_003, dtype=np.uint64)
+    probes = np.concatenate([keys[:500_001], rng.integers(0, 2**64, size=1_000_037, dtype=np.uint64)])
+    seed = 20160216
+    dk, dp = dev(keys, cuda), dev(probes, cuda)
+    from paper_2101_01719_b200 import hash_u64_keys
+    hk = hash_u64_keys(dk, seed)
+    hp = hash_u64_keys(dp, seed)
+    # the device hash equals the oracle's XXH64 of the key's 8 LE bytes
+    sample = probes[-1000:]
+    want_h = np.array([oracle.xxh64(int(k).to_bytes(8, "little"), seed) for k in sample], np.uint64)
+    assert np.array_equal(hp[-1000:].cpu().numpy().view(np.uint64), want_h)
+    f = SplitBlockFilter(nb, hasher_id=1)
+    f.add_keys(dk, seed)
+    want = oracle.build(nb, hk.cpu().numpy().view(np.uint64))
+    assert np.array_equal(f.blocks(), want)
+    want_res = oracle.find_hashes(want, hp.cpu().numpy().view(np.uint64))
+    assert np.array_equal(f.find_keys(dp, seed).cpu().numpy(), want_res)
+    bits = u32(f.find_keys_bits(dp, seed))
+    assert np.array_equal(bits_to_bytes(bits, probes.size), want_res)

@@ -519,3 +519,122 @@ def test_bench_world2_code_path(cuda):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["config_id"] == 5 and d["value"] > 0
     assert "peer-memory windows" in d["config"]["workload"]
+
+
+def _dist_hooks_worker(rank, world, port, total, q):
+    """One rank of the C sharded layer (sbbf_dist_*) at world > 1 on ONE GPU:
+    NCCL refuses two ranks on one device, so the collectives come from the
+    caller (sbbf_dist_create_hooks) — a gloo process group here — while the
+    data path is the product's: CUDA IPC receive windows, fused dispatch,
+    owner-side window insert / find, combine."""
+    import ctypes as C
+    import datetime
+    import traceback
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=120))
+    try:
+        _dist_hooks_body(rank, world, total, q)
+    except BaseException:  # report instead of leaving the parent waiting
+        q.put((rank, "error", traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _dist_hooks_body(rank, world, total, q):
+    if True:
+        import ctypes as C
+        from paper_2101_01719_b200 import _lib
+        L = _lib.lib()
+        torch.cuda.set_device(0)
+
+        AG = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
+        BAR = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)
+        calls = {"barrier": 0, "allgather": 0}
+
+        hook_errors = []
+
+        def allgather(ctx, send, recv, nbytes):
+            try:
+                mine = torch.from_numpy(np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)), (nbytes,)).copy())
+                outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(outs, mine)
+                joined = torch.cat(outs).numpy()   # keep it alive across the copy
+                C.memmove(recv, joined.ctypes.data, nbytes * world)
+                calls["allgather"] += 1
+                return 0
+            except BaseException as exc:  # noqa: BLE001 - surfaced through the return code
+                hook_errors.append(repr(exc))
+                return 1
+
+        def barrier(ctx, stream):
+            try:
+                torch.cuda.synchronize()        # this rank's queued work is done ...
+                dist.barrier()                  # ... and every other rank's too
+                calls["barrier"] += 1
+                return 0
+            except BaseException as exc:  # noqa: BLE001
+                hook_errors.append(repr(exc))
+                return 1
+
+        class Hooks(C.Structure):
+            _fields_ = [("rank", C.c_int), ("world", C.c_int), ("ctx", C.c_void_p), ("allgather", AG),
+                        ("barrier", BAR)]
+
+        ag, br = AG(allgather), BAR(barrier)
+        hooks = Hooks(rank, world, None, ag, br)
+        d = C.c_void_p()
+        rc = L.sbbf_dist_create_hooks(C.byref(hooks), total, 1 << 20, 0, C.byref(d))
+        assert rc == 0, (rc, L.sbbf_gpu_last_error(), hook_errors)
+        assert L.sbbf_dist_rank(d) == rank and L.sbbf_dist_world(d) == world
+        rng = np.random.default_rng(77 + rank)
+        h = rng.integers(0, 2**64, size=300_000 + 1001 * rank, dtype=np.uint64)
+        look = np.concatenate([h[:2000], rng.integers(0, 2**64, size=100_003, dtype=np.uint64)])
+        dh = torch.from_numpy(h.view(np.int64)).cuda()
+        dl = torch.from_numpy(look.view(np.int64)).cuda()
+        s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(L.sbbf_dist_insert(d, C.c_void_p(dh.data_ptr()), h.size, s), "dist_insert")
+        out = torch.empty(look.size, dtype=torch.uint8, device="cuda")
+        _lib.check(L.sbbf_dist_find(d, C.c_void_p(dl.data_ptr()), look.size, C.c_void_p(out.data_ptr()), s),
+                   "dist_find")
+        bits = torch.empty((look.size + 31) // 32, dtype=torch.int32, device="cuda")
+        _lib.check(L.sbbf_dist_find_bits(d, C.c_void_p(dl.data_ptr()), look.size, C.c_void_p(bits.data_ptr()), s),
+                   "dist_find_bits")
+        _lib.check(L.sbbf_dist_sync(d, s, 60_000), "dist_sync")
+        crc = C.c_uint32(0)
+        _lib.check(L.sbbf_dist_image_crc(d, C.byref(crc)), "dist_image_crc")
+        full = np.zeros((total, 8), np.uint32) if rank == 0 else np.zeros(1, np.uint32)
+        _lib.check(L.sbbf_dist_gather(d, full.ctypes.data_as(C.c_void_p), 0), "dist_gather")
+        q.put((rank, h, look, out.cpu().numpy(), bits.cpu().numpy().view(np.uint32), full if rank == 0 else None,
+               int(crc.value), dict(calls)))
+        L.sbbf_dist_destroy(d)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,total", [(2, 1 << 20), (3, 7919 * 13)])
+def test_dist_c_abi_world_gt1_one_gpu(cuda, oracle, world, total):
+    """sbbf_dist_* at world 2 and 3 (every rank on this one GPU, collectives
+    by hook): inserts routed to their owner shards through the peer windows,
+    lookups answered and combined in source order, the gathered filter and
+    its image CRC equal to the single-filter reference."""
+    from oracle import bits_to_bytes
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_dist_hooks_worker, args=(r, world, port, total, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    errors = [g[2] for g in got if isinstance(g[1], str)]
+    assert not errors, "\n".join(errors)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = oracle.build(total, np.concatenate([g[1] for g in got]))
+    assert np.array_equal(got[0][5], want)
+    assert all(g[6] == oracle.image_crc(want) for g in got)
+    for rank, h, look, out, bits, _, _, calls in got:
+        res = oracle.find_hashes(want, look)
+        assert np.array_equal(out, res), rank
+        assert np.array_equal(bits_to_bytes(bits, look.size), res), rank
+        assert calls["barrier"] >= 5 and calls["allgather"] >= 2
