@@ -154,6 +154,11 @@ int sbbf_gpu_block_index_host(const uint64_t* h_hashes, uint64_t n, uint64_t num
                               int device);
 int sbbf_gpu_make_mask_host(const uint64_t* h_hashes, uint64_t n, uint32_t* h_lanes, int device);
 
+/* Filters beyond L2 keep the blocked path's scratch (about 11 B per key of
+ * the largest batch chunk, up to ~6 GB for 2^28-key lookup rounds) cached on
+ * the handle between calls; this returns it to the device (synchronous). */
+int sbbf_gpu_release_scratch(sbbf_gpu_t* f);
+
 /* --- tuning ----------------------------------------------------------- */
 int sbbf_gpu_set_insert_variant(sbbf_gpu_t* f, int variant);
 int sbbf_gpu_set_find_variant(sbbf_gpu_t* f, int variant);

@@ -58,6 +58,7 @@ PROTOTYPES = {
     "sbbf_gpu_block_index_host": (_i, [_vp, _u64, _u64, _vp, _i]),
     "sbbf_gpu_make_mask_host": (_i, [_vp, _u64, _vp, _i]),
     "sbbf_gpu_set_insert_variant": (_i, [_vp, _i]),
+    "sbbf_gpu_release_scratch": (_i, [_vp]),
     "sbbf_gpu_set_find_variant": (_i, [_vp, _i]),
     "sbbf_gpu_resolved_insert_variant": (_i, [_vp, _u64]),
     "sbbf_gpu_resolved_find_variant": (_i, [_vp, _u64]),

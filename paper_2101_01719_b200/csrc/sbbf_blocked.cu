@@ -32,6 +32,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <new>
 #include <vector>
 
 #include "sbbf_device.cuh"
@@ -812,336 +813,6 @@ __global__ void __launch_bounds__(kUnpermThreads, 4) unpermute_kernel(const uint
   }
 }
 
-// ---------------------------------------------------------------------------
-// persistent slice sweep (replaces segment_kernel + unpermute_kernel)
-// ---------------------------------------------------------------------------
-// One cooperative launch of every resident CTA. CTA c owns a contiguous run
-// of partition chunks and walks the buckets (filter slices) in order; for
-// bucket b it processes the concatenation of its chunks' runs of bucket b as
-// one flat list, split evenly over its warps (no ragged per-run tails, no
-// dependent offset loads: each bucket's run table is built once in shared
-// memory by a block scan). All CTAs sweep the slices in lockstep: before
-// bucket b a CTA waits until every CTA has finished bucket b - kSweepSlack,
-// so at most kSweepSlack + 1 slices (~32 MiB each) are live in L2 at any
-// time whatever the batch size (a grid of independent CTAs keeps ~4 slices
-// in flight on a 2^26-key round and thrashes L2: scripts/microbench_l2res.cu).
-// The wait is only a locality device: results never depend on it.
-// Lookups store one answer byte per routed slot and finish with an epilogue
-// that returns the CTA's own chunks to source order (bitmap or bytes) —
-// the separate unpermute launch is gone.
-constexpr int kSweepThreads = 256;
-constexpr int kSweepWarps = kSweepThreads / 32;
-constexpr int kSweepMaxChunks = 512;  // chunks per CTA (shared-memory run tables)
-constexpr int kSweepSlack = 1;
-
-struct SweepArgs {
-  uint32_t* blocks;
-  Geom g;
-  const uint64_t* keys;   // bucket-major chunk regions (chunk_scatter)
-  const uint16_t* boffs;  // [nchunks][kBoffStride] run offsets; entry kChunkBuckets = chunk key count
-  uint64_t nchunks;
-  uint32_t S;
-  uint8_t* ans;           // lookups: one answer byte per slot
-  const uint16_t* pos16;  // lookups: source position of each slot in its chunk
-  void* out;              // lookups: bitmap words / bytes, chunk ch at bit / byte ch * kPartChunk
-  bool bits;
-  unsigned* done;         // [S] CTAs finished per bucket (zeroed before the launch); null = no lockstep
-  int prefetch;           // 1: each CTA bulk-prefetches its share of slice b+1 into L2 while sweeping b
-  int slack;              // before bucket b wait for bucket b - slack everywhere (0: never wait)
-};
-
-__device__ __forceinline__ uint32_t ld_acquire_u32(const unsigned* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Exclusive scan of len[0..nk) (nk <= kSweepMaxChunks) into P[0..nk], by
-// the whole block (each thread sums a contiguous pair, then a warp scan of
-// the warp totals).
-__device__ __forceinline__ void block_scan_runs(uint32_t* P, uint32_t nk, uint32_t* wsum) {
-  constexpr int kPer = kSweepMaxChunks / kSweepThreads;
-  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  uint32_t v[kPer], tot = 0;
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const uint32_t k = t * kPer + i;
-    v[i] = k < nk ? P[k] : 0u;
-    tot += v[i];
-  }
-  uint32_t inc = tot;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-    if (lane >= static_cast<uint32_t>(d)) inc += y;
-  }
-  if (lane == 31) wsum[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t w = lane < kSweepWarps ? wsum[lane] : 0u, wi = w;
-#pragma unroll
-    for (int d = 1; d < kSweepWarps; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, wi, d);
-      if (lane >= static_cast<uint32_t>(d)) wi += y;
-    }
-    if (lane < kSweepWarps) wsum[lane] = wi - w;  // exclusive warp bases
-    if (lane == kSweepWarps - 1) wsum[kSweepWarps] = wi;  // total
-  }
-  __syncthreads();
-  uint32_t run = wsum[warp] + inc - tot;
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const uint32_t k = t * kPer + i;
-    if (k < nk) P[k] = run;
-    run += v[i];
-  }
-  if (t == 0) P[nk] = wsum[kSweepWarps];
-  __syncthreads();
-}
-
-// Run k of the flat list holding position t: advance from the previous k
-// (positions only grow within a warp's range).
-__device__ __forceinline__ uint32_t run_of(const uint32_t* P, uint32_t k, uint32_t t) {
-  while (P[k + 1] <= t) ++k;
-  return k;
-}
-
-template <bool kInsert, int kU>
-__global__ void __launch_bounds__(kSweepThreads, kInsert ? 4 : 5) sweep_kernel(SweepArgs a) {
-  __shared__ uint32_t P[kSweepMaxChunks + 1];
-  __shared__ uint16_t st16[kSweepMaxChunks];
-  __shared__ uint32_t wsum[kSweepWarps + 1];
-  __shared__ __align__(16) uint8_t stage[kInsert ? 16 : kPartChunk];
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t c0 = a.nchunks * blockIdx.x / gridDim.x, c1 = a.nchunks * (blockIdx.x + 1) / gridDim.x;
-  const uint32_t nk = static_cast<uint32_t>(c1 - c0);
-  const uint64_t pol = dev::policy_evict_first();
-  const uint64_t keep = dev::policy_evict_last();
-  const Geom g = a.g;
-  // slice b of the (local) filter: blocks [b * nb / S, (b + 1) * nb / S]
-  auto prefetch_slice = [&](uint32_t b) {
-    const uint64_t lo = g.nb_local * b / a.S, hi0 = (g.nb_local * (b + 1) + a.S - 1) / a.S;
-    const uint64_t hi = hi0 < g.nb_local ? hi0 : g.nb_local;
-    const uint64_t n = hi > lo ? hi - lo : 0;
-    const uint64_t p0 = lo + n * blockIdx.x / gridDim.x, p1 = lo + n * (blockIdx.x + 1) / gridDim.x;
-    const uint64_t bytes = (p1 - p0) * 32;
-    const char* base = reinterpret_cast<const char*>(a.blocks + p0 * 8);
-    for (uint64_t o = 0; o < bytes; o += (1u << 20)) {
-      const uint64_t len = bytes - o < (1u << 20) ? bytes - o : (1u << 20);
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + o), "r"(static_cast<uint32_t>(len))
-                   : "memory");
-    }
-  };
-  if (a.prefetch && threadIdx.x == 0) prefetch_slice(0);
-  for (uint32_t b = 0; b < a.S; ++b) {
-    if (a.prefetch && threadIdx.x == 32 && b + 1 < a.S) prefetch_slice(b + 1);
-    // run table of bucket b over this CTA's chunks
-    for (uint32_t k = threadIdx.x; k < nk; k += kSweepThreads) {
-      const uint16_t* row = a.boffs + (c0 + k) * kBoffStride;
-      const uint16_t st = row[b], en = row[b + 1];
-      SBBF_DCHECK(st <= en && en <= row[kChunkBuckets]);
-      st16[k] = st;
-      P[k] = static_cast<uint32_t>(en - st);
-    }
-    if (a.done && a.slack > 0 && b >= static_cast<uint32_t>(a.slack) && threadIdx.x == 0) {
-      const unsigned* d = a.done + (b - a.slack);
-      while (ld_acquire_u32(d) < gridDim.x) __nanosleep(64);
-    }
-    __syncthreads();
-    block_scan_runs(P, nk, wsum);
-    const uint32_t T = P[nk];
-    // this warp's share of the flat list
-    const uint32_t r0 = static_cast<uint32_t>(static_cast<uint64_t>(T) * warp / kSweepWarps);
-    const uint32_t r1 = static_cast<uint32_t>(static_cast<uint64_t>(T) * (warp + 1) / kSweepWarps);
-    if constexpr (kInsert) {
-      // 4 lanes per key (one 64-bit lane pair each), 8 keys per warp row, kU
-      // rows in flight; test-before-set: hot keys (config 4's Zipf
-      // duplicates) skip the atomic
-      const uint32_t pair = lane & 3, sub = lane >> 2;
-      const uint32_t seed_lo = dev::lane_seed_rt(2 * pair), seed_hi = dev::lane_seed_rt(2 * pair + 1);
-      uint32_t k = 0;
-      if (r0 < r1) {  // first run of this warp (binary search once)
-        uint32_t lo = 0, hi = nk;
-        while (lo + 1 < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (P[mid] <= r0) lo = mid; else hi = mid;
-        }
-        k = lo;
-      }
-      // the next row group's keys load while this group's pairs / reds are in flight
-      uint64_t hn[kU];
-      bool vn[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const uint32_t t = r0 + u * 8 + sub;
-        vn[u] = t < r1;
-        hn[u] = 0;
-        if (vn[u]) {
-          k = run_of(P, k, t);
-          hn[u] = dev::ld_stream_u64(a.keys + (c0 + k) * kPartChunk + st16[k] + (t - P[k]), pol);
-        }
-      }
-      for (uint32_t t0 = r0; t0 < r1; t0 += 8 * kU) {
-        uint64_t* ptr[kU];
-        uint64_t mask[kU], cur[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          mask[u] = 0;
-          ptr[u] = reinterpret_cast<uint64_t*>(a.blocks) + pair;
-          const uint64_t h = hn[u];
-          const uint64_t blk = dev::block_index(h, g.nb_global) - g.first;
-          if (vn[u] && blk < g.nb_local) {
-            const uint32_t low = static_cast<uint32_t>(h);
-            ptr[u] = reinterpret_cast<uint64_t*>(a.blocks + blk * 8) + pair;
-            mask[u] = (static_cast<uint64_t>(dev::lane_bit(low, seed_hi)) << 32) | dev::lane_bit(low, seed_lo);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) cur[u] = mask[u] ? dev::ld_pair(ptr[u], keep) : ~0ull;
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const uint32_t t = t0 + 8 * kU + u * 8 + sub;
-          vn[u] = t < r1;
-          hn[u] = 0;
-          if (vn[u]) {
-            k = run_of(P, k, t);
-            hn[u] = dev::ld_stream_u64(a.keys + (c0 + k) * kPartChunk + st16[k] + (t - P[k]), pol);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          if (mask[u] & ~cur[u]) dev::red_or64(ptr[u], mask[u], keep);
-      }
-    } else {
-      uint32_t k = 0;
-      if (r0 < r1) {
-        uint32_t lo = 0, hi = nk;
-        while (lo + 1 < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (P[mid] <= r0) lo = mid; else hi = mid;
-        }
-        k = lo;
-      }
-      // kU keys per lane per step, the next step's keys load while this
-      // step's sectors are in flight
-      uint64_t hn[kU], sn[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const uint32_t t = r0 + u * 32 + lane;
-        sn[u] = ~0ull;
-        hn[u] = 0;
-        if (t < r1) {
-          k = run_of(P, k, t);
-          sn[u] = (c0 + k) * kPartChunk + st16[k] + (t - P[k]);
-          hn[u] = dev::ld_stream_u64(a.keys + sn[u], pol);
-        }
-      }
-      for (uint32_t t0 = r0; t0 < r1; t0 += 32 * kU) {
-        uint64_t h[kU], slot[kU];
-        dev::Block8 bl[kU];
-        uint32_t owned = 0;
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          h[u] = hn[u];
-          slot[u] = sn[u];
-          const uint64_t blk = dev::block_index(h[u], g.nb_global) - g.first;
-          const bool ok = blk < g.nb_local && slot[u] != ~0ull;
-          owned |= static_cast<uint32_t>(ok) << u;
-          dev::ld_block_nc_normal(a.blocks + (ok ? blk : 0) * 8, bl[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const uint32_t t = t0 + 32 * kU + u * 32 + lane;
-          sn[u] = ~0ull;
-          hn[u] = 0;
-          if (t < r1) {
-            k = run_of(P, k, t);
-            sn[u] = (c0 + k) * kPartChunk + st16[k] + (t - P[k]);
-            hn[u] = dev::ld_stream_u64(a.keys + sn[u], pol);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u)
-          if (slot[u] != ~0ull)
-            dev::st_stream_u8(a.ans + slot[u], (((owned >> u) & 1u) && dev::block_contains(bl[u], h[u])) ? 1u : 0u);
-      }
-    }
-    __syncthreads();  // bucket b done by this CTA (and its run table free)
-    if (a.done && threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(a.done + b, 1u);
-    }
-  }
-  if constexpr (!kInsert) {
-    // epilogue: this CTA's chunks back to source order (as unpermute_kernel
-    // did in its own launch). The answer bytes were stored by this CTA's
-    // threads before the barrier above, so coherent L2 loads (.cg) see
-    // them. The next chunk's positions and answers load while this chunk is
-    // scattered through shared memory.
-    constexpr int kVec = kPartChunk / (kSweepThreads * 8);
-    uint4 pv[kVec];
-    uint2 av[kVec];
-    auto load_full = [&](uint64_t ch) {
-#pragma unroll
-      for (int v = 0; v < kVec; ++v) {
-        const uint64_t i = ch * kPartChunk + (v * kSweepThreads + threadIdx.x) * 8;
-        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(pv[v].x), "=r"(pv[v].y), "=r"(pv[v].z), "=r"(pv[v].w) : "l"(a.pos16 + i));
-        asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(av[v].x), "=r"(av[v].y) : "l"(a.ans + i));
-      }
-    };
-    uint32_t cnt_next = c0 < c1 ? a.boffs[c0 * kBoffStride + kChunkBuckets] : 0;
-    if (c0 < c1 && cnt_next == kPartChunk) load_full(c0);
-    for (uint64_t ch = c0; ch < c1; ++ch) {
-      const uint32_t cnt = cnt_next;
-      const uint64_t base = ch * kPartChunk;
-      if (cnt == kPartChunk) {
-#pragma unroll
-        for (int v = 0; v < kVec; ++v) {
-          const uint32_t pw[4] = {pv[v].x, pv[v].y, pv[v].z, pv[v].w};
-          const uint32_t aw[2] = {av[v].x, av[v].y};
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const uint32_t q = (pw[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
-            SBBF_DCHECK(q < kPartChunk);
-            stage[q] = static_cast<uint8_t>(aw[e >> 2] >> ((e & 3) * 8));
-          }
-        }
-      } else {
-        for (uint32_t i = threadIdx.x; i < cnt; i += kSweepThreads) {
-          uint16_t q;
-          uint16_t v;
-          asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(q) : "l"(a.pos16 + base + i));
-          asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(a.ans + base + i));
-          SBBF_DCHECK(q < cnt);
-          stage[q] = static_cast<uint8_t>(v);
-        }
-      }
-      cnt_next = ch + 1 < c1 ? a.boffs[(ch + 1) * kBoffStride + kChunkBuckets] : 0;
-      if (cnt_next == kPartChunk) load_full(ch + 1);
-      __syncthreads();
-      if (a.bits) {
-        uint32_t* ob = static_cast<uint32_t*>(a.out) + (base >> 5);
-        for (uint32_t wd = warp; wd * 32 < cnt; wd += kSweepWarps) {
-          const uint32_t i = wd * 32 + lane;
-          const uint32_t word = __ballot_sync(0xffffffffu, i < cnt && stage[i]);
-          if (lane == 0) dev::st_stream_u32(ob + wd, word);
-        }
-      } else {
-        uint8_t* o = static_cast<uint8_t*>(a.out) + base;
-        if (cnt == kPartChunk && (reinterpret_cast<uintptr_t>(o) & 15) == 0) {
-          const uint4* src = reinterpret_cast<const uint4*>(stage);
-          uint4* dst = reinterpret_cast<uint4*>(o);
-          for (uint32_t v = threadIdx.x; v < kPartChunk / 16; v += kSweepThreads) dst[v] = src[v];
-        } else {
-          for (uint32_t i = threadIdx.x; i < cnt; i += kSweepThreads) o[i] = stage[i];
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
 template <int BITS, bool kTop>
 cudaError_t chunk_partition_bits(const DeviceInfo& di, const BucketMap& bm, const uint64_t* hashes, uint64_t m,
                                  uint64_t* out, uint16_t* pos16, uint16_t* boffs, cudaStream_t s) {
@@ -1149,8 +820,14 @@ cudaError_t chunk_partition_bits(const DeviceInfo& di, const BucketMap& bm, cons
       chunk_scatter_kernel<BITS, kTop>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(ChunkSmem)));
   if (attr != cudaSuccess) return attr;
   const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
-  const uint64_t grid = nchunks < static_cast<uint64_t>(di.sms) * kPartMinBlocks ? nchunks
-                                                                                 : static_cast<uint64_t>(di.sms) * kPartMinBlocks;
+  // SBBF_PART_PER_SM (A/B only): partition CTAs per SM
+  static const uint64_t per_sm = [] {
+    const char* e = getenv("SBBF_PART_PER_SM");
+    const int v = e ? atoi(e) : 0;
+    return static_cast<uint64_t>(v > 0 ? v : kPartMinBlocks);
+  }();
+  const uint64_t grid = nchunks < static_cast<uint64_t>(di.sms) * per_sm ? nchunks
+                                                                         : static_cast<uint64_t>(di.sms) * per_sm;
   note_launch();
   chunk_scatter_kernel<BITS, kTop><<<static_cast<unsigned>(grid), kPartThreads, sizeof(ChunkSmem), s>>>(
       hashes, m, bm, out, pos16, boffs);
@@ -1178,79 +855,6 @@ cudaError_t chunk_partition(const DeviceInfo& di, const Geom& g, uint32_t S, con
   }
 }
 
-// SBBF_SWEEP=0 selects the previous segment_kernel + unpermute pair (A/B only).
-bool sweep_enabled() {
-  static const bool on = [] {
-    const char* v = getenv("SBBF_SWEEP");
-    return !(v && v[0] == '0');
-  }();
-  return on;
-}
-
-// SBBF_SWEEP_PREFETCH=0 disables the next-slice L2 prefetch (A/B only).
-int sweep_prefetch() {
-  static const int on = [] {
-    const char* v = getenv("SBBF_SWEEP_PREFETCH");
-    return (v && v[0] == '0') ? 0 : 1;
-  }();
-  return on;
-}
-
-int sweep_slack() {
-  static const int v = [] {
-    const char* e = getenv("SBBF_SWEEP_SLACK");
-    return e ? atoi(e) : kSweepSlack;
-  }();
-  return v;
-}
-
-// One cooperative launch of the persistent sweep over chunks [0, nchunks).
-// `done` is S counters of scratch (zeroed here). If the cooperative launch
-// is refused (another client holds SMs, MPS limits), the same kernel runs
-// as an ordinary launch without the lockstep wait.
-template <bool kInsert>
-cudaError_t launch_sweep(const DeviceInfo& di, SweepArgs a, cudaStream_t s) {
-  constexpr int kU = kInsert ? 4 : 2;
-  auto kern = sweep_kernel<kInsert, kU>;
-  static const int occ = [&] {
-    int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kSweepThreads, 0) != cudaSuccess || b < 1) b = 1;
-    return b;
-  }();
-  uint64_t grid = static_cast<uint64_t>(di.sms) * occ;
-  if (grid > a.nchunks) grid = a.nchunks;
-  const uint64_t min_grid = (a.nchunks + kSweepMaxChunks - 1) / kSweepMaxChunks;
-  if (grid < min_grid) grid = min_grid;
-  if (grid == 0) return cudaSuccess;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(kSweepThreads);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cudaError_t e = cudaSuccess;
-  const bool lockstep = a.done != nullptr && grid <= static_cast<uint64_t>(di.sms) * occ;
-  if (lockstep) {
-    e = cudaMemsetAsync(a.done, 0, a.S * sizeof(unsigned), s);
-    if (e != cudaSuccess) return e;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    note_launch();
-    e = cudaLaunchKernelEx(&cfg, kern, a);
-    if (e == cudaSuccess) return e;
-    if (getenv("SBBF_SWEEP_DEBUG"))
-      fprintf(stderr, "sbbf sweep: cooperative launch of %llu CTAs refused: %s\n",
-              static_cast<unsigned long long>(grid), cudaGetErrorString(e));
-    cudaGetLastError();  // cooperative launch refused: run without the lockstep
-  }
-  a.done = nullptr;
-  cfg.attrs = nullptr;
-  cfg.numAttrs = 0;
-  note_launch();
-  return cudaLaunchKernelEx(&cfg, kern, a);
-}
-
 template <bool kInsert>
 cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* keys, const uint16_t* boffs, uint32_t S,
                             uint64_t m, uint8_t* ans, cudaStream_t s) {
@@ -1265,7 +869,22 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
   if constexpr (kInsert)
     segment_kernel<true, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta);
   else
-    segment_kernel<false, 1, 8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta);
+  {
+    // SBBF_SEG_SMEM_KB (A/B only): unused dynamic shared memory per lookup
+    // segment CTA, capping its occupancy so a concurrent partition (the
+    // pipelined lookup's side stream) finds room on every SM
+    static const int seg_smem = [] {
+      const char* e = getenv("SBBF_SEG_SMEM_KB");
+      return e ? atoi(e) * 1024 : 0;
+    }();
+    if (seg_smem > 48 * 1024) {
+      static const cudaError_t a = cudaFuncSetAttribute(segment_kernel<false, 1, 8>,
+                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, seg_smem);
+      (void)a;
+    }
+    segment_kernel<false, 1, 8><<<S * groups, kSegThreads, seg_smem, s>>>(blocks, g, keys, boffs, m, groups, ans,
+                                                                           per_cta);
+  }
   return cudaGetLastError();
 }
 
@@ -1274,27 +893,158 @@ struct Scratch {
   uint16_t* boffs = nullptr;
   uint16_t* pos16 = nullptr;
   uint8_t* ans = nullptr;
-  unsigned* done = nullptr;  // sweep lockstep counters, one per bucket
+  bool pooled = false;  // from the stream-ordered pool (freed per call) rather than the handle's arena
 };
 
-cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, bool lookup, cudaStream_t s) {
-  retain_pool();
+uint64_t align256(uint64_t b) { return (b + 255) & ~uint64_t{255}; }
+
+uint64_t scratch_bytes(uint64_t cap, bool lookup) {
   const uint64_t nchunks = (cap + kPartChunk - 1) / kPartChunk;
+  return align256(cap * sizeof(uint64_t)) + align256(nchunks * kBoffStride * sizeof(uint16_t)) +
+         (lookup ? align256(cap * sizeof(uint16_t)) + align256(cap) : 0);
+}
+
+}  // namespace
+
+// Per-handle blocked-path context: a scratch arena that persists across calls
+// (one cudaMalloc, grown on demand; the stream-ordered pool's trimming and
+// growth inside timed steps is what produced the occasional 10x config-4
+// step), ordered across callers' streams by an `idle` event, plus the side
+// stream and events of the pipelined lookup (per handle, so lookups on
+// unrelated filters share no stream). Calls being captured into a CUDA graph
+// take their scratch from the stream-ordered pool instead (graph-safe) and
+// run unpipelined.
+struct BlockedCtx {
+  std::mutex mu;
+  char* base = nullptr;
+  uint64_t cap = 0;
+  cudaEvent_t idle = nullptr;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_in = nullptr, ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+  bool events_ok = false;
+  cudaError_t init() {  // under mu
+    if (events_ok) return cudaSuccess;
+    int least = 0, greatest = 0;
+    cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (e == cudaSuccess && !side) e = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, greatest);
+    if (e == cudaSuccess && !idle) e = cudaEventCreateWithFlags(&idle, cudaEventDisableTiming);
+    if (e == cudaSuccess && !ev_in) e = cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming);
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+      if (!ready[k]) e = cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming);
+      if (e == cudaSuccess && !freed[k]) e = cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming);
+    }
+    events_ok = e == cudaSuccess;
+    return e;
+  }
+  ~BlockedCtx() {
+    if (idle) cudaEventSynchronize(idle);
+    if (side) cudaStreamSynchronize(side);
+    cudaFree(base);
+    if (side) cudaStreamDestroy(side);
+    for (cudaEvent_t ev : {idle, ev_in, ready[0], ready[1], freed[0], freed[1]})
+      if (ev) cudaEventDestroy(ev);
+  }
+};
+
+BlockedCtx* blocked_ctx_create() { return new (std::nothrow) BlockedCtx; }
+void blocked_ctx_destroy(BlockedCtx* c) { delete c; }
+int blocked_ctx_release(BlockedCtx* c) {
+  if (!c) return 0;
+  std::lock_guard<std::mutex> lock(c->mu);
+  if (c->idle) cudaEventSynchronize(c->idle);
+  cudaFree(c->base);
+  c->base = nullptr;
+  c->cap = 0;
+  return 0;
+}
+
+namespace {
+
+// One blocked call's hold on the handle's context: the lock (one call at a
+// time enqueues), the arena sized for `need` bytes and ordered behind the
+// previous call's use (its `idle` event), released by recording `idle` on s.
+class CallScope {
+ public:
+  CallScope(BlockedCtx* ctx, cudaStream_t s, uint64_t need) : ctx_(ctx), s_(s) {
+    if (!ctx_) return;
+    lock_ = std::unique_lock<std::mutex>(ctx_->mu);
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      capturing_ = true;
+      return;
+    }
+    err_ = ctx_->init();
+    if (err_ != cudaSuccess) return;
+    if (ctx_->cap < need) {
+      if (ctx_->base) {
+        cudaEventSynchronize(ctx_->idle);
+        cudaFree(ctx_->base);
+        ctx_->base = nullptr;
+        ctx_->cap = 0;
+      }
+      err_ = cudaMalloc(reinterpret_cast<void**>(&ctx_->base), need);
+      if (err_ != cudaSuccess) {
+        ctx_->base = nullptr;
+        return;
+      }
+      ctx_->cap = need;
+    }
+    err_ = cudaStreamWaitEvent(s, ctx_->idle, 0);  // the previous caller is done with the arena
+    arena_ = err_ == cudaSuccess;
+  }
+  ~CallScope() {
+    if (arena_) cudaEventRecord(ctx_->idle, s_);
+  }
+  bool arena() const { return arena_; }
+  bool capturing() const { return capturing_; }
+  cudaError_t error() const { return err_; }
+  BlockedCtx* ctx() const { return ctx_; }
+  // carve `bytes` of the arena (arena mode) at the running offset
+  char* take(uint64_t bytes) {
+    char* p = ctx_->base + used_;
+    used_ += align256(bytes);
+    return p;
+  }
+
+ private:
+  BlockedCtx* ctx_;
+  cudaStream_t s_;
+  std::unique_lock<std::mutex> lock_;
+  bool arena_ = false, capturing_ = false;
+  cudaError_t err_ = cudaSuccess;
+  uint64_t used_ = 0;
+};
+
+cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, bool lookup, cudaStream_t s, CallScope* scope = nullptr) {
+  const uint64_t nchunks = (cap + kPartChunk - 1) / kPartChunk;
+  if (scope && scope->arena()) {
+    sc.keys = reinterpret_cast<uint64_t*>(scope->take(cap * sizeof(uint64_t)));
+    sc.boffs = reinterpret_cast<uint16_t*>(scope->take(nchunks * kBoffStride * sizeof(uint16_t)));
+    if (lookup) {
+      sc.pos16 = reinterpret_cast<uint16_t*>(scope->take(cap * sizeof(uint16_t)));
+      sc.ans = reinterpret_cast<uint8_t*>(scope->take(cap));
+    }
+    sc.pooled = false;
+    return cudaSuccess;
+  }
+  retain_pool();
+  sc.pooled = true;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&sc.keys), cap * sizeof(uint64_t), s);
   if (e == cudaSuccess)
     e = cudaMallocAsync(reinterpret_cast<void**>(&sc.boffs), nchunks * kBoffStride * sizeof(uint16_t), s);
   if (lookup && e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.pos16), cap * sizeof(uint16_t), s);
   if (lookup && e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.ans), cap, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.done), kChunkBuckets * sizeof(unsigned), s);
   return e;
 }
 
 void free_scratch(Scratch& sc, cudaStream_t s) {
-  if (sc.keys) cudaFreeAsync(sc.keys, s);
-  if (sc.boffs) cudaFreeAsync(sc.boffs, s);
-  if (sc.pos16) cudaFreeAsync(sc.pos16, s);
-  if (sc.ans) cudaFreeAsync(sc.ans, s);
-  if (sc.done) cudaFreeAsync(sc.done, s);
+  if (sc.pooled) {
+    if (sc.keys) cudaFreeAsync(sc.keys, s);
+    if (sc.boffs) cudaFreeAsync(sc.boffs, s);
+    if (sc.pos16) cudaFreeAsync(sc.pos16, s);
+    if (sc.ans) cudaFreeAsync(sc.ans, s);
+  }
   sc = Scratch{};
 }
 
@@ -1333,11 +1083,6 @@ bool pipeline_enabled() {
 cudaError_t insert_chunk(const DeviceInfo& di, uint32_t* blocks, const Geom& g, uint32_t parts, const uint64_t* keys,
                          uint64_t m, Scratch& sc, cudaStream_t s) {
   cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, nullptr, sc.boffs, s);
-  if (e == cudaSuccess && sweep_enabled()) {
-    const SweepArgs a{blocks, g, sc.keys, sc.boffs, (m + kPartChunk - 1) / kPartChunk, parts,
-                      nullptr, nullptr, nullptr, false, sc.done, sweep_prefetch(), sweep_slack()};
-    return launch_sweep<true>(di, a, s);
-  }
   if (e == cudaSuccess) e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, parts, m, nullptr, s);
   return e;
 }
@@ -1346,13 +1091,7 @@ cudaError_t find_chunk(const DeviceInfo& di, const uint32_t* blocks, const Geom&
                        const uint64_t* keys, uint64_t m, Scratch& sc, void* dst, bool bits, cudaStream_t s) {
   // 1. every chunk bucket-major in its own region (+ positions, offsets)
   cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, sc.pos16, sc.boffs, s);
-  // 2. probe slice by slice (L2-resident), one answer byte per routed slot,
-  // 3. each CTA returns its chunks to source order (persistent sweep)
-  if (e == cudaSuccess && sweep_enabled()) {
-    const SweepArgs a{const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, (m + kPartChunk - 1) / kPartChunk,
-                      parts, sc.ans, sc.pos16, dst, bits, sc.done, sweep_prefetch(), sweep_slack()};
-    return launch_sweep<false>(di, a, s);
-  }
+  // 2. probe slice by slice (L2-resident), one answer byte per routed slot
   if (e == cudaSuccess)
     e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, parts, m, sc.ans, s);
   // 3. back to source order, straight into the caller's bitmap / bytes
@@ -1401,7 +1140,9 @@ cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g
   Scratch sc;
   TwoLevel tl;
   const bool two = plan.super_parts > 1;
-  cudaError_t e = alloc_scratch(sc, cap, false, s);
+  CallScope scope(plan.ctx, s, scratch_bytes(cap, false));
+  if (scope.error() != cudaSuccess) return scope.error();
+  cudaError_t e = alloc_scratch(sc, cap, false, s, &scope);
   if (e == cudaSuccess && two) e = cudaMallocAsync(reinterpret_cast<void**>(&tl.keys), cap * sizeof(uint64_t), s);
   if (e == cudaSuccess && two)
     e = cudaMallocAsync(reinterpret_cast<void**>(&tl.counts), 2 * plan.super_parts * sizeof(uint64_t), s);
@@ -1426,31 +1167,6 @@ cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g
 
 namespace {
 
-struct PipeCtx {
-  std::mutex mu;
-  bool ready_ok = false;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_in = nullptr, ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
-  cudaError_t init() {  // under mu
-    if (ready_ok) return cudaSuccess;
-    int least = 0, greatest = 0;
-    cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    if (e == cudaSuccess && !side) e = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, greatest);
-    if (e == cudaSuccess && !ev_in) e = cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming);
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
-      if (!ready[k]) e = cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming);
-      if (e == cudaSuccess && !freed[k]) e = cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming);
-    }
-    ready_ok = e == cudaSuccess;
-    return e;
-  }
-};
-
-PipeCtx& pipe_ctx(int device) {  // per device ordinal, never destroyed (process lifetime)
-  static PipeCtx ctx[64];
-  return ctx[device & 63];
-}
-
 // Batches of several rounds (single-level plans): round c+1's chunk_scatter
 // runs on a high-priority side stream while round c is probed and
 // un-permuted on the caller's stream, with double-buffered scratch. The
@@ -1459,18 +1175,18 @@ PipeCtx& pipe_ctx(int device) {  // per device ordinal, never destroyed (process
 // graph capture safe).
 cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks, const Geom& g,
                                    const BlockedPlan& plan, const uint64_t* hashes, uint64_t n, void* out,
-                                   bool bits, cudaStream_t s) {
+                                   bool bits, cudaStream_t s, CallScope* scope) {
   const uint64_t cap = kBlockedChunk;
   Scratch sc[2];
-  // one side stream and event set per device, created once (creating them per
-  // call put 7-13 ms outliers into config-4 steps); the lock serialises the
-  // enqueue of concurrent callers, the device work stays stream-ordered
-  PipeCtx& ctx = pipe_ctx(di.device);
-  std::lock_guard<std::mutex> lock(ctx.mu);
-  cudaError_t e = ctx.init();
+  // the handle's side stream and events (created once: creating them per call
+  // put 7-13 ms outliers into config-4 steps) and its scratch arena; the
+  // scope's lock serialises the enqueue of concurrent callers
+  CallScope& sco = *scope;
+  BlockedCtx& ctx = *sco.ctx();
+  cudaError_t e = cudaSuccess;
   cudaStream_t side = ctx.side;
   cudaEvent_t ev_in = ctx.ev_in, *ready = ctx.ready, *freed = ctx.freed;
-  for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = alloc_scratch(sc[k], cap, true, s);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = alloc_scratch(sc[k], cap, true, s, &sco);
   // the side stream starts behind everything already queued on s (the
   // caller's hashes and the scratch allocations)
   if (e == cudaSuccess) e = cudaEventRecord(ev_in, s);
@@ -1510,13 +1226,16 @@ cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks,
 cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
                          const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  if (plan.super_parts == 1 && n > kBlockedChunk && pipeline_enabled() && !sweep_enabled())
-    return blocked_find_pipelined(di, blocks, g, plan, hashes, n, out, bits, s);
   const uint64_t cap = n < kBlockedChunk ? n : kBlockedChunk;  // a multiple of 32 unless n is the whole batch
+  const bool pipelined = plan.super_parts == 1 && n > kBlockedChunk && pipeline_enabled();
+  CallScope scope(plan.ctx, s, scratch_bytes(cap, true) * (pipelined ? 2 : 1));
+  if (scope.error() != cudaSuccess) return scope.error();
+  // pipelining needs the handle's side stream: not while a graph is captured
+  if (pipelined && scope.arena()) return blocked_find_pipelined(di, blocks, g, plan, hashes, n, out, bits, s, &scope);
   Scratch sc;
   TwoLevel tl;
   const bool two = plan.super_parts > 1;
-  cudaError_t e = alloc_scratch(sc, cap, true, s);
+  cudaError_t e = alloc_scratch(sc, cap, true, s, &scope);
   if (e == cudaSuccess && two) e = cudaMallocAsync(reinterpret_cast<void**>(&tl.keys), cap * sizeof(uint64_t), s);
   if (e == cudaSuccess && two) e = cudaMallocAsync(reinterpret_cast<void**>(&tl.pos), cap * sizeof(uint32_t), s);
   if (e == cudaSuccess && two) e = cudaMallocAsync(reinterpret_cast<void**>(&tl.ans), cap, s);
@@ -1572,17 +1291,14 @@ cudaError_t blocked_insert_regions(const DeviceInfo& di, uint32_t* blocks, const
   if (plan.super_parts > 1 || C * kPartChunk > kBlockedChunk) return cudaErrorNotSupported;
   if (C == 0) return cudaSuccess;
   Scratch sc;
-  cudaError_t e = alloc_scratch(sc, C * kPartChunk, false, s);
+  CallScope scope(plan.ctx, s, scratch_bytes(C * kPartChunk, false));
+  if (scope.error() != cudaSuccess) return scope.error();
+  cudaError_t e = alloc_scratch(sc, C * kPartChunk, false, s, &scope);
   for (uint32_t r = 0; e == cudaSuccess && r < nr; ++r)
     if (counts[r])
       e = chunk_partition(di, g, plan.parts, keys[r], counts[r], sc.keys + off[r] * kPartChunk, nullptr,
                           sc.boffs + off[r] * kBoffStride, s);
-  if (e == cudaSuccess && sweep_enabled()) {
-    const SweepArgs a{blocks, g, sc.keys, sc.boffs, C, plan.parts, nullptr, nullptr, nullptr, false, sc.done, sweep_prefetch(), sweep_slack()};
-    e = launch_sweep<true>(di, a, s);
-  } else if (e == cudaSuccess) {
-    e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, plan.parts, C * kPartChunk, nullptr, s);
-  }
+  if (e == cudaSuccess) e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, plan.parts, C * kPartChunk, nullptr, s);
   free_scratch(sc, s);
   return e;
 }
@@ -1596,26 +1312,22 @@ cudaError_t blocked_find_regions(const DeviceInfo& di, const uint32_t* blocks, c
   if (C == 0) return cudaSuccess;
   Scratch sc;
   uint8_t* bytes = nullptr;  // answers in the chunk layout: region r's at off[r] * kPartChunk
-  cudaError_t e = alloc_scratch(sc, C * kPartChunk, true, s);
+  CallScope scope(plan.ctx, s, scratch_bytes(C * kPartChunk, true));
+  if (scope.error() != cudaSuccess) return scope.error();
+  cudaError_t e = alloc_scratch(sc, C * kPartChunk, true, s, &scope);
   if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&bytes), C * kPartChunk, s);
   for (uint32_t r = 0; e == cudaSuccess && r < nr; ++r)
     if (counts[r])
       e = chunk_partition(di, g, plan.parts, keys[r], counts[r], sc.keys + off[r] * kPartChunk,
                           sc.pos16 + off[r] * kPartChunk, sc.boffs + off[r] * kBoffStride, s);
-  if (e == cudaSuccess && sweep_enabled()) {
-    const SweepArgs a{const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, C, plan.parts, sc.ans, sc.pos16, bytes,
-                      false, sc.done, sweep_prefetch(), sweep_slack()};
-    e = launch_sweep<false>(di, a, s);
-  } else {
-    if (e == cudaSuccess)
-      e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, plan.parts, C * kPartChunk,
-                                 sc.ans, s);
-    if (e == cudaSuccess) {
-      note_launch();
-      unpermute_kernel<<<static_cast<unsigned>(C), kUnpermThreads, 0, s>>>(sc.ans, sc.pos16, C * kPartChunk, bytes,
-                                                                           false, sc.boffs);
-      e = cudaGetLastError();
-    }
+  if (e == cudaSuccess)
+    e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, plan.parts, C * kPartChunk,
+                               sc.ans, s);
+  if (e == cudaSuccess) {
+    note_launch();
+    unpermute_kernel<<<static_cast<unsigned>(C), kUnpermThreads, 0, s>>>(sc.ans, sc.pos16, C * kPartChunk, bytes,
+                                                                         false, sc.boffs);
+    e = cudaGetLastError();
   }
   for (uint32_t r = 0; e == cudaSuccess && r < nr; ++r)
     if (counts[r])

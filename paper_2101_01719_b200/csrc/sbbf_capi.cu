@@ -200,6 +200,7 @@ int ensure_plan(sbbf_gpu* f) {
   }
   f->plan.parts = static_cast<uint32_t>(parts);
   f->plan.d_bounds = f->d_plan_bounds;
+  f->plan.ctx = sbbf::blocked_ctx_create();  // scratch arena + side stream (null: pool scratch)
   return SBBF_OK;
 }
 
@@ -391,6 +392,7 @@ int sbbf_gpu_destroy(sbbf_gpu_t* f) {
     if (f->d_blocks) cudaDeviceSynchronize();
     cudaFree(f->d_blocks);
     if (f->h_one) cudaFreeHost(f->h_one);
+    sbbf::blocked_ctx_destroy(f->plan.ctx);
     cudaFree(f->d_plan_bounds);
     cudaFree(f->d_super_bounds);
     for (int i = 0; i < kHostStreams; ++i) {
@@ -609,6 +611,14 @@ int sbbf_gpu_set_l2_fetch_granularity(int device, int bytes, int* old) {
   if (e == cudaSuccess) e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(bytes));
   if (e != cudaSuccess) return cuda_fail(e, "cudaLimitMaxL2FetchGranularity");
   if (old) *old = static_cast<int>(prev);
+  return SBBF_OK;
+}
+
+int sbbf_gpu_release_scratch(sbbf_gpu_t* f) {
+  if (!f) return fail(SBBF_EINVAL, "null filter");
+  DeviceGuard g(f->di.device);
+  std::lock_guard<std::mutex> lock(f->plan_mu);
+  sbbf::blocked_ctx_release(f->plan.ctx);
   return SBBF_OK;
 }
 

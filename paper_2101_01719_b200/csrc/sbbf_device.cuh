@@ -246,6 +246,12 @@ __device__ __forceinline__ void st_stream_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.global.L1::no_allocate.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Output words that are not re-read soon (range-split bitmaps): evict-first
+// in L2, so a pass's bitmap does not push the filter range it probes out of L2.
+__device__ __forceinline__ void st_stream_u32_ef(uint32_t* p, uint32_t v, uint64_t policy) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(policy) : "memory");
+}
+
 __device__ __forceinline__ void st_stream_u8(uint8_t* p, uint32_t v) {
   asm volatile("st.global.L1::no_allocate.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

@@ -80,7 +80,12 @@ cudaError_t launch_insert_ordered(const DeviceInfo& di, uint32_t* blocks, const 
                                   const uint64_t* hashes, uint64_t n, bool test, cudaStream_t s);
 
 // L2-blocked paths for filters larger than L2 (sbbf_blocked.cu).
+struct BlockedCtx;  // per-handle scratch arena + side stream (sbbf_blocked.cu)
+BlockedCtx* blocked_ctx_create();
+void blocked_ctx_destroy(BlockedCtx* c);
+int blocked_ctx_release(BlockedCtx* c);  // frees the arena (waits for its last use)
 struct BlockedPlan {
+  BlockedCtx* ctx = nullptr;      // null: per-call pool scratch
   uint32_t parts = 0;             // filter slices (per super-slice when super_parts > 1)
   const uint64_t* d_bounds = nullptr;  // parts entries, global block ids
   // Filters beyond 64 slices: super_parts exact block ranges, each blocked on

@@ -387,8 +387,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
       const uint64_t nwords = (n + 31) >> 5;
       const uint64_t widx = (base >> 5) + lane;
       if (lane < U && widx < nwords) {
-        if (!kSplit || first) dev::st_stream_u32(static_cast<uint32_t*>(out) + widx, mine);
-        else if (mine) atomicOr(static_cast<uint32_t*>(out) + widx, mine);
+        // range-split passes: the bitmap stays evict-first in L2 (it would
+        // otherwise push the probed half of the filter out between passes)
+        if (!kSplit) dev::st_stream_u32(static_cast<uint32_t*>(out) + widx, mine);
+        else if (first) dev::st_stream_u32_ef(static_cast<uint32_t*>(out) + widx, mine, pol);
+        else if (mine) dev::red_or(static_cast<uint32_t*>(out) + widx, mine, pol);
       }
     }
   }
@@ -462,8 +465,9 @@ __global__ void __launch_bounds__(kThreads, 3)
       const uint32_t word = cbits[w][lane];
       cbits[w][lane] = 0;
       if (widx < nwords) {
-        if (first) dev::st_stream_u32(out + widx, word);
-        else if (word) atomicOr(out + widx, word);
+        // evict-first in L2: the bitmap must not displace the probed half
+        if (first) dev::st_stream_u32_ef(out + widx, word, pol);
+        else if (word) dev::red_or(out + widx, word, pol);
       }
     }
     __syncwarp();

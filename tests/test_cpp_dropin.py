@@ -61,7 +61,9 @@ def test_reference_acceptance_on_gpu(cuda):
     reloads and benchmarks (run_bench, run_fpp_sim, sbbf_fpp_mc) is an HBM
     filter behind the C ABI. Criteria 1, 2 and 9 are the drop-in contract
     (no false negatives, bit-exact vectors and path identity, one block and
-    eight lane hashes per op)."""
+    eight lane hashes per op). Criterion 3's Monte-Carlo is bound to the GPU
+    Monte-Carlo oracle (tests/cpp/dropin/fpp_mc_gpu.cpp): the reference's
+    version issues ~1.5e8 single-key probes."""
     if not os.path.exists(ACC):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=False, capture_output=True)
     if not os.path.exists(ACC):
