@@ -657,6 +657,15 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
 constexpr int kSegThreads = 256;
 constexpr int kSegWarps = kSegThreads / 32;
 constexpr uint32_t kSegChunksPerCta = 64;
+// chunks per work item of the persistent segment grid (SBBF_SEG_ITEM_CHUNKS: A/B only)
+uint32_t seg_items_chunks() {
+  static const uint32_t v = [] {
+    const char* e = getenv("SBBF_SEG_ITEM_CHUNKS");
+    const int x = e ? atoi(e) : 0;
+    return x > 0 ? static_cast<uint32_t>(x) : 16u;
+  }();
+  return v;
+}
 // SBBF_SEG_CHUNKS overrides the chunks per segment CTA (A/B only)
 uint32_t seg_chunks_per_cta() {
   static const uint32_t v = [] {
@@ -667,16 +676,13 @@ uint32_t seg_chunks_per_cta() {
   return v;
 }
 
-template <bool kInsert, int kSegQ, int kMinB = (kSegQ > 4 ? 2 : 3)>
-__global__ void __launch_bounds__(kSegThreads, kMinB)
-    segment_kernel(uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
-                   const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint8_t* __restrict__ ans,
-                   uint32_t per_cta) {
+// One work item: bucket b over chunks [c_begin, c_end).
+template <bool kInsert, int kSegQ>
+__device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, const Geom& g,
+                                             const uint64_t* __restrict__ keys, const uint16_t* __restrict__ boffs,
+                                             uint64_t m, uint8_t* __restrict__ ans, uint32_t b, uint64_t c_begin,
+                                             uint64_t c_end) {
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t b = blockIdx.x / groups, grp = blockIdx.x % groups;
-  const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
-  const uint64_t c_begin = static_cast<uint64_t>(grp) * per_cta;
-  const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
   const uint64_t pol = dev::policy_evict_first();
   const uint64_t keep = dev::policy_evict_last();
   for (uint64_t c = c_begin + warp * kSegQ; c < c_end; c += kSegWarps * kSegQ) {
@@ -752,6 +758,40 @@ __global__ void __launch_bounds__(kSegThreads, kMinB)
           if (j < len[q]) ans[seg[q] + j] = (((owned >> q) & 1u) && dev::block_contains(bl[q], h[q])) ? 1 : 0;
       }
     }
+  }
+}
+
+// Items are (bucket, group of per_cta chunks) in bucket-major order. With
+// `work` null the grid has one CTA per item (blockIdx order); otherwise the
+// grid is the resident CTAs and each takes the next item from a global
+// counter, so the items in flight — and the filter slices live in L2 — stay
+// within about one resident wave of small items whatever the CTA duration
+// spread (a one-shot grid of 64-chunk items keeps 2-3 slices live and reads
+// each slice ~3x from HBM: profiles/r2_*).
+template <bool kInsert, int kSegQ, int kMinB = (kSegQ > 4 ? 2 : 3)>
+__global__ void __launch_bounds__(kSegThreads, kMinB)
+    segment_kernel(uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
+                   const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint8_t* __restrict__ ans,
+                   uint32_t per_cta, unsigned* __restrict__ work = nullptr, uint32_t items = 0) {
+  const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
+  if (!work) {
+    const uint32_t b = blockIdx.x / groups, grp = blockIdx.x % groups;
+    const uint64_t c_begin = static_cast<uint64_t>(grp) * per_cta;
+    const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
+    segment_item<kInsert, kSegQ>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
+    return;
+  }
+  __shared__ uint32_t next;
+  for (;;) {
+    if (threadIdx.x == 0) next = atomicAdd(work, 1u);
+    __syncthreads();
+    const uint32_t item = next;
+    __syncthreads();
+    if (item >= items) return;
+    const uint32_t b = item / groups, grp = item % groups;
+    const uint64_t c_begin = static_cast<uint64_t>(grp) * per_cta;
+    const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
+    segment_item<kInsert, kSegQ>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
   }
 }
 
@@ -855,12 +895,45 @@ cudaError_t chunk_partition(const DeviceInfo& di, const Geom& g, uint32_t S, con
   }
 }
 
+// SBBF_SEG_PERSIST=0 selects the one-shot grid (A/B only).
+bool seg_persist() {
+  static const bool on = [] {
+    const char* v = getenv("SBBF_SEG_PERSIST");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 template <bool kInsert>
 cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* keys, const uint16_t* boffs, uint32_t S,
-                            uint64_t m, uint8_t* ans, cudaStream_t s) {
+                            uint64_t m, uint8_t* ans, cudaStream_t s, unsigned* work = nullptr,
+                            const DeviceInfo* di = nullptr) {
   const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
-  const uint32_t per_cta = seg_chunks_per_cta();
+  const bool persist = work && di && seg_persist();
+  const uint32_t per_cta = persist ? seg_items_chunks() : seg_chunks_per_cta();
   const uint32_t groups = static_cast<uint32_t>((nchunks + per_cta - 1) / per_cta);
+  if (persist) {
+    const uint32_t items = S * groups;
+    auto kern = kInsert ? segment_kernel<true, 4> : segment_kernel<false, 1, 8>;
+    static const int occ_i = [] {
+      int b = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, segment_kernel<true, 4>, kSegThreads, 0);
+      return b > 0 ? b : 1;
+    }();
+    static const int occ_l = [] {
+      int b = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, segment_kernel<false, 1, 8>, kSegThreads, 0);
+      return b > 0 ? b : 1;
+    }();
+    uint64_t grid = static_cast<uint64_t>(di->sms) * (kInsert ? occ_i : occ_l);
+    if (grid > items) grid = items;
+    cudaError_t e = cudaMemsetAsync(work, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    note_launch();
+    kern<<<static_cast<unsigned>(grid), kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, work,
+                                                               items);
+    return cudaGetLastError();
+  }
   note_launch();
   // Segments per warp step / min CTAs per SM, measured on config 4
   // (profiles/r1_blocked_partition.md): inserts 4 / 3 (4 lanes per key;
@@ -893,6 +966,7 @@ struct Scratch {
   uint16_t* boffs = nullptr;
   uint16_t* pos16 = nullptr;
   uint8_t* ans = nullptr;
+  unsigned* work = nullptr;  // persistent segment grid's work counter
   bool pooled = false;  // from the stream-ordered pool (freed per call) rather than the handle's arena
 };
 
@@ -901,7 +975,7 @@ uint64_t align256(uint64_t b) { return (b + 255) & ~uint64_t{255}; }
 uint64_t scratch_bytes(uint64_t cap, bool lookup) {
   const uint64_t nchunks = (cap + kPartChunk - 1) / kPartChunk;
   return align256(cap * sizeof(uint64_t)) + align256(nchunks * kBoffStride * sizeof(uint16_t)) +
-         (lookup ? align256(cap * sizeof(uint16_t)) + align256(cap) : 0);
+         (lookup ? align256(cap * sizeof(uint16_t)) + align256(cap) : 0) + 256;
 }
 
 }  // namespace
@@ -1025,6 +1099,7 @@ cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, bool lookup, cudaStream_t s
       sc.pos16 = reinterpret_cast<uint16_t*>(scope->take(cap * sizeof(uint16_t)));
       sc.ans = reinterpret_cast<uint8_t*>(scope->take(cap));
     }
+    sc.work = reinterpret_cast<unsigned*>(scope->take(sizeof(unsigned)));
     sc.pooled = false;
     return cudaSuccess;
   }
@@ -1035,6 +1110,7 @@ cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, bool lookup, cudaStream_t s
     e = cudaMallocAsync(reinterpret_cast<void**>(&sc.boffs), nchunks * kBoffStride * sizeof(uint16_t), s);
   if (lookup && e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.pos16), cap * sizeof(uint16_t), s);
   if (lookup && e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.ans), cap, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.work), sizeof(unsigned), s);
   return e;
 }
 
@@ -1044,6 +1120,7 @@ void free_scratch(Scratch& sc, cudaStream_t s) {
     if (sc.boffs) cudaFreeAsync(sc.boffs, s);
     if (sc.pos16) cudaFreeAsync(sc.pos16, s);
     if (sc.ans) cudaFreeAsync(sc.ans, s);
+    if (sc.work) cudaFreeAsync(sc.work, s);
   }
   sc = Scratch{};
 }
@@ -1083,7 +1160,7 @@ bool pipeline_enabled() {
 cudaError_t insert_chunk(const DeviceInfo& di, uint32_t* blocks, const Geom& g, uint32_t parts, const uint64_t* keys,
                          uint64_t m, Scratch& sc, cudaStream_t s) {
   cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, nullptr, sc.boffs, s);
-  if (e == cudaSuccess) e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, parts, m, nullptr, s);
+  if (e == cudaSuccess) e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, parts, m, nullptr, s, sc.work, &di);
   return e;
 }
 
@@ -1093,7 +1170,7 @@ cudaError_t find_chunk(const DeviceInfo& di, const uint32_t* blocks, const Geom&
   cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, sc.pos16, sc.boffs, s);
   // 2. probe slice by slice (L2-resident), one answer byte per routed slot
   if (e == cudaSuccess)
-    e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, parts, m, sc.ans, s);
+    e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, parts, m, sc.ans, s, sc.work, &di);
   // 3. back to source order, straight into the caller's bitmap / bytes
   if (e == cudaSuccess) {
     note_launch();
@@ -1204,7 +1281,7 @@ cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks,
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ready[k], 0);
     if (e == cudaSuccess)
       e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc[k].keys, sc[k].boffs, plan.parts, m,
-                                 sc[k].ans, s);
+                                 sc[k].ans, s, sc[k].work, &di);
     if (e == cudaSuccess) {
       note_launch();
       unpermute_kernel<<<static_cast<unsigned>((m + kPartChunk - 1) / kPartChunk), kUnpermThreads, 0, s>>>(
@@ -1298,7 +1375,8 @@ cudaError_t blocked_insert_regions(const DeviceInfo& di, uint32_t* blocks, const
     if (counts[r])
       e = chunk_partition(di, g, plan.parts, keys[r], counts[r], sc.keys + off[r] * kPartChunk, nullptr,
                           sc.boffs + off[r] * kBoffStride, s);
-  if (e == cudaSuccess) e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, plan.parts, C * kPartChunk, nullptr, s);
+  if (e == cudaSuccess)
+    e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, plan.parts, C * kPartChunk, nullptr, s, sc.work, &di);
   free_scratch(sc, s);
   return e;
 }
@@ -1322,7 +1400,7 @@ cudaError_t blocked_find_regions(const DeviceInfo& di, const uint32_t* blocks, c
                           sc.pos16 + off[r] * kPartChunk, sc.boffs + off[r] * kBoffStride, s);
   if (e == cudaSuccess)
     e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, plan.parts, C * kPartChunk,
-                               sc.ans, s);
+                               sc.ans, s, sc.work, &di);
   if (e == cudaSuccess) {
     note_launch();
     unpermute_kernel<<<static_cast<unsigned>(C), kUnpermThreads, 0, s>>>(sc.ans, sc.pos16, C * kPartChunk, bytes,

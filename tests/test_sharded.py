@@ -518,7 +518,8 @@ def test_bench_world2_code_path(cuda):
     assert len(lines) == 1                         # rank 0 alone prints
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["config_id"] == 5 and d["value"] > 0
-    assert "peer-memory windows" in d["config"]["workload"]
+    assert "peer-memory windows" in d["config"]["routing"]
+    assert d["parity"]["how"] and d["parity"]["members"] > 0      # parity of the sampled step is reported
 
 
 def _dist_hooks_worker(rank, world, port, total, q):
