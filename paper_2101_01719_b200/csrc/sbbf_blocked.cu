@@ -896,12 +896,26 @@ cudaError_t chunk_partition(const DeviceInfo& di, const Geom& g, uint32_t S, con
 }
 
 // SBBF_SEG_PERSIST=0 selects the one-shot grid (A/B only).
+// Measured neutral on config 4 (profiles/r2p_*: the filter is read 1.3x
+// instead of 3x, but the sweep is latency-bound, not DRAM-bound), so the
+// one-shot grid stays the default; SBBF_SEG_PERSIST=1 selects it.
 bool seg_persist() {
   static const bool on = [] {
     const char* v = getenv("SBBF_SEG_PERSIST");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
   }();
   return on;
+}
+
+// SBBF_SEG_INS_Q (A/B only): segments per warp step of the insert segment
+// kernel (2, 4 = default, 8).
+int seg_ins_q() {
+  static const int v = [] {
+    const char* e = getenv("SBBF_SEG_INS_Q");
+    const int x = e ? atoi(e) : 4;
+    return (x == 2 || x == 8) ? x : 4;
+  }();
+  return v;
 }
 
 template <bool kInsert>
@@ -939,9 +953,15 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
   // (profiles/r1_blocked_partition.md): inserts 4 / 3 (4 lanes per key;
   // 1 or 2 segments: same or slower); lookups 1 / 8 — 1.54 ms per 2^28 keys,
   // vs 1.82 (2 segments), 1.89 (4), 2.37 (8): occupancy beats per-lane MLP.
-  if constexpr (kInsert)
-    segment_kernel<true, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta);
-  else
+  if constexpr (kInsert) {
+    const int q = seg_ins_q();
+    if (q == 2)
+      segment_kernel<true, 2, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta);
+    else if (q == 8)
+      segment_kernel<true, 8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta);
+    else
+      segment_kernel<true, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta);
+  } else
   {
     // SBBF_SEG_SMEM_KB (A/B only): unused dynamic shared memory per lookup
     // segment CTA, capping its occupancy so a concurrent partition (the

@@ -404,7 +404,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 // assembles the 8 bitmap words of the 256 keys in shared memory. The first
 // pass stores the words, later passes OR theirs in.
 constexpr int kSplitTile = 256;
-__global__ void __launch_bounds__(kThreads, 3)
+template <int kPU = 4, int kMinSB = 3>
+__global__ void __launch_bounds__(kThreads, kMinSB)
     find_split_kernel(const uint32_t* __restrict__ blocks, uint64_t nb, const uint64_t* __restrict__ hashes,
                       uint64_t n, uint32_t* __restrict__ out, uint32_t psh, uint64_t pid, bool first) {
   __shared__ uint64_t ckey[kThreads / 32][kSplitTile];
@@ -441,17 +442,17 @@ __global__ void __launch_bounds__(kThreads, 3)
       total += __popc(bal);
     }
     __syncwarp();
-    for (uint32_t r0 = 0; r0 < total; r0 += 128) {
-      Block8 b[4];
-      uint64_t hk[4];
+    for (uint32_t r0 = 0; r0 < total; r0 += 32 * kPU) {
+      Block8 b[kPU];
+      uint64_t hk[kPU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kPU; ++u) {
         const uint32_t j = r0 + u * 32 + lane;
         hk[u] = j < total ? ckey[w][j] : 0;
         if (j < total) dev::ld_block_nc(blocks + dev::block_index(hk[u], nb) * 8, b[u]);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kPU; ++u) {
         const uint32_t j = r0 + u * 32 + lane;
         if (j < total && dev::block_contains(b[u], hk[u])) {
           const uint32_t ci = cidx[w][j];
@@ -847,14 +848,21 @@ cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* block
         static const int occ_s = resident_blocks(find_whole_kernel<kUS, true, kMinS, false, true>, kThreads, 0);
         cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kUS, di.sms, occ_s)));
         cudaError_t e = cudaSuccess;
-        static const int occ_c = resident_blocks(find_split_kernel, kThreads, 0);
+        // SBBF_SPLIT_VARIANT (A/B only): 0 = 4 probes/lane at 3 CTAs/SM,
+        // 1 = 2 probes/lane at 4 CTAs/SM, 2 = 2 probes at 5
+        static const int sv = [] {
+          const char* v = getenv("SBBF_SPLIT_VARIANT");
+          return v ? atoi(v) : 0;
+        }();
+        auto ksplit = sv == 1 ? find_split_kernel<2, 4> : sv == 2 ? find_split_kernel<2, 5> : find_split_kernel<4, 3>;
+        const int occ_c = resident_blocks(ksplit, kThreads, 0);
         for (uint64_t p = 0; p < (uint64_t{1} << split_log) && e == cudaSuccess; ++p) {
           const uint32_t psh = static_cast<uint32_t>(64 - split_log);
           const bool first = p == 0;
           if (bits && split_compact()) {
             cudaLaunchConfig_t cc = cfg;
             cc.gridDim = dim3(static_cast<unsigned>(grid_for(n, kSplitTile * (kThreads / 32), di.sms, occ_c)));
-            e = cudaLaunchKernelEx(&cc, find_split_kernel, blocks, g.nb_global, hashes, n,
+            e = cudaLaunchKernelEx(&cc, ksplit, blocks, g.nb_global, hashes, n,
                                    static_cast<uint32_t*>(out), psh, p, first);
           } else {
             e = bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kUS, true, kMinS, false, true>, blocks, g.nb_global,

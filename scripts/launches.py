@@ -23,7 +23,7 @@ for r in rows[1:]:
         pass
     d[r[mi]] = (v, r[ui])
 SC = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-TS = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1, "second": 1e3}
+TS = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1, "ms": 1, "second": 1e3}
 for d in list(L.values())[-last:]:
     t = d["gpu__time_duration.sum"]
     ms = t[0] * TS.get(t[1], 1)

@@ -17,7 +17,7 @@ sys.path.insert(0, ROOT)
 from paper_2101_01719_b200 import workload as W  # noqa: E402
 
 SC = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-TS = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1}
+TS = {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1, "s": 1}
 
 
 def launches(path):
