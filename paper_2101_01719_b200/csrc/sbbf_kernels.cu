@@ -403,8 +403,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 // only those (full warps, up to 4 sector loads in flight per lane), and
 // assembles the 8 bitmap words of the 256 keys in shared memory. The first
 // pass stores the words, later passes OR theirs in.
-constexpr int kSplitTile = 256;
-template <int kPU = 4, int kMinSB = 3>
+template <int kPU = 4, int kMinSB = 3, int kSplitTile = 256>
 __global__ void __launch_bounds__(kThreads, kMinSB)
     find_split_kernel(const uint32_t* __restrict__ blocks, uint64_t nb, const uint64_t* __restrict__ hashes,
                       uint64_t n, uint32_t* __restrict__ out, uint32_t psh, uint64_t pid, bool first) {
@@ -848,20 +847,25 @@ cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* block
         static const int occ_s = resident_blocks(find_whole_kernel<kUS, true, kMinS, false, true>, kThreads, 0);
         cfg.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kUS, di.sms, occ_s)));
         cudaError_t e = cudaSuccess;
-        // SBBF_SPLIT_VARIANT (A/B only): 0 = 4 probes/lane at 3 CTAs/SM,
-        // 1 = 2 probes/lane at 4 CTAs/SM, 2 = 2 probes at 5
+        // Probes in flight per lane x CTAs per SM x keys per warp tile, config 3
+        // (profiles/r2q_*): 2 x 4 x 256 (default) 159.6 Gkeys/s; 4 x 3 x 256
+        // 147.9; 2 x 5 x 256 (spills) 106.6. SBBF_SPLIT_VARIANT selects others
+        // (A/B only): 1 = 4x3x256, 3 = 1x6x128, 4 = 2x5x128, 5 = 2x6x128.
         static const int sv = [] {
           const char* v = getenv("SBBF_SPLIT_VARIANT");
           return v ? atoi(v) : 0;
         }();
-        auto ksplit = sv == 1 ? find_split_kernel<2, 4> : sv == 2 ? find_split_kernel<2, 5> : find_split_kernel<4, 3>;
+        auto ksplit = sv == 0 ? find_split_kernel<2, 4> : sv == 3 ? find_split_kernel<1, 6, 128>
+                      : sv == 4 ? find_split_kernel<2, 5, 128> : sv == 5 ? find_split_kernel<2, 6, 128>
+                                                                 : find_split_kernel<4, 3>;
+        const int tile = (sv == 3 || sv == 4 || sv == 5) ? 128 : 256;
         const int occ_c = resident_blocks(ksplit, kThreads, 0);
         for (uint64_t p = 0; p < (uint64_t{1} << split_log) && e == cudaSuccess; ++p) {
           const uint32_t psh = static_cast<uint32_t>(64 - split_log);
           const bool first = p == 0;
           if (bits && split_compact()) {
             cudaLaunchConfig_t cc = cfg;
-            cc.gridDim = dim3(static_cast<unsigned>(grid_for(n, kSplitTile * (kThreads / 32), di.sms, occ_c)));
+            cc.gridDim = dim3(static_cast<unsigned>(grid_for(n, tile * (kThreads / 32), di.sms, occ_c)));
             e = cudaLaunchKernelEx(&cc, ksplit, blocks, g.nb_global, hashes, n,
                                    static_cast<uint32_t*>(out), psh, p, first);
           } else {
