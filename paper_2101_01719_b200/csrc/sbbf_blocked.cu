@@ -41,7 +41,16 @@
 namespace sbbf {
 namespace {
 
-constexpr uint64_t kBlockedChunk = uint64_t{1} << 28;  // keys per blocked round (~3 GB of scratch for lookups)
+constexpr int kBlockedRoundLog2 = 28;  // keys per blocked round (~3 GB of scratch for lookups)
+// SBBF_BLOCKED_ROUND_LOG2 overrides the round size (A/B only, 24..31).
+uint64_t blocked_round() {
+  static const uint64_t v = [] {
+    const char* e = getenv("SBBF_BLOCKED_ROUND_LOG2");
+    const int x = e ? atoi(e) : 0;
+    return uint64_t{1} << (x >= 24 && x <= 31 ? x : kBlockedRoundLog2);
+  }();
+  return v;
+}
 
 // ---------------------------------------------------------------------------
 // bucket partition
@@ -677,7 +686,7 @@ uint32_t seg_chunks_per_cta() {
 }
 
 // One work item: bucket b over chunks [c_begin, c_end).
-template <bool kInsert, int kSegQ>
+template <bool kInsert, int kSegQ, bool kTest = true>
 __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, const Geom& g,
                                              const uint64_t* __restrict__ keys, const uint16_t* __restrict__ boffs,
                                              uint64_t m, uint8_t* __restrict__ ans, uint32_t b, uint64_t c_begin,
@@ -724,7 +733,7 @@ __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, cons
           const uint32_t low = static_cast<uint32_t>(h[q]);
           ptr[q] = reinterpret_cast<uint64_t*>(blocks + (ok ? blk : 0) * 8) + pair;
           mask[q] = ok ? (static_cast<uint64_t>(dev::lane_bit(low, seed_hi)) << 32) | dev::lane_bit(low, seed_lo) : 0;
-          cur[q] = mask[q] ? dev::ld_pair(ptr[q], keep) : ~0ull;
+          cur[q] = !mask[q] ? ~0ull : kTest ? dev::ld_pair(ptr[q], keep) : 0ull;
         }
 #pragma unroll
         for (int q = 0; q < kSegQ; ++q) hn[q] = j + 8 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 8, pol) : 0;
@@ -768,7 +777,7 @@ __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, cons
 // within about one resident wave of small items whatever the CTA duration
 // spread (a one-shot grid of 64-chunk items keeps 2-3 slices live and reads
 // each slice ~3x from HBM: profiles/r2_*).
-template <bool kInsert, int kSegQ, int kMinB = (kSegQ > 4 ? 2 : 3)>
+template <bool kInsert, int kSegQ, int kMinB = (kSegQ > 4 ? 2 : 3), bool kTest = true>
 __global__ void __launch_bounds__(kSegThreads, kMinB)
     segment_kernel(uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
                    const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint8_t* __restrict__ ans,
@@ -778,7 +787,7 @@ __global__ void __launch_bounds__(kSegThreads, kMinB)
     const uint32_t b = blockIdx.x / groups, grp = blockIdx.x % groups;
     const uint64_t c_begin = static_cast<uint64_t>(grp) * per_cta;
     const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
-    segment_item<kInsert, kSegQ>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
+    segment_item<kInsert, kSegQ, kTest>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
     return;
   }
   __shared__ uint32_t next;
@@ -791,7 +800,7 @@ __global__ void __launch_bounds__(kSegThreads, kMinB)
     const uint32_t b = item / groups, grp = item % groups;
     const uint64_t c_begin = static_cast<uint64_t>(grp) * per_cta;
     const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
-    segment_item<kInsert, kSegQ>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
+    segment_item<kInsert, kSegQ, kTest>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
   }
 }
 
@@ -908,12 +917,13 @@ bool seg_persist() {
 }
 
 // SBBF_SEG_INS_Q (A/B only): segments per warp step of the insert segment
-// kernel (2, 4 = default, 8).
+// kernel (2, 4 = default, 8); 1004 = 4 segments with plain reds (no
+// test-before-set load).
 int seg_ins_q() {
   static const int v = [] {
     const char* e = getenv("SBBF_SEG_INS_Q");
     const int x = e ? atoi(e) : 4;
-    return (x == 2 || x == 8) ? x : 4;
+    return (x == 2 || x == 8 || x == 1004) ? x : 4;
   }();
   return v;
 }
@@ -957,6 +967,9 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
     const int q = seg_ins_q();
     if (q == 2)
       segment_kernel<true, 2, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta);
+    else if (q == 1004)
+      segment_kernel<true, 4, 3, false><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans,
+                                                                           per_cta);
     else if (q == 8)
       segment_kernel<true, 8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta);
     else
@@ -1176,7 +1189,7 @@ bool pipeline_enabled() {
   return on;
 }
 
-// One batch chunk (m <= kBlockedChunk keys) through the single-level path.
+// One batch chunk (m <= blocked_round() keys) through the single-level path.
 cudaError_t insert_chunk(const DeviceInfo& di, uint32_t* blocks, const Geom& g, uint32_t parts, const uint64_t* keys,
                          uint64_t m, Scratch& sc, cudaStream_t s) {
   cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, nullptr, sc.boffs, s);
@@ -1233,7 +1246,7 @@ Geom sub_geom(const Geom& g, const std::vector<uint64_t>& sb, uint32_t k) {
 cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
                            const uint64_t* hashes, uint64_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  const uint64_t cap = n < kBlockedChunk ? n : kBlockedChunk;
+  const uint64_t cap = n < blocked_round() ? n : blocked_round();
   Scratch sc;
   TwoLevel tl;
   const bool two = plan.super_parts > 1;
@@ -1273,7 +1286,7 @@ namespace {
 cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks, const Geom& g,
                                    const BlockedPlan& plan, const uint64_t* hashes, uint64_t n, void* out,
                                    bool bits, cudaStream_t s, CallScope* scope) {
-  const uint64_t cap = kBlockedChunk;
+  const uint64_t cap = blocked_round();
   Scratch sc[2];
   // the handle's side stream and events (created once: creating them per call
   // put 7-13 ms outliers into config-4 steps) and its scratch arena; the
@@ -1323,8 +1336,8 @@ cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks,
 cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
                          const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  const uint64_t cap = n < kBlockedChunk ? n : kBlockedChunk;  // a multiple of 32 unless n is the whole batch
-  const bool pipelined = plan.super_parts == 1 && n > kBlockedChunk && pipeline_enabled();
+  const uint64_t cap = n < blocked_round() ? n : blocked_round();  // a multiple of 32 unless n is the whole batch
+  const bool pipelined = plan.super_parts == 1 && n > blocked_round() && pipeline_enabled();
   CallScope scope(plan.ctx, s, scratch_bytes(cap, true) * (pipelined ? 2 : 1));
   if (scope.error() != cudaSuccess) return scope.error();
   // pipelining needs the handle's side stream: not while a graph is captured
@@ -1371,7 +1384,7 @@ cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geo
 // Keys given as several arrays (a rank's receive-window regions): each
 // region's chunks take consecutive chunk slots of one scratch, so a single
 // segment pass — one sweep of the filter through L2 — covers them all, with
-// no staging copy. Single-level plans and batches up to kBlockedChunk keys;
+// no staging copy. Single-level plans and batches up to blocked_round() keys;
 // anything else returns cudaErrorNotSupported (the caller gathers instead).
 namespace {
 uint64_t region_chunks(const uint64_t* counts, uint32_t nr, std::vector<uint64_t>& off) {
@@ -1385,7 +1398,7 @@ cudaError_t blocked_insert_regions(const DeviceInfo& di, uint32_t* blocks, const
                                    const uint64_t* const* keys, const uint64_t* counts, uint32_t nr, cudaStream_t s) {
   std::vector<uint64_t> off;
   const uint64_t C = region_chunks(counts, nr, off);
-  if (plan.super_parts > 1 || C * kPartChunk > kBlockedChunk) return cudaErrorNotSupported;
+  if (plan.super_parts > 1 || C * kPartChunk > blocked_round()) return cudaErrorNotSupported;
   if (C == 0) return cudaSuccess;
   Scratch sc;
   CallScope scope(plan.ctx, s, scratch_bytes(C * kPartChunk, false));
@@ -1406,7 +1419,7 @@ cudaError_t blocked_find_regions(const DeviceInfo& di, const uint32_t* blocks, c
                                  cudaStream_t s) {
   std::vector<uint64_t> off;
   const uint64_t C = region_chunks(counts, nr, off);
-  if (plan.super_parts > 1 || C * kPartChunk > kBlockedChunk) return cudaErrorNotSupported;
+  if (plan.super_parts > 1 || C * kPartChunk > blocked_round()) return cudaErrorNotSupported;
   if (C == 0) return cudaSuccess;
   Scratch sc;
   uint8_t* bytes = nullptr;  // answers in the chunk layout: region r's at off[r] * kPartChunk
