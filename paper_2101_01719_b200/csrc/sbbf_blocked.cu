@@ -656,6 +656,153 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
   }
 }
 
+// chunk_scatter with the data movement on the TMA engine: each CTA's next
+// chunk of keys is bulk-loaded (cp.async.bulk + mbarrier) into a second
+// input buffer while this one is ranked, and the bucket-major staging is
+// written out by bulk stores (cp.async.bulk.global.shared::cta), so the
+// threads only read keys from shared memory, rank and place them. Full
+// chunks with 16-byte aligned keys only; the caller sends a partial last
+// chunk through chunk_scatter_kernel.
+struct ChunkTmaSmem {
+  uint64_t in[2][kPartChunk];  // input ring (bulk loads)
+  uint64_t key[kPartChunk];    // bucket-major staging (bulk stores)
+  alignas(16) uint16_t pos[kPartChunk];
+  uint32_t wcnt[kPartWarps][kChunkBuckets];
+  uint32_t boff[kChunkBuckets + 1];
+  alignas(8) uint64_t bar[2];
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(smem_addr(bar)), "r"(parity)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+               "r"(bytes)
+               : "memory");
+}
+
+template <int BITS, bool kTop>
+__global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
+    chunk_scatter_tma_kernel(const uint64_t* __restrict__ hashes, uint64_t nfull, BucketMap bm,
+                             uint64_t* __restrict__ out, uint16_t* __restrict__ pos16, uint16_t* __restrict__ boffs) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  ChunkTmaSmem& sm = *reinterpret_cast<ChunkTmaSmem*>(smem_raw);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const OwnerMasks om(lane);
+  constexpr uint32_t kBytes = kPartChunk * sizeof(uint64_t);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("fence.proxy.async.shared::cta;");
+    if (blockIdx.x < nfull) bulk_load(sm.in[0], hashes + blockIdx.x * kPartChunk, kBytes, &sm.bar[0]);
+  }
+  __syncthreads();
+  uint32_t it = 0;
+  for (uint64_t ch = blockIdx.x; ch < nfull; ch += gridDim.x, ++it) {
+    const uint32_t k = it & 1;
+    const uint64_t base = ch * kPartChunk;
+    if (threadIdx.x == 0 && ch + gridDim.x < nfull) {
+      // the other buffer's last readers passed this iteration's barriers
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bulk_load(sm.in[k ^ 1], hashes + (ch + gridDim.x) * kPartChunk, kBytes, &sm.bar[k ^ 1]);
+    }
+    bulk_wait(&sm.bar[k], (it >> 1) & 1);
+    uint64_t h[kPartPerThread];
+    uint32_t bk[kPartPerThread], off[kPartPerThread];
+#pragma unroll
+    for (int j = 0; j < kPartPerThread; ++j) h[j] = sm.in[k][j * kPartThreads + threadIdx.x];
+    uint32_t c[owned<BITS>()] = {};
+#pragma unroll
+    for (int j = 0; j < kPartPerThread; ++j) {
+      bk[j] = bucket_of<kTop>(h[j], bm);
+      off[j] = warp_rank<BITS>(bk[j], true, lane, om, c);
+    }
+#pragma unroll
+    for (int i = 0; i < kChunkBuckets / 32; ++i) sm.wcnt[warp][lane + 32 * i] = i < owned<BITS>() ? c[i] : 0u;
+    __syncthreads();
+    if (warp == 0) {
+      constexpr int kO = owned<BITS>();
+      uint32_t t[kO] = {};
+#pragma unroll
+      for (int w = 0; w < kPartWarps; ++w) {
+#pragma unroll
+        for (int i = 0; i < kO; ++i) {
+          const uint32_t a = sm.wcnt[w][lane + 32 * i];
+          sm.wcnt[w][lane + 32 * i] = t[i];
+          t[i] += a;
+        }
+      }
+      uint32_t sc[kO];
+#pragma unroll
+      for (int i = 0; i < kO; ++i) sc[i] = t[i];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+        for (int i = 0; i < kO; ++i) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, sc[i], d);
+          if (lane >= static_cast<uint32_t>(d)) sc[i] += y;
+        }
+      }
+      uint16_t* bo = boffs + ch * kBoffStride;
+      uint32_t carry = 0;
+#pragma unroll
+      for (int i = 0; i < kChunkBuckets / 32; ++i) {
+        const uint32_t b = lane + 32 * i;
+        uint32_t o = kPartChunk;
+        if (i < kO) {
+          o = carry + sc[i] - t[i];
+          carry += __shfl_sync(0xffffffffu, sc[i], 31);
+          sm.boff[b] = o;
+        }
+        bo[b] = static_cast<uint16_t>(b < bm.S ? o : kPartChunk);
+      }
+      if (lane == 0) {
+        bo[kChunkBuckets] = static_cast<uint16_t>(kPartChunk);
+        // the previous chunk's bulk stores have finished reading the staging
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+    }
+    __syncthreads();
+    uint32_t sbase[owned<BITS>()];
+#pragma unroll
+    for (int i = 0; i < owned<BITS>(); ++i) sbase[i] = sm.boff[lane + 32 * i] + sm.wcnt[warp][lane + 32 * i];
+#pragma unroll
+    for (int j = 0; j < kPartPerThread; ++j) {
+      const uint32_t loc = slot_base<BITS>(bk[j], sbase) + off[j];
+      SBBF_DCHECK(loc < kPartChunk && bk[j] < bm.S);
+      sm.key[loc] = h[j];
+      sm.pos[loc] = static_cast<uint16_t>(j * kPartThreads + threadIdx.x);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bulk_store(out + base, sm.key, kBytes);
+      if (pos16) bulk_store(pos16 + base, sm.pos, kPartChunk * sizeof(uint16_t));
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // Probe (lookup) or OR (insert) bucket by bucket: CTA blockIdx handles bucket
 // b = blockIdx / groups over chunks [grp*G, grp*G + G); CTAs run in blockIdx
 // order, so the keys in flight all fall in one or two ~32 MiB filter slices
@@ -686,7 +833,7 @@ uint32_t seg_chunks_per_cta() {
 }
 
 // One work item: bucket b over chunks [c_begin, c_end).
-template <bool kInsert, int kSegQ, bool kTest = true>
+template <bool kInsert, int kSegQ, bool kTest = true, bool kPf = false, int kLd = 0>
 __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, const Geom& g,
                                              const uint64_t* __restrict__ keys, const uint16_t* __restrict__ boffs,
                                              uint64_t m, uint8_t* __restrict__ ans, uint32_t b, uint64_t c_begin,
@@ -716,14 +863,29 @@ __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, cons
       // test-before-set: grouped duplicates (config 4's hot keys) skip the atomic
       const uint32_t pair = lane & 3;
       const uint32_t seed_lo = dev::lane_seed_rt(2 * pair), seed_hi = dev::lane_seed_rt(2 * pair + 1);
-      uint64_t hn[kSegQ];
+      uint64_t hn[kSegQ], hp[kSegQ];
 #pragma unroll
-      for (int q = 0; q < kSegQ; ++q)
+      for (int q = 0; q < kSegQ; ++q) {
         hn[q] = (lane >> 2) < len[q] ? dev::ld_stream_u64(keys + seg[q] + (lane >> 2), pol) : 0;
+        if constexpr (kPf) hp[q] = (lane >> 2) + 8 < len[q] ? dev::ld_stream_u64(keys + seg[q] + (lane >> 2) + 8, pol) : 0;
+      }
       for (uint32_t j = lane >> 2; j < maxlen; j += 8) {
         uint64_t h[kSegQ];
 #pragma unroll
         for (int q = 0; q < kSegQ; ++q) h[q] = hn[q];
+        if constexpr (kPf) {
+          // keys two steps ahead: the step after this one has its keys
+          // (loaded a step ago) and its filter lines are prefetched into L2
+          // now, so its test loads hit L2 (one prefetch per key: pair 0)
+#pragma unroll
+          for (int q = 0; q < kSegQ; ++q) {
+            hn[q] = hp[q];
+            const uint64_t blk = dev::block_index(hn[q], g.nb_global) - g.first;
+            if (pair == 0 && j + 8 < len[q] && blk < g.nb_local) dev::prefetch_l2(blocks + blk * 8);
+          }
+#pragma unroll
+          for (int q = 0; q < kSegQ; ++q) hp[q] = j + 16 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 16, pol) : 0;
+        }
         uint64_t* ptr[kSegQ];
         uint64_t mask[kSegQ], cur[kSegQ];
 #pragma unroll
@@ -733,23 +895,44 @@ __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, cons
           const uint32_t low = static_cast<uint32_t>(h[q]);
           ptr[q] = reinterpret_cast<uint64_t*>(blocks + (ok ? blk : 0) * 8) + pair;
           mask[q] = ok ? (static_cast<uint64_t>(dev::lane_bit(low, seed_hi)) << 32) | dev::lane_bit(low, seed_lo) : 0;
-          cur[q] = !mask[q] ? ~0ull : kTest ? dev::ld_pair(ptr[q], keep) : 0ull;
+          cur[q] = !mask[q] ? ~0ull
+                   : !kTest   ? 0ull
+                   : kLd == 1 ? dev::ld_pair_cg(ptr[q], keep)
+                   : kLd == 2 ? dev::ld_pair_nc(ptr[q], keep)
+                              : dev::ld_pair(ptr[q], keep);
         }
+        if constexpr (!kPf) {
 #pragma unroll
-        for (int q = 0; q < kSegQ; ++q) hn[q] = j + 8 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 8, pol) : 0;
+          for (int q = 0; q < kSegQ; ++q) hn[q] = j + 8 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 8, pol) : 0;
+        }
 #pragma unroll
         for (int q = 0; q < kSegQ; ++q)
           if (mask[q] & ~cur[q]) dev::red_or64(ptr[q], mask[q], keep);
       }
     } else {
       // the next step's keys load while this step's sectors are in flight
-      uint64_t hn[kSegQ];
+      uint64_t hn[kSegQ], hp[kSegQ];
 #pragma unroll
-      for (int q = 0; q < kSegQ; ++q) hn[q] = lane < len[q] ? dev::ld_stream_u64(keys + seg[q] + lane, pol) : 0;
+      for (int q = 0; q < kSegQ; ++q) {
+        hn[q] = lane < len[q] ? dev::ld_stream_u64(keys + seg[q] + lane, pol) : 0;
+        if constexpr (kPf) hp[q] = lane + 32 < len[q] ? dev::ld_stream_u64(keys + seg[q] + lane + 32, pol) : 0;
+      }
       for (uint32_t j = lane; j < maxlen; j += 32) {
         uint64_t h[kSegQ];
 #pragma unroll
         for (int q = 0; q < kSegQ; ++q) h[q] = hn[q];
+        if constexpr (kPf) {
+          // the next step's keys arrived a step ago: prefetch their sectors
+          // into L2 now, load the keys two steps ahead
+#pragma unroll
+          for (int q = 0; q < kSegQ; ++q) {
+            hn[q] = hp[q];
+            const uint64_t blk = dev::block_index(hn[q], g.nb_global) - g.first;
+            if (j + 32 < len[q] && blk < g.nb_local) dev::prefetch_l2(blocks + blk * 8);
+          }
+#pragma unroll
+          for (int q = 0; q < kSegQ; ++q) hp[q] = j + 64 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 64, pol) : 0;
+        }
         dev::Block8 bl[kSegQ];
         uint32_t owned = 0;
 #pragma unroll
@@ -759,14 +942,81 @@ __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, cons
           owned |= static_cast<uint32_t>(ok) << q;
           dev::ld_block_nc_normal(blocks + (ok ? blk : 0) * 8, bl[q]);
         }
+        if constexpr (!kPf) {
 #pragma unroll
-        for (int q = 0; q < kSegQ; ++q)
-          hn[q] = j + 32 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 32, pol) : 0;
+          for (int q = 0; q < kSegQ; ++q)
+            hn[q] = j + 32 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 32, pol) : 0;
+        }
 #pragma unroll
         for (int q = 0; q < kSegQ; ++q)
           if (j < len[q]) ans[seg[q] + j] = (((owned >> q) & 1u) && dev::block_contains(bl[q], h[q])) ? 1 : 0;
       }
     }
+  }
+}
+
+// Insert sweep with little live state per key, so more keys are in flight
+// per SM: each warp takes kQ chunk segments at a time (their starts and
+// lengths in shared memory), 4 lanes per key, and between the test load and
+// the red holds only the key's low hash word, its local block and the loaded
+// lane pair (the mask and address are recomputed). kQ = 8 at 4 CTAs/SM keeps
+// ~2.7x the keys of segment_kernel<insert, 4> (3 CTAs/SM) in flight.
+template <int kQ, int kMinB>
+__global__ void __launch_bounds__(kSegThreads, kMinB)
+    segment_insert_lean_kernel(uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
+                               const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint32_t per_cta,
+                               uint32_t rev) {
+  __shared__ uint32_t s_start[kSegWarps][kQ], s_len[kSegWarps][kQ];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, pair = lane & 3;
+  const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
+  uint32_t b = blockIdx.x / groups;
+  if (rev) b = gridDim.x / groups - 1 - b;
+  const uint64_t c_begin = static_cast<uint64_t>(blockIdx.x % groups) * per_cta;
+  const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
+  const uint64_t pol = dev::policy_evict_first(), keep = dev::policy_evict_last();
+  const uint32_t seed_lo = dev::lane_seed_rt(2 * pair), seed_hi = dev::lane_seed_rt(2 * pair + 1);
+  const uint32_t nb32 = static_cast<uint32_t>(g.nb_local);  // host guarantees nb_local < 2^32
+  for (uint64_t c = c_begin + warp * kQ; c < c_end; c += kSegWarps * kQ) {
+    uint32_t len = 0;
+    if (lane < kQ) {
+      const uint64_t ch = c + lane;
+      uint32_t st = 0, en = 0;
+      if (ch < c_end) {
+        st = boffs[ch * kBoffStride + b];
+        en = boffs[ch * kBoffStride + b + 1];
+      }
+      s_start[warp][lane] = static_cast<uint32_t>(ch * kPartChunk + st);
+      s_len[warp][lane] = len = en - st;
+    }
+    const uint32_t maxlen = __reduce_max_sync(0xffffffffu, len);
+    __syncwarp();
+    uint64_t hn[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q)
+      hn[q] = (lane >> 2) < s_len[warp][q] ? dev::ld_stream_u64(keys + s_start[warp][q] + (lane >> 2), pol) : 0;
+    for (uint32_t j = lane >> 2; j < maxlen; j += 8) {
+      uint32_t low[kQ], blk[kQ];
+      uint64_t cur[kQ];
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const uint64_t bl = dev::block_index(hn[q], g.nb_global) - g.first;
+        const bool ok = j < s_len[warp][q] && bl < g.nb_local;
+        blk[q] = ok ? static_cast<uint32_t>(bl) : nb32;
+        low[q] = static_cast<uint32_t>(hn[q]);
+        cur[q] = ok ? dev::ld_pair(reinterpret_cast<const uint64_t*>(blocks + bl * 8) + pair, keep) : ~0ull;
+      }
+#pragma unroll
+      for (int q = 0; q < kQ; ++q)
+        hn[q] = j + 8 < s_len[warp][q] ? dev::ld_stream_u64(keys + s_start[warp][q] + j + 8, pol) : 0;
+#pragma unroll
+      for (int q = 0; q < kQ; ++q) {
+        const uint64_t mask = (static_cast<uint64_t>(dev::lane_bit(low[q], seed_hi)) << 32) |
+                              dev::lane_bit(low[q], seed_lo);
+        if (blk[q] != nb32 && (mask & ~cur[q]))
+          dev::red_or64(reinterpret_cast<uint64_t*>(blocks + static_cast<uint64_t>(blk[q]) * 8) + pair, mask, keep);
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -777,17 +1027,22 @@ __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, cons
 // within about one resident wave of small items whatever the CTA duration
 // spread (a one-shot grid of 64-chunk items keeps 2-3 slices live and reads
 // each slice ~3x from HBM: profiles/r2_*).
-template <bool kInsert, int kSegQ, int kMinB = (kSegQ > 4 ? 2 : 3), bool kTest = true>
+template <bool kInsert, int kSegQ, int kMinB = (kSegQ > 4 ? 2 : 3), bool kTest = true, bool kPf = false,
+          int kLd = 0>
 __global__ void __launch_bounds__(kSegThreads, kMinB)
     segment_kernel(uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
                    const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint8_t* __restrict__ ans,
-                   uint32_t per_cta, unsigned* __restrict__ work = nullptr, uint32_t items = 0) {
+                   uint32_t per_cta, unsigned* __restrict__ work = nullptr, uint32_t items = 0, uint32_t rev = 0) {
   const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
   if (!work) {
-    const uint32_t b = blockIdx.x / groups, grp = blockIdx.x % groups;
+    // rev: this sweep runs the slices last-to-first (alternate sweeps do, so a
+    // sweep starts on the slices the previous one left in L2)
+    uint32_t b = blockIdx.x / groups;
+    if (rev) b = gridDim.x / groups - 1 - b;
+    const uint32_t grp = blockIdx.x % groups;
     const uint64_t c_begin = static_cast<uint64_t>(grp) * per_cta;
     const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
-    segment_item<kInsert, kSegQ, kTest>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
+    segment_item<kInsert, kSegQ, kTest, kPf, kLd>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
     return;
   }
   __shared__ uint32_t next;
@@ -797,10 +1052,10 @@ __global__ void __launch_bounds__(kSegThreads, kMinB)
     const uint32_t item = next;
     __syncthreads();
     if (item >= items) return;
-    const uint32_t b = item / groups, grp = item % groups;
+    const uint32_t b = rev ? items / groups - 1 - item / groups : item / groups, grp = item % groups;
     const uint64_t c_begin = static_cast<uint64_t>(grp) * per_cta;
     const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
-    segment_item<kInsert, kSegQ, kTest>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
+    segment_item<kInsert, kSegQ, kTest, kPf, kLd>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
   }
 }
 
@@ -862,12 +1117,156 @@ __global__ void __launch_bounds__(kUnpermThreads, 4) unpermute_kernel(const uint
   }
 }
 
+// SBBF_SCATTER_TMA=1 (A/B): full chunks through chunk_scatter_tma_kernel.
+bool scatter_tma() {
+  static const bool on = [] {
+    const char* v = getenv("SBBF_SCATTER_TMA");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+// unpermute with the loads on the TMA engine: persistent CTAs, each chunk's
+// positions (8 KB) and answer bytes (4 KB) bulk-loaded into one of two
+// shared buffers while the previous chunk is scattered into source order.
+// Full chunks only (the caller sends a partial last chunk through
+// unpermute_kernel).
+struct UnpermTmaSmem {
+  alignas(16) uint16_t pos[2][kPartChunk];
+  alignas(16) uint8_t ans[2][kPartChunk];
+  alignas(16) uint8_t a[kPartChunk];
+  alignas(8) uint64_t bar[2];
+};
+
+__global__ void __launch_bounds__(kUnpermThreads, 4)
+    unpermute_tma_kernel(const uint8_t* __restrict__ ans, const uint16_t* __restrict__ pos16, uint64_t nfull,
+                         void* __restrict__ out, bool bits) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  UnpermTmaSmem& sm = *reinterpret_cast<UnpermTmaSmem*>(smem_raw);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t kPosBytes = kPartChunk * sizeof(uint16_t), kAnsBytes = kPartChunk;
+  auto issue = [&](uint64_t ch, uint32_t k) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&sm.bar[k])),
+                 "r"(kPosBytes + kAnsBytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(sm.pos[k])),
+                 "l"(pos16 + ch * kPartChunk), "r"(kPosBytes), "r"(smem_addr(&sm.bar[k]))
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(sm.ans[k])),
+                 "l"(ans + ch * kPartChunk), "r"(kAnsBytes), "r"(smem_addr(&sm.bar[k]))
+                 : "memory");
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("fence.proxy.async.shared::cta;");
+    if (blockIdx.x < nfull) issue(blockIdx.x, 0);
+  }
+  __syncthreads();
+  uint32_t it = 0;
+  for (uint64_t ch = blockIdx.x; ch < nfull; ch += gridDim.x, ++it) {
+    const uint32_t k = it & 1;
+    if (threadIdx.x == 0 && ch + gridDim.x < nfull) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(ch + gridDim.x, k ^ 1);
+    }
+    bulk_wait(&sm.bar[k], (it >> 1) & 1);
+    constexpr int kVec = kPartChunk / (kUnpermThreads * 8);
+#pragma unroll
+    for (int v = 0; v < kVec; ++v) {
+      const uint32_t i = (v * kUnpermThreads + threadIdx.x) * 8;
+      const uint4 pv = *reinterpret_cast<const uint4*>(&sm.pos[k][i]);
+      const uint2 av = *reinterpret_cast<const uint2*>(&sm.ans[k][i]);
+      const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+      const uint32_t aw[2] = {av.x, av.y};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        SBBF_DCHECK(((pw[e >> 1] >> ((e & 1) * 16)) & 0xffffu) < kPartChunk);
+        sm.a[(pw[e >> 1] >> ((e & 1) * 16)) & 0xffffu] = static_cast<uint8_t>(aw[e >> 2] >> ((e & 3) * 8));
+      }
+    }
+    __syncthreads();
+    const uint64_t base = ch * kPartChunk;
+    if (bits) {
+      uint32_t* ob = static_cast<uint32_t*>(out) + (base >> 5);
+      for (uint32_t wd = warp; wd < kPartChunk / 32; wd += kUnpermThreads / 32) {
+        const uint32_t word = __ballot_sync(0xffffffffu, sm.a[wd * 32 + lane] != 0);
+        if (lane == 0) ob[wd] = word;
+      }
+    } else {
+      uint4* o = reinterpret_cast<uint4*>(static_cast<uint8_t*>(out) + base);
+      const uint4* src = reinterpret_cast<const uint4*>(sm.a);
+      for (uint32_t v = threadIdx.x; v < kPartChunk / 16; v += kUnpermThreads) o[v] = src[v];
+    }
+    __syncthreads();
+  }
+}
+
+// SBBF_UNPERM_TMA=1 (A/B): full chunks through unpermute_tma_kernel.
+bool unperm_tma() {
+  static const bool on = [] {
+    const char* v = getenv("SBBF_UNPERM_TMA");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+// Answers of m keys (chunk layout) back to source order into `dst`.
+cudaError_t launch_unpermute(const DeviceInfo& di, const uint8_t* ans, const uint16_t* pos16, uint64_t m, void* dst,
+                             bool bits, cudaStream_t s) {
+  const uint64_t nfull = m / kPartChunk;
+  // byte output needs 16-byte aligned chunk rows; bit output 4-byte words
+  const bool aligned = bits || (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  if (unperm_tma() && nfull && aligned) {
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        unpermute_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(UnpermTmaSmem)));
+    if (attr != cudaSuccess) return attr;
+    const uint64_t cap = static_cast<uint64_t>(di.sms) * 4;
+    note_launch();
+    unpermute_tma_kernel<<<static_cast<unsigned>(nfull < cap ? nfull : cap), kUnpermThreads, sizeof(UnpermTmaSmem),
+                           s>>>(ans, pos16, nfull, dst, bits);
+    cudaError_t e = cudaGetLastError();
+    const uint64_t done = nfull * kPartChunk;
+    if (e != cudaSuccess || done == m) return e;
+    note_launch();
+    void* rest = bits ? static_cast<void*>(static_cast<uint32_t*>(dst) + done / 32)
+                      : static_cast<void*>(static_cast<uint8_t*>(dst) + done);
+    unpermute_kernel<<<1, kUnpermThreads, 0, s>>>(ans + done, pos16 + done, m - done, rest, bits);
+    return cudaGetLastError();
+  }
+  note_launch();
+  unpermute_kernel<<<static_cast<unsigned>((m + kPartChunk - 1) / kPartChunk), kUnpermThreads, 0, s>>>(ans, pos16, m,
+                                                                                                        dst, bits);
+  return cudaGetLastError();
+}
+
 template <int BITS, bool kTop>
 cudaError_t chunk_partition_bits(const DeviceInfo& di, const BucketMap& bm, const uint64_t* hashes, uint64_t m,
                                  uint64_t* out, uint16_t* pos16, uint16_t* boffs, cudaStream_t s) {
   static const cudaError_t attr = cudaFuncSetAttribute(
       chunk_scatter_kernel<BITS, kTop>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(ChunkSmem)));
   if (attr != cudaSuccess) return attr;
+  if (scatter_tma() && (reinterpret_cast<uintptr_t>(hashes) & 15) == 0 && m >= kPartChunk) {
+    static const cudaError_t attr_t =
+        cudaFuncSetAttribute(chunk_scatter_tma_kernel<BITS, kTop>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sizeof(ChunkTmaSmem)));
+    if (attr_t != cudaSuccess) return attr_t;
+    const uint64_t nfull = m / kPartChunk;
+    const uint64_t cap = static_cast<uint64_t>(di.sms) * kPartMinBlocks;
+    note_launch();
+    chunk_scatter_tma_kernel<BITS, kTop><<<static_cast<unsigned>(nfull < cap ? nfull : cap), kPartThreads,
+                                           sizeof(ChunkTmaSmem), s>>>(hashes, nfull, bm, out, pos16, boffs);
+    cudaError_t e = cudaGetLastError();
+    const uint64_t done = nfull * kPartChunk;
+    if (e != cudaSuccess || done == m) return e;
+    note_launch();  // the partial last chunk
+    chunk_scatter_kernel<BITS, kTop><<<1, kPartThreads, sizeof(ChunkSmem), s>>>(
+        hashes + done, m - done, bm, out + done, pos16 ? pos16 + done : nullptr, boffs + nfull * kBoffStride);
+    return cudaGetLastError();
+  }
   const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
   // SBBF_PART_PER_SM (A/B only): partition CTAs per SM
   static const uint64_t per_sm = [] {
@@ -904,26 +1303,31 @@ cudaError_t chunk_partition(const DeviceInfo& di, const Geom& g, uint32_t S, con
   }
 }
 
-// SBBF_SEG_PERSIST=0 selects the one-shot grid (A/B only).
-// Measured neutral on config 4 (profiles/r2p_*: the filter is read 1.3x
-// instead of 3x, but the sweep is latency-bound, not DRAM-bound), so the
-// one-shot grid stays the default; SBBF_SEG_PERSIST=1 selects it.
-bool seg_persist() {
-  static const bool on = [] {
+// The persistent segment grid measured neutral on config 4 (profiles/r2p_*:
+// the filter is read 1.3x instead of 3x, but the sweep is latency-bound, not
+// DRAM-bound), so the one-shot grid stays the default (A/B only):
+// SBBF_SEG_PERSIST=1 selects it for both phases, =2 for lookups only.
+bool seg_persist(bool insert) {
+  static const int on = [] {
     const char* v = getenv("SBBF_SEG_PERSIST");
-    return v && v[0] == '1';
+    return v ? atoi(v) : 0;
   }();
-  return on;
+  return on == 1 || (on == 2 && !insert);
 }
 
 // SBBF_SEG_INS_Q (A/B only): segments per warp step of the insert segment
 // kernel (2, 4 = default, 8); 1004 = 4 segments with plain reds (no
-// test-before-set load).
+// test-before-set load; measured 8.4 Gkeys/s on config 4: the hot keys' reds
+// serialise at L2); 2004 = 4 segments with the next step's filter lines
+// prefetched into L2.
 int seg_ins_q() {
   static const int v = [] {
     const char* e = getenv("SBBF_SEG_INS_Q");
     const int x = e ? atoi(e) : 4;
-    return (x == 2 || x == 8 || x == 1004) ? x : 4;
+    return (x == 2 || x == 8 || x == 1004 || x == 2004 || x == 3004 || x == 4004 || x == 5004 || x == 6004 ||
+            x == 6006 || x == 6008)
+               ? x
+               : 4;
   }();
   return v;
 }
@@ -931,14 +1335,29 @@ int seg_ins_q() {
 template <bool kInsert>
 cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* keys, const uint16_t* boffs, uint32_t S,
                             uint64_t m, uint8_t* ans, cudaStream_t s, unsigned* work = nullptr,
-                            const DeviceInfo* di = nullptr) {
+                            const DeviceInfo* di = nullptr, bool* flip = nullptr) {
+  // alternate the sweep direction per handle (SBBF_SEG_ALTERNATE=0 disables it: A/B only)
+  static const bool alt = [] {
+    const char* v = getenv("SBBF_SEG_ALTERNATE");
+    return !(v && v[0] == '0');
+  }();
+  uint32_t rev = 0;
+  if (flip && alt) {
+    rev = *flip ? 1u : 0u;
+    *flip = !*flip;
+  }
   const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
-  const bool persist = work && di && seg_persist();
+  const bool persist = work && di && seg_persist(kInsert);
   const uint32_t per_cta = persist ? seg_items_chunks() : seg_chunks_per_cta();
   const uint32_t groups = static_cast<uint32_t>((nchunks + per_cta - 1) / per_cta);
   if (persist) {
     const uint32_t items = S * groups;
-    auto kern = kInsert ? segment_kernel<true, 4> : segment_kernel<false, 1, 8>;
+    // SBBF_SEG_LOOK_Q=2 (A/B only): two segments per warp step at 4 CTAs/SM
+    static const bool look_q2 = [] {
+      const char* e = getenv("SBBF_SEG_LOOK_Q");
+      return e && atoi(e) == 2;
+    }();
+    auto kern = kInsert ? segment_kernel<true, 4> : look_q2 ? segment_kernel<false, 2, 4> : segment_kernel<false, 1, 8>;
     static const int occ_i = [] {
       int b = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, segment_kernel<true, 4>, kSegThreads, 0);
@@ -946,16 +1365,24 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
     }();
     static const int occ_l = [] {
       int b = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, segment_kernel<false, 1, 8>, kSegThreads, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, look_q2 ? segment_kernel<false, 2, 4> : segment_kernel<false, 1, 8>,
+                                                    kSegThreads, 0);
       return b > 0 ? b : 1;
     }();
-    uint64_t grid = static_cast<uint64_t>(di->sms) * (kInsert ? occ_i : occ_l);
+    // SBBF_SEG_PERSIST_CTAS (A/B only): resident CTAs per SM of the persistent
+    // grid (fewer leave room for a concurrent partition on the side stream)
+    static const int ctas = [] {
+      const char* e = getenv("SBBF_SEG_PERSIST_CTAS");
+      return e ? atoi(e) : 0;
+    }();
+    const int occ = kInsert ? occ_i : occ_l;
+    uint64_t grid = static_cast<uint64_t>(di->sms) * (ctas > 0 && ctas < occ ? ctas : occ);
     if (grid > items) grid = items;
     cudaError_t e = cudaMemsetAsync(work, 0, sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
     note_launch();
     kern<<<static_cast<unsigned>(grid), kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, work,
-                                                               items);
+                                                               items, rev);
     return cudaGetLastError();
   }
   note_launch();
@@ -966,14 +1393,36 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
   if constexpr (kInsert) {
     const int q = seg_ins_q();
     if (q == 2)
-      segment_kernel<true, 2, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta);
+      segment_kernel<true, 2, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u, rev);
+    else if (q == 3004)  // test loads .cg
+      segment_kernel<true, 4, 3, true, false, 1><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups,
+                                                                                    ans, per_cta, nullptr, 0u, rev);
+    else if (q == 4004)  // test loads .nc, no L1 allocation
+      segment_kernel<true, 4, 3, true, false, 2><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups,
+                                                                                    ans, per_cta, nullptr, 0u, rev);
+    else if (q == 5004)  // .cg test loads at 4 CTAs/SM (64 registers)
+      segment_kernel<true, 4, 4, true, false, 1><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups,
+                                                                                    ans, per_cta, nullptr, 0u, rev);
+    else if ((q == 6008 || q == 6006 || q == 6004) && g.nb_local < 0xffffffffull) {
+      if (q == 6008)
+        segment_insert_lean_kernel<8, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, per_cta,
+                                                                            rev);
+      else if (q == 6006)
+        segment_insert_lean_kernel<6, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, per_cta,
+                                                                            rev);
+      else
+        segment_insert_lean_kernel<4, 5><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, per_cta,
+                                                                            rev);
+    } else if (q == 2004)
+      segment_kernel<true, 4, 3, true, true><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans,
+                                                                                per_cta, nullptr, 0u, rev);
     else if (q == 1004)
       segment_kernel<true, 4, 3, false><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans,
-                                                                           per_cta);
+                                                                           per_cta, nullptr, 0u, rev);
     else if (q == 8)
-      segment_kernel<true, 8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta);
+      segment_kernel<true, 8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u, rev);
     else
-      segment_kernel<true, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta);
+      segment_kernel<true, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u, rev);
   } else
   {
     // SBBF_SEG_SMEM_KB (A/B only): unused dynamic shared memory per lookup
@@ -988,13 +1437,23 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, seg_smem);
       (void)a;
     }
-    segment_kernel<false, 1, 8><<<S * groups, kSegThreads, seg_smem, s>>>(blocks, g, keys, boffs, m, groups, ans,
-                                                                           per_cta);
+    // SBBF_SEG_LOOK_PF=1 (A/B only): the next step's sectors prefetched into L2
+    static const bool look_pf = [] {
+      const char* e = getenv("SBBF_SEG_LOOK_PF");
+      return e && e[0] == '1';
+    }();
+    if (look_pf)
+      segment_kernel<false, 1, 8, true, true><<<S * groups, kSegThreads, seg_smem, s>>>(blocks, g, keys, boffs, m,
+                                                                                       groups, ans, per_cta, nullptr, 0u, rev);
+    else
+      segment_kernel<false, 1, 8><<<S * groups, kSegThreads, seg_smem, s>>>(blocks, g, keys, boffs, m, groups, ans,
+                                                                             per_cta, nullptr, 0u, rev);
   }
   return cudaGetLastError();
 }
 
 struct Scratch {
+  bool* flip = nullptr;  // the handle's sweep-direction toggle (arena mode)
   uint64_t* keys = nullptr;
   uint16_t* boffs = nullptr;
   uint16_t* pos16 = nullptr;
@@ -1027,8 +1486,9 @@ struct BlockedCtx {
   uint64_t cap = 0;
   cudaEvent_t idle = nullptr;
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_in = nullptr, ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in = nullptr, ready[3] = {nullptr, nullptr, nullptr}, freed[3] = {nullptr, nullptr, nullptr};
   bool events_ok = false;
+  bool flip = false;  // direction of the next segment sweep
   cudaError_t init() {  // under mu
     if (events_ok) return cudaSuccess;
     int least = 0, greatest = 0;
@@ -1036,7 +1496,7 @@ struct BlockedCtx {
     if (e == cudaSuccess && !side) e = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, greatest);
     if (e == cudaSuccess && !idle) e = cudaEventCreateWithFlags(&idle, cudaEventDisableTiming);
     if (e == cudaSuccess && !ev_in) e = cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming);
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
       if (!ready[k]) e = cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming);
       if (e == cudaSuccess && !freed[k]) e = cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming);
     }
@@ -1048,7 +1508,7 @@ struct BlockedCtx {
     if (side) cudaStreamSynchronize(side);
     cudaFree(base);
     if (side) cudaStreamDestroy(side);
-    for (cudaEvent_t ev : {idle, ev_in, ready[0], ready[1], freed[0], freed[1]})
+    for (cudaEvent_t ev : {idle, ev_in, ready[0], ready[1], ready[2], freed[0], freed[1], freed[2]})
       if (ev) cudaEventDestroy(ev);
   }
 };
@@ -1133,6 +1593,7 @@ cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, bool lookup, cudaStream_t s
       sc.ans = reinterpret_cast<uint8_t*>(scope->take(cap));
     }
     sc.work = reinterpret_cast<unsigned*>(scope->take(sizeof(unsigned)));
+    sc.flip = &scope->ctx()->flip;
     sc.pooled = false;
     return cudaSuccess;
   }
@@ -1189,11 +1650,22 @@ bool pipeline_enabled() {
   return on;
 }
 
+// SBBF_PIPE_BUFS=3 (A/B only): scratch buffers of the pipelined lookup, so a
+// partition can run up to two rounds ahead of the probes.
+int pipe_bufs() {
+  static const int v = [] {
+    const char* e = getenv("SBBF_PIPE_BUFS");
+    return e && atoi(e) == 3 ? 3 : 2;
+  }();
+  return v;
+}
+
 // One batch chunk (m <= blocked_round() keys) through the single-level path.
 cudaError_t insert_chunk(const DeviceInfo& di, uint32_t* blocks, const Geom& g, uint32_t parts, const uint64_t* keys,
                          uint64_t m, Scratch& sc, cudaStream_t s) {
   cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, nullptr, sc.boffs, s);
-  if (e == cudaSuccess) e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, parts, m, nullptr, s, sc.work, &di);
+  if (e == cudaSuccess)
+    e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, parts, m, nullptr, s, sc.work, &di, sc.flip);
   return e;
 }
 
@@ -1203,13 +1675,11 @@ cudaError_t find_chunk(const DeviceInfo& di, const uint32_t* blocks, const Geom&
   cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, sc.pos16, sc.boffs, s);
   // 2. probe slice by slice (L2-resident), one answer byte per routed slot
   if (e == cudaSuccess)
-    e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, parts, m, sc.ans, s, sc.work, &di);
+    e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, parts, m, sc.ans, s, sc.work, &di,
+                                  sc.flip);
   // 3. back to source order, straight into the caller's bitmap / bytes
   if (e == cudaSuccess) {
-    note_launch();
-    unpermute_kernel<<<static_cast<unsigned>((m + kPartChunk - 1) / kPartChunk), kUnpermThreads, 0, s>>>(
-        sc.ans, sc.pos16, m, dst, bits);
-    e = cudaGetLastError();
+    e = launch_unpermute(di, sc.ans, sc.pos16, m, dst, bits, s);
   }
   return e;
 }
@@ -1287,7 +1757,8 @@ cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks,
                                    const BlockedPlan& plan, const uint64_t* hashes, uint64_t n, void* out,
                                    bool bits, cudaStream_t s, CallScope* scope) {
   const uint64_t cap = blocked_round();
-  Scratch sc[2];
+  const int nbuf = pipe_bufs();
+  Scratch sc[3];
   // the handle's side stream and events (created once: creating them per call
   // put 7-13 ms outliers into config-4 steps) and its scratch arena; the
   // scope's lock serialises the enqueue of concurrent callers
@@ -1296,7 +1767,7 @@ cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks,
   cudaError_t e = cudaSuccess;
   cudaStream_t side = ctx.side;
   cudaEvent_t ev_in = ctx.ev_in, *ready = ctx.ready, *freed = ctx.freed;
-  for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = alloc_scratch(sc[k], cap, true, s, &sco);
+  for (int k = 0; k < nbuf && e == cudaSuccess; ++k) e = alloc_scratch(sc[k], cap, true, s, &sco);
   // the side stream starts behind everything already queued on s (the
   // caller's hashes and the scratch allocations)
   if (e == cudaSuccess) e = cudaEventRecord(ev_in, s);
@@ -1304,22 +1775,19 @@ cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks,
   uint64_t c = 0;
   for (uint64_t off = 0; e == cudaSuccess && off < n; off += cap, ++c) {
     const uint64_t m = n - off < cap ? n - off : cap;
-    const int k = static_cast<int>(c & 1);
+    const int k = static_cast<int>(c % nbuf);
     void* dst = bits ? static_cast<void*>(static_cast<uint32_t*>(out) + off / 32)
                      : static_cast<void*>(static_cast<uint8_t*>(out) + off);
-    if (c >= 2) e = cudaStreamWaitEvent(side, freed[k], 0);  // round c-2 done with this scratch
+    if (c >= static_cast<uint64_t>(nbuf)) e = cudaStreamWaitEvent(side, freed[k], 0);  // round c-nbuf done with it
     if (e == cudaSuccess) e = chunk_partition(di, g, plan.parts, hashes + off, m, sc[k].keys, sc[k].pos16,
                                               sc[k].boffs, side);
     if (e == cudaSuccess) e = cudaEventRecord(ready[k], side);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ready[k], 0);
     if (e == cudaSuccess)
       e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc[k].keys, sc[k].boffs, plan.parts, m,
-                                 sc[k].ans, s, sc[k].work, &di);
+                                 sc[k].ans, s, sc[k].work, &di, sc[k].flip);
     if (e == cudaSuccess) {
-      note_launch();
-      unpermute_kernel<<<static_cast<unsigned>((m + kPartChunk - 1) / kPartChunk), kUnpermThreads, 0, s>>>(
-          sc[k].ans, sc[k].pos16, m, dst, bits);
-      e = cudaGetLastError();
+      e = launch_unpermute(di, sc[k].ans, sc[k].pos16, m, dst, bits, s);
     }
     if (e == cudaSuccess) e = cudaEventRecord(freed[k], s);
   }
@@ -1327,7 +1795,7 @@ cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks,
   // side launch and its ready[] wait), so the scratch frees on s are ordered
   // behind every partition that writes it
   if (side && ev_in && cudaEventRecord(ev_in, side) == cudaSuccess) cudaStreamWaitEvent(s, ev_in, 0);
-  for (int k = 0; k < 2; ++k) free_scratch(sc[k], s);
+  for (int k = 0; k < nbuf; ++k) free_scratch(sc[k], s);
   return e;
 }
 
@@ -1338,7 +1806,7 @@ cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geo
   if (n == 0) return cudaSuccess;
   const uint64_t cap = n < blocked_round() ? n : blocked_round();  // a multiple of 32 unless n is the whole batch
   const bool pipelined = plan.super_parts == 1 && n > blocked_round() && pipeline_enabled();
-  CallScope scope(plan.ctx, s, scratch_bytes(cap, true) * (pipelined ? 2 : 1));
+  CallScope scope(plan.ctx, s, scratch_bytes(cap, true) * (pipelined ? pipe_bufs() : 1));
   if (scope.error() != cudaSuccess) return scope.error();
   // pipelining needs the handle's side stream: not while a graph is captured
   if (pipelined && scope.arena()) return blocked_find_pipelined(di, blocks, g, plan, hashes, n, out, bits, s, &scope);
@@ -1409,7 +1877,8 @@ cudaError_t blocked_insert_regions(const DeviceInfo& di, uint32_t* blocks, const
       e = chunk_partition(di, g, plan.parts, keys[r], counts[r], sc.keys + off[r] * kPartChunk, nullptr,
                           sc.boffs + off[r] * kBoffStride, s);
   if (e == cudaSuccess)
-    e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, plan.parts, C * kPartChunk, nullptr, s, sc.work, &di);
+    e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, plan.parts, C * kPartChunk, nullptr, s, sc.work, &di,
+                              sc.flip);
   free_scratch(sc, s);
   return e;
 }
@@ -1433,7 +1902,7 @@ cudaError_t blocked_find_regions(const DeviceInfo& di, const uint32_t* blocks, c
                           sc.pos16 + off[r] * kPartChunk, sc.boffs + off[r] * kBoffStride, s);
   if (e == cudaSuccess)
     e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, plan.parts, C * kPartChunk,
-                               sc.ans, s, sc.work, &di);
+                               sc.ans, s, sc.work, &di, sc.flip);
   if (e == cudaSuccess) {
     note_launch();
     unpermute_kernel<<<static_cast<unsigned>(C), kUnpermThreads, 0, s>>>(sc.ans, sc.pos16, C * kPartChunk, bytes,
