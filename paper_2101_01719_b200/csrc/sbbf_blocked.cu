@@ -74,7 +74,7 @@ constexpr uint64_t kPartChunk = kPartThreads * kPartPerThread;
 constexpr int kMaxBuckets = 64;     // whole-batch partition (shard routing, super-slices)
 constexpr int kMaxBits = 6;
 constexpr int kChunkBuckets = 128;  // chunk-local partition (blocked path): up to 128 slices
-constexpr int kChunkBits = 7;
+constexpr int kChunkBits = 8;  // bal[] capacity: chunk-local ids use <= 7 bits, tile ids 8
 // buckets each lane owns (lane + 32 i) for BITS-bit bucket ids
 template <int BITS>
 constexpr int owned() { return BITS > 5 ? 1 << (BITS - 5) : 1; }
@@ -142,6 +142,7 @@ __device__ __forceinline__ void owner_masks(const OwnerMasks& om, const uint32_t
     uint32_t x = base;
     if constexpr (BITS > 5) x &= (i & 1) ? bal[5] : ~bal[5];
     if constexpr (BITS > 6) x &= (i & 2) ? bal[6] : ~bal[6];
+    if constexpr (BITS > 7) x &= (i & 4) ? bal[7] : ~bal[7];
     m[i] = x;
   }
 }
@@ -1020,6 +1021,487 @@ __global__ void __launch_bounds__(kSegThreads, kMinB)
   }
 }
 
+// Lookup sweep over a CTA's segments as one flat sequence: the CTA stages
+// its chunks' segment starts and a prefix of their lengths in shared memory,
+// then each warp step takes 32 consecutive flat positions (the CTA 256), so
+// no lane idles at a segment's tail and the next step's keys load across
+// segment boundaries. A lane's segment only moves forward: a short smem walk.
+template <int kMinB>
+__global__ void __launch_bounds__(kSegThreads, kMinB)
+    segment_find_flat_kernel(const uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
+                             const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint8_t* __restrict__ ans,
+                             uint32_t per_cta, uint32_t rev) {
+  constexpr int kMaxSeg = 128;  // per_cta <= kMaxSeg (host check)
+  __shared__ uint32_t s_start[kMaxSeg], s_pre[kMaxSeg + 1];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
+  uint32_t b = blockIdx.x / groups;
+  if (rev) b = gridDim.x / groups - 1 - b;
+  const uint64_t c_begin = static_cast<uint64_t>(blockIdx.x % groups) * per_cta;
+  const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
+  const uint32_t nseg = static_cast<uint32_t>(c_end - c_begin);
+  // segment table: warps 0-3 read the run bounds (one chunk per thread), warp 0 scans
+  uint32_t len = 0;
+  if (threadIdx.x < kMaxSeg && threadIdx.x < nseg) {
+    const uint64_t ch = c_begin + threadIdx.x;
+    const uint32_t st = boffs[ch * kBoffStride + b], en = boffs[ch * kBoffStride + b + 1];
+    s_start[threadIdx.x] = static_cast<uint32_t>(ch * kPartChunk + st);
+    len = en - st;
+  }
+  if (threadIdx.x < kMaxSeg) s_pre[threadIdx.x + 1] = len;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t v[kMaxSeg / 32], run = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxSeg / 32; ++i) {
+      v[i] = s_pre[1 + lane * (kMaxSeg / 32) + i];
+      run += v[i];
+    }
+    __syncwarp();  // every lane has read its lengths before any prefix overwrites them
+    uint32_t incl = run;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= static_cast<uint32_t>(d)) incl += y;
+    }
+    uint32_t acc = incl - run;
+#pragma unroll
+    for (int i = 0; i < kMaxSeg / 32; ++i) {
+      s_pre[lane * (kMaxSeg / 32) + i] = acc;
+      acc += v[i];
+    }
+    if (lane == 31) s_pre[kMaxSeg] = acc;
+  }
+  __syncthreads();
+  const uint32_t total = s_pre[nseg];
+  const uint64_t pol = dev::policy_evict_first();
+  uint32_t f = warp * 32 + lane, seg = 0;
+  // key index of flat position f (advances seg; f < total)
+  auto key_at = [&](uint32_t pos, uint32_t& sg) -> uint32_t {
+    while (sg + 1 < nseg && s_pre[sg + 1] <= pos) ++sg;
+    return s_start[sg] + (pos - s_pre[sg]);
+  };
+  uint32_t kidx = f < total ? key_at(f, seg) : 0;
+  uint64_t hn = f < total ? dev::ld_stream_u64(keys + kidx, pol) : 0;
+  for (; f < total; f += kSegThreads) {
+    const uint64_t h = hn;
+    const uint32_t cur = kidx;
+    const uint64_t blk = dev::block_index(h, g.nb_global) - g.first;
+    const bool ok = blk < g.nb_local;
+    dev::Block8 bl;
+    dev::ld_block_nc_normal(blocks + (ok ? blk : 0) * 8, bl);
+    const uint32_t fn = f + kSegThreads;
+    if (fn < total) {
+      kidx = key_at(fn, seg);
+      hn = dev::ld_stream_u64(keys + kidx, pol);
+    }
+    ans[cur] = (ok && dev::block_contains(bl, h)) ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tile insert (filters beyond L2, whole power-of-two filters)
+// ---------------------------------------------------------------------------
+// The segment sweep ORs keys into an L2-resident slice with one L2 atomic
+// (plus a test load) per key, ~55-65 G/s whatever the MLP (profiles/r2_ab).
+// The tile path instead applies each 64 KiB tile of the filter in shared
+// memory: a second partition groups every slice's keys by tile, then one CTA
+// per tile bulk-loads the tile, ORs its keys with shared-memory atomics and
+// bulk-stores it back, so the filter streams through HBM once per call and
+// no key touches L2 atomically.
+//   1. chunk_scatter(_tma): keys chunk-local by slice (S = nb / 2^19 slices
+//      of 256 tiles), as the other paths;
+//   2. tile_scatter_kernel: CTA (slice b, chunk group g) gathers its chunks'
+//      runs of slice b and writes them tile-major into the same positions of
+//      a second buffer (group g's region, slice b's share of it), with the
+//      absolute start of every tile's run (tile_runs[b][g][0..256]);
+//   3. tile_apply_kernel: CTA (b, t) applies the G runs of tile t.
+constexpr int kTileBits = 8;
+constexpr uint32_t kTilesPerSlice = 1u << kTileBits;
+constexpr uint32_t kTileBlocks = 2048;  // 64 KiB
+constexpr int kTileLog2 = 11;
+constexpr uint32_t kTileGroupChunks = 64;  // chunks per tile_scatter CTA
+constexpr int kTileScatterThreads = 512;
+constexpr int kTileScatterWarps = kTileScatterThreads / 32;
+constexpr int kTilePiece = 4096;           // keys placed per smem pass
+constexpr int kTilePerThread = kTilePiece / kTileScatterThreads;
+
+struct TileScatterSmem {
+  uint64_t key[kTilePiece];   // one piece staged tile-major
+  uint8_t tile[kTilePiece];
+  uint16_t kp[kTilePiece + 1];  // exclusive prefix of kept slots (staged order); kp[pn] = kept
+  uint32_t wcnt[kTileScatterWarps][kTilesPerSlice];
+  uint32_t poff[kTilesPerSlice];  // piece-local staged offset of each tile (before dedup)
+  uint32_t off[kTilesPerSlice];   // CTA: kept-key offset of each tile (several pieces)
+  uint32_t cur[kTilesPerSlice];   // CTA: kept keys of each tile written so far
+  uint32_t wsum[kTileScatterWarps];
+  uint32_t s_start[kTileGroupChunks];
+  uint32_t s_pre[kTileGroupChunks + 1];
+  uint32_t s_st[kTileGroupChunks];
+};
+
+// key index of flat position pos within the CTA's runs (seg only advances)
+__device__ __forceinline__ uint32_t flat_key(const uint32_t* s_start, const uint32_t* s_pre, uint32_t nseg,
+                                             uint32_t pos, uint32_t& seg) {
+  while (seg + 1 < nseg && s_pre[seg + 1] <= pos) ++seg;
+  return s_start[seg] + (pos - s_pre[seg]);
+}
+
+// Warp 0: per-tile totals over the warps' counters (wcnt becomes each warp's
+// exclusive prefix per tile) and their exclusive prefix over tiles (out).
+__device__ __forceinline__ void tile_scan_warp0(uint32_t (&wcnt)[kTileScatterWarps][kTilesPerSlice], uint32_t* out,
+                                                uint32_t lane) {
+  constexpr int kO = kTilesPerSlice / 32;
+  uint32_t t[kO] = {};
+#pragma unroll
+  for (int w = 0; w < kTileScatterWarps; ++w) {
+#pragma unroll
+    for (int i = 0; i < kO; ++i) {
+      const uint32_t a = wcnt[w][lane + 32 * i];
+      wcnt[w][lane + 32 * i] = t[i];
+      t[i] += a;
+    }
+  }
+  uint32_t sc[kO];
+#pragma unroll
+  for (int i = 0; i < kO; ++i) sc[i] = t[i];
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+    for (int i = 0; i < kO; ++i) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, sc[i], d);
+      if (lane >= static_cast<uint32_t>(d)) sc[i] += y;
+    }
+  }
+  uint32_t carry = 0;
+#pragma unroll
+  for (int i = 0; i < kO; ++i) {
+    out[lane + 32 * i] = carry + sc[i] - t[i];
+    carry += __shfl_sync(0xffffffffu, sc[i], 31);
+  }
+}
+
+// Exclusive prefix of a[0..256) over tiles into out (warp 0; a and out may alias).
+__device__ __forceinline__ uint32_t scan256_warp0(const uint32_t* a, uint32_t* out, uint32_t lane) {
+  constexpr int kO = kTilesPerSlice / 32;
+  uint32_t v[kO], run = 0;
+#pragma unroll
+  for (int i = 0; i < kO; ++i) {
+    v[i] = a[lane * kO + i];
+    run += v[i];
+  }
+  __syncwarp();
+  uint32_t incl = run;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= static_cast<uint32_t>(d)) incl += y;
+  }
+  uint32_t acc = incl - run;
+#pragma unroll
+  for (int i = 0; i < kO; ++i) {
+    out[lane * kO + i] = acc;
+    acc += v[i];
+  }
+  return __shfl_sync(0xffffffffu, incl, 31);
+}
+
+// One piece of up to kTilePiece flat keys: loaded, ranked by tile, staged
+// tile-major in smem, then de-duplicated — a slot whose key equals the slot
+// before it in the same tile's run is dropped (config 4's hot keys arrive as
+// long runs of one key: ~99 % of a hot tile's slots). On return (after a
+// barrier): sm.key/tile staged, sm.poff the staged tile offsets, sm.kp the
+// kept-slot prefix (kp[pn] = kept keys).
+__device__ __forceinline__ void tile_piece(TileScatterSmem& sm, const uint64_t* __restrict__ keys, uint32_t p0,
+                                           uint32_t pn, uint32_t nseg, uint32_t& seg, uint64_t nb, uint64_t slice_first,
+                                           uint64_t pol, const OwnerMasks& om, uint32_t lane, uint32_t warp) {
+  uint64_t h[kTilePerThread];
+  uint32_t tl[kTilePerThread], off[kTilePerThread];
+  uint32_t c[owned<kTileBits>()] = {};
+#pragma unroll
+  for (int j = 0; j < kTilePerThread; ++j) {
+    const uint32_t i = j * kTileScatterThreads + threadIdx.x;
+    h[j] = i < pn ? dev::ld_stream_u64(keys + flat_key(sm.s_start, sm.s_pre, nseg, p0 + i, seg), pol) : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < kTilePerThread; ++j) {
+    const uint32_t i = j * kTileScatterThreads + threadIdx.x;
+    const bool valid = i < pn;
+    tl[j] = valid ? static_cast<uint32_t>((dev::block_index(h[j], nb) - slice_first) >> kTileLog2) : 0;
+    off[j] = warp_rank<kTileBits>(tl[j], valid, lane, om, c);
+    if (!valid) tl[j] = 0xffffffffu;
+  }
+#pragma unroll
+  for (int i = 0; i < owned<kTileBits>(); ++i) sm.wcnt[warp][lane + 32 * i] = c[i];
+  __syncthreads();
+  if (warp == 0) tile_scan_warp0(sm.wcnt, sm.poff, lane);
+  __syncthreads();
+  uint32_t sbase[owned<kTileBits>()];
+#pragma unroll
+  for (int i = 0; i < owned<kTileBits>(); ++i) sbase[i] = sm.poff[lane + 32 * i] + sm.wcnt[warp][lane + 32 * i];
+#pragma unroll
+  for (int j = 0; j < kTilePerThread; ++j) {
+    const uint32_t loc = slot_base<kTileBits>(tl[j] & 0xffu, sbase) + off[j];
+    if (tl[j] != 0xffffffffu) {
+      SBBF_DCHECK(loc < pn);
+      sm.key[loc] = h[j];
+      sm.tile[loc] = static_cast<uint8_t>(tl[j]);
+    }
+  }
+  __syncthreads();
+  // keep flags of 8 consecutive staged slots per thread, block-wide prefix
+  const uint32_t i0 = threadIdx.x * kTilePerThread;
+  uint32_t keep = 0, cnt = 0;
+#pragma unroll
+  for (int k = 0; k < kTilePerThread; ++k) {
+    const uint32_t i = i0 + k;
+    bool kept = false;
+    if (i < pn) {
+      const uint32_t t = sm.tile[i];
+      kept = !(i > sm.poff[t] && sm.key[i] == sm.key[i - 1]);
+    }
+    keep |= static_cast<uint32_t>(kept) << k;
+    cnt += kept;
+  }
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= static_cast<uint32_t>(d)) incl += y;
+  }
+  if (lane == 31) sm.wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = lane < kTileScatterWarps ? sm.wsum[lane] : 0;
+    uint32_t wi = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, wi, d);
+      if (lane >= static_cast<uint32_t>(d)) wi += y;
+    }
+    if (lane < kTileScatterWarps) sm.wsum[lane] = wi - v;
+  }
+  __syncthreads();
+  uint32_t run = sm.wsum[warp] + incl - cnt;
+#pragma unroll
+  for (int k = 0; k < kTilePerThread; ++k) {
+    const uint32_t i = i0 + k;
+    if (i <= pn) sm.kp[i] = static_cast<uint16_t>(run);
+    run += (keep >> k) & 1u;
+  }
+  if (i0 + kTilePerThread == pn) sm.kp[pn] = static_cast<uint16_t>(run);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kTileScatterThreads, 2)
+    tile_scatter_kernel(uint64_t nb, uint32_t S, const uint64_t* __restrict__ keys, const uint16_t* __restrict__ boffs,
+                        uint64_t m, uint32_t groups, uint64_t* __restrict__ out, uint32_t* __restrict__ runs) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileScatterSmem& sm = *reinterpret_cast<TileScatterSmem*>(smem_raw);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const OwnerMasks om(lane);
+  const uint32_t b = blockIdx.x / groups, g = blockIdx.x % groups;
+  const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
+  const uint64_t c0 = static_cast<uint64_t>(g) * kTileGroupChunks;
+  const uint32_t nseg = static_cast<uint32_t>(c0 + kTileGroupChunks < nchunks ? kTileGroupChunks : nchunks - c0);
+  const uint64_t slice_first = static_cast<uint64_t>(b) * (nb / S);
+  const uint64_t pol = dev::policy_evict_first();
+  // segment table: run starts, prefix of lengths; this CTA's output base =
+  // group region + the keys of slices < b in the group's chunks
+  if (threadIdx.x < kTileGroupChunks) {
+    uint32_t st = 0, len = 0;
+    if (threadIdx.x < nseg) {
+      const uint64_t ch = c0 + threadIdx.x;
+      st = boffs[ch * kBoffStride + b];
+      len = boffs[ch * kBoffStride + b + 1] - st;
+      sm.s_start[threadIdx.x] = static_cast<uint32_t>(ch * kPartChunk + st);
+    }
+    sm.s_st[threadIdx.x] = st;
+    sm.s_pre[threadIdx.x + 1] = len;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v0 = sm.s_pre[1 + 2 * lane], v1 = sm.s_pre[2 + 2 * lane];
+    uint32_t a0 = sm.s_st[2 * lane] + sm.s_st[2 * lane + 1];
+    __syncwarp();
+    uint32_t incl = v0 + v1;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= static_cast<uint32_t>(d)) incl += y;
+    }
+    sm.s_pre[2 * lane] = incl - v0 - v1;
+    sm.s_pre[2 * lane + 1] = incl - v1;
+    if (lane == 31) sm.s_pre[kTileGroupChunks] = incl;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) a0 += __shfl_xor_sync(0xffffffffu, a0, d);
+    if (lane == 0) sm.s_st[0] = a0;  // sum of starts: keys of slices < b in the group
+  }
+  __syncthreads();
+  const uint32_t n = sm.s_pre[nseg];
+  const uint64_t base = c0 * kPartChunk + sm.s_st[0];
+  uint32_t* r = runs + static_cast<uint64_t>(blockIdx.x) * (kTilesPerSlice + 1);
+  if (n <= static_cast<uint32_t>(kTilePiece)) {
+    // one piece: staged order is the output order (kept slots only)
+    uint32_t seg = 0;
+    tile_piece(sm, keys, 0, n, nseg, seg, nb, slice_first, pol, om, lane, warp);
+    for (uint32_t t = threadIdx.x; t < kTilesPerSlice; t += kTileScatterThreads)
+      r[t] = static_cast<uint32_t>(base + sm.kp[sm.poff[t]]);
+    if (threadIdx.x == 0) r[kTilesPerSlice] = static_cast<uint32_t>(base + sm.kp[n]);
+    for (uint32_t i = threadIdx.x; i < n; i += kTileScatterThreads)
+      if (sm.kp[i + 1] != sm.kp[i]) out[base + sm.kp[i]] = sm.key[i];
+    return;
+  }
+  // several pieces: pass 1 counts the kept keys per tile, pass 2 writes them
+  for (uint32_t t = threadIdx.x; t < kTilesPerSlice; t += kTileScatterThreads) sm.off[t] = 0;
+  uint32_t seg = 0;
+  for (uint32_t p0 = 0; p0 < n; p0 += kTilePiece) {
+    const uint32_t pn = n - p0 < static_cast<uint32_t>(kTilePiece) ? n - p0 : kTilePiece;
+    tile_piece(sm, keys, p0, pn, nseg, seg, nb, slice_first, pol, om, lane, warp);
+    for (uint32_t t = threadIdx.x; t < kTilesPerSlice; t += kTileScatterThreads) {
+      const uint32_t e = t + 1 < kTilesPerSlice ? sm.poff[t + 1] : pn;
+      sm.off[t] += sm.kp[e] - sm.kp[sm.poff[t]];
+    }
+    __syncthreads();
+  }
+  if (warp == 0) {
+    const uint32_t total = scan256_warp0(sm.off, sm.off, lane);
+    if (lane == 0) r[kTilesPerSlice] = static_cast<uint32_t>(base + total);
+  }
+  __syncthreads();
+  for (uint32_t t = threadIdx.x; t < kTilesPerSlice; t += kTileScatterThreads) {
+    r[t] = static_cast<uint32_t>(base + sm.off[t]);
+    sm.cur[t] = 0;
+  }
+  __syncthreads();
+  seg = 0;
+  for (uint32_t p0 = 0; p0 < n; p0 += kTilePiece) {
+    const uint32_t pn = n - p0 < static_cast<uint32_t>(kTilePiece) ? n - p0 : kTilePiece;
+    tile_piece(sm, keys, p0, pn, nseg, seg, nb, slice_first, pol, om, lane, warp);
+    for (uint32_t i = threadIdx.x; i < pn; i += kTileScatterThreads)
+      if (sm.kp[i + 1] != sm.kp[i]) {
+        const uint32_t t = sm.tile[i];
+        const uint64_t dst = base + sm.off[t] + sm.cur[t] + (sm.kp[i] - sm.kp[sm.poff[t]]);
+        SBBF_DCHECK(dst < m);
+        out[dst] = sm.key[i];
+      }
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < kTilesPerSlice; t += kTileScatterThreads) {
+      const uint32_t e = t + 1 < kTilesPerSlice ? sm.poff[t + 1] : pn;
+      sm.cur[t] += sm.kp[e] - sm.kp[sm.poff[t]];
+    }
+    __syncthreads();
+  }
+}
+
+constexpr int kTileApplyThreads = 512;
+constexpr uint32_t kTileMaxGroups = 1024;  // runs per tile held in smem (host check)
+
+struct TileApplySmem {
+  uint32_t w[kTileBlocks * 8];  // the tile (64 KiB)
+  uint32_t r_lo[kTileMaxGroups];
+  uint32_t r_pre[kTileMaxGroups + 1];
+  alignas(8) uint64_t bar;
+};
+
+__global__ void __launch_bounds__(kTileApplyThreads, 3)
+    tile_apply_kernel(uint32_t* __restrict__ blocks, uint64_t nb, uint32_t S, const uint64_t* __restrict__ keys,
+                      const uint32_t* __restrict__ runs, uint32_t groups, uint32_t rev) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  TileApplySmem& sm = *reinterpret_cast<TileApplySmem*>(smem_raw);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t bt = blockIdx.x;
+  if (rev) bt = gridDim.x - 1 - bt;
+  const uint32_t b = bt >> kTileBits, t = bt & (kTilesPerSlice - 1);
+  const uint64_t tile_first = static_cast<uint64_t>(b) * (nb / S) + static_cast<uint64_t>(t) * kTileBlocks;
+  uint32_t* gtile = blocks + tile_first * 8;
+  constexpr uint32_t kBytes = kTileBlocks * 32;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&sm.bar)), "r"(kBytes)
+                 : "memory");
+#pragma unroll
+    for (uint32_t o = 0; o < kBytes; o += 16384)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_addr(reinterpret_cast<char*>(sm.w) + o)),
+                   "l"(reinterpret_cast<const char*>(gtile) + o), "r"(16384u), "r"(smem_addr(&sm.bar))
+                   : "memory");
+  }
+  // run table: group g's run of tile t is [runs[bg][t], runs[bg][t+1])
+  uint32_t len = 0;
+  for (uint32_t g = threadIdx.x; g < groups; g += kTileApplyThreads) {
+    const uint32_t* r = runs + (static_cast<uint64_t>(b) * groups + g) * (kTilesPerSlice + 1) + t;
+    const uint32_t lo = r[0], hi = r[1];
+    sm.r_lo[g] = lo;
+    sm.r_pre[g + 1] = hi - lo;
+    (void)len;
+  }
+  __syncthreads();
+  // prefix of run lengths (warp 0, groups <= kTileMaxGroups)
+  if (warp == 0) {
+    uint32_t carry = 0;
+    for (uint32_t g0 = 0; g0 < groups; g0 += 32) {
+      const uint32_t g = g0 + lane;
+      const uint32_t v = g < groups ? sm.r_pre[g + 1] : 0;
+      uint32_t incl = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= static_cast<uint32_t>(d)) incl += y;
+      }
+      if (g < groups) sm.r_pre[g] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) sm.r_pre[groups] = carry;
+  }
+  __syncthreads();
+  const uint32_t n = sm.r_pre[groups];
+  // the tile has landed
+  {
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(smem_addr(&sm.bar))
+                   : "memory");
+  }
+  // 8 threads per key, one lane word each: test, then a shared atomic OR.
+  // kU keys per thread group in flight: the group's keys f = it + u * 64 + slot.
+  constexpr int kU = 8;
+  constexpr uint32_t kSlots = kTileApplyThreads / 8;
+  const uint32_t word = lane & 7, slot = threadIdx.x >> 3;
+  const uint32_t seed = dev::lane_seed_rt(static_cast<int>(word));
+  const uint64_t pol = dev::policy_evict_first();
+  uint32_t seg = 0;
+  for (uint32_t it = 0; it < n; it += kSlots * kU) {
+    uint64_t h[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t f = it + u * kSlots + slot;
+      h[u] = f < n ? dev::ld_stream_u64(keys + flat_key(sm.r_lo, sm.r_pre, groups, f, seg), pol) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (it + u * kSlots + slot < n) {
+        const uint64_t blk = dev::block_index(h[u], nb) - tile_first;
+        SBBF_DCHECK(blk < kTileBlocks);
+        const uint32_t bit = dev::lane_bit(static_cast<uint32_t>(h[u]), seed);
+        uint32_t* p = &sm.w[static_cast<uint32_t>(blk) * 8 + word];
+        if ((*p & bit) == 0) atomicOr(p, bit);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    bulk_store(gtile, sm.w, kBytes);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+}
+
 // Items are (bucket, group of per_cta chunks) in bucket-major order. With
 // `work` null the grid has one CTA per item (blockIdx order); otherwise the
 // grid is the resident CTAs and each takes the next item from a global
@@ -1032,14 +1514,27 @@ template <bool kInsert, int kSegQ, int kMinB = (kSegQ > 4 ? 2 : 3), bool kTest =
 __global__ void __launch_bounds__(kSegThreads, kMinB)
     segment_kernel(uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
                    const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint8_t* __restrict__ ans,
-                   uint32_t per_cta, unsigned* __restrict__ work = nullptr, uint32_t items = 0, uint32_t rev = 0) {
+                   uint32_t per_cta, unsigned* __restrict__ work = nullptr, uint32_t items = 0, uint32_t rev = 0,
+                   int32_t pf_ahead = 0) {
   const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
   if (!work) {
     // rev: this sweep runs the slices last-to-first (alternate sweeps do, so a
     // sweep starts on the slices the previous one left in L2)
+    const uint32_t S = gridDim.x / groups;
     uint32_t b = blockIdx.x / groups;
-    if (rev) b = gridDim.x / groups - 1 - b;
+    if (rev) b = S - 1 - b;
     const uint32_t grp = blockIdx.x % groups;
+    if (pf_ahead != 0 && threadIdx.x == 0) {
+      // A/B: stream this CTA's share of the slice pf_ahead steps ahead in the
+      // sweep (pf_ahead < 0: its own slice) into L2 by a bulk prefetch
+      const int32_t step = pf_ahead < 0 ? 0 : pf_ahead;
+      const int64_t nb = rev ? static_cast<int64_t>(b) - step : static_cast<int64_t>(b) + step;
+      if (nb >= 0 && nb < static_cast<int64_t>(S)) {
+        const uint64_t sbytes = g.nb_local * 32 / S, share = (sbytes / groups) & ~uint64_t{15};
+        const char* p = reinterpret_cast<const char*>(blocks) + static_cast<uint64_t>(nb) * sbytes + grp * share;
+        if (share) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(static_cast<uint32_t>(share)) : "memory");
+      }
+    }
     const uint64_t c_begin = static_cast<uint64_t>(grp) * per_cta;
     const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
     segment_item<kInsert, kSegQ, kTest, kPf, kLd>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
@@ -1117,11 +1612,14 @@ __global__ void __launch_bounds__(kUnpermThreads, 4) unpermute_kernel(const uint
   }
 }
 
-// SBBF_SCATTER_TMA=1 (A/B): full chunks through chunk_scatter_tma_kernel.
+// Full chunks of 16-byte aligned keys go through chunk_scatter_tma_kernel
+// (config 4, ncu: 2^28-key lookup partition 0.98 -> 0.78 ms, 2^26-key insert
+// partition 0.24 -> 0.18 ms; profiles/r2x_*). SBBF_SCATTER_TMA=0 selects the
+// LSU kernel (A/B only).
 bool scatter_tma() {
   static const bool on = [] {
     const char* v = getenv("SBBF_SCATTER_TMA");
-    return v && v[0] == '1';
+    return !(v && v[0] == '0');
   }();
   return on;
 }
@@ -1205,11 +1703,13 @@ __global__ void __launch_bounds__(kUnpermThreads, 4)
   }
 }
 
-// SBBF_UNPERM_TMA=1 (A/B): full chunks through unpermute_tma_kernel.
+// Full chunks go through unpermute_tma_kernel (config 4 lookups 103.3 ->
+// 104.7 Gkeys/s, profiles/r2z_*); SBBF_UNPERM_TMA=0 selects unpermute_kernel
+// (A/B only).
 bool unperm_tma() {
   static const bool on = [] {
     const char* v = getenv("SBBF_UNPERM_TMA");
-    return v && v[0] == '1';
+    return !(v && v[0] == '0');
   }();
   return on;
 }
@@ -1382,7 +1882,7 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
     if (e != cudaSuccess) return e;
     note_launch();
     kern<<<static_cast<unsigned>(grid), kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, work,
-                                                               items, rev);
+                                                               items, rev, 0);
     return cudaGetLastError();
   }
   note_launch();
@@ -1421,8 +1921,16 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
                                                                            per_cta, nullptr, 0u, rev);
     else if (q == 8)
       segment_kernel<true, 8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u, rev);
-    else
-      segment_kernel<true, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u, rev);
+    else {
+      // SBBF_SEG_INS_PF (A/B only): bulk L2 prefetch of the slice this many
+      // sweep steps ahead (-1: the CTA's own slice)
+      static const int pf = [] {
+        const char* e = getenv("SBBF_SEG_INS_PF");
+        return e ? atoi(e) : 0;
+      }();
+      segment_kernel<true, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta,
+                                                                 nullptr, 0u, rev, pf);
+    }
   } else
   {
     // SBBF_SEG_SMEM_KB (A/B only): unused dynamic shared memory per lookup
@@ -1442,7 +1950,15 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
       const char* e = getenv("SBBF_SEG_LOOK_PF");
       return e && e[0] == '1';
     }();
-    if (look_pf)
+    // SBBF_SEG_FLAT=1 (A/B only): the flat-sequence lookup sweep
+    static const bool flat = [] {
+      const char* e = getenv("SBBF_SEG_FLAT");
+      return e && e[0] == '1';
+    }();
+    if (flat && per_cta <= 128)
+      segment_find_flat_kernel<8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta,
+                                                                     rev);
+    else if (look_pf)
       segment_kernel<false, 1, 8, true, true><<<S * groups, kSegThreads, seg_smem, s>>>(blocks, g, keys, boffs, m,
                                                                                        groups, ans, per_cta, nullptr, 0u, rev);
     else
@@ -1459,15 +1975,26 @@ struct Scratch {
   uint16_t* pos16 = nullptr;
   uint8_t* ans = nullptr;
   unsigned* work = nullptr;  // persistent segment grid's work counter
+  uint64_t* keys2 = nullptr;  // tile inserts: keys grouped by tile
+  uint32_t* runs = nullptr;   // tile inserts: run starts per (slice, group, tile)
   bool pooled = false;  // from the stream-ordered pool (freed per call) rather than the handle's arena
 };
+
+// tile_scatter CTAs per slice for a batch chunk of cap keys, and the run table's entries
+uint64_t tile_groups(uint64_t cap) {
+  const uint64_t nchunks = (cap + kPartChunk - 1) / kPartChunk;
+  return (nchunks + kTileGroupChunks - 1) / kTileGroupChunks;
+}
+uint64_t tile_runs_entries(uint64_t cap) { return 128 * tile_groups(cap) * (kTilesPerSlice + 1); }
 
 uint64_t align256(uint64_t b) { return (b + 255) & ~uint64_t{255}; }
 
 uint64_t scratch_bytes(uint64_t cap, bool lookup) {
   const uint64_t nchunks = (cap + kPartChunk - 1) / kPartChunk;
   return align256(cap * sizeof(uint64_t)) + align256(nchunks * kBoffStride * sizeof(uint16_t)) +
-         (lookup ? align256(cap * sizeof(uint16_t)) + align256(cap) : 0) + 256;
+         (lookup ? align256(cap * sizeof(uint16_t)) + align256(cap)
+                 : align256(cap * sizeof(uint64_t)) + align256(tile_runs_entries(cap) * sizeof(uint32_t))) +
+         256;
 }
 
 }  // namespace
@@ -1591,6 +2118,9 @@ cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, bool lookup, cudaStream_t s
     if (lookup) {
       sc.pos16 = reinterpret_cast<uint16_t*>(scope->take(cap * sizeof(uint16_t)));
       sc.ans = reinterpret_cast<uint8_t*>(scope->take(cap));
+    } else {
+      sc.keys2 = reinterpret_cast<uint64_t*>(scope->take(cap * sizeof(uint64_t)));
+      sc.runs = reinterpret_cast<uint32_t*>(scope->take(tile_runs_entries(cap) * sizeof(uint32_t)));
     }
     sc.work = reinterpret_cast<unsigned*>(scope->take(sizeof(unsigned)));
     sc.flip = &scope->ctx()->flip;
@@ -1604,6 +2134,9 @@ cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, bool lookup, cudaStream_t s
     e = cudaMallocAsync(reinterpret_cast<void**>(&sc.boffs), nchunks * kBoffStride * sizeof(uint16_t), s);
   if (lookup && e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.pos16), cap * sizeof(uint16_t), s);
   if (lookup && e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.ans), cap, s);
+  if (!lookup && e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.keys2), cap * sizeof(uint64_t), s);
+  if (!lookup && e == cudaSuccess)
+    e = cudaMallocAsync(reinterpret_cast<void**>(&sc.runs), tile_runs_entries(cap) * sizeof(uint32_t), s);
   if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.work), sizeof(unsigned), s);
   return e;
 }
@@ -1615,6 +2148,8 @@ void free_scratch(Scratch& sc, cudaStream_t s) {
     if (sc.pos16) cudaFreeAsync(sc.pos16, s);
     if (sc.ans) cudaFreeAsync(sc.ans, s);
     if (sc.work) cudaFreeAsync(sc.work, s);
+    if (sc.keys2) cudaFreeAsync(sc.keys2, s);
+    if (sc.runs) cudaFreeAsync(sc.runs, s);
   }
   sc = Scratch{};
 }
@@ -1641,11 +2176,16 @@ cudaError_t route_partition(const DeviceInfo& di, uint64_t total, uint32_t parts
 
 namespace {
 
-// SBBF_BLOCKED_PIPELINE=0 disables the overlapped multi-round lookup (A/B only).
+// The overlapped multi-round lookup (round c+1's partition on a side stream
+// while round c is probed) gained 1.6-3 % with the LSU partition but costs
+// 6 % with the TMA partition (config 4 lookups 104.8 -> 92.6 Gkeys/s,
+// profiles/r2y_*): the partition's 104 KB of shared memory per CTA and the
+// probe's all-L1 carveout cannot share an SM. Off by default;
+// SBBF_BLOCKED_PIPELINE=1 enables it (A/B only).
 bool pipeline_enabled() {
   static const bool on = [] {
     const char* v = getenv("SBBF_BLOCKED_PIPELINE");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
   }();
   return on;
 }
@@ -1661,8 +2201,50 @@ int pipe_bufs() {
 }
 
 // One batch chunk (m <= blocked_round() keys) through the single-level path.
+// Tile inserts (tile_scatter_kernel / tile_apply_kernel) apply to whole
+// power-of-two filters of 2^20..2^26 blocks (32 MiB - 2 GiB): S = nb / 2^19
+// slices of 256 tiles of 2048 blocks, slice = the hash's top bits.
+// SBBF_INSERT_TILES=0 selects the segment sweep (A/B only).
+uint32_t tile_slices(const Geom& g, uint64_t m, const Scratch& sc) {
+  static const bool on = [] {
+    const char* v = getenv("SBBF_INSERT_TILES");
+    return v && v[0] == '1';
+  }();
+  const uint64_t nb = g.nb_global;
+  if (!on || !sc.keys2 || !sc.runs || g.first != 0 || g.nb_local != nb || (nb & (nb - 1)) != 0) return 0;
+  if (nb < (uint64_t{1} << 20) || nb > (uint64_t{1} << 26) || tile_groups(m) > kTileMaxGroups) return 0;
+  return static_cast<uint32_t>(nb >> (kTileBits + kTileLog2));
+}
+
+cudaError_t insert_tiles(const DeviceInfo& di, uint32_t* blocks, const Geom& g, uint32_t S, const uint64_t* keys,
+                         uint64_t m, Scratch& sc, cudaStream_t s) {
+  cudaError_t e = chunk_partition(di, g, S, keys, m, sc.keys, nullptr, sc.boffs, s);
+  if (e != cudaSuccess) return e;
+  static const cudaError_t a1 = cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     static_cast<int>(sizeof(TileScatterSmem)));
+  static const cudaError_t a2 = cudaFuncSetAttribute(tile_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     static_cast<int>(sizeof(TileApplySmem)));
+  if (a1 != cudaSuccess) return a1;
+  if (a2 != cudaSuccess) return a2;
+  const uint32_t groups = static_cast<uint32_t>(tile_groups(m));
+  note_launch();
+  tile_scatter_kernel<<<S * groups, kTileScatterThreads, sizeof(TileScatterSmem), s>>>(g.nb_global, S, sc.keys,
+                                                                                       sc.boffs, m, groups, sc.keys2,
+                                                                                       sc.runs);
+  uint32_t rev = 0;
+  if (sc.flip) {
+    rev = *sc.flip ? 1u : 0u;
+    *sc.flip = !*sc.flip;
+  }
+  note_launch();
+  tile_apply_kernel<<<S * kTilesPerSlice, kTileApplyThreads, sizeof(TileApplySmem), s>>>(blocks, g.nb_global, S,
+                                                                                         sc.keys2, sc.runs, groups, rev);
+  return cudaGetLastError();
+}
+
 cudaError_t insert_chunk(const DeviceInfo& di, uint32_t* blocks, const Geom& g, uint32_t parts, const uint64_t* keys,
                          uint64_t m, Scratch& sc, cudaStream_t s) {
+  if (const uint32_t S = tile_slices(g, m, sc)) return insert_tiles(di, blocks, g, S, keys, m, sc, s);
   cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, nullptr, sc.boffs, s);
   if (e == cudaSuccess)
     e = launch_segments<true>(blocks, g, sc.keys, sc.boffs, parts, m, nullptr, s, sc.work, &di, sc.flip);

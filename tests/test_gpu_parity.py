@@ -267,6 +267,35 @@ def test_blocked_path_skew(cuda, oracle, nb, shape):
     assert np.array_equal(bits_to_bytes(bits, probes.size), want_res)
 
 
+@pytest.mark.parametrize("nb", [2**20, 2**21, 2**23, 2**26])
+def test_blocked_tile_insert(cuda, oracle, nb):
+    """Whole power-of-two filters of 2^20..2^26 blocks take the tile insert
+    (slices of 256 tiles of 2048 blocks; tile_scatter then tile_apply in
+    shared memory). Several calls (the sweep direction alternates), batches
+    spanning several 64-chunk groups with a partial last chunk, a hot key
+    repeated ~half of one call, keys packed into one tile, then lookups.
+    Bit-exact against the oracle after every call."""
+    rng = np.random.default_rng(nb ^ 0x711E)
+    tile_lo = np.uint64(0x0123456789ABCDEF) >> np.uint64(24) << np.uint64(24)  # one tile's worth of top bits
+    calls = [
+        rng.integers(0, 2**64, size=64 * 4096 * 3 + 4097, dtype=np.uint64),
+        np.concatenate([np.full(200_000, 0xFEEDFACECAFEBEEF, dtype=np.uint64),
+                        rng.integers(0, 2**64, size=250_001, dtype=np.uint64)]),
+        tile_lo | rng.integers(0, 2**20, size=100_003, dtype=np.uint64),
+        rng.integers(0, 2**64, size=1, dtype=np.uint64),
+    ]
+    f = SplitBlockFilter(nb)
+    f.set_insert_variant(_lib.INSERT_BLOCKED)
+    want = oracle.new_blocks(nb)
+    for hs in calls:
+        rng.shuffle(hs)
+        f.add_hashes(dev(hs, cuda))
+        oracle.add_hashes(want, hs)
+        assert np.array_equal(f.blocks(), want)
+    probes = np.concatenate([calls[0][:100_000], calls[2][:5000], rng.integers(0, 2**64, size=300_000, dtype=np.uint64)])
+    assert np.array_equal(f.find_hashes(dev(probes, cuda)).cpu().numpy(), oracle.find_hashes(want, probes))
+
+
 @pytest.mark.parametrize("nb", [2**27, 3 * 2**25 + 5, 2**27 + 12345])
 def test_blocked_two_level(cuda, oracle, nb):
     """Filters up to 128 slices of 32 MiB (4 GiB) take the single-level
