@@ -1140,11 +1140,20 @@ struct TileScatterSmem {
   uint32_t s_st[kTileGroupChunks];
 };
 
-// key index of flat position pos within the CTA's runs (seg only advances)
+// key index of flat position pos within the CTA's runs: the last run whose
+// prefix is <= pos, by binary search over s_pre[0..nseg) (empty runs share
+// their successor's prefix, so the last match is the non-empty one). seg is
+// kept for the callers' interface: a lower bound that only advances.
 __device__ __forceinline__ uint32_t flat_key(const uint32_t* s_start, const uint32_t* s_pre, uint32_t nseg,
                                              uint32_t pos, uint32_t& seg) {
-  while (seg + 1 < nseg && s_pre[seg + 1] <= pos) ++seg;
-  return s_start[seg] + (pos - s_pre[seg]);
+  uint32_t lo = seg, hi = nseg;  // invariant: s_pre[lo] <= pos, answer in [lo, hi)
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (s_pre[mid] <= pos) lo = mid;
+    else hi = mid;
+  }
+  seg = lo;
+  return s_start[lo] + (pos - s_pre[lo]);
 }
 
 // Warp 0: per-tile totals over the warps' counters (wcnt becomes each warp's
@@ -1500,6 +1509,150 @@ __global__ void __launch_bounds__(kTileApplyThreads, 3)
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
+}
+
+// Persistent tile apply: one CTA per SM walks its tiles (c, c + grid, ...)
+// in sweep order with three 64 KiB tile buffers — the tile two ahead loads by
+// TMA while this one is applied and the previous one is stored — and the next
+// tile's run table prefetched. One thread per key (all of a tile's keys in
+// flight at once for tiles up to 4 keys per thread); each thread walks its
+// block's eight words from a rotated start so a warp's shared accesses spread
+// over the banks.
+constexpr int kTileP2Threads = 1024;
+constexpr int kTileP2Bufs = 3;
+constexpr int kTileP2U = 4;
+
+struct TileApply2Smem {
+  uint32_t w[kTileP2Bufs][kTileBlocks * 8];
+  uint32_t r_lo[2][kTileMaxGroups];
+  uint32_t r_pre[2][kTileMaxGroups + 1];
+  uint32_t seeds[8];
+  alignas(8) uint64_t bar[kTileP2Bufs];
+};
+
+__global__ void __launch_bounds__(kTileP2Threads, 1)
+    tile_apply_persistent_kernel(uint32_t* __restrict__ blocks, uint64_t nb, uint32_t S,
+                                 const uint64_t* __restrict__ keys, const uint32_t* __restrict__ runs, uint32_t groups,
+                                 uint32_t rev) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  TileApply2Smem& sm = *reinterpret_cast<TileApply2Smem*>(smem_raw);
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t ntiles = S * kTilesPerSlice;
+  const uint64_t slice_blocks = nb / S;
+  constexpr uint32_t kBytes = kTileBlocks * 32;
+  auto tile_of = [&](uint32_t k) -> uint32_t { return rev ? ntiles - 1 - k : k; };  // k-th tile of the sweep
+  auto first_block = [&](uint32_t bt) -> uint64_t {
+    return static_cast<uint64_t>(bt >> kTileBits) * slice_blocks + static_cast<uint64_t>(bt & (kTilesPerSlice - 1)) * kTileBlocks;
+  };
+  auto issue_load = [&](uint32_t k, uint32_t buf) {
+    const uint32_t* src = blocks + first_block(tile_of(k)) * 8;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&sm.bar[buf])), "r"(kBytes)
+                 : "memory");
+#pragma unroll
+    for (uint32_t o = 0; o < kBytes; o += 16384)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_addr(reinterpret_cast<char*>(sm.w[buf]) + o)),
+                   "l"(reinterpret_cast<const char*>(src) + o), "r"(16384u), "r"(smem_addr(&sm.bar[buf]))
+                   : "memory");
+  };
+  auto load_runs = [&](uint32_t k, uint32_t rb) {
+    const uint32_t bt = tile_of(k), b = bt >> kTileBits, t = bt & (kTilesPerSlice - 1);
+    for (uint32_t g = threadIdx.x; g < groups; g += kTileP2Threads) {
+      const uint32_t* r = runs + (static_cast<uint64_t>(b) * groups + g) * (kTilesPerSlice + 1) + t;
+      const uint32_t lo = r[0], hi = r[1];
+      sm.r_lo[rb][g] = lo;
+      sm.r_pre[rb][g + 1] = hi - lo;
+    }
+  };
+  if (threadIdx.x < 8) sm.seeds[threadIdx.x] = dev::lane_seed_rt(static_cast<int>(threadIdx.x));
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < kTileP2Bufs; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar[k])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("fence.proxy.async.shared::cta;");
+    if (blockIdx.x < ntiles) issue_load(blockIdx.x, 0);
+    if (blockIdx.x + gridDim.x < ntiles) issue_load(blockIdx.x + gridDim.x, 1);
+  }
+  if (blockIdx.x < ntiles) load_runs(blockIdx.x, 0);
+  const uint64_t pol = dev::policy_evict_first();
+  uint32_t it = 0;
+  for (uint32_t k = blockIdx.x; k < ntiles; k += gridDim.x, ++it) {
+    const uint32_t buf = it % kTileP2Bufs, rb = it & 1;
+    __syncthreads();  // run table rb written; previous tile's apply done
+    if (warp == 0) {
+      uint32_t carry = 0;
+      for (uint32_t g0 = 0; g0 < groups; g0 += 32) {
+        const uint32_t g = g0 + lane;
+        const uint32_t v = g < groups ? sm.r_pre[rb][g + 1] : 0;
+        uint32_t incl = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= static_cast<uint32_t>(d)) incl += y;
+        }
+        __syncwarp();
+        if (g < groups) sm.r_pre[rb][g] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) sm.r_pre[rb][groups] = carry;
+    }
+    __syncthreads();
+    // the next tile's run table loads while this one is applied
+    if (k + gridDim.x < ntiles) load_runs(k + gridDim.x, rb ^ 1);
+    const uint32_t n = sm.r_pre[rb][groups];
+    const uint64_t tfirst = first_block(tile_of(k));
+    uint32_t seg = 0;
+    // keys of this thread: f = base + u * 1024 + tid
+    uint64_t h[kTileP2U];
+#pragma unroll
+    for (int u = 0; u < kTileP2U; ++u) {
+      const uint32_t f = u * kTileP2Threads + threadIdx.x;
+      h[u] = f < n ? dev::ld_stream_u64(keys + flat_key(sm.r_lo[rb], sm.r_pre[rb], groups, f, seg), pol) : 0;
+    }
+    bulk_wait(&sm.bar[buf], (it / kTileP2Bufs) & 1);
+    uint32_t* tw = sm.w[buf];
+    for (uint32_t base = 0; base < n; base += kTileP2U * kTileP2Threads) {
+#pragma unroll
+      for (int u = 0; u < kTileP2U; ++u) {
+        const uint32_t f = base + u * kTileP2Threads + threadIdx.x;
+        if (f < n) {
+          const uint32_t blk = static_cast<uint32_t>(dev::block_index(h[u], nb) - tfirst);
+          SBBF_DCHECK(blk < kTileBlocks);
+          const uint32_t low = static_cast<uint32_t>(h[u]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t wi = (i + threadIdx.x) & 7;
+            const uint32_t bit = dev::lane_bit(low, sm.seeds[wi]);
+            uint32_t* p = tw + blk * 8 + wi;
+            if ((*p & bit) == 0) atomicOr(p, bit);
+          }
+        }
+      }
+      const uint32_t nb2 = base + kTileP2U * kTileP2Threads;
+      if (nb2 < n) {
+#pragma unroll
+        for (int u = 0; u < kTileP2U; ++u) {
+          const uint32_t f = nb2 + u * kTileP2Threads + threadIdx.x;
+          h[u] = f < n ? dev::ld_stream_u64(keys + flat_key(sm.r_lo[rb], sm.r_pre[rb], groups, f, seg), pol) : 0;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bulk_store(blocks + tfirst * 8, tw, kBytes);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      // the tile two ahead goes into the buffer whose store was committed last
+      // iteration: wait until that store has read it
+      const uint32_t k2 = k + 2 * gridDim.x;
+      if (k2 < ntiles) {
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_load(k2, (it + 2) % kTileP2Bufs);
+      }
+    }
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Items are (bucket, group of per_cta chunks) in bucket-major order. With
@@ -2237,8 +2390,24 @@ cudaError_t insert_tiles(const DeviceInfo& di, uint32_t* blocks, const Geom& g, 
     *sc.flip = !*sc.flip;
   }
   note_launch();
-  tile_apply_kernel<<<S * kTilesPerSlice, kTileApplyThreads, sizeof(TileApplySmem), s>>>(blocks, g.nb_global, S,
-                                                                                         sc.keys2, sc.runs, groups, rev);
+  // SBBF_TILE_APPLY=1 (A/B): one tile per CTA instead of the persistent kernel
+  static const bool one = [] {
+    const char* v = getenv("SBBF_TILE_APPLY");
+    return v && v[0] == '1';
+  }();
+  if (one) {
+    tile_apply_kernel<<<S * kTilesPerSlice, kTileApplyThreads, sizeof(TileApplySmem), s>>>(blocks, g.nb_global, S,
+                                                                                           sc.keys2, sc.runs, groups,
+                                                                                           rev);
+  } else {
+    static const cudaError_t a3 = cudaFuncSetAttribute(
+        tile_apply_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(TileApply2Smem)));
+    if (a3 != cudaSuccess) return a3;
+    const uint32_t ntiles = S * kTilesPerSlice;
+    tile_apply_persistent_kernel<<<static_cast<unsigned>(ntiles < static_cast<uint32_t>(di.sms) ? ntiles : di.sms),
+                                   kTileP2Threads, sizeof(TileApply2Smem), s>>>(blocks, g.nb_global, S, sc.keys2,
+                                                                                sc.runs, groups, rev);
+  }
   return cudaGetLastError();
 }
 
