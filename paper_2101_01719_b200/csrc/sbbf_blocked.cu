@@ -1677,7 +1677,20 @@ __global__ void __launch_bounds__(kSegThreads, kMinB)
     uint32_t b = blockIdx.x / groups;
     if (rev) b = S - 1 - b;
     const uint32_t grp = blockIdx.x % groups;
-    if (pf_ahead != 0 && threadIdx.x == 0) {
+    if (pf_ahead == -2) {
+      // A/B: read this CTA's share of its own slice with coalesced 16-B loads
+      // before its random tests and reds (first touches in address order)
+      const uint64_t sbytes = g.nb_local * 32 / S, share = (sbytes / groups) & ~uint64_t{15};
+      const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(blocks) + b * sbytes + grp * share);
+      uint32_t acc = 0;
+      for (uint64_t i = threadIdx.x; i < share / 16; i += blockDim.x) {
+        uint4 v;
+        asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p + i));
+        acc ^= v.x;
+      }
+      if (acc == 0x9E3779B9u && threadIdx.x == 0xFFFFu) ans[0] = 1;  // keeps the loads; never true
+      __syncthreads();
+    } else if (pf_ahead != 0 && threadIdx.x == 0) {
       // A/B: stream this CTA's share of the slice pf_ahead steps ahead in the
       // sweep (pf_ahead < 0: its own slice) into L2 by a bulk prefetch
       const int32_t step = pf_ahead < 0 ? 0 : pf_ahead;
@@ -2069,9 +2082,14 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
     } else if (q == 2004)
       segment_kernel<true, 4, 3, true, true><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans,
                                                                                 per_cta, nullptr, 0u, rev);
-    else if (q == 1004)
+    else if (q == 1004) {
+      static const int pf = [] {
+        const char* e = getenv("SBBF_SEG_INS_PF");
+        return e ? atoi(e) : 0;
+      }();
       segment_kernel<true, 4, 3, false><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans,
-                                                                           per_cta, nullptr, 0u, rev);
+                                                                           per_cta, nullptr, 0u, rev, pf);
+    }
     else if (q == 8)
       segment_kernel<true, 8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u, rev);
     else {
@@ -2108,7 +2126,15 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
       const char* e = getenv("SBBF_SEG_FLAT");
       return e && e[0] == '1';
     }();
-    if (flat && per_cta <= 128)
+    // SBBF_SEG_LOOK_Q=3 (A/B only): two segments per warp step at 8 CTAs/SM
+    static const bool q2x8 = [] {
+      const char* e = getenv("SBBF_SEG_LOOK_Q");
+      return e && atoi(e) == 3;
+    }();
+    if (q2x8)
+      segment_kernel<false, 2, 8><<<S * groups, kSegThreads, seg_smem, s>>>(blocks, g, keys, boffs, m, groups, ans,
+                                                                             per_cta, nullptr, 0u, rev);
+    else if (flat && per_cta <= 128)
       segment_find_flat_kernel<8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta,
                                                                      rev);
     else if (look_pf)
