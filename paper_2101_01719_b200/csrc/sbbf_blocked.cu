@@ -834,7 +834,7 @@ uint32_t seg_chunks_per_cta() {
 }
 
 // One work item: bucket b over chunks [c_begin, c_end).
-template <bool kInsert, int kSegQ, bool kTest = true, bool kPf = false, int kLd = 0>
+template <bool kInsert, int kSegQ>
 __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, const Geom& g,
                                              const uint64_t* __restrict__ keys, const uint16_t* __restrict__ boffs,
                                              uint64_t m, uint8_t* __restrict__ ans, uint32_t b, uint64_t c_begin,
@@ -861,32 +861,18 @@ __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, cons
     }
     if constexpr (kInsert) {
       // 4 lanes per key, one 64-bit lane pair each (as insert_wide_kernel);
-      // test-before-set: grouped duplicates (config 4's hot keys) skip the atomic
+      // test-before-set: grouped duplicates (config 4's hot keys) skip the
+      // atomic, and their test loads hit L1 (.ca: .cg / .nc measured slower)
       const uint32_t pair = lane & 3;
       const uint32_t seed_lo = dev::lane_seed_rt(2 * pair), seed_hi = dev::lane_seed_rt(2 * pair + 1);
-      uint64_t hn[kSegQ], hp[kSegQ];
+      uint64_t hn[kSegQ];
 #pragma unroll
-      for (int q = 0; q < kSegQ; ++q) {
+      for (int q = 0; q < kSegQ; ++q)
         hn[q] = (lane >> 2) < len[q] ? dev::ld_stream_u64(keys + seg[q] + (lane >> 2), pol) : 0;
-        if constexpr (kPf) hp[q] = (lane >> 2) + 8 < len[q] ? dev::ld_stream_u64(keys + seg[q] + (lane >> 2) + 8, pol) : 0;
-      }
       for (uint32_t j = lane >> 2; j < maxlen; j += 8) {
         uint64_t h[kSegQ];
 #pragma unroll
         for (int q = 0; q < kSegQ; ++q) h[q] = hn[q];
-        if constexpr (kPf) {
-          // keys two steps ahead: the step after this one has its keys
-          // (loaded a step ago) and its filter lines are prefetched into L2
-          // now, so its test loads hit L2 (one prefetch per key: pair 0)
-#pragma unroll
-          for (int q = 0; q < kSegQ; ++q) {
-            hn[q] = hp[q];
-            const uint64_t blk = dev::block_index(hn[q], g.nb_global) - g.first;
-            if (pair == 0 && j + 8 < len[q] && blk < g.nb_local) dev::prefetch_l2(blocks + blk * 8);
-          }
-#pragma unroll
-          for (int q = 0; q < kSegQ; ++q) hp[q] = j + 16 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 16, pol) : 0;
-        }
         uint64_t* ptr[kSegQ];
         uint64_t mask[kSegQ], cur[kSegQ];
 #pragma unroll
@@ -896,44 +882,23 @@ __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, cons
           const uint32_t low = static_cast<uint32_t>(h[q]);
           ptr[q] = reinterpret_cast<uint64_t*>(blocks + (ok ? blk : 0) * 8) + pair;
           mask[q] = ok ? (static_cast<uint64_t>(dev::lane_bit(low, seed_hi)) << 32) | dev::lane_bit(low, seed_lo) : 0;
-          cur[q] = !mask[q] ? ~0ull
-                   : !kTest   ? 0ull
-                   : kLd == 1 ? dev::ld_pair_cg(ptr[q], keep)
-                   : kLd == 2 ? dev::ld_pair_nc(ptr[q], keep)
-                              : dev::ld_pair(ptr[q], keep);
+          cur[q] = mask[q] ? dev::ld_pair(ptr[q], keep) : ~0ull;
         }
-        if constexpr (!kPf) {
 #pragma unroll
-          for (int q = 0; q < kSegQ; ++q) hn[q] = j + 8 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 8, pol) : 0;
-        }
+        for (int q = 0; q < kSegQ; ++q) hn[q] = j + 8 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 8, pol) : 0;
 #pragma unroll
         for (int q = 0; q < kSegQ; ++q)
           if (mask[q] & ~cur[q]) dev::red_or64(ptr[q], mask[q], keep);
       }
     } else {
       // the next step's keys load while this step's sectors are in flight
-      uint64_t hn[kSegQ], hp[kSegQ];
+      uint64_t hn[kSegQ];
 #pragma unroll
-      for (int q = 0; q < kSegQ; ++q) {
-        hn[q] = lane < len[q] ? dev::ld_stream_u64(keys + seg[q] + lane, pol) : 0;
-        if constexpr (kPf) hp[q] = lane + 32 < len[q] ? dev::ld_stream_u64(keys + seg[q] + lane + 32, pol) : 0;
-      }
+      for (int q = 0; q < kSegQ; ++q) hn[q] = lane < len[q] ? dev::ld_stream_u64(keys + seg[q] + lane, pol) : 0;
       for (uint32_t j = lane; j < maxlen; j += 32) {
         uint64_t h[kSegQ];
 #pragma unroll
         for (int q = 0; q < kSegQ; ++q) h[q] = hn[q];
-        if constexpr (kPf) {
-          // the next step's keys arrived a step ago: prefetch their sectors
-          // into L2 now, load the keys two steps ahead
-#pragma unroll
-          for (int q = 0; q < kSegQ; ++q) {
-            hn[q] = hp[q];
-            const uint64_t blk = dev::block_index(hn[q], g.nb_global) - g.first;
-            if (j + 32 < len[q] && blk < g.nb_local) dev::prefetch_l2(blocks + blk * 8);
-          }
-#pragma unroll
-          for (int q = 0; q < kSegQ; ++q) hp[q] = j + 64 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 64, pol) : 0;
-        }
         dev::Block8 bl[kSegQ];
         uint32_t owned = 0;
 #pragma unroll
@@ -943,159 +908,14 @@ __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, cons
           owned |= static_cast<uint32_t>(ok) << q;
           dev::ld_block_nc_normal(blocks + (ok ? blk : 0) * 8, bl[q]);
         }
-        if constexpr (!kPf) {
 #pragma unroll
-          for (int q = 0; q < kSegQ; ++q)
-            hn[q] = j + 32 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 32, pol) : 0;
-        }
+        for (int q = 0; q < kSegQ; ++q)
+          hn[q] = j + 32 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 32, pol) : 0;
 #pragma unroll
         for (int q = 0; q < kSegQ; ++q)
           if (j < len[q]) ans[seg[q] + j] = (((owned >> q) & 1u) && dev::block_contains(bl[q], h[q])) ? 1 : 0;
       }
     }
-  }
-}
-
-// Insert sweep with little live state per key, so more keys are in flight
-// per SM: each warp takes kQ chunk segments at a time (their starts and
-// lengths in shared memory), 4 lanes per key, and between the test load and
-// the red holds only the key's low hash word, its local block and the loaded
-// lane pair (the mask and address are recomputed). kQ = 8 at 4 CTAs/SM keeps
-// ~2.7x the keys of segment_kernel<insert, 4> (3 CTAs/SM) in flight.
-template <int kQ, int kMinB>
-__global__ void __launch_bounds__(kSegThreads, kMinB)
-    segment_insert_lean_kernel(uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
-                               const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint32_t per_cta,
-                               uint32_t rev) {
-  __shared__ uint32_t s_start[kSegWarps][kQ], s_len[kSegWarps][kQ];
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, pair = lane & 3;
-  const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
-  uint32_t b = blockIdx.x / groups;
-  if (rev) b = gridDim.x / groups - 1 - b;
-  const uint64_t c_begin = static_cast<uint64_t>(blockIdx.x % groups) * per_cta;
-  const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
-  const uint64_t pol = dev::policy_evict_first(), keep = dev::policy_evict_last();
-  const uint32_t seed_lo = dev::lane_seed_rt(2 * pair), seed_hi = dev::lane_seed_rt(2 * pair + 1);
-  const uint32_t nb32 = static_cast<uint32_t>(g.nb_local);  // host guarantees nb_local < 2^32
-  for (uint64_t c = c_begin + warp * kQ; c < c_end; c += kSegWarps * kQ) {
-    uint32_t len = 0;
-    if (lane < kQ) {
-      const uint64_t ch = c + lane;
-      uint32_t st = 0, en = 0;
-      if (ch < c_end) {
-        st = boffs[ch * kBoffStride + b];
-        en = boffs[ch * kBoffStride + b + 1];
-      }
-      s_start[warp][lane] = static_cast<uint32_t>(ch * kPartChunk + st);
-      s_len[warp][lane] = len = en - st;
-    }
-    const uint32_t maxlen = __reduce_max_sync(0xffffffffu, len);
-    __syncwarp();
-    uint64_t hn[kQ];
-#pragma unroll
-    for (int q = 0; q < kQ; ++q)
-      hn[q] = (lane >> 2) < s_len[warp][q] ? dev::ld_stream_u64(keys + s_start[warp][q] + (lane >> 2), pol) : 0;
-    for (uint32_t j = lane >> 2; j < maxlen; j += 8) {
-      uint32_t low[kQ], blk[kQ];
-      uint64_t cur[kQ];
-#pragma unroll
-      for (int q = 0; q < kQ; ++q) {
-        const uint64_t bl = dev::block_index(hn[q], g.nb_global) - g.first;
-        const bool ok = j < s_len[warp][q] && bl < g.nb_local;
-        blk[q] = ok ? static_cast<uint32_t>(bl) : nb32;
-        low[q] = static_cast<uint32_t>(hn[q]);
-        cur[q] = ok ? dev::ld_pair(reinterpret_cast<const uint64_t*>(blocks + bl * 8) + pair, keep) : ~0ull;
-      }
-#pragma unroll
-      for (int q = 0; q < kQ; ++q)
-        hn[q] = j + 8 < s_len[warp][q] ? dev::ld_stream_u64(keys + s_start[warp][q] + j + 8, pol) : 0;
-#pragma unroll
-      for (int q = 0; q < kQ; ++q) {
-        const uint64_t mask = (static_cast<uint64_t>(dev::lane_bit(low[q], seed_hi)) << 32) |
-                              dev::lane_bit(low[q], seed_lo);
-        if (blk[q] != nb32 && (mask & ~cur[q]))
-          dev::red_or64(reinterpret_cast<uint64_t*>(blocks + static_cast<uint64_t>(blk[q]) * 8) + pair, mask, keep);
-      }
-    }
-    __syncwarp();
-  }
-}
-
-// Lookup sweep over a CTA's segments as one flat sequence: the CTA stages
-// its chunks' segment starts and a prefix of their lengths in shared memory,
-// then each warp step takes 32 consecutive flat positions (the CTA 256), so
-// no lane idles at a segment's tail and the next step's keys load across
-// segment boundaries. A lane's segment only moves forward: a short smem walk.
-template <int kMinB>
-__global__ void __launch_bounds__(kSegThreads, kMinB)
-    segment_find_flat_kernel(const uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
-                             const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint8_t* __restrict__ ans,
-                             uint32_t per_cta, uint32_t rev) {
-  constexpr int kMaxSeg = 128;  // per_cta <= kMaxSeg (host check)
-  __shared__ uint32_t s_start[kMaxSeg], s_pre[kMaxSeg + 1];
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
-  uint32_t b = blockIdx.x / groups;
-  if (rev) b = gridDim.x / groups - 1 - b;
-  const uint64_t c_begin = static_cast<uint64_t>(blockIdx.x % groups) * per_cta;
-  const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
-  const uint32_t nseg = static_cast<uint32_t>(c_end - c_begin);
-  // segment table: warps 0-3 read the run bounds (one chunk per thread), warp 0 scans
-  uint32_t len = 0;
-  if (threadIdx.x < kMaxSeg && threadIdx.x < nseg) {
-    const uint64_t ch = c_begin + threadIdx.x;
-    const uint32_t st = boffs[ch * kBoffStride + b], en = boffs[ch * kBoffStride + b + 1];
-    s_start[threadIdx.x] = static_cast<uint32_t>(ch * kPartChunk + st);
-    len = en - st;
-  }
-  if (threadIdx.x < kMaxSeg) s_pre[threadIdx.x + 1] = len;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t v[kMaxSeg / 32], run = 0;
-#pragma unroll
-    for (int i = 0; i < kMaxSeg / 32; ++i) {
-      v[i] = s_pre[1 + lane * (kMaxSeg / 32) + i];
-      run += v[i];
-    }
-    __syncwarp();  // every lane has read its lengths before any prefix overwrites them
-    uint32_t incl = run;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= static_cast<uint32_t>(d)) incl += y;
-    }
-    uint32_t acc = incl - run;
-#pragma unroll
-    for (int i = 0; i < kMaxSeg / 32; ++i) {
-      s_pre[lane * (kMaxSeg / 32) + i] = acc;
-      acc += v[i];
-    }
-    if (lane == 31) s_pre[kMaxSeg] = acc;
-  }
-  __syncthreads();
-  const uint32_t total = s_pre[nseg];
-  const uint64_t pol = dev::policy_evict_first();
-  uint32_t f = warp * 32 + lane, seg = 0;
-  // key index of flat position f (advances seg; f < total)
-  auto key_at = [&](uint32_t pos, uint32_t& sg) -> uint32_t {
-    while (sg + 1 < nseg && s_pre[sg + 1] <= pos) ++sg;
-    return s_start[sg] + (pos - s_pre[sg]);
-  };
-  uint32_t kidx = f < total ? key_at(f, seg) : 0;
-  uint64_t hn = f < total ? dev::ld_stream_u64(keys + kidx, pol) : 0;
-  for (; f < total; f += kSegThreads) {
-    const uint64_t h = hn;
-    const uint32_t cur = kidx;
-    const uint64_t blk = dev::block_index(h, g.nb_global) - g.first;
-    const bool ok = blk < g.nb_local;
-    dev::Block8 bl;
-    dev::ld_block_nc_normal(blocks + (ok ? blk : 0) * 8, bl);
-    const uint32_t fn = f + kSegThreads;
-    if (fn < total) {
-      kidx = key_at(fn, seg);
-      hn = dev::ld_stream_u64(keys + kidx, pol);
-    }
-    ans[cur] = (ok && dev::block_contains(bl, h)) ? 1 : 0;
   }
 }
 
@@ -1115,7 +935,8 @@ __global__ void __launch_bounds__(kSegThreads, kMinB)
 //      runs of slice b and writes them tile-major into the same positions of
 //      a second buffer (group g's region, slice b's share of it), with the
 //      absolute start of every tile's run (tile_runs[b][g][0..256]);
-//   3. tile_apply_kernel: CTA (b, t) applies the G runs of tile t.
+//   3. tile_apply_persistent_kernel: persistent CTAs apply tile t's G runs
+//      in shared memory, tile after tile.
 constexpr int kTileBits = 8;
 constexpr uint32_t kTilesPerSlice = 1u << kTileBits;
 constexpr uint32_t kTileBlocks = 2048;  // 64 KiB
@@ -1403,113 +1224,7 @@ __global__ void __launch_bounds__(kTileScatterThreads, 2)
   }
 }
 
-constexpr int kTileApplyThreads = 512;
 constexpr uint32_t kTileMaxGroups = 1024;  // runs per tile held in smem (host check)
-
-struct TileApplySmem {
-  uint32_t w[kTileBlocks * 8];  // the tile (64 KiB)
-  uint32_t r_lo[kTileMaxGroups];
-  uint32_t r_pre[kTileMaxGroups + 1];
-  alignas(8) uint64_t bar;
-};
-
-__global__ void __launch_bounds__(kTileApplyThreads, 3)
-    tile_apply_kernel(uint32_t* __restrict__ blocks, uint64_t nb, uint32_t S, const uint64_t* __restrict__ keys,
-                      const uint32_t* __restrict__ runs, uint32_t groups, uint32_t rev) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  TileApplySmem& sm = *reinterpret_cast<TileApplySmem*>(smem_raw);
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t bt = blockIdx.x;
-  if (rev) bt = gridDim.x - 1 - bt;
-  const uint32_t b = bt >> kTileBits, t = bt & (kTilesPerSlice - 1);
-  const uint64_t tile_first = static_cast<uint64_t>(b) * (nb / S) + static_cast<uint64_t>(t) * kTileBlocks;
-  uint32_t* gtile = blocks + tile_first * 8;
-  constexpr uint32_t kBytes = kTileBlocks * 32;
-  if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar)));
-    asm volatile("fence.mbarrier_init.release.cluster;");
-    asm volatile("fence.proxy.async.shared::cta;");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&sm.bar)), "r"(kBytes)
-                 : "memory");
-#pragma unroll
-    for (uint32_t o = 0; o < kBytes; o += 16384)
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                       smem_addr(reinterpret_cast<char*>(sm.w) + o)),
-                   "l"(reinterpret_cast<const char*>(gtile) + o), "r"(16384u), "r"(smem_addr(&sm.bar))
-                   : "memory");
-  }
-  // run table: group g's run of tile t is [runs[bg][t], runs[bg][t+1])
-  uint32_t len = 0;
-  for (uint32_t g = threadIdx.x; g < groups; g += kTileApplyThreads) {
-    const uint32_t* r = runs + (static_cast<uint64_t>(b) * groups + g) * (kTilesPerSlice + 1) + t;
-    const uint32_t lo = r[0], hi = r[1];
-    sm.r_lo[g] = lo;
-    sm.r_pre[g + 1] = hi - lo;
-    (void)len;
-  }
-  __syncthreads();
-  // prefix of run lengths (warp 0, groups <= kTileMaxGroups)
-  if (warp == 0) {
-    uint32_t carry = 0;
-    for (uint32_t g0 = 0; g0 < groups; g0 += 32) {
-      const uint32_t g = g0 + lane;
-      const uint32_t v = g < groups ? sm.r_pre[g + 1] : 0;
-      uint32_t incl = v;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= static_cast<uint32_t>(d)) incl += y;
-      }
-      if (g < groups) sm.r_pre[g] = carry + incl - v;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (lane == 0) sm.r_pre[groups] = carry;
-  }
-  __syncthreads();
-  const uint32_t n = sm.r_pre[groups];
-  // the tile has landed
-  {
-    uint32_t done = 0;
-    while (!done)
-      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-                   : "=r"(done)
-                   : "r"(smem_addr(&sm.bar))
-                   : "memory");
-  }
-  // 8 threads per key, one lane word each: test, then a shared atomic OR.
-  // kU keys per thread group in flight: the group's keys f = it + u * 64 + slot.
-  constexpr int kU = 8;
-  constexpr uint32_t kSlots = kTileApplyThreads / 8;
-  const uint32_t word = lane & 7, slot = threadIdx.x >> 3;
-  const uint32_t seed = dev::lane_seed_rt(static_cast<int>(word));
-  const uint64_t pol = dev::policy_evict_first();
-  uint32_t seg = 0;
-  for (uint32_t it = 0; it < n; it += kSlots * kU) {
-    uint64_t h[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const uint32_t f = it + u * kSlots + slot;
-      h[u] = f < n ? dev::ld_stream_u64(keys + flat_key(sm.r_lo, sm.r_pre, groups, f, seg), pol) : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      if (it + u * kSlots + slot < n) {
-        const uint64_t blk = dev::block_index(h[u], nb) - tile_first;
-        SBBF_DCHECK(blk < kTileBlocks);
-        const uint32_t bit = dev::lane_bit(static_cast<uint32_t>(h[u]), seed);
-        uint32_t* p = &sm.w[static_cast<uint32_t>(blk) * 8 + word];
-        if ((*p & bit) == 0) atomicOr(p, bit);
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    bulk_store(gtile, sm.w, kBytes);
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  }
-}
 
 // Persistent tile apply: one CTA per SM walks its tiles (c, c + grid, ...)
 // in sweep order with three 64 KiB tile buffers — the tile two ahead loads by
@@ -1662,48 +1377,21 @@ __global__ void __launch_bounds__(kTileP2Threads, 1)
 // within about one resident wave of small items whatever the CTA duration
 // spread (a one-shot grid of 64-chunk items keeps 2-3 slices live and reads
 // each slice ~3x from HBM: profiles/r2_*).
-template <bool kInsert, int kSegQ, int kMinB = (kSegQ > 4 ? 2 : 3), bool kTest = true, bool kPf = false,
-          int kLd = 0>
+template <bool kInsert, int kSegQ, int kMinB = (kSegQ > 4 ? 2 : 3)>
 __global__ void __launch_bounds__(kSegThreads, kMinB)
     segment_kernel(uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
                    const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint8_t* __restrict__ ans,
-                   uint32_t per_cta, unsigned* __restrict__ work = nullptr, uint32_t items = 0, uint32_t rev = 0,
-                   int32_t pf_ahead = 0) {
+                   uint32_t per_cta, unsigned* __restrict__ work = nullptr, uint32_t items = 0, uint32_t rev = 0) {
   const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
   if (!work) {
     // rev: this sweep runs the slices last-to-first (alternate sweeps do, so a
     // sweep starts on the slices the previous one left in L2)
-    const uint32_t S = gridDim.x / groups;
     uint32_t b = blockIdx.x / groups;
-    if (rev) b = S - 1 - b;
+    if (rev) b = gridDim.x / groups - 1 - b;
     const uint32_t grp = blockIdx.x % groups;
-    if (pf_ahead == -2) {
-      // A/B: read this CTA's share of its own slice with coalesced 16-B loads
-      // before its random tests and reds (first touches in address order)
-      const uint64_t sbytes = g.nb_local * 32 / S, share = (sbytes / groups) & ~uint64_t{15};
-      const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(blocks) + b * sbytes + grp * share);
-      uint32_t acc = 0;
-      for (uint64_t i = threadIdx.x; i < share / 16; i += blockDim.x) {
-        uint4 v;
-        asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p + i));
-        acc ^= v.x;
-      }
-      if (acc == 0x9E3779B9u && threadIdx.x == 0xFFFFu) ans[0] = 1;  // keeps the loads; never true
-      __syncthreads();
-    } else if (pf_ahead != 0 && threadIdx.x == 0) {
-      // A/B: stream this CTA's share of the slice pf_ahead steps ahead in the
-      // sweep (pf_ahead < 0: its own slice) into L2 by a bulk prefetch
-      const int32_t step = pf_ahead < 0 ? 0 : pf_ahead;
-      const int64_t nb = rev ? static_cast<int64_t>(b) - step : static_cast<int64_t>(b) + step;
-      if (nb >= 0 && nb < static_cast<int64_t>(S)) {
-        const uint64_t sbytes = g.nb_local * 32 / S, share = (sbytes / groups) & ~uint64_t{15};
-        const char* p = reinterpret_cast<const char*>(blocks) + static_cast<uint64_t>(nb) * sbytes + grp * share;
-        if (share) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(static_cast<uint32_t>(share)) : "memory");
-      }
-    }
     const uint64_t c_begin = static_cast<uint64_t>(grp) * per_cta;
     const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
-    segment_item<kInsert, kSegQ, kTest, kPf, kLd>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
+    segment_item<kInsert, kSegQ>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
     return;
   }
   __shared__ uint32_t next;
@@ -1716,7 +1404,7 @@ __global__ void __launch_bounds__(kSegThreads, kMinB)
     const uint32_t b = rev ? items / groups - 1 - item / groups : item / groups, grp = item % groups;
     const uint64_t c_begin = static_cast<uint64_t>(grp) * per_cta;
     const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
-    segment_item<kInsert, kSegQ, kTest, kPf, kLd>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
+    segment_item<kInsert, kSegQ>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end);
   }
 }
 
@@ -1982,18 +1670,15 @@ bool seg_persist(bool insert) {
 }
 
 // SBBF_SEG_INS_Q (A/B only): segments per warp step of the insert segment
-// kernel (2, 4 = default, 8); 1004 = 4 segments with plain reds (no
-// test-before-set load; measured 8.4 Gkeys/s on config 4: the hot keys' reds
-// serialise at L2); 2004 = 4 segments with the next step's filter lines
-// prefetched into L2.
+// kernel (2, 4 = default, 8). Measured and removed (profiles/r2_ab): plain
+// reds without the test load (8.5 Gkeys/s on config 4: the hot keys' reds
+// serialise at L2), .cg / .nc test loads, an L2 prefetch of the next step's
+// lines, bulk prefetch of the slice ahead, 4 CTAs/SM at 64 registers.
 int seg_ins_q() {
   static const int v = [] {
     const char* e = getenv("SBBF_SEG_INS_Q");
     const int x = e ? atoi(e) : 4;
-    return (x == 2 || x == 8 || x == 1004 || x == 2004 || x == 3004 || x == 4004 || x == 5004 || x == 6004 ||
-            x == 6006 || x == 6008)
-               ? x
-               : 4;
+    return (x == 2 || x == 8) ? x : 4;
   }();
   return v;
 }
@@ -2018,12 +1703,7 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
   const uint32_t groups = static_cast<uint32_t>((nchunks + per_cta - 1) / per_cta);
   if (persist) {
     const uint32_t items = S * groups;
-    // SBBF_SEG_LOOK_Q=2 (A/B only): two segments per warp step at 4 CTAs/SM
-    static const bool look_q2 = [] {
-      const char* e = getenv("SBBF_SEG_LOOK_Q");
-      return e && atoi(e) == 2;
-    }();
-    auto kern = kInsert ? segment_kernel<true, 4> : look_q2 ? segment_kernel<false, 2, 4> : segment_kernel<false, 1, 8>;
+    auto kern = kInsert ? segment_kernel<true, 4> : segment_kernel<false, 1, 8>;
     static const int occ_i = [] {
       int b = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, segment_kernel<true, 4>, kSegThreads, 0);
@@ -2031,118 +1711,39 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
     }();
     static const int occ_l = [] {
       int b = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, look_q2 ? segment_kernel<false, 2, 4> : segment_kernel<false, 1, 8>,
-                                                    kSegThreads, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, segment_kernel<false, 1, 8>, kSegThreads, 0);
       return b > 0 ? b : 1;
     }();
-    // SBBF_SEG_PERSIST_CTAS (A/B only): resident CTAs per SM of the persistent
-    // grid (fewer leave room for a concurrent partition on the side stream)
-    static const int ctas = [] {
-      const char* e = getenv("SBBF_SEG_PERSIST_CTAS");
-      return e ? atoi(e) : 0;
-    }();
-    const int occ = kInsert ? occ_i : occ_l;
-    uint64_t grid = static_cast<uint64_t>(di->sms) * (ctas > 0 && ctas < occ ? ctas : occ);
+    uint64_t grid = static_cast<uint64_t>(di->sms) * (kInsert ? occ_i : occ_l);
     if (grid > items) grid = items;
     cudaError_t e = cudaMemsetAsync(work, 0, sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
     note_launch();
     kern<<<static_cast<unsigned>(grid), kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, work,
-                                                               items, rev, 0);
+                                                               items, rev);
     return cudaGetLastError();
   }
   note_launch();
   // Segments per warp step / min CTAs per SM, measured on config 4
   // (profiles/r1_blocked_partition.md): inserts 4 / 3 (4 lanes per key;
   // 1 or 2 segments: same or slower); lookups 1 / 8 — 1.54 ms per 2^28 keys,
-  // vs 1.82 (2 segments), 1.89 (4), 2.37 (8): occupancy beats per-lane MLP.
+  // vs 1.82 (2 segments), 1.89 (4), 2.37 (8): occupancy beats per-lane MLP
+  // (round 2: 2 segments at 8 CTAs/SM spill and reach 86 vs 104 Gkeys/s).
+  const unsigned grid = S * groups;
   if constexpr (kInsert) {
     const int q = seg_ins_q();
     if (q == 2)
-      segment_kernel<true, 2, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u, rev);
-    else if (q == 3004)  // test loads .cg
-      segment_kernel<true, 4, 3, true, false, 1><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups,
-                                                                                    ans, per_cta, nullptr, 0u, rev);
-    else if (q == 4004)  // test loads .nc, no L1 allocation
-      segment_kernel<true, 4, 3, true, false, 2><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups,
-                                                                                    ans, per_cta, nullptr, 0u, rev);
-    else if (q == 5004)  // .cg test loads at 4 CTAs/SM (64 registers)
-      segment_kernel<true, 4, 4, true, false, 1><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups,
-                                                                                    ans, per_cta, nullptr, 0u, rev);
-    else if ((q == 6008 || q == 6006 || q == 6004) && g.nb_local < 0xffffffffull) {
-      if (q == 6008)
-        segment_insert_lean_kernel<8, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, per_cta,
-                                                                            rev);
-      else if (q == 6006)
-        segment_insert_lean_kernel<6, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, per_cta,
-                                                                            rev);
-      else
-        segment_insert_lean_kernel<4, 5><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, per_cta,
-                                                                            rev);
-    } else if (q == 2004)
-      segment_kernel<true, 4, 3, true, true><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans,
-                                                                                per_cta, nullptr, 0u, rev);
-    else if (q == 1004) {
-      static const int pf = [] {
-        const char* e = getenv("SBBF_SEG_INS_PF");
-        return e ? atoi(e) : 0;
-      }();
-      segment_kernel<true, 4, 3, false><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans,
-                                                                           per_cta, nullptr, 0u, rev, pf);
-    }
+      segment_kernel<true, 2, 4><<<grid, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr,
+                                                              0u, rev);
     else if (q == 8)
-      segment_kernel<true, 8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u, rev);
-    else {
-      // SBBF_SEG_INS_PF (A/B only): bulk L2 prefetch of the slice this many
-      // sweep steps ahead (-1: the CTA's own slice)
-      static const int pf = [] {
-        const char* e = getenv("SBBF_SEG_INS_PF");
-        return e ? atoi(e) : 0;
-      }();
-      segment_kernel<true, 4><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta,
-                                                                 nullptr, 0u, rev, pf);
-    }
-  } else
-  {
-    // SBBF_SEG_SMEM_KB (A/B only): unused dynamic shared memory per lookup
-    // segment CTA, capping its occupancy so a concurrent partition (the
-    // pipelined lookup's side stream) finds room on every SM
-    static const int seg_smem = [] {
-      const char* e = getenv("SBBF_SEG_SMEM_KB");
-      return e ? atoi(e) * 1024 : 0;
-    }();
-    if (seg_smem > 48 * 1024) {
-      static const cudaError_t a = cudaFuncSetAttribute(segment_kernel<false, 1, 8>,
-                                                        cudaFuncAttributeMaxDynamicSharedMemorySize, seg_smem);
-      (void)a;
-    }
-    // SBBF_SEG_LOOK_PF=1 (A/B only): the next step's sectors prefetched into L2
-    static const bool look_pf = [] {
-      const char* e = getenv("SBBF_SEG_LOOK_PF");
-      return e && e[0] == '1';
-    }();
-    // SBBF_SEG_FLAT=1 (A/B only): the flat-sequence lookup sweep
-    static const bool flat = [] {
-      const char* e = getenv("SBBF_SEG_FLAT");
-      return e && e[0] == '1';
-    }();
-    // SBBF_SEG_LOOK_Q=3 (A/B only): two segments per warp step at 8 CTAs/SM
-    static const bool q2x8 = [] {
-      const char* e = getenv("SBBF_SEG_LOOK_Q");
-      return e && atoi(e) == 3;
-    }();
-    if (q2x8)
-      segment_kernel<false, 2, 8><<<S * groups, kSegThreads, seg_smem, s>>>(blocks, g, keys, boffs, m, groups, ans,
-                                                                             per_cta, nullptr, 0u, rev);
-    else if (flat && per_cta <= 128)
-      segment_find_flat_kernel<8><<<S * groups, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta,
-                                                                     rev);
-    else if (look_pf)
-      segment_kernel<false, 1, 8, true, true><<<S * groups, kSegThreads, seg_smem, s>>>(blocks, g, keys, boffs, m,
-                                                                                       groups, ans, per_cta, nullptr, 0u, rev);
+      segment_kernel<true, 8><<<grid, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u,
+                                                           rev);
     else
-      segment_kernel<false, 1, 8><<<S * groups, kSegThreads, seg_smem, s>>>(blocks, g, keys, boffs, m, groups, ans,
-                                                                             per_cta, nullptr, 0u, rev);
+      segment_kernel<true, 4><<<grid, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u,
+                                                           rev);
+  } else {
+    segment_kernel<false, 1, 8><<<grid, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr,
+                                                             0u, rev);
   }
   return cudaGetLastError();
 }
@@ -2369,18 +1970,8 @@ bool pipeline_enabled() {
   return on;
 }
 
-// SBBF_PIPE_BUFS=3 (A/B only): scratch buffers of the pipelined lookup, so a
-// partition can run up to two rounds ahead of the probes.
-int pipe_bufs() {
-  static const int v = [] {
-    const char* e = getenv("SBBF_PIPE_BUFS");
-    return e && atoi(e) == 3 ? 3 : 2;
-  }();
-  return v;
-}
-
 // One batch chunk (m <= blocked_round() keys) through the single-level path.
-// Tile inserts (tile_scatter_kernel / tile_apply_kernel) apply to whole
+// Tile inserts (tile_scatter_kernel / tile_apply_persistent_kernel) apply to whole
 // power-of-two filters of 2^20..2^26 blocks (32 MiB - 2 GiB): S = nb / 2^19
 // slices of 256 tiles of 2048 blocks, slice = the hash's top bits.
 // SBBF_INSERT_TILES=0 selects the segment sweep (A/B only).
@@ -2401,8 +1992,9 @@ cudaError_t insert_tiles(const DeviceInfo& di, uint32_t* blocks, const Geom& g, 
   if (e != cudaSuccess) return e;
   static const cudaError_t a1 = cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      static_cast<int>(sizeof(TileScatterSmem)));
-  static const cudaError_t a2 = cudaFuncSetAttribute(tile_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     static_cast<int>(sizeof(TileApplySmem)));
+  static const cudaError_t a2 =
+      cudaFuncSetAttribute(tile_apply_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sizeof(TileApply2Smem)));
   if (a1 != cudaSuccess) return a1;
   if (a2 != cudaSuccess) return a2;
   const uint32_t groups = static_cast<uint32_t>(tile_groups(m));
@@ -2416,24 +2008,10 @@ cudaError_t insert_tiles(const DeviceInfo& di, uint32_t* blocks, const Geom& g, 
     *sc.flip = !*sc.flip;
   }
   note_launch();
-  // SBBF_TILE_APPLY=1 (A/B): one tile per CTA instead of the persistent kernel
-  static const bool one = [] {
-    const char* v = getenv("SBBF_TILE_APPLY");
-    return v && v[0] == '1';
-  }();
-  if (one) {
-    tile_apply_kernel<<<S * kTilesPerSlice, kTileApplyThreads, sizeof(TileApplySmem), s>>>(blocks, g.nb_global, S,
-                                                                                           sc.keys2, sc.runs, groups,
-                                                                                           rev);
-  } else {
-    static const cudaError_t a3 = cudaFuncSetAttribute(
-        tile_apply_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(TileApply2Smem)));
-    if (a3 != cudaSuccess) return a3;
-    const uint32_t ntiles = S * kTilesPerSlice;
-    tile_apply_persistent_kernel<<<static_cast<unsigned>(ntiles < static_cast<uint32_t>(di.sms) ? ntiles : di.sms),
-                                   kTileP2Threads, sizeof(TileApply2Smem), s>>>(blocks, g.nb_global, S, sc.keys2,
-                                                                                sc.runs, groups, rev);
-  }
+  const uint32_t ntiles = S * kTilesPerSlice;
+  tile_apply_persistent_kernel<<<static_cast<unsigned>(ntiles < static_cast<uint32_t>(di.sms) ? ntiles : di.sms),
+                                 kTileP2Threads, sizeof(TileApply2Smem), s>>>(blocks, g.nb_global, S, sc.keys2, sc.runs,
+                                                                              groups, rev);
   return cudaGetLastError();
 }
 
@@ -2534,8 +2112,8 @@ cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks,
                                    const BlockedPlan& plan, const uint64_t* hashes, uint64_t n, void* out,
                                    bool bits, cudaStream_t s, CallScope* scope) {
   const uint64_t cap = blocked_round();
-  const int nbuf = pipe_bufs();
-  Scratch sc[3];
+  constexpr int nbuf = 2;
+  Scratch sc[nbuf];
   // the handle's side stream and events (created once: creating them per call
   // put 7-13 ms outliers into config-4 steps) and its scratch arena; the
   // scope's lock serialises the enqueue of concurrent callers
@@ -2583,7 +2161,7 @@ cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geo
   if (n == 0) return cudaSuccess;
   const uint64_t cap = n < blocked_round() ? n : blocked_round();  // a multiple of 32 unless n is the whole batch
   const bool pipelined = plan.super_parts == 1 && n > blocked_round() && pipeline_enabled();
-  CallScope scope(plan.ctx, s, scratch_bytes(cap, true) * (pipelined ? pipe_bufs() : 1));
+  CallScope scope(plan.ctx, s, scratch_bytes(cap, true) * (pipelined ? 2 : 1));
   if (scope.error() != cudaSuccess) return scope.error();
   // pipelining needs the handle's side stream: not while a graph is captured
   if (pipelined && scope.arena()) return blocked_find_pipelined(di, blocks, g, plan, hashes, n, out, bits, s, &scope);

@@ -242,26 +242,6 @@ __device__ __forceinline__ uint64_t ld_pair(const uint64_t* p, uint64_t policy) 
   return v;
 }
 
-// Fire-and-forget L2 prefetch of the line holding p (no register result).
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
-}
-
-// Test-before-set reads that skip L1 (no L1 allocation, no sector promotion):
-// .cg (coherent at L2) and the non-coherent read-only path. Either may return
-// a value older than a concurrent red; bits are monotone, so that only costs a
-// redundant red.
-__device__ __forceinline__ uint64_t ld_pair_cg(const uint64_t* p, uint64_t policy) {
-  uint64_t v;
-  asm volatile("ld.global.cg.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(policy));
-  return v;
-}
-__device__ __forceinline__ uint64_t ld_pair_nc(const uint64_t* p, uint64_t policy) {
-  uint64_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(policy));
-  return v;
-}
-
 __device__ __forceinline__ void st_stream_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.global.L1::no_allocate.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

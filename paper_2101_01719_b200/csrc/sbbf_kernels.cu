@@ -684,47 +684,6 @@ bool split_compact() {  // SBBF_SPLIT_COMPACT=0 selects the uncompacted pass ker
   return on;
 }
 
-// SBBF_SPLIT_PERSIST_MB (A/B only): an L2 persisting access-policy window on
-// each range-split pass's filter range, with that many MiB of L2 set aside
-// for persisting lines (0 = off).
-size_t split_persist_bytes() {
-  static const size_t v = [] {
-    const char* e = getenv("SBBF_SPLIT_PERSIST_MB");
-    const long mb = e ? atol(e) : 0;
-    if (mb <= 0) return size_t{0};
-    int dev = 0, mx = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    size_t want = static_cast<size_t>(mb) << 20;
-    if (mx > 0 && want > static_cast<size_t>(mx)) want = static_cast<size_t>(mx);
-    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
-      cudaGetLastError();
-      return size_t{0};
-    }
-    return want;
-  }();
-  return v;
-}
-
-void split_window(cudaLaunchAttribute& a, const uint32_t* blocks, uint64_t nb, int split_log, uint64_t p) {
-  const uint64_t b0 = (p * nb) >> split_log, b1 = ((p + 1) * nb) >> split_log;
-  static const size_t max_win = [] {
-    int dev = 0, w = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&w, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-    return static_cast<size_t>(w > 0 ? w : 0);
-  }();
-  size_t bytes = (b1 - b0) * 32;
-  if (bytes > max_win) bytes = max_win;
-  const double ratio = static_cast<double>(split_persist_bytes()) / static_cast<double>(bytes ? bytes : 1);
-  a.id = cudaLaunchAttributeAccessPolicyWindow;
-  a.val.accessPolicyWindow.base_ptr = const_cast<uint32_t*>(blocks + b0 * 8);
-  a.val.accessPolicyWindow.num_bytes = bytes;
-  a.val.accessPolicyWindow.hitRatio = static_cast<float>(ratio < 1.0 ? ratio : 1.0);
-  a.val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  a.val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-}
-
 int split_log2(const DeviceInfo& di, const Geom& g, bool lookup) {
   if (g.first != 0 || g.nb_local != g.nb_global) return 0;  // top hash bits = block ranges of a whole filter only
   const double part = 0.6 * static_cast<double>(di.l2_bytes);
@@ -762,24 +721,9 @@ cudaError_t launch_insert(const DeviceInfo& di, int variant, uint32_t* blocks, c
     const uint64_t grid = (n + kThreads * 4 - 1) / (kThreads * 4);
     const int split_log = split_log2(di, g, false);
     if (split_log > 0) {
-      for (uint64_t p = 0; p < (uint64_t{1} << split_log); ++p) {
-        if (split_persist_bytes()) {
-          cudaLaunchConfig_t cc = {};
-          cudaLaunchAttribute at[1];
-          split_window(at[0], blocks, g.nb_global, split_log, p);
-          cc.gridDim = dim3(static_cast<unsigned>(grid));
-          cc.blockDim = dim3(kThreads);
-          cc.stream = s;
-          cc.attrs = at;
-          cc.numAttrs = 1;
-          cudaError_t e = cudaLaunchKernelEx(&cc, insert_wide_kernel<false, false, 4, true, true>, blocks, g, hashes,
-                                             n, uint64_t{0}, static_cast<uint32_t>(64 - split_log), p);
-          if (e != cudaSuccess) return e;
-          continue;
-        }
+      for (uint64_t p = 0; p < (uint64_t{1} << split_log); ++p)
         insert_wide_kernel<false, false, 4, true, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(
             blocks, g, hashes, n, 0, static_cast<uint32_t>(64 - split_log), p);
-      }
     } else if (red_hint(di, g))
       insert_wide_kernel<false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(blocks, g, hashes, n);
     else
@@ -919,22 +863,15 @@ cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* block
         for (uint64_t p = 0; p < (uint64_t{1} << split_log) && e == cudaSuccess; ++p) {
           const uint32_t psh = static_cast<uint32_t>(64 - split_log);
           const bool first = p == 0;
-          cudaLaunchAttribute at2[2] = {attr[0], attr[0]};
-          cudaLaunchConfig_t cfgp = cfg;
-          if (split_persist_bytes()) {
-            split_window(at2[1], blocks, g.nb_global, split_log, p);
-            cfgp.attrs = at2;
-            cfgp.numAttrs = 2;
-          }
           if (bits && split_compact()) {
-            cudaLaunchConfig_t cc = cfgp;
+            cudaLaunchConfig_t cc = cfg;
             cc.gridDim = dim3(static_cast<unsigned>(grid_for(n, tile * (kThreads / 32), di.sms, occ_c)));
             e = cudaLaunchKernelEx(&cc, ksplit, blocks, g.nb_global, hashes, n,
                                    static_cast<uint32_t*>(out), psh, p, first);
           } else {
-            e = bits ? cudaLaunchKernelEx(&cfgp, find_whole_kernel<kUS, true, kMinS, false, true>, blocks, g.nb_global,
+            e = bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kUS, true, kMinS, false, true>, blocks, g.nb_global,
                                           hashes, n, out, uint64_t{0}, psh, p, first)
-                     : cudaLaunchKernelEx(&cfgp, find_whole_kernel<kUS, false, kMinS, false, true>, blocks,
+                     : cudaLaunchKernelEx(&cfg, find_whole_kernel<kUS, false, kMinS, false, true>, blocks,
                                           g.nb_global, hashes, n, out, uint64_t{0}, psh, p, first);
           }
         }
