@@ -296,6 +296,30 @@ def test_blocked_tile_insert(cuda, oracle, nb):
     assert np.array_equal(f.find_hashes(dev(probes, cuda)).cpu().numpy(), oracle.find_hashes(want, probes))
 
 
+def test_blocked_unaligned_buffers(cuda, oracle):
+    """The TMA partition and unpermute need 16-byte aligned keys and byte
+    output; a caller's hashes at an odd 8-byte offset and a byte output at
+    an odd offset take the LSU kernels instead. Bit-exact either way."""
+    nb = 2**21 + 3
+    rng = np.random.default_rng(0xA11E)
+    hs = rng.integers(0, 2**64, size=4096 * 50 + 7, dtype=np.uint64)
+    probes = np.concatenate([hs[:20_000], rng.integers(0, 2**64, size=4096 * 30 + 5, dtype=np.uint64)])
+    want = oracle.build(nb, hs)
+    want_res = oracle.find_hashes(want, probes)
+    for off in (0, 1):
+        f = SplitBlockFilter(nb)
+        f.set_insert_variant(_lib.INSERT_BLOCKED)
+        f.set_find_variant(_lib.FIND_BLOCKED)
+        d = dev(np.concatenate([np.zeros(off, np.uint64), hs]), cuda)[off:]
+        f.add_hashes(d)
+        assert np.array_equal(f.blocks(), want)
+        p = dev(np.concatenate([np.zeros(off, np.uint64), probes]), cuda)[off:]
+        res = torch.zeros(probes.size + 1, dtype=torch.uint8, device="cuda")[off:]
+        f.find_hashes(p, res)
+        assert np.array_equal(res.cpu().numpy(), want_res)
+        assert np.array_equal(bits_to_bytes(u32(f.find_hashes_bits(p)), probes.size), want_res)
+
+
 @pytest.mark.parametrize("nb", [2**27, 3 * 2**25 + 5, 2**27 + 12345])
 def test_blocked_two_level(cuda, oracle, nb):
     """Filters up to 128 slices of 32 MiB (4 GiB) take the single-level
