@@ -314,7 +314,7 @@ def test_blocked_unaligned_buffers(cuda, oracle):
         f.add_hashes(d)
         assert np.array_equal(f.blocks(), want)
         p = dev(np.concatenate([np.zeros(off, np.uint64), probes]), cuda)[off:]
-        res = torch.zeros(probes.size + 1, dtype=torch.uint8, device="cuda")[off:]
+        res = torch.zeros(probes.size + off, dtype=torch.uint8, device="cuda")[off:]
         f.find_hashes(p, res)
         assert np.array_equal(res.cpu().numpy(), want_res)
         assert np.array_equal(bits_to_bytes(u32(f.find_hashes_bits(p)), probes.size), want_res)
