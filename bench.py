@@ -131,6 +131,42 @@ class ClockSampler:
 # --------------------------------------------------------------------------------
 # device-timed config runs
 # --------------------------------------------------------------------------------
+KERNEL_KINDS = ["partition", "probe_sweep", "insert_sweep", "unpermute", "tile_insert"]
+
+
+def kernel_times(step, steps: int, device):
+    """Live per-kernel times of the L2-blocked path: `steps` extra steps with
+    the library's event pairs around every blocked launch group
+    (sbbf_bench_kernel_timing), summed per kind; None when nothing blocked ran.
+    These steps are not the headline's (their events add gaps)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2101_01719_b200 import _lib
+    L = _lib.lib()
+    L.sbbf_bench_kernel_timing(1)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+    try:
+        for k in range(steps):
+            step(evs[k])
+        torch.cuda.synchronize(device)
+        ms = (C.c_double * len(KERNEL_KINDS))()
+        n = (C.c_uint64 * len(KERNEL_KINDS))()
+        rc = L.sbbf_bench_kernel_times(ms, n, len(KERNEL_KINDS))
+    finally:
+        L.sbbf_bench_kernel_timing(0)
+    if rc != 0 or sum(n) == 0:
+        return None
+    t_step = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    return {"ms_per_step": t_step, "steps": steps,
+            "kinds": {k: {"ms_per_step": ms[i] / steps, "launch_groups_per_step": n[i] / steps,
+                          "share_of_step": ms[i] / steps / t_step}
+                      for i, k in enumerate(KERNEL_KINDS) if n[i]},
+            "how": "CUDA event pairs recorded by the library around each blocked-path launch group on its "
+                   "stream (sbbf_bench_kernel_timing), in separate untimed steps"}
+
+
 def run_config_device(cid: int, steps: int, warmup: int, device, collect_parity=True) -> dict:
     import numpy as np
     import torch
@@ -193,6 +229,7 @@ def run_config_device(cid: int, steps: int, warmup: int, device, collect_parity=
     torch.cuda.synchronize(device)
     t_ins = [e[0].elapsed_time(e[1]) for e in evb]
     t_find = [e[1].elapsed_time(e[2]) for e in evb]
+    ktimes = kernel_times(lambda ev: (f.clear(), flush_l2(), one_step(ev)), min(steps, 3), device)
     out = {
         "config": cid, "name": cfg.name, "num_buckets": cfg.num_buckets,
         "filter_bytes": cfg.filter_bytes, "inserts": N, "lookups": L,
@@ -206,6 +243,8 @@ def run_config_device(cid: int, steps: int, warmup: int, device, collect_parity=
         "launches_per_step": launches / steps,
         "insert_variant": f.resolved_variants(chunk)[0], "find_variant": f.resolved_variants(L)[1],
     }
+    if ktimes:
+        out["kernel_times"] = ktimes
     out["value"] = (N + L) / (out["ms_per_step"] * 1e-3) / 1e9
     # the reference's run_bench reports the median of its reps
     # (harness.cpp:233-242): printed beside the mean
@@ -629,7 +668,58 @@ def roofline(res: dict, hbm_peak: float, peak_note: str, l2_bytes: int, l2_read_
           "traffic_note": ("ncu DRAM bytes of every kernel of the insert phase "
                            f"({ti['source']}), {ti['dram_bytes_per_key']:.2f} B/key" if ti else
                            "no ncu capture committed for this config")}
+    kt = res.get("kernel_times")
+    if kt:
+        rl["dominant_kernel"], rl["kernels"] = kernel_rooflines(res, kt, hbm_peak)
     return rl, ri
+
+
+# SM count and clock of the part: the L2->SM sector port moves one 32-B sector
+# per SM-clock (148 x 1.965 GHz = 290.8 G sectors/s; the round-1 microbenchmark
+# measured 288 G/s for random 32-B reads of an L2-resident buffer).
+SMS, SM_GHZ = 148, 1.965
+
+
+def kernel_rooflines(res: dict, kt: dict, hbm_peak: float):
+    """Each blocked-path kernel kind against its own bound, from the live
+    per-kind times (kernel_times): achieved = algorithmic bytes (or sectors)
+    per launch group / its average live duration. The dominant kind is the
+    one with the largest share of the step."""
+    N, L = res["inserts"], res["lookups"]
+    port_peak = SMS * SM_GHZ  # G sectors/s
+    out = {}
+    for kind, v in kt["kinds"].items():
+        groups, ms = v["launch_groups_per_step"], v["ms_per_step"]
+        avg_ms = ms / groups
+        d = {"launch_groups_per_step": groups, "avg_launch_group_ms": avg_ms, "share_of_step": v["share_of_step"]}
+        if kind == "probe_sweep":
+            keys = L / groups
+            d.update({"keys_per_launch": keys, "bound": "L2->SM sector port (1 sector / SM-clock)",
+                      "algorithmic": "one 32-B probe sector + 8-B key per lookup (1.25 sectors)",
+                      "achieved_gsectors_s": keys * 1.25 / (avg_ms * 1e-3) / 1e9, "peak_gsectors_s": port_peak,
+                      "frac": keys * 1.25 / (avg_ms * 1e-3) / 1e9 / port_peak,
+                      "north_star_gbs": keys * 32 / (avg_ms * 1e-3) / 1e9})
+        elif kind == "insert_sweep":
+            keys = N / groups
+            d.update({"keys_per_launch": keys, "bound": "L2 test-and-red rate (DESIGN.md section 3)",
+                      "achieved_gkeys_s": keys / (avg_ms * 1e-3) / 1e9,
+                      "north_star_gbs": keys * 64 / (avg_ms * 1e-3) / 1e9,
+                      "north_star_frac": keys * 64 / (avg_ms * 1e-3) / 1e9 / hbm_peak})
+        elif kind == "partition":
+            # every insert call and lookup round: keys read once, written bucket-major
+            # (+ 2-B positions for lookups)
+            byts = (N * 16 + L * 18) / groups
+            d.update({"bound": "hbm", "algorithmic_bytes_per_launch": byts,
+                      "achieved_gbs": byts / (avg_ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
+                      "frac": byts / (avg_ms * 1e-3) / 1e9 / hbm_peak})
+        elif kind == "unpermute":
+            byts = L * (1 + 2 + 1 / 8) / groups
+            d.update({"bound": "hbm", "algorithmic_bytes_per_launch": byts,
+                      "achieved_gbs": byts / (avg_ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
+                      "frac": byts / (avg_ms * 1e-3) / 1e9 / hbm_peak})
+        out[kind] = d
+    dom = max(out, key=lambda k: out[k]["share_of_step"])
+    return dict(kernel=dom, **out[dom]), out
 
 
 def main() -> None:

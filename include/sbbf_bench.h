@@ -25,6 +25,16 @@ int sbbf_bench_sector_read(const uint32_t* d_buf, uint64_t num_blocks, uint64_t 
 int sbbf_bench_sector_red(uint32_t* d_buf, uint64_t num_blocks, uint64_t n, uint64_t seed,
                           void* stream);
 
+/* Live per-kernel timing of the L2-blocked path (bench.py's dominant-kernel
+ * roofline). enable != 0 starts recording a CUDA event pair around every
+ * blocked-path launch group on its stream and clears the totals; 0 stops.
+ * sbbf_bench_kernel_times synchronises the recorded events and returns the
+ * summed milliseconds and launch-group counts per kind, up to n kinds:
+ * 0 partition (chunk_scatter), 1 lookup probe sweep, 2 insert sweep,
+ * 3 unpermute, 4 tile insert (tile_scatter + tile_apply). */
+int sbbf_bench_kernel_timing(int enable);
+int sbbf_bench_kernel_times(double* ms, uint64_t* launches, int n);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

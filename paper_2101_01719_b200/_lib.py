@@ -121,6 +121,8 @@ PROTOTYPES = {
     "sbbf_gen_inserts": (_i, [_vp, _u64, _u64, _vp, _vp]),
     "sbbf_bench_sector_read": (_i, [_vp, _u64, _u64, _u64, _vp, _vp]),
     "sbbf_bench_sector_red": (_i, [_vp, _u64, _u64, _u64, _vp]),
+    "sbbf_bench_kernel_timing": (_i, [_i]),
+    "sbbf_bench_kernel_times": (_i, [_vp, _vp, _i]),
     "sbbf_gen_lookups": (_i, [_vp, _u64, _u64, _u64, _u64, _u64, _u64, _u64, _vp, _vp]),
 }
 

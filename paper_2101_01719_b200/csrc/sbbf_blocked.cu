@@ -33,6 +33,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <new>
+#include <tuple>
 #include <vector>
 
 #include "sbbf_device.cuh"
@@ -51,6 +52,60 @@ uint64_t blocked_round() {
   }();
   return v;
 }
+
+// ---------------------------------------------------------------------------
+// per-kernel live timing for bench.py (sbbf_bench_kernel_timing / _times)
+// ---------------------------------------------------------------------------
+// When enabled, every blocked-path launch group is bracketed by two CUDA
+// events on its stream; sbbf_bench_kernel_times() synchronises them and sums
+// the durations per kind. Off by default (no events are recorded).
+enum KernelKind { kKPartition = 0, kKProbe = 1, kKInsertSweep = 2, kKUnpermute = 3, kKTile = 4, kKNum = 5 };
+
+struct KTimer {
+  std::mutex mu;
+  std::atomic<bool> on{false};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> pending;
+  double ms[kKNum] = {};
+  uint64_t n[kKNum] = {};
+};
+KTimer& ktimer() {
+  static KTimer* t = new KTimer;  // never destroyed: events may outlive static teardown order
+  return *t;
+}
+
+class KTime {
+ public:
+  KTime(int kind, cudaStream_t s) : kind_(kind), s_(s) {
+    KTimer& t = ktimer();
+    if (!t.on.load(std::memory_order_relaxed)) return;
+    std::lock_guard<std::mutex> lock(t.mu);
+    if (t.pool.empty()) {
+      cudaEvent_t a = nullptr, b = nullptr;
+      if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+      }
+      t.pool.emplace_back(a, b);
+    }
+    ev_ = t.pool.back();
+    t.pool.pop_back();
+    active_ = cudaEventRecord(ev_.first, s_) == cudaSuccess;
+  }
+  ~KTime() {
+    if (!active_) return;
+    KTimer& t = ktimer();
+    cudaEventRecord(ev_.second, s_);
+    std::lock_guard<std::mutex> lock(t.mu);
+    t.pending.emplace_back(kind_, ev_.first, ev_.second);
+  }
+
+ private:
+  int kind_;
+  cudaStream_t s_;
+  std::pair<cudaEvent_t, cudaEvent_t> ev_{nullptr, nullptr};
+  bool active_ = false;
+};
 
 // ---------------------------------------------------------------------------
 // bucket partition
@@ -1571,6 +1626,7 @@ bool unperm_tma() {
 // Answers of m keys (chunk layout) back to source order into `dst`.
 cudaError_t launch_unpermute(const DeviceInfo& di, const uint8_t* ans, const uint16_t* pos16, uint64_t m, void* dst,
                              bool bits, cudaStream_t s) {
+  KTime kt(kKUnpermute, s);
   const uint64_t nfull = m / kPartChunk;
   // byte output needs 16-byte aligned chunk rows; bit output 4-byte words
   const bool aligned = bits || (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
@@ -1638,6 +1694,7 @@ cudaError_t chunk_partition_bits(const DeviceInfo& di, const BucketMap& bm, cons
 
 cudaError_t chunk_partition(const DeviceInfo& di, const Geom& g, uint32_t S, const uint64_t* hashes, uint64_t m,
                             uint64_t* out, uint16_t* pos16, uint16_t* boffs, cudaStream_t s) {
+  KTime kt(kKPartition, s);
   const BucketMap bm = make_map(g, S);
   switch (bm.bits * 2 + (bm.top_bits ? 1 : 0)) {
 #define SBBF_CHUNK_CASE(B)                                                                  \
@@ -1687,6 +1744,7 @@ template <bool kInsert>
 cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* keys, const uint16_t* boffs, uint32_t S,
                             uint64_t m, uint8_t* ans, cudaStream_t s, unsigned* work = nullptr,
                             const DeviceInfo* di = nullptr, bool* flip = nullptr) {
+  KTime kt(kInsert ? kKInsertSweep : kKProbe, s);
   // alternate the sweep direction per handle (SBBF_SEG_ALTERNATE=0 disables it: A/B only)
   static const bool alt = [] {
     const char* v = getenv("SBBF_SEG_ALTERNATE");
@@ -1998,6 +2056,7 @@ cudaError_t insert_tiles(const DeviceInfo& di, uint32_t* blocks, const Geom& g, 
   if (a1 != cudaSuccess) return a1;
   if (a2 != cudaSuccess) return a2;
   const uint32_t groups = static_cast<uint32_t>(tile_groups(m));
+  KTime kt(kKTile, s);
   note_launch();
   tile_scatter_kernel<<<S * groups, kTileScatterThreads, sizeof(TileScatterSmem), s>>>(g.nb_global, S, sc.keys,
                                                                                        sc.boffs, m, groups, sc.keys2,
@@ -2273,3 +2332,40 @@ cudaError_t blocked_find_regions(const DeviceInfo& di, const uint32_t* blocks, c
 }
 
 }  // namespace sbbf
+
+extern "C" int sbbf_bench_kernel_timing(int enable) {
+  sbbf::KTimer& t = sbbf::ktimer();
+  std::lock_guard<std::mutex> lock(t.mu);
+  for (auto& p : t.pending) t.pool.emplace_back(std::get<1>(p), std::get<2>(p));
+  t.pending.clear();
+  for (int k = 0; k < sbbf::kKNum; ++k) {
+    t.ms[k] = 0;
+    t.n[k] = 0;
+  }
+  t.on.store(enable != 0, std::memory_order_relaxed);
+  return SBBF_OK;
+}
+
+extern "C" int sbbf_bench_kernel_times(double* ms, uint64_t* launches, int n) {
+  sbbf::KTimer& t = sbbf::ktimer();
+  std::lock_guard<std::mutex> lock(t.mu);
+  int rc = SBBF_OK;
+  for (auto& p : t.pending) {
+    float e = 0;
+    const cudaEvent_t a = std::get<1>(p), b = std::get<2>(p);
+    if (cudaEventSynchronize(b) == cudaSuccess && cudaEventElapsedTime(&e, a, b) == cudaSuccess) {
+      t.ms[std::get<0>(p)] += e;
+      t.n[std::get<0>(p)] += 1;
+    } else {
+      cudaGetLastError();
+      rc = SBBF_ECUDA;
+    }
+    t.pool.emplace_back(a, b);
+  }
+  t.pending.clear();
+  for (int k = 0; k < n && k < sbbf::kKNum; ++k) {
+    if (ms) ms[k] = t.ms[k];
+    if (launches) launches[k] = t.n[k];
+  }
+  return rc;
+}
