@@ -1545,7 +1545,7 @@ struct UnpermTmaSmem {
   alignas(8) uint64_t bar[2];
 };
 
-__global__ void __launch_bounds__(kUnpermThreads, 4)
+__global__ void __launch_bounds__(kUnpermThreads, 8)
     unpermute_tma_kernel(const uint8_t* __restrict__ ans, const uint16_t* __restrict__ pos16, uint64_t nfull,
                          void* __restrict__ out, bool bits) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1634,7 +1634,14 @@ cudaError_t launch_unpermute(const DeviceInfo& di, const uint8_t* ans, const uin
     static const cudaError_t attr = cudaFuncSetAttribute(
         unpermute_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(UnpermTmaSmem)));
     if (attr != cudaSuccess) return attr;
-    const uint64_t cap = static_cast<uint64_t>(di.sms) * 4;
+    // SBBF_UNPERM_CTAS (A/B only): resident CTAs per SM (28 KB smem each;
+    // 8: 0.205 ms per 2^28-key round, 4: 0.214, profiles/r2_ab/r2aq_*)
+    static const uint64_t per_sm = [] {
+      const char* e = getenv("SBBF_UNPERM_CTAS");
+      const int v = e ? atoi(e) : 0;
+      return static_cast<uint64_t>(v > 0 && v <= 8 ? v : 8);
+    }();
+    const uint64_t cap = static_cast<uint64_t>(di.sms) * per_sm;
     note_launch();
     unpermute_tma_kernel<<<static_cast<unsigned>(nfull < cap ? nfull : cap), kUnpermThreads, sizeof(UnpermTmaSmem),
                            s>>>(ans, pos16, nfull, dst, bits);
