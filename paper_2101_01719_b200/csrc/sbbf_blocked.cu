@@ -996,7 +996,8 @@ constexpr int kTileBits = 8;
 constexpr uint32_t kTilesPerSlice = 1u << kTileBits;
 constexpr uint32_t kTileBlocks = 2048;  // 64 KiB
 constexpr int kTileLog2 = 11;
-constexpr uint32_t kTileGroupChunks = 64;  // chunks per tile_scatter CTA
+constexpr uint32_t kTileGroupChunks = 48;  // chunks per tile_scatter CTA (~3072 keys: one smem piece)
+constexpr uint32_t kTileSegTable = 64;     // run-table capacity (warp-0 scan: 2 entries per lane)
 constexpr int kTileScatterThreads = 512;
 constexpr int kTileScatterWarps = kTileScatterThreads / 32;
 constexpr int kTilePiece = 4096;           // keys placed per smem pass
@@ -1006,14 +1007,17 @@ struct TileScatterSmem {
   uint64_t key[kTilePiece];   // one piece staged tile-major
   uint8_t tile[kTilePiece];
   uint16_t kp[kTilePiece + 1];  // exclusive prefix of kept slots (staged order); kp[pn] = kept
-  uint32_t wcnt[kTileScatterWarps][kTilesPerSlice];
+  union {
+    uint32_t wcnt[kTileScatterWarps][kTilesPerSlice];  // multisplit counters (several pieces)
+    uint32_t map[kTilePiece];                          // flat position -> key index (one piece)
+  } u;
   uint32_t poff[kTilesPerSlice];  // piece-local staged offset of each tile (before dedup)
   uint32_t off[kTilesPerSlice];   // CTA: kept-key offset of each tile (several pieces)
   uint32_t cur[kTilesPerSlice];   // CTA: kept keys of each tile written so far
   uint32_t wsum[kTileScatterWarps];
-  uint32_t s_start[kTileGroupChunks];
-  uint32_t s_pre[kTileGroupChunks + 1];
-  uint32_t s_st[kTileGroupChunks];
+  uint32_t s_start[kTileSegTable];
+  uint32_t s_pre[kTileSegTable + 1];
+  uint32_t s_st[kTileSegTable];
 };
 
 // key index of flat position pos within the CTA's runs: the last run whose
@@ -1091,6 +1095,8 @@ __device__ __forceinline__ uint32_t scan256_warp0(const uint32_t* a, uint32_t* o
   return __shfl_sync(0xffffffffu, incl, 31);
 }
 
+__device__ __forceinline__ void tile_dedup(TileScatterSmem& sm, uint32_t pn, uint32_t lane, uint32_t warp);
+
 // One piece of up to kTilePiece flat keys: loaded, ranked by tile, staged
 // tile-major in smem, then de-duplicated — a slot whose key equals the slot
 // before it in the same tile's run is dropped (config 4's hot keys arrive as
@@ -1117,13 +1123,13 @@ __device__ __forceinline__ void tile_piece(TileScatterSmem& sm, const uint64_t* 
     if (!valid) tl[j] = 0xffffffffu;
   }
 #pragma unroll
-  for (int i = 0; i < owned<kTileBits>(); ++i) sm.wcnt[warp][lane + 32 * i] = c[i];
+  for (int i = 0; i < owned<kTileBits>(); ++i) sm.u.wcnt[warp][lane + 32 * i] = c[i];
   __syncthreads();
-  if (warp == 0) tile_scan_warp0(sm.wcnt, sm.poff, lane);
+  if (warp == 0) tile_scan_warp0(sm.u.wcnt, sm.poff, lane);
   __syncthreads();
   uint32_t sbase[owned<kTileBits>()];
 #pragma unroll
-  for (int i = 0; i < owned<kTileBits>(); ++i) sbase[i] = sm.poff[lane + 32 * i] + sm.wcnt[warp][lane + 32 * i];
+  for (int i = 0; i < owned<kTileBits>(); ++i) sbase[i] = sm.poff[lane + 32 * i] + sm.u.wcnt[warp][lane + 32 * i];
 #pragma unroll
   for (int j = 0; j < kTilePerThread; ++j) {
     const uint32_t loc = slot_base<kTileBits>(tl[j] & 0xffu, sbase) + off[j];
@@ -1134,6 +1140,12 @@ __device__ __forceinline__ void tile_piece(TileScatterSmem& sm, const uint64_t* 
     }
   }
   __syncthreads();
+  tile_dedup(sm, pn, lane, warp);
+}
+
+// Drop staged slots whose key equals the previous slot of the same tile run;
+// sm.kp = exclusive prefix of the kept slots (kp[pn] = kept). Ends on a barrier.
+__device__ __forceinline__ void tile_dedup(TileScatterSmem& sm, uint32_t pn, uint32_t lane, uint32_t warp) {
   // keep flags of 8 consecutive staged slots per thread, block-wide prefix
   const uint32_t i0 = threadIdx.x * kTilePerThread;
   uint32_t keep = 0, cnt = 0;
@@ -1193,7 +1205,7 @@ __global__ void __launch_bounds__(kTileScatterThreads, 2)
   const uint64_t pol = dev::policy_evict_first();
   // segment table: run starts, prefix of lengths; this CTA's output base =
   // group region + the keys of slices < b in the group's chunks
-  if (threadIdx.x < kTileGroupChunks) {
+  if (threadIdx.x < kTileSegTable) {
     uint32_t st = 0, len = 0;
     if (threadIdx.x < nseg) {
       const uint64_t ch = c0 + threadIdx.x;
@@ -1217,7 +1229,7 @@ __global__ void __launch_bounds__(kTileScatterThreads, 2)
     }
     sm.s_pre[2 * lane] = incl - v0 - v1;
     sm.s_pre[2 * lane + 1] = incl - v1;
-    if (lane == 31) sm.s_pre[kTileGroupChunks] = incl;
+    if (lane == 31) sm.s_pre[kTileSegTable] = incl;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) a0 += __shfl_xor_sync(0xffffffffu, a0, d);
     if (lane == 0) sm.s_st[0] = a0;  // sum of starts: keys of slices < b in the group
@@ -1227,9 +1239,44 @@ __global__ void __launch_bounds__(kTileScatterThreads, 2)
   const uint64_t base = c0 * kPartChunk + sm.s_st[0];
   uint32_t* r = runs + static_cast<uint64_t>(blockIdx.x) * (kTilesPerSlice + 1);
   if (n <= static_cast<uint32_t>(kTilePiece)) {
-    // one piece: staged order is the output order (kept slots only)
-    uint32_t seg = 0;
-    tile_piece(sm, keys, 0, n, nseg, seg, nb, slice_first, pol, om, lane, warp);
+    // One piece: a counting sort by tile through shared-memory atomics (tile
+    // order within a run does not matter for inserts), keys addressed through
+    // a flat-position map built from the run table. Staged order is the
+    // output order (kept slots only).
+    for (uint32_t r = warp; r < nseg; r += kTileScatterWarps) {
+      const uint32_t st = sm.s_start[r], p = sm.s_pre[r], len = sm.s_pre[r + 1] - p;
+      for (uint32_t k = lane; k < len; k += 32) sm.u.map[p + k] = st + k;
+    }
+    for (uint32_t t = threadIdx.x; t < kTilesPerSlice; t += kTileScatterThreads) sm.off[t] = 0;
+    __syncthreads();
+    uint64_t h[kTilePerThread];
+    uint32_t tl[kTilePerThread];
+#pragma unroll
+    for (int j = 0; j < kTilePerThread; ++j) {
+      const uint32_t f = j * kTileScatterThreads + threadIdx.x;
+      h[j] = f < n ? dev::ld_stream_u64(keys + sm.u.map[f], pol) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < kTilePerThread; ++j) {
+      const uint32_t f = j * kTileScatterThreads + threadIdx.x;
+      tl[j] = static_cast<uint32_t>((dev::block_index(h[j], nb) - slice_first) >> kTileLog2);
+      if (f < n) atomicAdd(&sm.off[tl[j]], 1u);
+    }
+    __syncthreads();
+    if (warp == 0) scan256_warp0(sm.off, sm.poff, lane);
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < kTilesPerSlice; t += kTileScatterThreads) sm.cur[t] = sm.poff[t];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kTilePerThread; ++j) {
+      if (j * kTileScatterThreads + threadIdx.x < n) {
+        const uint32_t pos = atomicAdd(&sm.cur[tl[j]], 1u);
+        sm.key[pos] = h[j];
+        sm.tile[pos] = static_cast<uint8_t>(tl[j]);
+      }
+    }
+    __syncthreads();
+    tile_dedup(sm, n, lane, warp);
     for (uint32_t t = threadIdx.x; t < kTilesPerSlice; t += kTileScatterThreads)
       r[t] = static_cast<uint32_t>(base + sm.kp[sm.poff[t]]);
     if (threadIdx.x == 0) r[kTilesPerSlice] = static_cast<uint32_t>(base + sm.kp[n]);
