@@ -879,13 +879,15 @@ uint32_t seg_items_chunks() {
   return v;
 }
 // SBBF_SEG_CHUNKS overrides the chunks per segment CTA (A/B only)
-uint32_t seg_chunks_per_cta() {
+// Config 4 (profiles/r2_ab/r2au_*): inserts 32 chunks per CTA (56.3 vs 55.4
+// Gkeys/s at 64), lookups 64 (107.1 vs 105.4 at 32; 96: 101.3, 128: 90.3).
+uint32_t seg_chunks_per_cta(bool insert) {
   static const uint32_t v = [] {
     const char* e = getenv("SBBF_SEG_CHUNKS");
     const int x = e ? atoi(e) : 0;
-    return x > 0 ? static_cast<uint32_t>(x) : kSegChunksPerCta;
+    return x > 0 ? static_cast<uint32_t>(x) : 0u;
   }();
-  return v;
+  return v ? v : insert ? kSegChunksPerCta / 2 : kSegChunksPerCta;
 }
 
 // One work item: bucket b over chunks [c_begin, c_end).
@@ -1811,7 +1813,7 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
   }
   const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
   const bool persist = work && di && seg_persist(kInsert);
-  const uint32_t per_cta = persist ? seg_items_chunks() : seg_chunks_per_cta();
+  const uint32_t per_cta = persist ? seg_items_chunks() : seg_chunks_per_cta(kInsert);
   const uint32_t groups = static_cast<uint32_t>((nchunks + per_cta - 1) / per_cta);
   if (persist) {
     const uint32_t items = S * groups;
