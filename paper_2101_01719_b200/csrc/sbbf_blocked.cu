@@ -879,15 +879,15 @@ uint32_t seg_items_chunks() {
   return v;
 }
 // SBBF_SEG_CHUNKS overrides the chunks per segment CTA (A/B only)
-// Config 4 (profiles/r2_ab/r2au_*): inserts 32 chunks per CTA (56.3 vs 55.4
-// Gkeys/s at 64), lookups 64 (107.1 vs 105.4 at 32; 96: 101.3, 128: 90.3).
+// Config 4 (profiles/r2_ab/r2au_*, r2ax_*): inserts 16 chunks per CTA at 2
+// segments per warp step, lookups 64 (107.1 vs 105.4 at 32; 96: 101.3, 128: 90.3).
 uint32_t seg_chunks_per_cta(bool insert) {
   static const uint32_t v = [] {
     const char* e = getenv("SBBF_SEG_CHUNKS");
     const int x = e ? atoi(e) : 0;
     return x > 0 ? static_cast<uint32_t>(x) : 0u;
   }();
-  return v ? v : insert ? kSegChunksPerCta / 2 : kSegChunksPerCta;
+  return v ? v : insert ? kSegChunksPerCta / 4 : kSegChunksPerCta;
 }
 
 // One work item: bucket b over chunks [c_begin, c_end).
@@ -1783,7 +1783,9 @@ bool seg_persist(bool insert) {
 }
 
 // SBBF_SEG_INS_Q (A/B only): segments per warp step of the insert segment
-// kernel (2, 4 = default, 8). Measured and removed (profiles/r2_ab): plain
+// kernel (2 = default, 4, 8). Config 4 inserts (profiles/r2_ab/r2ax_*, r2ay_*):
+// 2 segments x 16 chunks per CTA 57.1 Gkeys/s, 4 x 32 56.2, 4 x 64 55.4,
+// 8 x 64 54.1, 1 x 16 54.2. Measured and removed (profiles/r2_ab): plain
 // reds without the test load (8.5 Gkeys/s on config 4: the hot keys' reds
 // serialise at L2), .cg / .nc test loads, an L2 prefetch of the next step's
 // lines, bulk prefetch of the slice ahead, 4 CTAs/SM at 64 registers.
@@ -1791,7 +1793,7 @@ int seg_ins_q() {
   static const int v = [] {
     const char* e = getenv("SBBF_SEG_INS_Q");
     const int x = e ? atoi(e) : 4;
-    return (x == 2 || x == 8) ? x : 4;
+    return (x == 4 || x == 8) ? x : 2;
   }();
   return v;
 }
@@ -1838,23 +1840,23 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
     return cudaGetLastError();
   }
   note_launch();
-  // Segments per warp step / min CTAs per SM, measured on config 4
-  // (profiles/r1_blocked_partition.md): inserts 4 / 3 (4 lanes per key;
-  // 1 or 2 segments: same or slower); lookups 1 / 8 — 1.54 ms per 2^28 keys,
-  // vs 1.82 (2 segments), 1.89 (4), 2.37 (8): occupancy beats per-lane MLP
-  // (round 2: 2 segments at 8 CTAs/SM spill and reach 86 vs 104 Gkeys/s).
+  // Segments per warp step / min CTAs per SM, measured on config 4: inserts
+  // 2 / 4 at 16 chunks per CTA (seg_ins_q); lookups 1 / 8 — 1.54 ms per 2^28
+  // keys, vs 1.82 (2 segments), 1.89 (4), 2.37 (8): occupancy beats per-lane
+  // MLP (profiles/r1_blocked_partition.md; round 2: 2 segments at 8 CTAs/SM
+  // spill and reach 86 vs 104 Gkeys/s).
   const unsigned grid = S * groups;
   if constexpr (kInsert) {
     const int q = seg_ins_q();
-    if (q == 2)
-      segment_kernel<true, 2, 4><<<grid, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr,
-                                                              0u, rev);
+    if (q == 4)
+      segment_kernel<true, 4><<<grid, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u,
+                                                           rev);
     else if (q == 8)
       segment_kernel<true, 8><<<grid, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u,
                                                            rev);
     else
-      segment_kernel<true, 4><<<grid, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u,
-                                                           rev);
+      segment_kernel<true, 2, 4><<<grid, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr,
+                                                              0u, rev);
   } else {
     segment_kernel<false, 1, 8><<<grid, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr,
                                                              0u, rev);
