@@ -891,11 +891,20 @@ uint32_t seg_chunks_per_cta(bool insert) {
 }
 
 // One work item: bucket b over chunks [c_begin, c_end).
-template <bool kInsert, int kSegQ>
+// Insert dedup table (kDedup): a per-CTA direct-mapped set of the hashes this
+// CTA has already ORed, indexed by the hash's low bits. Entry e starts as
+// e ^ 1, which no hash indexed to e can equal, so a hit is always a hash this
+// CTA has issued its reds for and skipping it is exact (OR is idempotent and
+// the reds land before the kernel ends). It replaces the test-before-set load:
+// config 4's hot keys are caught in shared memory, and distinct keys cost one
+// L2 atomic instead of a test load plus an atomic.
+constexpr uint32_t kDedupSlots = 2048;
+
+template <bool kInsert, int kSegQ, bool kDedup = false>
 __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, const Geom& g,
                                              const uint64_t* __restrict__ keys, const uint16_t* __restrict__ boffs,
                                              uint64_t m, uint8_t* __restrict__ ans, uint32_t b, uint64_t c_begin,
-                                             uint64_t c_end) {
+                                             uint64_t c_end, uint64_t* __restrict__ dtab = nullptr) {
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t pol = dev::policy_evict_first();
   const uint64_t keep = dev::policy_evict_last();
@@ -926,7 +935,9 @@ __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, cons
 #pragma unroll
       for (int q = 0; q < kSegQ; ++q)
         hn[q] = (lane >> 2) < len[q] ? dev::ld_stream_u64(keys + seg[q] + (lane >> 2), pol) : 0;
-      for (uint32_t j = lane >> 2; j < maxlen; j += 8) {
+      // warp-uniform trip count (the dedup path synchronises the warp)
+      for (uint32_t j0 = 0; j0 < maxlen; j0 += 8) {
+        const uint32_t j = j0 + (lane >> 2);
         uint64_t h[kSegQ];
 #pragma unroll
         for (int q = 0; q < kSegQ; ++q) h[q] = hn[q];
@@ -939,7 +950,18 @@ __device__ __forceinline__ void segment_item(uint32_t* __restrict__ blocks, cons
           const uint32_t low = static_cast<uint32_t>(h[q]);
           ptr[q] = reinterpret_cast<uint64_t*>(blocks + (ok ? blk : 0) * 8) + pair;
           mask[q] = ok ? (static_cast<uint64_t>(dev::lane_bit(low, seed_hi)) << 32) | dev::lane_bit(low, seed_lo) : 0;
-          cur[q] = mask[q] ? dev::ld_pair(ptr[q], keep) : ~0ull;
+          if constexpr (kDedup) {
+            cur[q] = mask[q] && dtab[low & (kDedupSlots - 1)] == h[q] ? ~0ull : 0;
+          } else {
+            cur[q] = mask[q] ? dev::ld_pair(ptr[q], keep) : ~0ull;
+          }
+        }
+        if constexpr (kDedup) {
+          // every lane of a key has read the table before any records it
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < kSegQ; ++q)
+            if (pair == 0 && mask[q] && !cur[q]) dtab[static_cast<uint32_t>(h[q]) & (kDedupSlots - 1)] = h[q];
         }
 #pragma unroll
         for (int q = 0; q < kSegQ; ++q) hn[q] = j + 8 < len[q] ? dev::ld_stream_u64(keys + seg[q] + j + 8, pol) : 0;
@@ -1481,12 +1503,25 @@ __global__ void __launch_bounds__(kTileP2Threads, 1)
 // within about one resident wave of small items whatever the CTA duration
 // spread (a one-shot grid of 64-chunk items keeps 2-3 slices live and reads
 // each slice ~3x from HBM: profiles/r2_*).
-template <bool kInsert, int kSegQ, int kMinB = (kSegQ > 4 ? 2 : 3)>
+template <bool kInsert, int kSegQ, int kMinB = (kSegQ > 4 ? 2 : 3), bool kDedup = false>
 __global__ void __launch_bounds__(kSegThreads, kMinB)
     segment_kernel(uint32_t* __restrict__ blocks, Geom g, const uint64_t* __restrict__ keys,
                    const uint16_t* __restrict__ boffs, uint64_t m, uint32_t groups, uint8_t* __restrict__ ans,
                    uint32_t per_cta, unsigned* __restrict__ work = nullptr, uint32_t items = 0, uint32_t rev = 0) {
   const uint64_t nchunks = (m + kPartChunk - 1) / kPartChunk;
+  if constexpr (kDedup) {
+    static_assert(kInsert, "the dedup table is for inserts");
+    __shared__ uint64_t dtab[kDedupSlots];
+    for (uint32_t e = threadIdx.x; e < kDedupSlots; e += kSegThreads) dtab[e] = e ^ 1u;
+    __syncthreads();
+    uint32_t b = blockIdx.x / groups;
+    if (rev) b = gridDim.x / groups - 1 - b;
+    const uint32_t grp = blockIdx.x % groups;
+    const uint64_t c_begin = static_cast<uint64_t>(grp) * per_cta;
+    const uint64_t c_end = c_begin + per_cta < nchunks ? c_begin + per_cta : nchunks;
+    segment_item<kInsert, kSegQ, true>(blocks, g, keys, boffs, m, ans, b, c_begin, c_end, dtab);
+    return;
+  }
   if (!work) {
     // rev: this sweep runs the slices last-to-first (alternate sweeps do, so a
     // sweep starts on the slices the previous one left in L2)
@@ -1792,10 +1827,20 @@ bool seg_persist(bool insert) {
 int seg_ins_q() {
   static const int v = [] {
     const char* e = getenv("SBBF_SEG_INS_Q");
-    const int x = e ? atoi(e) : 4;
+    const int x = e ? atoi(e) : 2;
     return (x == 4 || x == 8) ? x : 2;
   }();
   return v;
+}
+
+// SBBF_SEG_DEDUP (A/B): 1 = the insert sweep skips hashes its CTA already
+// ORed (shared-memory table) instead of test-loading each key's lane pair.
+bool seg_dedup() {
+  static const bool on = [] {
+    const char* v = getenv("SBBF_SEG_DEDUP");
+    return v && v[0] == '1';
+  }();
+  return on;
 }
 
 template <bool kInsert>
@@ -1848,7 +1893,14 @@ cudaError_t launch_segments(uint32_t* blocks, const Geom& g, const uint64_t* key
   const unsigned grid = S * groups;
   if constexpr (kInsert) {
     const int q = seg_ins_q();
-    if (q == 4)
+    if (seg_dedup()) {
+      if (q == 4)
+        segment_kernel<true, 4, 3, true><<<grid, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta,
+                                                                      nullptr, 0u, rev);
+      else
+        segment_kernel<true, 2, 4, true><<<grid, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta,
+                                                                      nullptr, 0u, rev);
+    } else if (q == 4)
       segment_kernel<true, 4><<<grid, kSegThreads, 0, s>>>(blocks, g, keys, boffs, m, groups, ans, per_cta, nullptr, 0u,
                                                            rev);
     else if (q == 8)

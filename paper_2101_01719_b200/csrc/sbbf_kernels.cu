@@ -398,7 +398,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 }
 
 // One range-split lookup pass, compacted (bitmap output): each warp takes
-// 256 consecutive keys, moves this pass's keys (top hash bits == pid) to
+// 256 consecutive keys, moves this pass's keys (top 32 hash bits in
+// [lo, lo + span): block_index is monotone in the hash, so that is one
+// contiguous block range) to
 // the front of a per-warp shared buffer with their in-tile index, probes
 // only those (full warps, up to 4 sector loads in flight per lane), and
 // assembles the 8 bitmap words of the 256 keys in shared memory. The first
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks)
 template <int kPU = 4, int kMinSB = 3, int kSplitTile = 256>
 __global__ void __launch_bounds__(kThreads, kMinSB)
     find_split_kernel(const uint32_t* __restrict__ blocks, uint64_t nb, const uint64_t* __restrict__ hashes,
-                      uint64_t n, uint32_t* __restrict__ out, uint32_t psh, uint64_t pid, bool first) {
+                      uint64_t n, uint32_t* __restrict__ out, uint64_t lo, uint64_t span, bool first) {
   __shared__ uint64_t ckey[kThreads / 32][kSplitTile];
   __shared__ uint8_t cidx[kThreads / 32][kSplitTile];
   __shared__ uint32_t cbits[kThreads / 32][kSplitTile / 32];
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, kMinSB)
     uint32_t total = 0;
 #pragma unroll
     for (int k = 0; k < kSplitTile / 32; ++k) {
-      const bool in = base + k * 32 + lane < n && (h[k] >> psh) == pid;
+      const bool in = base + k * 32 + lane < n && (h[k] >> 32) - lo < span;
       const uint32_t bal = __ballot_sync(0xffffffffu, in);
       if (in) {
         const uint32_t pos = total + __popc(bal & ((1u << lane) - 1u));
@@ -860,15 +862,25 @@ cudaError_t launch_find(const DeviceInfo& di, int variant, const uint32_t* block
                                                                  : find_split_kernel<4, 3>;
         const int tile = (sv == 3 || sv == 4 || sv == 5) ? 128 : 256;
         const int occ_c = resident_blocks(ksplit, kThreads, 0);
-        for (uint64_t p = 0; p < (uint64_t{1} << split_log) && e == cudaSuccess; ++p) {
-          const uint32_t psh = static_cast<uint32_t>(64 - split_log);
+        // SBBF_SPLIT_PASSES (A/B only): compacted passes over equal ranges of
+        // the top 32 hash bits (default 2^split_log)
+        static const int np_env = [] {
+          const char* v = getenv("SBBF_SPLIT_PASSES");
+          const int x = v ? atoi(v) : 0;
+          return x >= 2 && x <= 8 ? x : 0;
+        }();
+        const bool compact = bits && split_compact();
+        const uint64_t passes = compact && np_env ? static_cast<uint64_t>(np_env) : uint64_t{1} << split_log;
+        for (uint64_t p = 0; p < passes && e == cudaSuccess; ++p) {
           const bool first = p == 0;
-          if (bits && split_compact()) {
+          if (compact) {
+            const uint64_t lo = (p << 32) / passes, hi = ((p + 1) << 32) / passes;
             cudaLaunchConfig_t cc = cfg;
             cc.gridDim = dim3(static_cast<unsigned>(grid_for(n, tile * (kThreads / 32), di.sms, occ_c)));
-            e = cudaLaunchKernelEx(&cc, ksplit, blocks, g.nb_global, hashes, n,
-                                   static_cast<uint32_t*>(out), psh, p, first);
+            e = cudaLaunchKernelEx(&cc, ksplit, blocks, g.nb_global, hashes, n, static_cast<uint32_t*>(out), lo,
+                                   hi - lo, first);
           } else {
+            const uint32_t psh = static_cast<uint32_t>(64 - split_log);
             e = bits ? cudaLaunchKernelEx(&cfg, find_whole_kernel<kUS, true, kMinS, false, true>, blocks, g.nb_global,
                                           hashes, n, out, uint64_t{0}, psh, p, first)
                      : cudaLaunchKernelEx(&cfg, find_whole_kernel<kUS, false, kMinS, false, true>, blocks,
