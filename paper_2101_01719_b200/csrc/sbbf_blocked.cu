@@ -139,7 +139,23 @@ struct BucketMap {
   uint32_t S, bits;
   const uint64_t* bounds;  // optional exact bucket starts (local block ids), S entries
   bool top_bits;           // whole filter, S = 2^bits: bucket = top bits of the hash
+  // Packed staging (fused lookups, chunk-local partition only): a slot holds
+  // (block offset inside its slice) << 44 | (source position in the chunk) << 32
+  // | the hash's low 32 bits — all the probe and the answer need — instead of
+  // the hash, so no position array is written. pack_shift (top_bits maps) is
+  // 64 - log2(blocks per slice); `sentinel` marks keys outside the shard.
+  uint32_t pack = 0, pack_shift = 0, sentinel = 0;
 };
+
+constexpr int kPackOffBits = 20;                           // slices of <= 2^20 blocks (32 MiB)
+constexpr uint32_t kPackForeign = (1u << kPackOffBits) - 1;  // offset of a key outside the shard (sentinel maps)
+
+// First local block of bucket q under bucket_of's fixed-point map:
+// q = floor(b * mult / 2^32) (clamped to S - 1) is monotone in b, so bucket q
+// starts at ceil(q * 2^32 / mult).
+__host__ __device__ __forceinline__ uint64_t bucket_start(uint64_t q, uint64_t mult) {
+  return ((q << 32) + mult - 1) / mult;
+}
 
 // kTop: the map is a whole filter split into S = 2^bits slices. block_index
 // is monotone in the hash, so the hash's top bits split the filter into S
@@ -255,6 +271,37 @@ __device__ __forceinline__ uint32_t slot_base(uint32_t bk, const uint32_t (&base
     if (owned<BITS>() == 1 || (bk >> 5) == static_cast<uint32_t>(i)) r = b;
   }
   return r;
+}
+
+// The value a chunk slot stores: the hash, or (packed maps) what the fused
+// lookup sweep needs of it. `starts` = the CTA's table of bucket starts
+// (maps without top_bits).
+template <bool kTop>
+__device__ __forceinline__ uint64_t slot_value(uint64_t h, uint32_t bk, uint32_t pos, const BucketMap& bm,
+                                               const uint64_t* starts) {
+  if (!bm.pack) return h;
+  uint64_t off;
+  if constexpr (kTop) {
+    // power-of-two filters: a bit field of the hash; otherwise bucket bk's first
+    // block is mulhi(bk << (64 - bits), nb) = (bk * nb) >> bits
+    off = bm.pack_shift ? (h << bm.bits) >> bm.pack_shift
+                        : dev::block_index(h, bm.nb_global) - ((static_cast<uint64_t>(bk) * bm.nb_global) >> bm.bits);
+    SBBF_DCHECK(off < (1u << kPackOffBits));
+  } else {
+    const uint64_t b = dev::block_index(h, bm.nb_global) - bm.first;
+    off = b < bm.nb_local ? b - starts[bk] : kPackForeign;
+    SBBF_DCHECK(b >= bm.nb_local || (b >= starts[bk] && b - starts[bk] < (1u << kPackOffBits) - bm.sentinel));
+  }
+  return off << 44 | static_cast<uint64_t>(pos) << 32 | static_cast<uint32_t>(h);
+}
+
+// Bucket starts of a packed map without top_bits, into shared memory.
+template <bool kTop>
+__device__ __forceinline__ void fill_starts(const BucketMap& bm, uint64_t* starts) {
+  if constexpr (!kTop) {
+    if (bm.pack)
+      for (uint32_t q = threadIdx.x; q < bm.S; q += blockDim.x) starts[q] = bucket_start(q, bm.mult);
+  }
 }
 
 // Both passes give CTA c the same contiguous run of chunks, so the count
@@ -611,6 +658,10 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
   const OwnerMasks om(lane);
   const uint64_t pol = dev::policy_evict_first();
   const uint64_t nchunks = (n + kPartChunk - 1) / kPartChunk;
+  // packed maps write no positions: the array's space holds the bucket starts
+  uint64_t* const starts = reinterpret_cast<uint64_t*>(sm.pos);
+  fill_starts<kTop>(bm, starts);
+  if (bm.pack) pos16 = nullptr;
   for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const uint64_t base = ch * kPartChunk;
     const uint32_t cnt = static_cast<uint32_t>(n - base < kPartChunk ? n - base : kPartChunk);
@@ -687,8 +738,8 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
       const uint32_t loc = slot_base<BITS>(bk[j], sbase) + off[j];
       if (bk[j] != 0xffffffffu) {
         SBBF_DCHECK(loc < cnt && bk[j] < bm.S && loc == sm.boff[bk[j]] + sm.wcnt[warp][bk[j]] + off[j]);
-        sm.key[loc] = h[j];
-        sm.pos[loc] = static_cast<uint16_t>(j * kPartThreads + threadIdx.x);
+        sm.key[loc] = slot_value<kTop>(h[j], bk[j], j * kPartThreads + threadIdx.x, bm, starts);
+        if (!bm.pack) sm.pos[loc] = static_cast<uint16_t>(j * kPartThreads + threadIdx.x);
       }
     }
     __syncthreads();
@@ -764,6 +815,10 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const OwnerMasks om(lane);
   constexpr uint32_t kBytes = kPartChunk * sizeof(uint64_t);
+  // packed maps write no positions: the array's space holds the bucket starts
+  uint64_t* const starts = reinterpret_cast<uint64_t*>(sm.pos);
+  fill_starts<kTop>(bm, starts);
+  if (bm.pack) pos16 = nullptr;
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar[0])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&sm.bar[1])));
@@ -845,8 +900,8 @@ __global__ void __launch_bounds__(kPartThreads, kPartMinBlocks)
     for (int j = 0; j < kPartPerThread; ++j) {
       const uint32_t loc = slot_base<BITS>(bk[j], sbase) + off[j];
       SBBF_DCHECK(loc < kPartChunk && bk[j] < bm.S);
-      sm.key[loc] = h[j];
-      sm.pos[loc] = static_cast<uint16_t>(j * kPartThreads + threadIdx.x);
+      sm.key[loc] = slot_value<kTop>(h[j], bk[j], j * kPartThreads + threadIdx.x, bm, starts);
+      if (!bm.pack) sm.pos[loc] = static_cast<uint16_t>(j * kPartThreads + threadIdx.x);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1744,6 +1799,228 @@ cudaError_t launch_unpermute(const DeviceInfo& di, const uint8_t* ans, const uin
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// fused lookup sweep (packed staging, answers gathered in shared memory)
+// ---------------------------------------------------------------------------
+// The segment_kernel + unpermute pair moves 3 B/key of positions and answer
+// bytes through HBM twice and relaunches per round. Here the partition stores
+// packed slots (BucketMap::pack: slice-relative block, source position, low
+// hash bits) and one persistent grid does the rest: every warp owns up to
+// kFusedChunks chunks for the whole sweep, walks the slices in order over its
+// chunks' runs, and sets the bit of each hit at its SOURCE position in the
+// warp's shared-memory copy of those chunks' result bitmaps (one 512-byte row
+// per chunk). When its runs are done it writes the rows out as the caller's
+// bitmap words or bytes. No position array, no answer bytes, no unpermute
+// launch; the warps free-run (equal work per slice keeps them within a slice
+// or two of each other, so the keys in flight still share an L2-resident part
+// of the filter).
+constexpr int kFusedThreads = 256;
+constexpr int kFusedWarps = kFusedThreads / 32;
+constexpr uint32_t kFusedChunks = 8;  // chunks per warp at most (6 CTAs/SM x 32 KB of bitmap rows)
+constexpr uint32_t kRowWords = kPartChunk / 32;
+
+struct FusedArgs {
+  const uint32_t* blocks;
+  const uint64_t* keys;   // packed slots, chunk layout
+  const uint16_t* boffs;  // [nchunks][kBoffStride]
+  void* out;              // bitmap words / bytes of this round, chunk ch at key ch * kPartChunk
+  uint64_t nchunks, m;
+  uint64_t nb_global, nb_local, mult;
+  uint32_t S, bits, W, rev, sentinel, out_bits;
+  // Slice pacing: CTAs count the sweep steps they finish in done[step]; a CTA
+  // enters step k only when every CTA has finished step k - slack, so the
+  // keys in flight span at most `slack` slices (free-running warps drift
+  // apart and thrash L2: ncu, 8 CTAs/SM read the filter 5.4x per round).
+  // Only a locality device: the wait is bounded and results never depend on
+  // it. done == nullptr: free-running.
+  unsigned* done;
+  uint32_t slack;
+};
+
+__device__ __forceinline__ uint32_t ld_relaxed_gpu_u32(const unsigned* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+constexpr uint32_t kPaceMaxPolls = 1u << 13;  // ~4 ms at 500 ns per poll, then the CTA stops pacing
+
+template <bool kTop, int kMinB>
+__global__ void __launch_bounds__(kFusedThreads, kMinB) sweep_find_kernel(const __grid_constant__ FusedArgs a) {
+  extern __shared__ __align__(16) unsigned char fs_raw[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t W = a.W, S = a.S, T = S + 1;
+  uint32_t* const rows = reinterpret_cast<uint32_t*>(fs_raw) + warp * W * kRowWords;  // [W][128] result bits
+  uint64_t* const starts = reinterpret_cast<uint64_t*>(fs_raw + kFusedWarps * W * kRowWords * sizeof(uint32_t));
+  uint16_t* const tab = reinterpret_cast<uint16_t*>(starts + (kTop ? 0 : S)) + warp * W * T;  // [W][S + 1] run offsets
+  const uint32_t TW = gridDim.x * kFusedWarps, gw = blockIdx.x * kFusedWarps + warp;  // nchunks < 2^32
+  const uint64_t pol = dev::policy_evict_first();  // lives in a uniform register (the load's descriptor)
+  auto ld_slot = [&](const uint64_t* q) { return dev::ld_stream_u64(q, pol); };
+  for (uint32_t k = lane; k < W * kRowWords; k += 32) rows[k] = 0;
+  for (uint32_t i = 0; i < W; ++i) {
+    const uint64_t ch = gw + static_cast<uint64_t>(i) * TW;
+    for (uint32_t l = lane; l < T; l += 32) tab[i * T + l] = ch < a.nchunks ? a.boffs[ch * kBoffStride + l] : uint16_t{0};
+  }
+  if constexpr (!kTop) {
+    for (uint32_t q = threadIdx.x; q < S; q += kFusedThreads) starts[q] = bucket_start(q, a.mult);
+    __syncthreads();
+  }
+  __syncwarp();
+  // run (bucket b, chunk row i) of this warp: first slot and length
+  auto run_of = [&](uint32_t b, uint32_t i, uint32_t& len) -> const uint64_t* {
+    const uint32_t st = tab[i * T + b], en = tab[i * T + b + 1];
+    SBBF_DCHECK(st <= en && en <= kPartChunk);
+    len = en - st;
+    return a.keys + (gw + static_cast<uint64_t>(i) * TW) * kPartChunk + st + lane;
+  };
+  auto slice_first = [&](uint32_t b) -> uint64_t {
+    if constexpr (kTop) return (static_cast<uint64_t>(b) * a.nb_global) >> a.bits;
+    return starts[b];
+  };
+  // one probe step of a lane: the slot's sector on its way (a zero block for a key outside the shard)
+  auto probe = [&](const uint32_t* slice, uint64_t h, dev::Block8& bl) {
+    const uint32_t off = static_cast<uint32_t>(h >> 44);
+    if (a.sentinel && off == kPackForeign) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) bl.w[k] = 0;
+    } else {
+      dev::ld_block_nc_normal(slice + static_cast<uint64_t>(off) * 8, bl);
+    }
+  };
+  auto record = [&](uint32_t* row, const dev::Block8& bl, uint64_t h) {
+    if (dev::block_contains(bl, h))
+      atomicOr(row + (static_cast<uint32_t>(h >> 37) & (kRowWords - 1)), 1u << (static_cast<uint32_t>(h >> 32) & 31u));
+  };
+  __shared__ uint32_t pace_on;
+  if (threadIdx.x == 0) pace_on = a.done != nullptr ? 1u : 0u;
+  for (uint32_t bb = 0; bb < S; ++bb) {
+    if (a.done) {
+      // CTA-level pacing: the CTA has issued step bb - 1; it enters step bb once
+      // every CTA has finished step bb - slack
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (bb > 0) atomicAdd(a.done + (bb - 1), 1u);
+        if (pace_on && bb >= a.slack) {
+          uint32_t polls = 0;
+          while (ld_relaxed_gpu_u32(a.done + (bb - a.slack)) < gridDim.x && ++polls < kPaceMaxPolls) __nanosleep(500);
+          if (polls >= kPaceMaxPolls) pace_on = 0;
+        }
+      }
+      __syncthreads();
+    }
+    const uint32_t b = a.rev ? S - 1 - bb : bb;
+    const uint32_t* const slice = a.blocks + slice_first(b) * 8;
+    for (uint32_t i = 0; i < W; ++i) {
+      uint32_t len;
+      const uint64_t* p = run_of(b, i, len);
+      uint32_t* const row = rows + i * kRowWords;
+      uint64_t hn = lane < len ? ld_slot(p) : 0;
+      for (uint32_t j = lane; j < len; j += 32, p += 32) {
+        const uint64_t h = hn;
+        dev::Block8 bl;
+        probe(slice, h, bl);
+        // the next step's slot loads while this step's sector is in flight
+        if (j + 32 < len) hn = ld_slot(p + 32);
+        record(row, bl, h);
+      }
+    }
+  }
+  __syncwarp();
+  for (uint32_t r = 0; r < W; ++r) {
+    const uint64_t ch = gw + static_cast<uint64_t>(r) * TW;
+    if (ch >= a.nchunks) break;
+    const uint64_t base = ch * kPartChunk;
+    const uint32_t cnt = static_cast<uint32_t>(a.m - base < kPartChunk ? a.m - base : kPartChunk);
+    const uint32_t* row = rows + r * kRowWords;
+    if (a.out_bits) {
+      uint32_t* ob = static_cast<uint32_t*>(a.out) + (base >> 5);
+      for (uint32_t k = lane; k * 32 < cnt; k += 32) ob[k] = row[k];
+    } else {
+      uint8_t* o = static_cast<uint8_t*>(a.out) + base;
+      const bool aligned = (reinterpret_cast<uintptr_t>(o) & 3) == 0;
+      for (uint32_t k = lane; k * 4 < cnt; k += 32) {
+        const uint32_t nib = (row[k >> 3] >> ((k & 7) * 4)) & 15u;
+        const uint32_t v = (nib & 1u) | (nib & 2u) << 7 | (nib & 4u) << 14 | (nib & 8u) << 21;
+        if (aligned && k * 4 + 4 <= cnt) {
+          *reinterpret_cast<uint32_t*>(o + k * 4) = v;
+        } else {
+          for (uint32_t e = 0; e < 4 && k * 4 + e < cnt; ++e) o[k * 4 + e] = static_cast<uint8_t>(v >> (8 * e));
+        }
+      }
+    }
+  }
+}
+
+// SBBF_FIND_FUSED=0 selects the partition + segment_kernel + unpermute lookups (A/B only).
+bool find_fused() {
+  static const bool on = [] {
+    const char* v = getenv("SBBF_FIND_FUSED");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+// SBBF_FUSED_VARIANT (A/B only): 0 = 6 CTAs/SM (default), 1 = 8 CTAs/SM. Config 4
+// lookups 105.8 vs 103.1 Gkeys/s; two sectors in flight per lane at 5 / 4
+// CTAs/SM measured 101.5 / 100.8 (profiles/r2_ab/r2cl_*).
+int fused_variant() {
+  static const int v = [] {
+    const char* e = getenv("SBBF_FUSED_VARIANT");
+    const int x = e ? atoi(e) : 0;
+    return x >= 0 && x <= 3 ? x : 0;
+  }();
+  return v;
+}
+
+// SBBF_FUSED_SLACK (A/B only): slices the sweep's warps may span (0 = free-running).
+uint32_t fused_slack() {
+  static const uint32_t v = [] {
+    const char* e = getenv("SBBF_FUSED_SLACK");
+    const int x = e ? atoi(e) : 2;
+    return static_cast<uint32_t>(x >= 0 && x <= 8 ? x : 2);
+  }();
+  return v;
+}
+// SBBF_FUSED_W (A/B only): chunks per warp per round (1..kFusedChunks).
+uint32_t fused_chunks() {
+  static const uint32_t v = [] {
+    const char* e = getenv("SBBF_FUSED_W");
+    const int x = e ? atoi(e) : 0;
+    return static_cast<uint32_t>(x >= 1 && x <= static_cast<int>(kFusedChunks) ? x : kFusedChunks);
+  }();
+  return v;
+}
+
+// Can this map's slots be packed (every slice within kPackOffBits of blocks)?
+// `trusted`: no key of the batch lies outside the map's block range.
+bool pack_map(BucketMap& bm, bool trusted) {
+  const uint64_t limit = uint64_t{1} << kPackOffBits;
+  bm.pack = 0;
+  bm.pack_shift = 0;
+  bm.sentinel = 0;
+  if (bm.top_bits) {
+    const uint64_t nb = bm.nb_global;
+    if ((nb & (nb - 1)) == 0) {
+      uint32_t lg = 0;
+      while ((uint64_t{1} << lg) < nb) ++lg;
+      if (lg <= bm.bits || lg - bm.bits > static_cast<uint32_t>(kPackOffBits)) return false;
+      bm.pack_shift = 64 - (lg - bm.bits);
+    } else if ((nb >> bm.bits) + 2 > limit) {
+      return false;
+    }
+    bm.pack = 1;
+    return true;
+  }
+  if (bm.mult == 0) return false;
+  const uint32_t sentinel = trusted ? 0u : 1u;
+  for (uint32_t q = 0; q < bm.S; ++q) {
+    const uint64_t lo = bucket_start(q, bm.mult);
+    const uint64_t hi = q + 1 < bm.S ? bucket_start(q + 1, bm.mult) : bm.nb_local;
+    if (hi > lo && hi - lo > limit - sentinel) return false;
+  }
+  bm.pack = 1;
+  bm.sentinel = sentinel;
+  return true;
+}
+
 template <int BITS, bool kTop>
 cudaError_t chunk_partition_bits(const DeviceInfo& di, const BucketMap& bm, const uint64_t* hashes, uint64_t m,
                                  uint64_t* out, uint16_t* pos16, uint16_t* boffs, cudaStream_t s) {
@@ -1784,9 +2061,10 @@ cudaError_t chunk_partition_bits(const DeviceInfo& di, const BucketMap& bm, cons
 }
 
 cudaError_t chunk_partition(const DeviceInfo& di, const Geom& g, uint32_t S, const uint64_t* hashes, uint64_t m,
-                            uint64_t* out, uint16_t* pos16, uint16_t* boffs, cudaStream_t s) {
+                            uint64_t* out, uint16_t* pos16, uint16_t* boffs, cudaStream_t s,
+                            const BucketMap* packed = nullptr) {
   KTime kt(kKPartition, s);
-  const BucketMap bm = make_map(g, S);
+  const BucketMap bm = packed ? *packed : make_map(g, S);
   switch (bm.bits * 2 + (bm.top_bits ? 1 : 0)) {
 #define SBBF_CHUNK_CASE(B)                                                                  \
   case 2 * B:                                                                               \
@@ -1942,7 +2220,7 @@ uint64_t scratch_bytes(uint64_t cap, bool lookup) {
   return align256(cap * sizeof(uint64_t)) + align256(nchunks * kBoffStride * sizeof(uint16_t)) +
          (lookup ? align256(cap * sizeof(uint16_t)) + align256(cap)
                  : align256(cap * sizeof(uint64_t)) + align256(tile_runs_entries(cap) * sizeof(uint32_t))) +
-         256;
+         align256(kChunkBuckets * sizeof(unsigned));
 }
 
 }  // namespace
@@ -2070,7 +2348,7 @@ cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, bool lookup, cudaStream_t s
       sc.keys2 = reinterpret_cast<uint64_t*>(scope->take(cap * sizeof(uint64_t)));
       sc.runs = reinterpret_cast<uint32_t*>(scope->take(tile_runs_entries(cap) * sizeof(uint32_t)));
     }
-    sc.work = reinterpret_cast<unsigned*>(scope->take(sizeof(unsigned)));
+    sc.work = reinterpret_cast<unsigned*>(scope->take(kChunkBuckets * sizeof(unsigned)));
     sc.flip = &scope->ctx()->flip;
     sc.pooled = false;
     return cudaSuccess;
@@ -2085,7 +2363,7 @@ cudaError_t alloc_scratch(Scratch& sc, uint64_t cap, bool lookup, cudaStream_t s
   if (!lookup && e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.keys2), cap * sizeof(uint64_t), s);
   if (!lookup && e == cudaSuccess)
     e = cudaMallocAsync(reinterpret_cast<void**>(&sc.runs), tile_runs_entries(cap) * sizeof(uint32_t), s);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.work), sizeof(unsigned), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&sc.work), kChunkBuckets * sizeof(unsigned), s);
   return e;
 }
 
@@ -2193,8 +2471,115 @@ cudaError_t insert_chunk(const DeviceInfo& di, uint32_t* blocks, const Geom& g, 
   return e;
 }
 
+// Fused lookups of one batch chunk: rounds of (resident warps x kFusedChunks)
+// chunks, each a packed partition and one persistent sweep.
+template <bool kTop>
+cudaError_t find_chunk_fused(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BucketMap& bm,
+                             const uint64_t* keys, uint64_t m, Scratch& sc, uint64_t scratch_keys, void* dst, bool bits,
+                             cudaStream_t s) {
+  auto smem_for = [&](uint32_t W) {
+    return static_cast<size_t>(kFusedWarps) * W * kRowWords * sizeof(uint32_t) + (kTop ? 0 : bm.S * sizeof(uint64_t)) +
+           static_cast<size_t>(kFusedWarps) * W * (bm.S + 1) * sizeof(uint16_t);
+  };
+  using Kern = void (*)(const FusedArgs);
+  static const Kern kerns[2] = {sweep_find_kernel<kTop, 6>, sweep_find_kernel<kTop, 8>};
+  static const int kern_ctas[2] = {6, 8};
+  const Kern kern = kerns[fused_variant()];
+  static const cudaError_t attr = [] {
+    cudaError_t r = cudaSuccess;
+    for (Kern k : kerns)
+      if (r == cudaSuccess) r = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    for (Kern k : kerns)
+      if (r == cudaSuccess) r = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    return r;
+  }();
+  if (attr != cudaSuccess) return attr;
+  // chunks per warp: as many as keep the kernel's register-limited occupancy
+  // (a round sweeps the whole filter once, so its cost per key falls with W)
+  const int want = kern_ctas[fused_variant()];
+  uint32_t Wmax = fused_chunks();
+  int occ = 0;
+  cudaError_t e = cudaSuccess;
+  for (;; --Wmax) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFusedThreads, smem_for(Wmax));
+    if (e != cudaSuccess) return e;
+    if (occ >= want || Wmax == 1) break;
+  }
+  if (occ < 1) return cudaErrorNotSupported;
+  const uint64_t max_ctas = static_cast<uint64_t>(di.sms) * occ;
+  uint64_t round = max_ctas * kFusedWarps * Wmax * kPartChunk;
+  if (round > scratch_keys) round = scratch_keys / kPartChunk * kPartChunk;  // the scratch holds one round
+  if (round == 0) return cudaErrorNotSupported;
+  static const bool dbg = getenv("SBBF_FUSED_DEBUG") != nullptr;
+  if (dbg) fprintf(stderr, "[sbbf] fused sweep: %d CTAs/SM, %llu keys per round, S=%u\n", occ,
+                   static_cast<unsigned long long>(round), bm.S);
+  uint32_t rev = 0;
+  for (uint64_t off = 0; e == cudaSuccess && off < m; off += round) {
+    const uint64_t mm = m - off < round ? m - off : round;
+    e = chunk_partition(di, g, bm.S, keys + off, mm, sc.keys, nullptr, sc.boffs, s, &bm);
+    if (e != cudaSuccess) break;
+    KTime kt(kKProbe, s);
+    if (sc.flip) {
+      rev = *sc.flip ? 1u : 0u;
+      *sc.flip = !*sc.flip;
+    }
+    FusedArgs a;
+    a.blocks = blocks + 0;
+    a.keys = sc.keys;
+    a.boffs = sc.boffs;
+    a.out = bits ? static_cast<void*>(static_cast<uint32_t*>(dst) + off / 32)
+                 : static_cast<void*>(static_cast<uint8_t*>(dst) + off);
+    a.nchunks = (mm + kPartChunk - 1) / kPartChunk;
+    a.m = mm;
+    a.nb_global = g.nb_global;
+    a.nb_local = g.nb_local;
+    a.mult = bm.mult;
+    a.S = bm.S;
+    a.bits = bm.bits;
+    a.W = static_cast<uint32_t>((a.nchunks + max_ctas * kFusedWarps - 1) / (max_ctas * kFusedWarps));
+    a.rev = rev;
+    a.sentinel = bm.sentinel;
+    a.out_bits = bits ? 1u : 0u;
+    a.done = sc.work;
+    a.slack = fused_slack();
+    if (a.done && a.slack) {
+      e = cudaMemsetAsync(a.done, 0, kChunkBuckets * sizeof(unsigned), s);
+      if (e != cudaSuccess) break;
+    } else {
+      a.done = nullptr;
+    }
+    const uint64_t grid = (a.nchunks + static_cast<uint64_t>(kFusedWarps) * a.W - 1) / (kFusedWarps * a.W);
+    note_launch();
+    kern<<<static_cast<unsigned>(grid), kFusedThreads, smem_for(a.W), s>>>(a);
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+// `trusted`: every key of the batch lies in g's block range (whole filters,
+// super-slices of a whole filter).
+// The fused lookup of m keys (any number of rounds; the scratch holds
+// scratch_keys slots), or cudaErrorNotSupported when the map cannot be packed.
+cudaError_t try_find_fused(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, uint32_t parts,
+                           const uint64_t* keys, uint64_t m, Scratch& sc, uint64_t scratch_keys, void* dst, bool bits,
+                           cudaStream_t s, bool trusted) {
+  if (!find_fused()) return cudaErrorNotSupported;
+  BucketMap bm = make_map(g, parts);
+  if (!pack_map(bm, trusted)) return cudaErrorNotSupported;
+  const cudaError_t e = bm.top_bits
+                            ? find_chunk_fused<true>(di, blocks, g, bm, keys, m, sc, scratch_keys, dst, bits, s)
+                            : find_chunk_fused<false>(di, blocks, g, bm, keys, m, sc, scratch_keys, dst, bits, s);
+  if (e == cudaErrorNotSupported) cudaGetLastError();
+  return e;
+}
+
 cudaError_t find_chunk(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, uint32_t parts,
-                       const uint64_t* keys, uint64_t m, Scratch& sc, void* dst, bool bits, cudaStream_t s) {
+                       const uint64_t* keys, uint64_t m, Scratch& sc, void* dst, bool bits, cudaStream_t s,
+                       bool trusted = false) {
+  {
+    const cudaError_t ef = try_find_fused(di, blocks, g, parts, keys, m, sc, m, dst, bits, s, trusted);
+    if (ef != cudaErrorNotSupported) return ef;
+  }
   // 1. every chunk bucket-major in its own region (+ positions, offsets)
   cudaError_t e = chunk_partition(di, g, parts, keys, m, sc.keys, sc.pos16, sc.boffs, s);
   // 2. probe slice by slice (L2-resident), one answer byte per routed slot
@@ -2337,6 +2722,7 @@ cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geo
   Scratch sc;
   TwoLevel tl;
   const bool two = plan.super_parts > 1;
+  const bool whole = g.first == 0 && g.nb_local == g.nb_global;  // no key can fall outside the filter
   cudaError_t e = alloc_scratch(sc, cap, true, s, &scope);
   if (e == cudaSuccess && two) e = cudaMallocAsync(reinterpret_cast<void**>(&tl.keys), cap * sizeof(uint64_t), s);
   if (e == cudaSuccess && two) e = cudaMallocAsync(reinterpret_cast<void**>(&tl.pos), cap * sizeof(uint32_t), s);
@@ -2345,19 +2731,26 @@ cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geo
   if (e == cudaSuccess && two)
     e = cudaMallocAsync(reinterpret_cast<void**>(&tl.counts), 2 * plan.super_parts * sizeof(uint64_t), s);
   std::vector<uint64_t> cnt;
-  for (uint64_t off = 0; e == cudaSuccess && off < n; off += cap) {
+  uint64_t start = 0;
+  if (e == cudaSuccess && !two) {
+    // the fused path sizes its own rounds over the whole batch
+    e = try_find_fused(di, blocks, g, plan.parts, hashes, n, sc, cap, out, bits, s, whole);
+    if (e == cudaErrorNotSupported) e = cudaSuccess;
+    else start = n;
+  }
+  for (uint64_t off = start; e == cudaSuccess && off < n; off += cap) {
     const uint64_t m = n - off < cap ? n - off : cap;
     void* dst = bits ? static_cast<void*>(static_cast<uint32_t*>(out) + off / 32)
                      : static_cast<void*>(static_cast<uint8_t*>(out) + off);
     if (!two) {
-      e = find_chunk(di, blocks, g, plan.parts, hashes + off, m, sc, dst, bits, s);
+      e = find_chunk(di, blocks, g, plan.parts, hashes + off, m, sc, dst, bits, s, whole);
       continue;
     }
     e = super_counts(di, g, plan, hashes + off, m, tl, true, s, cnt);
     for (uint32_t k = 0, pre = 0; e == cudaSuccess && k < plan.super_parts; pre += cnt[k], ++k)
       if (cnt[k])
         e = find_chunk(di, blocks + plan.h_super_bounds[k] * 8, sub_geom(g, plan.h_super_bounds, k), plan.parts,
-                       tl.keys + pre, cnt[k], sc, tl.ans + pre, false, s);
+                       tl.keys + pre, cnt[k], sc, tl.ans + pre, false, s, whole);
     // grouped answers back to source order (then packed for bit output)
     uint8_t* bytes = bits ? tl.bytes : static_cast<uint8_t*>(dst);
     if (e == cudaSuccess && sbbf_scatter_u8(tl.ans, tl.pos, m, bytes, s) != SBBF_OK) e = cudaGetLastError();
