@@ -8,18 +8,24 @@
 //
 //   1. chunk_scatter: every 4096-key chunk of the batch is rewritten
 //      bucket-major (bucket = filter slice of ~32 MiB) inside its own region,
-//      with 16-bit bucket offsets per chunk (and, for lookups, each slot's
-//      16-bit source position): one read, coalesced writes, no count pass;
-//   2. segment_kernel: bucket by bucket over every chunk's run of that
-//      bucket; the keys in flight share one slice, so their probes /
-//      atomics are served by L2 and each filter line comes from HBM about
-//      once per batch chunk; lookups store an answer byte per routed slot;
-//   3. unpermute_kernel (lookups): each chunk's answers back to source order
-//      through shared memory, written as the caller's bits or bytes.
+//      with 16-bit bucket offsets per chunk: one read, coalesced writes, no
+//      count pass;
+//   2. inserts — segment_kernel: bucket by bucket over every chunk's run of
+//      that bucket; the keys in flight share one slice, so their atomics are
+//      served by L2 and each filter line comes from HBM about once per call;
+//   3. lookups — sweep_find_kernel (the fused sweep): the partition stores
+//      packed slots (slice-relative block, source position, low hash bits)
+//      and one persistent, slice-paced grid probes them and sets each hit's
+//      bit at its source position in per-chunk result rows in shared memory,
+//      written out as the caller's bits or bytes. Maps whose slices exceed
+//      2^20 blocks, and the multi-region calls of the sharded layer, keep the
+//      older form: segment_kernel storing an answer byte per routed slot,
+//      then unpermute_kernel (each chunk's answers back to source order
+//      through shared memory).
 //
-// Per-key HBM traffic ~ 8 + 10 (scatter) + 8 + 1 (probe) + 3 (unpermute) +
-// filter_bytes / batch-chunk keys, and no atomics besides the filter ORs
-// (profiles/r1_blocked_partition.md).
+// Per-key HBM traffic of a config-4 lookup ~ 8 + 8 (scatter) + 8 (sweep) +
+// filter_bytes x ~1.3 / round keys + 1/8 (ncu: profiles/traffic.json); the
+// unfused form adds 2 + 2 (positions) + 1 + 1 (answer bytes).
 //
 // The shard routing (shard_partition / route_partition) needs one
 // bucket-major layout over the whole batch instead: bucket_count ->

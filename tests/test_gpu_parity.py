@@ -320,6 +320,37 @@ def test_blocked_unaligned_buffers(cuda, oracle):
         assert np.array_equal(bits_to_bytes(u32(f.find_hashes_bits(p)), probes.size), want_res)
 
 
+@pytest.mark.parametrize("total,first,count", [
+    (3 * 2**22 + 11, 2**22 + 3, 2**22 + 5),      # a middle shard, odd bounds
+    (2**24, 0, 2**23),                            # the first half of a power-of-two filter
+    (2**24 + 1, 2**23 + 1, 2**23),                # slices of exactly 2^20 blocks plus foreign keys
+])
+def test_blocked_lookup_on_a_shard_with_foreign_keys(cuda, oracle, total, first, count):
+    """Blocked lookups on a block-range shard (sbbf_gpu_create_shard) with
+    keys the shard does not own in the batch: the packed staging of the fused
+    sweep marks them (or, when a slice has no spare offset for the mark, the
+    partition + segment + unpermute kernels take the call); they answer 0,
+    owned keys answer as the whole filter would. Bytes and bits."""
+    from paper_2101_01719_b200 import sharded as S
+    rng = np.random.default_rng(total ^ first)
+    hs = rng.integers(0, 2**64, size=1_500_007, dtype=np.uint64)
+    probes = np.concatenate([hs[:400_000], rng.integers(0, 2**64, size=4096 * 150 + 13, dtype=np.uint64)])
+    rng.shuffle(probes)
+    want = oracle.build(total, hs)
+    f = S.CudaShardOps(0).create(total, first, count)
+    f.set_insert_variant(_lib.INSERT_BLOCKED)
+    f.add_hashes(dev(hs, cuda))                   # foreign keys are ignored
+    assert np.array_equal(f.blocks(), want[first:first + count])
+    blk = np.array([(int(h) * total) >> 64 for h in probes], dtype=np.uint64)
+    owned = (blk >= first) & (blk < first + count)
+    assert 0 < owned.sum() < probes.size
+    want_res = oracle.find_hashes(want, probes) * owned
+    f.set_find_variant(_lib.FIND_BLOCKED)
+    assert np.array_equal(f.find_hashes(dev(probes, cuda)).cpu().numpy(), want_res)
+    bits = u32(f.find_hashes_bits(dev(probes, cuda)))
+    assert np.array_equal(bits_to_bytes(bits, probes.size), want_res)
+
+
 @pytest.mark.parametrize("nb", [2**27, 3 * 2**25 + 5, 2**27 + 12345])
 def test_blocked_two_level(cuda, oracle, nb):
     """Filters up to 128 slices of 32 MiB (4 GiB) take the single-level
