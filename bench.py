@@ -706,9 +706,9 @@ def kernel_rooflines(res: dict, kt: dict, hbm_peak: float):
                       "north_star_gbs": keys * 64 / (avg_ms * 1e-3) / 1e9,
                       "north_star_frac": keys * 64 / (avg_ms * 1e-3) / 1e9 / hbm_peak})
         elif kind == "partition":
-            # every insert call and lookup round: keys read once, written bucket-major
-            # (+ 2-B positions for lookups)
-            byts = (N * 16 + L * 18) / groups
+            # every insert call and lookup round: keys read once, written bucket-major;
+            # the unfused lookups (an unpermute kind in the times) also write 2-B positions
+            byts = (N * 16 + L * (18 if "unpermute" in kt["kinds"] else 16)) / groups
             d.update({"bound": "hbm", "algorithmic_bytes_per_launch": byts,
                       "achieved_gbs": byts / (avg_ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
                       "frac": byts / (avg_ms * 1e-3) / 1e9 / hbm_peak})

@@ -30,8 +30,9 @@ int sbbf_bench_sector_red(uint32_t* d_buf, uint64_t num_blocks, uint64_t n, uint
  * blocked-path launch group on its stream and clears the totals; 0 stops.
  * sbbf_bench_kernel_times synchronises the recorded events and returns the
  * summed milliseconds and launch-group counts per kind, up to n kinds:
- * 0 partition (chunk_scatter), 1 lookup probe sweep, 2 insert sweep,
- * 3 unpermute, 4 tile insert (tile_scatter + tile_apply). */
+ * 0 partition (chunk_scatter), 1 lookup probe sweep (sweep_find_kernel, or
+ * segment_kernel in the unfused form), 2 insert sweep, 3 unpermute (unfused
+ * lookups only), 4 tile insert (tile_scatter + tile_apply). */
 int sbbf_bench_kernel_timing(int enable);
 int sbbf_bench_kernel_times(double* ms, uint64_t* launches, int n);
 
