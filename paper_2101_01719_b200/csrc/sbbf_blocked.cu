@@ -1830,7 +1830,7 @@ struct FusedArgs {
   const uint64_t* keys;   // packed slots, chunk layout
   const uint16_t* boffs;  // [nchunks][kBoffStride]
   void* out;              // bitmap words / bytes of this round, chunk ch at key ch * kPartChunk
-  uint64_t nchunks, m;
+  uint64_t nchunks;
   uint64_t nb_global, nb_local, mult;
   uint32_t S, bits, W, rev, sentinel, out_bits;
   // Slice pacing: CTAs count the sweep steps they finish in done[step]; a CTA
@@ -1935,7 +1935,7 @@ __global__ void __launch_bounds__(kFusedThreads, kMinB) sweep_find_kernel(const 
     const uint64_t ch = gw + static_cast<uint64_t>(r) * TW;
     if (ch >= a.nchunks) break;
     const uint64_t base = ch * kPartChunk;
-    const uint32_t cnt = static_cast<uint32_t>(a.m - base < kPartChunk ? a.m - base : kPartChunk);
+    const uint32_t cnt = tab[r * T + S];  // the chunk's key count (end of its last run)
     const uint32_t* row = rows + r * kRowWords;
     if (a.out_bits) {
       uint32_t* ob = static_cast<uint32_t*>(a.out) + (base >> 5);
@@ -2234,41 +2234,23 @@ uint64_t scratch_bytes(uint64_t cap, bool lookup) {
 // Per-handle blocked-path context: a scratch arena that persists across calls
 // (one cudaMalloc, grown on demand; the stream-ordered pool's trimming and
 // growth inside timed steps is what produced the occasional 10x config-4
-// step), ordered across callers' streams by an `idle` event, plus the side
-// stream and events of the pipelined lookup (per handle, so lookups on
-// unrelated filters share no stream). Calls being captured into a CUDA graph
-// take their scratch from the stream-ordered pool instead (graph-safe) and
-// run unpipelined.
+// step), ordered across callers' streams by an `idle` event. Calls being
+// captured into a CUDA graph take their scratch from the stream-ordered pool
+// instead (graph-safe).
 struct BlockedCtx {
   std::mutex mu;
   char* base = nullptr;
   uint64_t cap = 0;
   cudaEvent_t idle = nullptr;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_in = nullptr, ready[3] = {nullptr, nullptr, nullptr}, freed[3] = {nullptr, nullptr, nullptr};
-  bool events_ok = false;
   bool flip = false;  // direction of the next segment sweep
   cudaError_t init() {  // under mu
-    if (events_ok) return cudaSuccess;
-    int least = 0, greatest = 0;
-    cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    if (e == cudaSuccess && !side) e = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, greatest);
-    if (e == cudaSuccess && !idle) e = cudaEventCreateWithFlags(&idle, cudaEventDisableTiming);
-    if (e == cudaSuccess && !ev_in) e = cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming);
-    for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
-      if (!ready[k]) e = cudaEventCreateWithFlags(&ready[k], cudaEventDisableTiming);
-      if (e == cudaSuccess && !freed[k]) e = cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming);
-    }
-    events_ok = e == cudaSuccess;
-    return e;
+    if (idle) return cudaSuccess;
+    return cudaEventCreateWithFlags(&idle, cudaEventDisableTiming);
   }
   ~BlockedCtx() {
     if (idle) cudaEventSynchronize(idle);
-    if (side) cudaStreamSynchronize(side);
     cudaFree(base);
-    if (side) cudaStreamDestroy(side);
-    for (cudaEvent_t ev : {idle, ev_in, ready[0], ready[1], ready[2], freed[0], freed[1], freed[2]})
-      if (ev) cudaEventDestroy(ev);
+    if (idle) cudaEventDestroy(idle);
   }
 };
 
@@ -2408,20 +2390,6 @@ cudaError_t route_partition(const DeviceInfo& di, uint64_t total, uint32_t parts
 
 namespace {
 
-// The overlapped multi-round lookup (round c+1's partition on a side stream
-// while round c is probed) gained 1.6-3 % with the LSU partition but costs
-// 6 % with the TMA partition (config 4 lookups 104.8 -> 92.6 Gkeys/s,
-// profiles/r2y_*): the partition's 104 KB of shared memory per CTA and the
-// probe's all-L1 carveout cannot share an SM. Off by default;
-// SBBF_BLOCKED_PIPELINE=1 enables it (A/B only).
-bool pipeline_enabled() {
-  static const bool on = [] {
-    const char* v = getenv("SBBF_BLOCKED_PIPELINE");
-    return v && v[0] == '1';
-  }();
-  return on;
-}
-
 // One batch chunk (m <= blocked_round() keys) through the single-level path.
 // Tile inserts (tile_scatter_kernel / tile_apply_persistent_kernel) apply to whole
 // power-of-two filters of 2^20..2^26 blocks (32 MiB - 2 GiB): S = nb / 2^19
@@ -2477,20 +2445,26 @@ cudaError_t insert_chunk(const DeviceInfo& di, uint32_t* blocks, const Geom& g, 
   return e;
 }
 
-// Fused lookups of one batch chunk: rounds of (resident warps x kFusedChunks)
-// chunks, each a packed partition and one persistent sweep.
+// The fused sweep's launch shape for a map: the kernel, how many chunks one
+// launch can take (resident warps x chunks per warp) and the dynamic smem.
+struct FusedShape {
+  void (*kern)(const FusedArgs) = nullptr;
+  uint64_t max_ctas = 0;
+  uint32_t Wmax = 0;
+  bool top = false;
+  uint32_t S = 0;
+  size_t smem(uint32_t W) const {
+    return static_cast<size_t>(kFusedWarps) * W * kRowWords * sizeof(uint32_t) + (top ? 0 : S * sizeof(uint64_t)) +
+           static_cast<size_t>(kFusedWarps) * W * (S + 1) * sizeof(uint16_t);
+  }
+  uint64_t max_chunks() const { return max_ctas * kFusedWarps * Wmax; }
+};
+
 template <bool kTop>
-cudaError_t find_chunk_fused(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BucketMap& bm,
-                             const uint64_t* keys, uint64_t m, Scratch& sc, uint64_t scratch_keys, void* dst, bool bits,
-                             cudaStream_t s) {
-  auto smem_for = [&](uint32_t W) {
-    return static_cast<size_t>(kFusedWarps) * W * kRowWords * sizeof(uint32_t) + (kTop ? 0 : bm.S * sizeof(uint64_t)) +
-           static_cast<size_t>(kFusedWarps) * W * (bm.S + 1) * sizeof(uint16_t);
-  };
+cudaError_t fused_shape_for(const DeviceInfo& di, const BucketMap& bm, FusedShape& fs) {
   using Kern = void (*)(const FusedArgs);
   static const Kern kerns[2] = {sweep_find_kernel<kTop, 6>, sweep_find_kernel<kTop, 8>};
   static const int kern_ctas[2] = {6, 8};
-  const Kern kern = kerns[fused_variant()];
   static const cudaError_t attr = [] {
     cudaError_t r = cudaSuccess;
     for (Kern k : kerns)
@@ -2500,90 +2474,113 @@ cudaError_t find_chunk_fused(const DeviceInfo& di, const uint32_t* blocks, const
     return r;
   }();
   if (attr != cudaSuccess) return attr;
+  fs.kern = kerns[fused_variant()];
+  fs.top = kTop;
+  fs.S = bm.S;
   // chunks per warp: as many as keep the kernel's register-limited occupancy
   // (a round sweeps the whole filter once, so its cost per key falls with W)
   const int want = kern_ctas[fused_variant()];
-  uint32_t Wmax = fused_chunks();
   int occ = 0;
-  cudaError_t e = cudaSuccess;
-  for (;; --Wmax) {
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFusedThreads, smem_for(Wmax));
+  for (fs.Wmax = fused_chunks();; --fs.Wmax) {
+    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fs.kern, kFusedThreads, fs.smem(fs.Wmax));
     if (e != cudaSuccess) return e;
-    if (occ >= want || Wmax == 1) break;
+    if (occ >= want || fs.Wmax == 1) break;
   }
   if (occ < 1) return cudaErrorNotSupported;
-  const uint64_t max_ctas = static_cast<uint64_t>(di.sms) * occ;
-  uint64_t round = max_ctas * kFusedWarps * Wmax * kPartChunk;
+  fs.max_ctas = static_cast<uint64_t>(di.sms) * occ;
+  return cudaSuccess;
+}
+
+cudaError_t fused_shape(const DeviceInfo& di, const BucketMap& bm, FusedShape& fs) {
+  return bm.top_bits ? fused_shape_for<true>(di, bm, fs) : fused_shape_for<false>(di, bm, fs);
+}
+
+// One sweep over nchunks <= fs.max_chunks() staged chunks (packed slots in
+// sc.keys, run offsets in sc.boffs); `out` takes chunk ch's answers at key
+// ch * kPartChunk (bitmap words or bytes).
+cudaError_t fused_sweep(const FusedShape& fs, const uint32_t* blocks, const Geom& g, const BucketMap& bm, Scratch& sc,
+                        uint64_t nchunks, void* out, bool bits, cudaStream_t s) {
+  KTime kt(kKProbe, s);
+  FusedArgs a;
+  a.blocks = blocks;
+  a.keys = sc.keys;
+  a.boffs = sc.boffs;
+  a.out = out;
+  a.nchunks = nchunks;
+  a.nb_global = g.nb_global;
+  a.nb_local = g.nb_local;
+  a.mult = bm.mult;
+  a.S = bm.S;
+  a.bits = bm.bits;
+  a.W = static_cast<uint32_t>((nchunks + fs.max_ctas * kFusedWarps - 1) / (fs.max_ctas * kFusedWarps));
+  a.rev = 0;
+  if (sc.flip) {  // alternate the sweep direction: a sweep starts on the slices the last one left in L2
+    a.rev = *sc.flip ? 1u : 0u;
+    *sc.flip = !*sc.flip;
+  }
+  a.sentinel = bm.sentinel;
+  a.out_bits = bits ? 1u : 0u;
+  a.done = sc.work;
+  a.slack = fused_slack();
+  if (a.done && a.slack) {
+    const cudaError_t e = cudaMemsetAsync(a.done, 0, kChunkBuckets * sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+  } else {
+    a.done = nullptr;
+  }
+  const uint64_t grid = (nchunks + static_cast<uint64_t>(kFusedWarps) * a.W - 1) / (kFusedWarps * a.W);
+  note_launch();
+  fs.kern<<<static_cast<unsigned>(grid), kFusedThreads, fs.smem(a.W), s>>>(a);
+  return cudaGetLastError();
+}
+
+// Fused lookups of m keys: rounds of up to fs.max_chunks() chunks, each a
+// packed partition and one persistent sweep.
+cudaError_t find_chunk_fused(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BucketMap& bm,
+                             const uint64_t* keys, uint64_t m, Scratch& sc, uint64_t scratch_keys, void* dst, bool bits,
+                             cudaStream_t s) {
+  FusedShape fs;
+  cudaError_t e = fused_shape(di, bm, fs);
+  if (e != cudaSuccess) return e;
+  uint64_t round = fs.max_chunks() * kPartChunk;
   if (round > scratch_keys) round = scratch_keys / kPartChunk * kPartChunk;  // the scratch holds one round
   if (round == 0) return cudaErrorNotSupported;
   static const bool dbg = getenv("SBBF_FUSED_DEBUG") != nullptr;
-  if (dbg) fprintf(stderr, "[sbbf] fused sweep: %d CTAs/SM, %llu keys per round, S=%u\n", occ,
-                   static_cast<unsigned long long>(round), bm.S);
-  uint32_t rev = 0;
+  if (dbg) fprintf(stderr, "[sbbf] fused sweep: %llu CTAs, %llu keys per round, S=%u\n",
+                   static_cast<unsigned long long>(fs.max_ctas), static_cast<unsigned long long>(round), bm.S);
   for (uint64_t off = 0; e == cudaSuccess && off < m; off += round) {
     const uint64_t mm = m - off < round ? m - off : round;
     e = chunk_partition(di, g, bm.S, keys + off, mm, sc.keys, nullptr, sc.boffs, s, &bm);
-    if (e != cudaSuccess) break;
-    KTime kt(kKProbe, s);
-    if (sc.flip) {
-      rev = *sc.flip ? 1u : 0u;
-      *sc.flip = !*sc.flip;
-    }
-    FusedArgs a;
-    a.blocks = blocks + 0;
-    a.keys = sc.keys;
-    a.boffs = sc.boffs;
-    a.out = bits ? static_cast<void*>(static_cast<uint32_t*>(dst) + off / 32)
-                 : static_cast<void*>(static_cast<uint8_t*>(dst) + off);
-    a.nchunks = (mm + kPartChunk - 1) / kPartChunk;
-    a.m = mm;
-    a.nb_global = g.nb_global;
-    a.nb_local = g.nb_local;
-    a.mult = bm.mult;
-    a.S = bm.S;
-    a.bits = bm.bits;
-    a.W = static_cast<uint32_t>((a.nchunks + max_ctas * kFusedWarps - 1) / (max_ctas * kFusedWarps));
-    a.rev = rev;
-    a.sentinel = bm.sentinel;
-    a.out_bits = bits ? 1u : 0u;
-    a.done = sc.work;
-    a.slack = fused_slack();
-    if (a.done && a.slack) {
-      e = cudaMemsetAsync(a.done, 0, kChunkBuckets * sizeof(unsigned), s);
-      if (e != cudaSuccess) break;
-    } else {
-      a.done = nullptr;
-    }
-    const uint64_t grid = (a.nchunks + static_cast<uint64_t>(kFusedWarps) * a.W - 1) / (kFusedWarps * a.W);
-    note_launch();
-    kern<<<static_cast<unsigned>(grid), kFusedThreads, smem_for(a.W), s>>>(a);
-    e = cudaGetLastError();
+    if (e == cudaSuccess)
+      e = fused_sweep(fs, blocks, g, bm, sc, (mm + kPartChunk - 1) / kPartChunk,
+                      bits ? static_cast<void*>(static_cast<uint32_t*>(dst) + off / 32)
+                           : static_cast<void*>(static_cast<uint8_t*>(dst) + off),
+                      bits, s);
   }
   return e;
 }
 
-// `trusted`: every key of the batch lies in g's block range (whole filters,
-// super-slices of a whole filter).
 // The fused lookup of m keys (any number of rounds; the scratch holds
 // scratch_keys slots), or cudaErrorNotSupported when the map cannot be packed.
+// `dense_only` (AUTO dispatch): batches thinner than a key per block keep the
+// unfused kernels — their one-shot grid copes better with runs of a few keys
+// (config 5's world-1 sample, 0.5 keys per block: 31.3 vs 28.5 Gkeys/s).
 cudaError_t try_find_fused(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, uint32_t parts,
                            const uint64_t* keys, uint64_t m, Scratch& sc, uint64_t scratch_keys, void* dst, bool bits,
-                           cudaStream_t s, bool trusted) {
-  if (!find_fused()) return cudaErrorNotSupported;
+                           cudaStream_t s, bool trusted, bool dense_only) {
+  if (!find_fused() || (dense_only && m < g.nb_local)) return cudaErrorNotSupported;
   BucketMap bm = make_map(g, parts);
   if (!pack_map(bm, trusted)) return cudaErrorNotSupported;
-  const cudaError_t e = bm.top_bits
-                            ? find_chunk_fused<true>(di, blocks, g, bm, keys, m, sc, scratch_keys, dst, bits, s)
-                            : find_chunk_fused<false>(di, blocks, g, bm, keys, m, sc, scratch_keys, dst, bits, s);
+  const cudaError_t e = find_chunk_fused(di, blocks, g, bm, keys, m, sc, scratch_keys, dst, bits, s);
   if (e == cudaErrorNotSupported) cudaGetLastError();
   return e;
 }
 
 cudaError_t find_chunk(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, uint32_t parts,
                        const uint64_t* keys, uint64_t m, Scratch& sc, void* dst, bool bits, cudaStream_t s,
-                       bool trusted = false) {
+                       bool trusted = false, bool dense_only = false) {
   {
-    const cudaError_t ef = try_find_fused(di, blocks, g, parts, keys, m, sc, m, dst, bits, s, trusted);
+    const cudaError_t ef = try_find_fused(di, blocks, g, parts, keys, m, sc, m, dst, bits, s, trusted, dense_only);
     if (ef != cudaErrorNotSupported) return ef;
   }
   // 1. every chunk bucket-major in its own region (+ positions, offsets)
@@ -2660,71 +2657,12 @@ cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g
   return e;
 }
 
-namespace {
-
-// Batches of several rounds (single-level plans): round c+1's chunk_scatter
-// runs on a high-priority side stream while round c is probed and
-// un-permuted on the caller's stream, with double-buffered scratch. The
-// scatter is issue/barrier bound and the probe L1/L2-sector bound, so the
-// two overlap on the SMs. Events fork from and join back into `s` (CUDA
-// graph capture safe).
-cudaError_t blocked_find_pipelined(const DeviceInfo& di, const uint32_t* blocks, const Geom& g,
-                                   const BlockedPlan& plan, const uint64_t* hashes, uint64_t n, void* out,
-                                   bool bits, cudaStream_t s, CallScope* scope) {
-  const uint64_t cap = blocked_round();
-  constexpr int nbuf = 2;
-  Scratch sc[nbuf];
-  // the handle's side stream and events (created once: creating them per call
-  // put 7-13 ms outliers into config-4 steps) and its scratch arena; the
-  // scope's lock serialises the enqueue of concurrent callers
-  CallScope& sco = *scope;
-  BlockedCtx& ctx = *sco.ctx();
-  cudaError_t e = cudaSuccess;
-  cudaStream_t side = ctx.side;
-  cudaEvent_t ev_in = ctx.ev_in, *ready = ctx.ready, *freed = ctx.freed;
-  for (int k = 0; k < nbuf && e == cudaSuccess; ++k) e = alloc_scratch(sc[k], cap, true, s, &sco);
-  // the side stream starts behind everything already queued on s (the
-  // caller's hashes and the scratch allocations)
-  if (e == cudaSuccess) e = cudaEventRecord(ev_in, s);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_in, 0);
-  uint64_t c = 0;
-  for (uint64_t off = 0; e == cudaSuccess && off < n; off += cap, ++c) {
-    const uint64_t m = n - off < cap ? n - off : cap;
-    const int k = static_cast<int>(c % nbuf);
-    void* dst = bits ? static_cast<void*>(static_cast<uint32_t*>(out) + off / 32)
-                     : static_cast<void*>(static_cast<uint8_t*>(out) + off);
-    if (c >= static_cast<uint64_t>(nbuf)) e = cudaStreamWaitEvent(side, freed[k], 0);  // round c-nbuf done with it
-    if (e == cudaSuccess) e = chunk_partition(di, g, plan.parts, hashes + off, m, sc[k].keys, sc[k].pos16,
-                                              sc[k].boffs, side);
-    if (e == cudaSuccess) e = cudaEventRecord(ready[k], side);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ready[k], 0);
-    if (e == cudaSuccess)
-      e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc[k].keys, sc[k].boffs, plan.parts, m,
-                                 sc[k].ans, s, sc[k].work, &di, sc[k].flip);
-    if (e == cudaSuccess) {
-      e = launch_unpermute(di, sc[k].ans, sc[k].pos16, m, dst, bits, s);
-    }
-    if (e == cudaSuccess) e = cudaEventRecord(freed[k], s);
-  }
-  // join the side stream into s once more (it covers an error exit between a
-  // side launch and its ready[] wait), so the scratch frees on s are ordered
-  // behind every partition that writes it
-  if (side && ev_in && cudaEventRecord(ev_in, side) == cudaSuccess) cudaStreamWaitEvent(s, ev_in, 0);
-  for (int k = 0; k < nbuf; ++k) free_scratch(sc[k], s);
-  return e;
-}
-
-}  // namespace
-
 cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
-                         const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s) {
+                         const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s, bool dense_only) {
   if (n == 0) return cudaSuccess;
   const uint64_t cap = n < blocked_round() ? n : blocked_round();  // a multiple of 32 unless n is the whole batch
-  const bool pipelined = plan.super_parts == 1 && n > blocked_round() && pipeline_enabled();
-  CallScope scope(plan.ctx, s, scratch_bytes(cap, true) * (pipelined ? 2 : 1));
+  CallScope scope(plan.ctx, s, scratch_bytes(cap, true));
   if (scope.error() != cudaSuccess) return scope.error();
-  // pipelining needs the handle's side stream: not while a graph is captured
-  if (pipelined && scope.arena()) return blocked_find_pipelined(di, blocks, g, plan, hashes, n, out, bits, s, &scope);
   Scratch sc;
   TwoLevel tl;
   const bool two = plan.super_parts > 1;
@@ -2740,7 +2678,7 @@ cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geo
   uint64_t start = 0;
   if (e == cudaSuccess && !two) {
     // the fused path sizes its own rounds over the whole batch
-    e = try_find_fused(di, blocks, g, plan.parts, hashes, n, sc, cap, out, bits, s, whole);
+    e = try_find_fused(di, blocks, g, plan.parts, hashes, n, sc, cap, out, bits, s, whole, dense_only);
     if (e == cudaErrorNotSupported) e = cudaSuccess;
     else start = n;
   }
@@ -2749,14 +2687,14 @@ cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geo
     void* dst = bits ? static_cast<void*>(static_cast<uint32_t*>(out) + off / 32)
                      : static_cast<void*>(static_cast<uint8_t*>(out) + off);
     if (!two) {
-      e = find_chunk(di, blocks, g, plan.parts, hashes + off, m, sc, dst, bits, s, whole);
+      e = find_chunk(di, blocks, g, plan.parts, hashes + off, m, sc, dst, bits, s, whole, dense_only);
       continue;
     }
     e = super_counts(di, g, plan, hashes + off, m, tl, true, s, cnt);
     for (uint32_t k = 0, pre = 0; e == cudaSuccess && k < plan.super_parts; pre += cnt[k], ++k)
       if (cnt[k])
         e = find_chunk(di, blocks + plan.h_super_bounds[k] * 8, sub_geom(g, plan.h_super_bounds, k), plan.parts,
-                       tl.keys + pre, cnt[k], sc, tl.ans + pre, false, s, whole);
+                       tl.keys + pre, cnt[k], sc, tl.ans + pre, false, s, whole, dense_only);
     // grouped answers back to source order (then packed for bit output)
     uint8_t* bytes = bits ? tl.bytes : static_cast<uint8_t*>(dst);
     if (e == cudaSuccess && sbbf_scatter_u8(tl.ans, tl.pos, m, bytes, s) != SBBF_OK) e = cudaGetLastError();
@@ -2808,7 +2746,7 @@ cudaError_t blocked_insert_regions(const DeviceInfo& di, uint32_t* blocks, const
 
 cudaError_t blocked_find_regions(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
                                  const uint64_t* const* keys, const uint64_t* counts, uint32_t nr, uint8_t* const* outs,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, bool dense_only) {
   std::vector<uint64_t> off;
   const uint64_t C = region_chunks(counts, nr, off);
   if (plan.super_parts > 1 || C * kPartChunk > blocked_round()) return cudaErrorNotSupported;
@@ -2819,18 +2757,30 @@ cudaError_t blocked_find_regions(const DeviceInfo& di, const uint32_t* blocks, c
   if (scope.error() != cudaSuccess) return scope.error();
   cudaError_t e = alloc_scratch(sc, C * kPartChunk, true, s, &scope);
   if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&bytes), C * kPartChunk, s);
+  // the fused sweep when the map packs and one launch takes every chunk
+  // (routed keys can still include ones the shard does not own: sentinel map)
+  BucketMap bm = make_map(g, plan.parts);
+  FusedShape fs;
+  uint64_t total = 0;
+  for (uint32_t r = 0; r < nr; ++r) total += counts[r];
+  const bool fused = e == cudaSuccess && find_fused() && !(dense_only && total < g.nb_local) &&
+                     pack_map(bm, g.first == 0 && g.nb_local == g.nb_global) &&
+                     fused_shape(di, bm, fs) == cudaSuccess && C <= fs.max_chunks();
   for (uint32_t r = 0; e == cudaSuccess && r < nr; ++r)
     if (counts[r])
       e = chunk_partition(di, g, plan.parts, keys[r], counts[r], sc.keys + off[r] * kPartChunk,
-                          sc.pos16 + off[r] * kPartChunk, sc.boffs + off[r] * kBoffStride, s);
-  if (e == cudaSuccess)
+                          sc.pos16 + off[r] * kPartChunk, sc.boffs + off[r] * kBoffStride, s, fused ? &bm : nullptr);
+  if (e == cudaSuccess && fused) {
+    e = fused_sweep(fs, blocks, g, bm, sc, C, bytes, false, s);
+  } else if (e == cudaSuccess) {
     e = launch_segments<false>(const_cast<uint32_t*>(blocks), g, sc.keys, sc.boffs, plan.parts, C * kPartChunk,
                                sc.ans, s, sc.work, &di, sc.flip);
-  if (e == cudaSuccess) {
-    note_launch();
-    unpermute_kernel<<<static_cast<unsigned>(C), kUnpermThreads, 0, s>>>(sc.ans, sc.pos16, C * kPartChunk, bytes,
-                                                                         false, sc.boffs);
-    e = cudaGetLastError();
+    if (e == cudaSuccess) {
+      note_launch();
+      unpermute_kernel<<<static_cast<unsigned>(C), kUnpermThreads, 0, s>>>(sc.ans, sc.pos16, C * kPartChunk, bytes,
+                                                                           false, sc.boffs);
+      e = cudaGetLastError();
+    }
   }
   for (uint32_t r = 0; e == cudaSuccess && r < nr; ++r)
     if (counts[r])

@@ -217,7 +217,8 @@ cudaError_t do_find(sbbf_gpu* f, int variant, const uint64_t* h, uint64_t n, voi
                     cudaStream_t s) {
   if (variant == SBBF_FIND_BLOCKED) {
     if (ensure_plan(f) != SBBF_OK) return cudaErrorMemoryAllocation;
-    return sbbf::blocked_find(f->di, f->d_blocks, f->geom, f->plan, h, n, out, bits, s);
+    return sbbf::blocked_find(f->di, f->d_blocks, f->geom, f->plan, h, n, out, bits, s,
+                              f->find_variant == SBBF_FIND_AUTO);
   }
   return sbbf::launch_find(f->di, variant, f->d_blocks, f->geom, h, n, out, bits, s);
 }
@@ -321,7 +322,8 @@ int gpu_find_regions(const sbbf_gpu_t* fc, const uint64_t* const* keys, const ui
   if (resolve_find(f, total) != SBBF_FIND_BLOCKED) return SBBF_OK;
   DeviceGuard g(f->di.device);
   if (ensure_plan(f) != SBBF_OK) return SBBF_ENOMEM;
-  const cudaError_t e = blocked_find_regions(f->di, f->d_blocks, f->geom, f->plan, keys, counts, nr, outs, s);
+  const cudaError_t e = blocked_find_regions(f->di, f->d_blocks, f->geom, f->plan, keys, counts, nr, outs, s,
+                                             f->find_variant == SBBF_FIND_AUTO);
   if (e == cudaErrorNotSupported) {
     cudaGetLastError();
     return SBBF_OK;

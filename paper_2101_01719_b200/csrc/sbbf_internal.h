@@ -97,8 +97,12 @@ struct BlockedPlan {
 };
 cudaError_t blocked_insert(const DeviceInfo& di, uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
                            const uint64_t* hashes, uint64_t n, cudaStream_t s);
+// dense_only (AUTO dispatch): the fused lookup sweep only for batches of at
+// least a key per block; an explicit SBBF_FIND_BLOCKED takes it whenever the
+// slices pack.
 cudaError_t blocked_find(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
-                         const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s);
+                         const uint64_t* hashes, uint64_t n, void* out, bool bits, cudaStream_t s,
+                         bool dense_only = false);
 
 // The same over several key arrays at once (a rank's receive-window
 // regions): one filter sweep, no staging copy. cudaErrorNotSupported when
@@ -107,7 +111,7 @@ cudaError_t blocked_insert_regions(const DeviceInfo& di, uint32_t* blocks, const
                                    const uint64_t* const* keys, const uint64_t* counts, uint32_t nr, cudaStream_t s);
 cudaError_t blocked_find_regions(const DeviceInfo& di, const uint32_t* blocks, const Geom& g, const BlockedPlan& plan,
                                  const uint64_t* const* keys, const uint64_t* counts, uint32_t nr, uint8_t* const* outs,
-                                 cudaStream_t s);
+                                 cudaStream_t s, bool dense_only = false);
 
 // Filter-handle entry points for the route layer (sbbf_capi.cu): the blocked
 // region path when AUTO would block the gathered batch; *handled = false

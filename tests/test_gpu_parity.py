@@ -511,10 +511,10 @@ def test_cuda_graph_capture(cuda, oracle, nb, variant):
 
 
 def test_blocked_pipelined_rounds(cuda, oracle):
-    """Lookups beyond one blocked round (2^28 keys) overlap round c+1's
-    partition with round c's probe on a side stream, double-buffered. Bytes
-    and bits must equal the direct lookup's (itself oracle-checked), also
-    when the call is captured into a CUDA graph (fork/join on events)."""
+    """Lookups spanning several rounds of the blocked path (a fused round is
+    ~2.3e8 keys on a B200; the second here is ragged). Bytes and bits must
+    equal the direct lookup's (itself oracle-checked), also when the call is
+    captured into a CUDA graph (pool scratch, the pacing counters' memsets)."""
     nb = (1 << 23) + 777                       # 256 MiB: blocked lookups
     rng = np.random.default_rng(1234)
     hs = rng.integers(0, 2**64, size=2_000_003, dtype=np.uint64)
