@@ -415,18 +415,27 @@ def test_fused_ipc_processes(cuda, oracle, world, total):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("forced", [False, True])
 @pytest.mark.parametrize("per_source", [1_500_000, 5_300_000])
-def test_fused_route_big_shards(cuda, oracle, per_source):
+def test_fused_route_big_shards(cuda, oracle, per_source, forced):
     """Shards beyond 2 x L2 (the config-5 regime). With few keys per owner
     the window goes through the direct path (gathered); with at least half a
     key per block, the blocked path takes the source regions as they are (one
-    filter sweep, no staging copy). Bit-exact either way."""
+    filter sweep, no staging copy). Under AUTO these batches (below one key
+    per block) keep the segment + unpermute kernels; `forced` sets the shards
+    to FIND_BLOCKED, which sends the regions through the fused lookup sweep
+    (packed slots with the foreign-key mark, partial chunks inside the chunk
+    layout). Bit-exact either way."""
     parts, total = 2, 2 * (300 << 20) // 32 + 3
     ops = S.CudaShardOps(0)
     bounds = S.shard_bounds(total, parts)
     db = ops._dev_bounds(bounds)
     shards = [ops.create(total, bounds[r], bounds[r + 1] - bounds[r]) for r in range(parts)]
     assert all(s.size_bytes() > 2 * (126 << 20) for s in shards)
+    if forced:
+        from paper_2101_01719_b200 import _lib
+        for s in shards:
+            s.set_find_variant(_lib.FIND_BLOCKED)
     routes = _linked_routes(parts, 1 << 23)
     rng = np.random.default_rng(4242)
     batch = [rng.integers(0, 2**64, size=per_source + 77 * r, dtype=np.uint64) for r in range(parts)]
